@@ -1,0 +1,383 @@
+"""Generate golden vectors by running the REFERENCE itself (numpy backend).
+
+Run in the build container only (needs /root/reference):
+
+    python oracle/gen_golden.py            # writes tests/golden/*.npz
+
+Every fixture is produced through the reference's public API:
+kernel_geom.build_adjacency / build_pairs, backends.reference.*,
+caseio.load_case / parse_case + build_case, stepper.Simulation, and
+expr.parse + expr.eval_field.  Inputs are seeded (numpy default_rng, whose
+streams are stable across numpy versions) or are the reference's own case
+files with scale overrides.  The fixtures pin both the oracle
+(tests/test_oracle.py) and the CUDA path (tests/test_gpu_*.py) on boxes
+where the reference is absent.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+os.environ["SOLIDSPH_BACKEND"] = "numpy"
+REF = "/root/reference/pkg"
+sys.path.insert(0, os.path.join(REF, "src"))
+sys.path.insert(0, os.path.join(REF, "tests"))
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from solidsph import caseio, kernel_geom as kg, stepper  # noqa: E402
+from solidsph import expr as rex  # noqa: E402
+from solidsph.backends import reference as ref  # noqa: E402
+from solidsph.core import KernelKind, Quad  # noqa: E402
+from conftest import lattice_2d, lattice_3d  # noqa: E402
+
+from paper_2602_15149_b200.cases import case_to_dict  # noqa: E402
+
+OUT = os.path.join(ROOT, "tests", "golden")
+CASES = os.path.join(REF, "cases")
+
+
+def save(name, **arrays):
+    os.makedirs(OUT, exist_ok=True)
+    path = os.path.join(OUT, name + ".npz")
+    np.savez_compressed(path, **arrays)
+    print(f"{path}: {os.path.getsize(path) / 1e3:.1f} kB")
+
+
+# ---------------------------------------------------------------------------
+def gen_adjacency():
+    out = {}
+
+    def add(tag, pos, dp, dim, kind, nbsrange=None, notches=(), correction=True,
+            h=None, full=True):
+        V0 = np.full(pos.shape[0], dp ** dim)
+        h = kg.smoothing_length(dp, 1.0, dim) if h is None else h
+        adj = kg.build_adjacency(pos, V0, h, dim, kind, nbsrange=nbsrange, dp_body=dp,
+                                 notches=[Quad(points=q) for q in notches],
+                                 correction=correction)
+        out[f"{tag}.X"] = pos
+        out[f"{tag}.V0"] = V0
+        out[f"{tag}.params"] = np.array([dp, dim, int(kind), -1 if nbsrange is None else nbsrange,
+                                         int(correction), h], dtype=np.float64)
+        out[f"{tag}.notches"] = np.asarray(notches, dtype=np.float64).reshape(-1, 4, 3)
+        out[f"{tag}.indptr"] = adj.indptr
+        out[f"{tag}.indices"] = adj.indices
+        out[f"{tag}.fallbacks"] = np.array([adj.correction_fallbacks])
+        if full:
+            out[f"{tag}.grad0"] = adj.grad0
+            out[f"{tag}.grad0r"] = adj.grad0r
+            out[f"{tag}.r0norm"] = adj.r0norm
+            out[f"{tag}.w0"] = adj.w0
+
+    W, C = KernelKind.WENDLAND, KernelKind.CUBIC_SPLINE
+    add("l2w", lattice_2d(12, 8, 1e-3), 1e-3, 2, W)
+    add("l2c", lattice_2d(12, 8, 1e-3), 1e-3, 2, C)
+    add("l3w", lattice_3d(7, 6, 5, 1e-3), 1e-3, 3, W)
+    add("l3c", lattice_3d(6, 5, 4, 1.0), 1.0, 3, C)
+    add("l3n", lattice_3d(7, 6, 5, 1e-3), 1e-3, 3, W, nbsrange=1)
+    add("l2n", lattice_2d(12, 8, 1e-3), 1e-3, 2, W, nbsrange=1)
+    add("l2n2", lattice_2d(9, 7, 1e-3), 1e-3, 2, W, nbsrange=2)
+    add("nocorr", lattice_2d(12, 8, 1e-3), 1e-3, 2, W, correction=False)
+    add("two", np.array([[0.0, 0.0, 0.0], [1.0, 0.0, 0.0]]), 1.0, 3, W, h=1.0)
+    # tie-heavy 3D lattice at dp=1e-3 (16% of candidate pairs sit on 2h)
+    add("tie3", lattice_3d(12, 10, 9, 1e-3), 1e-3, 3, W, full=False)
+    add("tie2", lattice_2d(40, 30, 1e-3), 1e-3, 2, W, full=False)
+    # notches: between rows (full), partial extent, 3D through-thickness
+    zc = 3.0
+    add("notch_rows", lattice_2d(6, 6, 1.0), 1.0, 2, W,
+        notches=[[[-1, -1, zc], [7, -1, zc], [7, 1, zc], [-1, 1, zc]]])
+    add("notch_part", lattice_2d(8, 6, 1.0), 1.0, 2, W,
+        notches=[[[-1, -1, zc], [3.2, -1, zc], [3.2, 1, zc], [-1, 1, zc]]])
+    add("notch3d", lattice_3d(10, 4, 10, 1e-3), 1e-3, 3, W, nbsrange=1,
+        notches=[[[0, -1e-3, 4.6e-3], [5e-3, -1e-3, 4.6e-3], [5e-3, 5e-3, 4.6e-3], [0, 5e-3, 4.6e-3]]])
+    add("notch3dr", lattice_3d(8, 4, 8, 1e-3), 1e-3, 3, W,
+        notches=[[[0, -1e-3, 4.0e-3], [5e-3, -1e-3, 4.0e-3], [5e-3, 5e-3, 4.0e-3], [0, 5e-3, 4.0e-3]]])
+    # random points (test_kernel_geom.py:98-118 input)
+    rng = np.random.default_rng(3)
+    pos = rng.uniform(0, 1, size=(300, 3))
+    pos[:, 1] = 0.0
+    rows, cols = kg.build_pairs(pos, 0.08)
+    out["rnd.X"] = pos
+    out["rnd.rows"] = rows
+    out["rnd.cols"] = cols
+    rng = np.random.default_rng(11)
+    pos = rng.uniform(0, 1, size=(400, 3))
+    rows, cols = kg.build_pairs(pos, 0.1, nbsrange=1, dp_body=0.07)
+    out["rndn.X"] = pos
+    out["rndn.rows"] = rows
+    out["rndn.cols"] = cols
+    save("adjacency", **out)
+
+
+# ---------------------------------------------------------------------------
+def _setup(dim, n1=10, n2=8, dp=1e-3, seed=0):
+    # mirrors test_backends.py:15-25
+    pos = lattice_2d(n1, n2, dp) if dim == 2 else lattice_3d(n1, n2, 5, dp)
+    V0 = np.full(pos.shape[0], dp ** dim)
+    h = kg.smoothing_length(dp, 1.0, dim)
+    adj = kg.build_adjacency(pos, V0, h, dim, KernelKind.WENDLAND)
+    rng = np.random.default_rng(seed)
+    n = pos.shape[0]
+    u = rng.normal(scale=2e-5, size=(n, 3))
+    v = rng.normal(scale=1.0, size=(n, 3))
+    if dim == 2:
+        u[:, 1] = 0.0
+        v[:, 1] = 0.0
+    return pos, V0, h, adj, u, v
+
+
+def gen_kernels():
+    out = {}
+    for dim in (2, 3):
+        pos, V0, h, adj, u, v = _setup(dim)
+        n = pos.shape[0]
+        s = np.random.default_rng(1).uniform(0.0, 1.0, n)
+        F = np.zeros((n, 3, 3))
+        ref.deformation_gradient(adj.indptr, adj.rows, adj.indices, adj.grad0, u, V0, s, 0.1,
+                                 True, F)
+        f = np.ascontiguousarray(pos[:, 0] ** 2 + 0.3 * pos[:, 2])
+        lap = np.zeros(n)
+        ref.sph_laplacian(adj.indptr, adj.rows, adj.indices, adj.grad0, adj.r0, adj.r0norm, V0,
+                          f, lap)
+        g = np.zeros((n, 3))
+        ref.sph_gradient(adj.indptr, adj.rows, adj.indices, adj.grad0, V0, f, g)
+        p = f"d{dim}."
+        out.update({p + "X": pos, p + "u": u, p + "v": v, p + "s": s, p + "F": F, p + "f": f,
+                    p + "lap": lap, p + "grad": g})
+        rng = np.random.default_rng(2)
+        Fm = np.broadcast_to(np.eye(3), (n, 3, 3)).copy()
+        Fm += rng.normal(scale=0.01, size=(n, 3, 3))
+        S = rng.normal(scale=1e5, size=(n, 3, 3))
+        S = 0.5 * (S + np.swapaxes(S, 1, 2))
+        P = np.matmul(Fm, S)
+        out[p + "Fm"] = Fm
+        out[p + "P"] = P
+        for tag, (b1, b2) in (("mom0", (0.0, 0.0)), ("mom1", (0.2, 0.1))):
+            a = np.zeros((n, 3))
+            nb = ref.momentum(adj.indptr, adj.rows, adj.indices, adj.grad0, adj.grad0r, adj.r0,
+                              adj.r0norm, P, 1000.0 * V0, 1000.0, v, h, 64.8, b1, b2, Fm, a)
+            out[p + tag] = a
+            out[p + tag + ".nbad"] = np.array([nb])
+    # constitutive batches (test_backends.py:82-149 inputs)
+    rng = np.random.default_rng(3)
+    n = 300
+    F = np.broadcast_to(np.eye(3), (n, 3, 3)).copy()
+    F += rng.normal(scale=0.08, size=(n, 3, 3))
+    s = rng.uniform(0, 1, n)
+    out["svk.F"], out["svk.s"] = F, s
+    for fr in (0, 1):
+        S, psi, psip = np.zeros((n, 3, 3)), np.zeros(n), np.zeros(n)
+        ref.svk_batch(F, 2.7733e6, 0.715e6, s, bool(fr), S, psi, psip)
+        out[f"svk{fr}.S"], out[f"svk{fr}.psi"], out[f"svk{fr}.psip"] = S, psi, psip
+    rng = np.random.default_rng(4)
+    F = np.broadcast_to(np.eye(3), (n, 3, 3)).copy()
+    F += rng.normal(scale=0.1, size=(n, 3, 3))
+    F[0] *= 1e-3
+    s = rng.uniform(0, 1, n)
+    out["nh.F"], out["nh.s"] = F, s
+    for fr in (0, 1):
+        S, psi, psip = np.zeros((n, 3, 3)), np.zeros(n), np.zeros(n)
+        nb = ref.nh_batch(F, 3.25e6, 0.715e6, s, bool(fr), S, psi, psip)
+        out[f"nh{fr}.S"], out[f"nh{fr}.psi"], out[f"nh{fr}.psip"] = S, psi, psip
+        out[f"nh{fr}.nbad"] = np.array([nb])
+    rng = np.random.default_rng(5)
+    n = 400
+    F = np.broadcast_to(np.eye(3), (n, 3, 3)).copy()
+    F += rng.normal(scale=0.015, size=(n, 3, 3))
+    F[7] *= 1e-3   # a degenerate lane
+    Cp = np.broadcast_to(np.eye(3), (n, 3, 3)).copy()
+    ep = np.zeros(n)
+    S, psi, dwp = np.zeros((n, 3, 3)), np.zeros(n), np.zeros(n)
+    nb, fb = ref.j2_batch(F, Cp, ep, 43.333e9, 130e9, 4e8, 1e8, S, psi, dwp)
+    out.update({"j2.F": F, "j2.Cp": Cp, "j2.ep": ep, "j2.S": S, "j2.psi": psi, "j2.dwp": dwp,
+                "j2.ret": np.array([nb, fb])})
+    # second J2 call from the updated state (history path)
+    F2 = F + rng.normal(scale=0.004, size=(n, 3, 3))
+    Cp2, ep2 = Cp.copy(), ep.copy()
+    S, psi, dwp = np.zeros((n, 3, 3)), np.zeros(n), np.zeros(n)
+    nb, fb = ref.j2_batch(F2, Cp2, ep2, 43.333e9, 130e9, 4e8, 1e8, S, psi, dwp)
+    out.update({"j2b.F": F2, "j2b.Cp": Cp2, "j2b.ep": ep2, "j2b.S": S, "j2b.psi": psi,
+                "j2b.dwp": dwp, "j2b.ret": np.array([nb, fb])})
+    # contact (test_backends.py:152-174)
+    rng = np.random.default_rng(6)
+    na, nbb = 40, 50
+    xa = rng.uniform(0, 0.05, (na, 3))
+    xb = rng.uniform(0.01, 0.06, (nbb, 3))
+    va = rng.normal(scale=10, size=(na, 3))
+    vb = rng.normal(scale=10, size=(nbb, 3))
+    pairs = np.array([(i, j) for i in range(na) for j in range(nbb)], dtype=np.int64)
+    aa, ab = np.zeros((na, 3)), np.zeros((nbb, 3))
+    w = ref.contact_pair_accumulate(xa, va, np.full(na, 0.3), xb, vb, np.full(nbb, 0.4), pairs,
+                                    0.012, 1e7, 30.0, 0.3, aa, ab)
+    out.update({"ct.xa": xa, "ct.xb": xb, "ct.va": va, "ct.vb": vb, "ct.aa": aa, "ct.ab": ab,
+                "ct.warn": np.array([w])})
+    # symmetric eigen problems for the Jacobi solver
+    rng = np.random.default_rng(7)
+    A = rng.normal(size=(200, 3, 3))
+    A = 0.5 * (A + np.swapaxes(A, 1, 2))
+    out["eig.A"] = A
+    out["eig.w"] = np.linalg.eigvalsh(A)
+    save("kernels", **out)
+
+
+# ---------------------------------------------------------------------------
+def _state(sim, full=True):
+    d = {}
+    keys = ("u", "v", "a", "s", "sdot", "sddot", "Hhist", "epbar", "psi_e", "F", "S", "Cp")
+    for bi, b in enumerate(sim.bodies):
+        st = b.state
+        for k in keys if full else ("u", "v", "a", "s", "sdot"):
+            d[f"b{bi}.{k}"] = getattr(st, k).copy()
+        d[f"b{bi}.plastic_work"] = np.array([b.plastic_work])
+        d[f"b{bi}.degenerate"] = np.array([b.degenerate_warnings])
+    d["t"] = np.array([sim.t])
+    return d
+
+
+def _kalthoff3d_raw():
+    raw = caseio.parse_case(os.path.join(CASES, "kalthoff2d.xml"))
+    raw.dim = 3
+    for q in raw.bodies[0].notches:
+        q.points[2, 1] = 11e-3
+        q.points[3, 1] = 11e-3
+    return raw
+
+
+def _perturb(cfg, seed):
+    """Seeded non-trivial initial state (step-1 parity on a
+    u=0 state is vacuous).  Mirrors backend_bench.py:29-34 scaling."""
+    rng = np.random.default_rng(seed)
+    for b in cfg.bodies:
+        st = b.state
+        n = st.X.shape[0]
+        st.u[:] = rng.normal(scale=2e-5 * b.dp_body / 1e-3, size=(n, 3))
+        st.v[:] = rng.normal(scale=1.0, size=(n, 3))
+        if b.fracture:
+            st.s[:] = rng.uniform(0.3, 1.0, n)
+        if b.dim == 2:
+            st.u[:, 1] = 0.0
+            st.v[:, 1] = 0.0
+    return cfg
+
+
+def gen_runs():
+    L = caseio.load_case
+    C = lambda f: os.path.join(CASES, f)  # noqa: E731
+    runs = [
+        # tag, config builder, perturbation seed (None = as loaded), steps, checkpoints
+        ("kalthoff2d", lambda: L(C("kalthoff2d.xml"), dp_scale=2, mapfac=1), None, 40, (1, 2, 10, 40)),
+        ("kalthoff2d_p", lambda: L(C("kalthoff2d.xml"), dp_scale=2, mapfac=1), 31, 20, (1, 2, 20)),
+        ("kalthoff2d_sym", lambda: _with_algo(L(C("kalthoff2d.xml"), dp_scale=2, mapfac=1), 2),
+         32, 20, (1, 2, 20)),
+        ("beam2d", lambda: L(C("beam2d.xml"), dp_scale=2, mapfac=2), None, 30, (1, 2, 30)),
+        ("taylor3d", lambda: L(C("taylor3d.xml"), dp_scale=4), 33, 20, (1, 2, 20)),
+        ("column3d", lambda: L(C("column3d.xml"), dp_scale=2, mapfac=1), 34, 20, (1, 2, 20)),
+        ("branch2d", lambda: L(C("branch2d.xml"), dp_scale=8, mapfac=1), 35, 20, (1, 2, 20)),
+        ("kalthoff3d", lambda: caseio.build_case(_kalthoff3d_raw(), dp_scale=6, mapfac=2), 36,
+         10, (1, 2, 10)),
+        ("twisting3d", lambda: L(C("twisting3d.xml"), dp_scale=4), 37, 10, (1, 10)),
+    ]
+    for tag, make, seed, steps, checks in runs:
+        cfg = make()
+        if seed is not None:
+            _perturb(cfg, seed)
+        out = dict(case_to_dict(cfg))
+        for bi, b in enumerate(cfg.bodies):
+            out[f"adj{bi}.indptr"] = b.adjacency.indptr
+            out[f"adj{bi}.indices"] = b.adjacency.indices
+            out[f"adj{bi}.fallbacks"] = np.array([b.adjacency.correction_fallbacks])
+            for k in ("u", "v", "s"):
+                out[f"init.b{bi}.{k}"] = getattr(b.state, k).copy()
+        sim = stepper.Simulation(cfg)
+        sim.initialize()
+        for k, v in _state(sim).items():
+            out[f"s0.{k}"] = v
+        dts = []
+        for step in range(1, steps + 1):
+            dt = sim.pick_dt()
+            dts.append(dt)
+            sim.step(dt)
+            if step in checks:
+                full = step in (checks[0], checks[-1])
+                for k, v in _state(sim, full).items():
+                    out[f"s{step}.{k}"] = v
+        out["dts"] = np.array(dts)
+        out["checkpoints"] = np.array(checks)
+        save(f"run_{tag}", **out)
+
+
+def _with_algo(cfg, algo):
+    from solidsph.core import StepAlgorithm
+    cfg.step_algorithm = StepAlgorithm(algo)
+    return cfg
+
+
+# ---------------------------------------------------------------------------
+EXPRS = [
+    ("if(t>ramt,maxv,t/ramt*maxv)", "maxv=16.5; ramt=1.0e-6"),
+    ("if(x0<=0.0,0.0,skip)", ""),
+    ("if(x0>xtip,if(t<=Tmax,t/Tmax,1.0)*Fmax,skip)", "Fmax=-1.75e9; Tmax=1.0; xtip=0.099;"),
+    ("if(z<1.0e-12,0.0,if(t<=0.0,Vinit,skip))", "Vinit=-227;"),
+    ("sin(x)*cos(y0) + tan(0.3*z) - cot(1+ux) + sinh(uy) - cosh(0.1*uz)", ""),
+    ("tanh(x0*10) + coth(2+y) + sqrt(abs(z)) + log(2+x) + ln(3+t)", ""),
+    ("pow(2, x0) + 2^3^0.5 - -x*-y + (x0 < 0.5 and y0 >= 0.2) + (z0 == 0 or t != 1)", ""),
+    ("if(x0 < 0.3, if(y0 < 0.5, skip, x0*dx), -dt*3 + t)", ""),
+    ("-2^2 + 3*-x0/(1+y0) - (z0 <= 0.5) * (x > 0.1)", ""),
+    ("x0 - 2*(x0 > 0.5)*x0 + if(abs(y0-0.5) < 0.25, 1, 0)", ""),
+]
+
+
+def gen_expr():
+    rng = np.random.default_rng(21)
+    n = 257
+    ctx = {"x0": rng.uniform(0, 1, n), "y0": rng.uniform(0, 1, n), "z0": rng.uniform(0, 1, n),
+           "ux": rng.normal(scale=1e-3, size=n), "uy": rng.normal(scale=1e-3, size=n),
+           "uz": rng.normal(scale=1e-3, size=n), "t": 2.5e-6, "dt": 1e-7, "dx": 0.002}
+    ctx["x"] = ctx["x0"] + ctx["ux"]
+    ctx["y"] = ctx["y0"] + ctx["uy"]
+    ctx["z"] = ctx["z0"] + ctx["uz"]
+    out = {k: np.asarray(v) for k, v in ctx.items()}
+    for k, (src, loc) in enumerate(EXPRS):
+        ast = rex.parse(src, loc)
+        vals, skip = rex.eval_field(ast, ctx, n)
+        out[f"e{k}.vals"] = vals
+        out[f"e{k}.skip"] = skip
+        out[f"e{k}.pretty"] = np.frombuffer(rex.pretty(ast).encode(), dtype=np.uint8)
+    out["sources"] = np.frombuffer("\n".join(f"{s}\t{l}" for s, l in EXPRS).encode(),
+                                   dtype=np.uint8)
+    save("expr", **out)
+
+
+def gen_targets():
+    """BC target sets resolved by the reference's loader for the C1-C5
+    geometries at reduced size (checks cases.make_case)."""
+    out = {}
+    specs = [("kalthoff2d", "kalthoff2d.xml", dict(dp_scale=2, mapfac=1)),
+             ("branch2d", "branch2d.xml", dict(dp_scale=8, mapfac=1)),
+             ("beam2d", "beam2d.xml", dict(dp_scale=2, mapfac=2)),
+             ("taylor3d", "taylor3d.xml", dict(dp_scale=4)),
+             ("column3d", "column3d.xml", dict(dp_scale=2, mapfac=1))]
+    for tag, f, kw in specs:
+        cfg = caseio.load_case(os.path.join(CASES, f), **kw)
+        b = cfg.bodies[0]
+        out[f"{tag}.X"] = b.state.X
+        out[f"{tag}.kw"] = np.array([kw.get("dp_scale", 1.0), kw.get("mapfac", 0)])
+        for ci, bc in enumerate(b.bcs):
+            if bc.target is not None:
+                out[f"{tag}.bc{ci}"] = bc.target
+    cfg = caseio.build_case(_kalthoff3d_raw(), dp_scale=6, mapfac=2)
+    out["kalthoff3d.X"] = cfg.bodies[0].state.X
+    out["kalthoff3d.kw"] = np.array([6.0, 2])
+    for ci, bc in enumerate(cfg.bodies[0].bcs):
+        if bc.target is not None:
+            out[f"kalthoff3d.bc{ci}"] = bc.target
+    save("targets", **out)
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["adjacency", "kernels", "runs", "expr", "targets"]
+    for w in which:
+        globals()[f"gen_{w}"]()

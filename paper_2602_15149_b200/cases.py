@@ -1,0 +1,378 @@
+"""Case assembly without the reference package.
+
+Two jobs:
+  1. ``case_to_dict`` / ``case_from_dict``: a flat, numpy-only snapshot of a
+     CaseConfig (reference or ours), so golden runs produced by the reference
+     in the build container can be replayed on a GPU box that has no
+     /root/reference.
+  2. ``make_case``: the BASELINE workloads (C1-C5) and the shipped cases the
+     parity suite uses, built from the same lattice rules as the reference's
+     case loader (caseio.py:71-138 box/cylinder lattices, :157-172 BC targets,
+     :481-598 assembly).  Parameters are transcribed from the reference's case
+     files (cited per spec) -- this module never reads them.
+
+Case I/O is not on the hot path; only the neighbour build is (hooked through
+``kernel_geom.build_adjacency``, which runs on the device).
+"""
+
+from __future__ import annotations
+
+import json
+import math
+
+import numpy as np
+
+from . import expr as ex
+from .core import (Body, BoundaryCondition, CaseConfig, CaseError, KernelKind,
+                   MaterialParams, Model, ParticleArrays, Quad, StepAlgorithm,
+                   normalize_elastic_constants)
+
+# ---------------------------------------------------------------------------
+# lattices (caseio.py:71-138)
+# ---------------------------------------------------------------------------
+
+
+def _centers(origin, length, dp, at_least_one):
+    count = int(round(length / dp))
+    if count >= 1:
+        return origin + (np.arange(count) + 0.5) * dp
+    if at_least_one:
+        return np.array([origin + 0.5 * length])
+    return np.array([])
+
+
+def box_lattice(origin, size, dp, dim=3, y_plane=0.0, at_least_one=False):
+    """Cell-centred lattice filling a box; x-major (meshgrid 'ij') order."""
+    origin = np.asarray(origin, dtype=np.float64)
+    size = np.asarray(size, dtype=np.float64)
+    axes = []
+    for ax in range(3):
+        if dim == 2 and ax == 1:
+            axes.append(np.array([y_plane]))
+            continue
+        c = _centers(origin[ax], size[ax], dp, at_least_one)
+        if c.size == 0:
+            raise CaseError(f"box produced zero particles (extent {size[ax]!r} at dp {dp!r})")
+        axes.append(c)
+    g = np.meshgrid(*axes, indexing="ij")
+    return np.column_stack([a.ravel() for a in g])
+
+
+def cylinder_lattice(p0, p1, radius, dp):
+    """Axis-aligned lattice clipped to a cylinder (caseio.py:107-138)."""
+    p0 = np.asarray(p0, dtype=np.float64)
+    p1 = np.asarray(p1, dtype=np.float64)
+    delta = p1 - p0
+    axis = int(np.argmax(np.abs(delta)))
+    lo, hi = sorted((p0[axis], p1[axis]))
+    axial = _centers(lo, hi - lo, dp, False)
+    k = int(math.ceil(radius / dp)) + 1
+    off = (np.arange(-k, k) + 0.5) * dp
+    g1, g2 = np.meshgrid(off, off, indexing="ij")
+    keep = g1 ** 2 + g2 ** 2 <= radius * radius
+    o1, o2 = g1[keep], g2[keep]
+    perp = [a for a in range(3) if a != axis]
+    pos = np.empty((o1.size * axial.size, 3))
+    pos[:, axis] = np.repeat(axial, o1.size)
+    pos[:, perp[0]] = np.tile(o1 + p0[perp[0]], axial.size)
+    pos[:, perp[1]] = np.tile(o2 + p0[perp[1]], axial.size)
+    return pos
+
+
+def _shapes_lattice(shapes, dp, dim, y_plane, at_least_one=False):
+    parts = []
+    for s in shapes:
+        if s["kind"] == "box":
+            parts.append(box_lattice(s["point"], s["size"], dp, dim, y_plane, at_least_one))
+        else:
+            parts.append(cylinder_lattice(s["p0"], s["p1"], s["radius"], dp))
+    return np.concatenate(parts)
+
+
+def bc_targets(X, aux, dp):
+    """Particles closer than dp to any auxiliary point (caseio.py:157-172).
+
+    Uses a uniform grid of cell size dp so it scales to 10^8 particles."""
+    aux = np.asarray(aux, dtype=np.float64)
+    lo = aux.min(axis=0) - dp
+    hi = aux.max(axis=0) + dp
+    near = np.all((X >= lo) & (X <= hi), axis=1)
+    cand = np.flatnonzero(near)
+    if cand.size == 0:
+        return cand.astype(np.int64)
+    cell = dp
+    key_aux = np.floor((aux - lo) / cell).astype(np.int64)
+    buckets = {}
+    for idx, k in enumerate(map(tuple, key_aux)):
+        buckets.setdefault(k, []).append(idx)
+    keys = np.floor((X[cand] - lo) / cell).astype(np.int64)
+    best = np.full(cand.size, np.inf)
+    offs = [(a, b, c) for a in (-1, 0, 1) for b in (-1, 0, 1) for c in (-1, 0, 1)]
+    uniq, inv = np.unique(keys, axis=0, return_inverse=True)
+    inv = inv.ravel()
+    for u_i, k in enumerate(uniq):
+        pts = [j for o in offs for j in buckets.get((k[0] + o[0], k[1] + o[1], k[2] + o[2]), ())]
+        if not pts:
+            continue
+        sel = np.flatnonzero(inv == u_i)
+        d = X[cand[sel]][:, None, :] - aux[pts][None, :, :]
+        d2 = d[..., 0] * d[..., 0] + d[..., 1] * d[..., 1]
+        d2 = d2 + d[..., 2] * d[..., 2]
+        best[sel] = np.sqrt(np.min(d2, axis=1))
+    return cand[best < dp].astype(np.int64)
+
+
+# ---------------------------------------------------------------------------
+# specs transcribed from /root/reference/pkg/cases/*.xml
+# ---------------------------------------------------------------------------
+
+def _kalthoff_spec(dim):
+    # kalthoff2d.xml:16-80, 84-89
+    return dict(
+        dp=1.0e-3, dim=dim, y_plane=0.5e-3, coefh=1.0, cfl=0.2,
+        kernel=2, algo=1, time_max=120e-6, time_out=1e-6,
+        shapes=[dict(mk=1, kind="box", point=[0.5e-3, 0.0, 0.5e-3], size=[99.5e-3, 10e-3, 99.5e-3]),
+                dict(mk=2, kind="box", point=[-0.5e-3, 0.0, 0.5e-3], size=[0.5e-3, 10e-3, 24.5e-3]),
+                dict(mk=3, kind="box", point=[0.5e-3, 0.0, -0.5e-3], size=[99.5e-3, 10e-3, 0.5e-3])],
+        expressions={2: ("if(t>ramt,maxv,t/ramt*maxv)", "maxv=16.5; ramt=1.0e-6")},
+        bodies=[dict(mk=1, cards=dict(nbsrange=1, density=8000.0, youngmod=190e9, poissratio=0.3,
+                                      constitmodel=1, beta1=0.1, beta2=0.0, fracture=True,
+                                      Gc=22.13e3, pflim=0.05, pflenscale=0.15e-3, mapfac=8),
+                     bcs=[dict(kind="vel", mkid=2, expr=(2, None, None)),
+                          dict(kind="vel", mkid=3, const=(None, None, 0.0))],
+                     # the 3D extrusion carries the notch through the thickness
+                     # (SURVEY.md 8(d) C4); 2D keeps the file's corners
+                     notches=[[[0.0, -1e-3, 25.6e-3], [50e-3, -1e-3, 25.6e-3],
+                               [50e-3, 11e-3 if dim == 3 else 1e-3, 25.6e-3],
+                               [0.0, 11e-3 if dim == 3 else 1e-3, 25.6e-3]]])])
+
+
+def _beam_spec():
+    # beam2d.xml:14-78
+    src1 = ("if(x0<=0.0,0.0,if(t<=0.0,0.01 * cs * ((cos(kw*L0)+cosh(kw*L0))*(cosh(kw*x0)-cos(kw*x0))"
+            " + (sin(kw*L0)-sinh(kw*L0))*(sinh(kw*x0)-sin(kw*x0)))/ ((cos(kw*L0)+cosh(kw*L0))"
+            "*(cosh(kw*L0)-cos(kw*L0)) + (sin(kw*L0)-sinh(kw*L0))*(sinh(kw*L0)-sin(kw*L0))),skip))")
+    return dict(
+        dp=1.0e-3, dim=2, y_plane=0.5e-3, coefh=1.0, cfl=0.2, kernel=2, algo=1,
+        time_max=1.0, time_out=1e-3,
+        shapes=[dict(mk=1, kind="box", point=[-1.5e-3, 0.5e-3, 0.5e-3], size=[200.5e-3, 19e-3, 19e-3])],
+        expressions={1: (src1, "L0=0.2; kw=9.375; cs=57.0"), 2: ("if(x0<=0.0,0.0,skip)", "")},
+        bodies=[dict(mk=1, cards=dict(density=1000.0, u_mu=0.715e6, u_bulk=3.25e6, constitmodel=1,
+                                      beta1=0.015, beta2=0.01, mapfac=4),
+                     bcs=[dict(kind="vel", expr=(2, 2, 1))], notches=[])])
+
+
+def _column_spec():
+    # column3d.xml:14-76
+    return dict(
+        dp=1.0e-3, dim=3, y_plane=0.0, coefh=1.0, cfl=0.2, kernel=2, algo=1,
+        time_max=2.0, time_out=0.002,
+        shapes=[dict(mk=1, kind="box", point=[-1.5e-3, 0.5e-3, 0.5e-3], size=[101e-3, 9e-3, 9e-3])],
+        expressions={1: ("if(x0>xtip,if(t<=Tmax,t/Tmax,1.0)*Fmax,skip)", "Fmax=-1.75e9; Tmax=1.0; xtip=0.099;"),
+                     2: ("if(x0<=0.0,0.0,skip)", "")},
+        bodies=[dict(mk=1, cards=dict(density=7800.0, youngmod=210e9, poissratio=0.3, constitmodel=2,
+                                      beta1=0.1, beta2=0.0, mapfac=1),
+                     bcs=[dict(kind="force", ftype=2, expr=(None, None, 1)),
+                          dict(kind="vel", expr=(2, 2, 2))], notches=[])])
+
+
+def _taylor_spec():
+    # taylor3d.xml:14-67
+    return dict(
+        dp=0.2e-3, dim=3, y_plane=0.0, coefh=1.0, cfl=0.02, kernel=2, algo=1,
+        time_max=2.5e-4, time_out=0.01e-4,
+        shapes=[dict(mk=1, kind="cylinder", radius=3.2e-3, p0=[0.0, 0.0, 0.0], p1=[0.0, 0.0, 32.4e-3])],
+        expressions={1: ("if(z<1.0e-12,0.0,if(t<=0.0,Vinit,skip))", "Vinit=-227;")},
+        bodies=[dict(mk=1, cards=dict(density=8930.0, youngmod=1.17e11, poissratio=0.35, beta1=0.05,
+                                      beta2=0.0, constitmodel=3, yieldstress=400e6, hardening=100e6),
+                     bcs=[dict(kind="vel", expr=(None, None, 1))], notches=[])])
+
+
+def _branch_spec():
+    # branch2d.xml:14-86
+    return dict(
+        dp=0.125e-3, dim=2, y_plane=0.5e-3, coefh=1.0, cfl=0.2, kernel=2, algo=1,
+        time_max=120e-6, time_out=1e-6,
+        shapes=[dict(mk=3, kind="box", point=[0.06125e-3, 0.06125e-3, 39.9385e-3], size=[99.9385e-3, 0.9385e-3, 0.125e-3]),
+                dict(mk=2, kind="box", point=[0.06125e-3, 0.06125e-3, -0.06125e-3], size=[99.9385e-3, 0.9385e-3, 0.06125e-3]),
+                dict(mk=1, kind="box", point=[0.06125e-3, 0.0, 0.06125e-3], size=[99.9385e-3, 1.0e-3, 39.9385e-3])],
+        expressions={},
+        bodies=[dict(mk=1, cards=dict(nbsrange=1, density=2450.0, youngmod=32e9, poissratio=0.2,
+                                      constitmodel=1, beta1=0.2, beta2=0.0, fracture=True, Gc=3.0,
+                                      pflim=0.05, pflenscale=0.12501e-3, mapfac=2),
+                     bcs=[dict(kind="force", ftype=2, mkid=3, const=(None, None, 1.0e6)),
+                          dict(kind="force", ftype=2, mkid=2, const=(None, None, -1.0e6))],
+                     notches=[[[-2e-3, -5e-3, 0.02], [50.030625e-3, -5e-3, 0.02],
+                               [50.030625e-3, 25e-3, 0.02], [-2e-3, 25e-3, 0.02]]])])
+
+
+SPECS = {
+    "kalthoff2d": lambda: _kalthoff_spec(2),
+    "kalthoff3d": lambda: _kalthoff_spec(3),
+    "beam2d": _beam_spec,
+    "column3d": _column_spec,
+    "taylor3d": _taylor_spec,
+    "branch2d": _branch_spec,
+}
+
+# BASELINE.json configs -> (spec, overrides); sizes per SURVEY.md 8(d)
+WORKLOADS = {
+    "C1": ("beam2d", dict(dp_scale=2.0, mapfac=2)),                 # N = 3,800
+    "C2": ("column3d", dict(mapfac=5)),                              # N = 1,022,625
+    "C3": ("taylor3d", dict(dp_scale=0.32)),                          # N = 3,977,160
+    "C4": ("kalthoff3d", dict(dp_scale=0.918, mapfac=5)),            # N = 15,863,256
+    "C5": ("branch2d", dict(dp_scale=0.0893, mapfac=2)),             # N = 128,135,336
+}
+
+
+def _material(cards, mk):
+    lam, mu, kappa = normalize_elastic_constants(
+        E=cards.get("youngmod"), nu=cards.get("poissratio"), lam=cards.get("u_lambda"),
+        mu=cards.get("u_mu"), kappa=cards.get("u_bulk"), where=f"mkbound={mk}")
+    return MaterialParams(
+        rho0=cards["density"], lam=lam, mu=mu, kappa=kappa,
+        model=Model(int(cards.get("constitmodel", 1))), beta1=cards.get("beta1", 0.2),
+        beta2=cards.get("beta2", 0.0), Gc=cards.get("Gc", 0.0), eps0=cards.get("pflenscale", 0.0),
+        s_l=cards.get("pflim", 0.1), sigma_y0=cards.get("yieldstress", 0.0),
+        H_hard=cards.get("hardening", 0.0))
+
+
+def make_case(name, dp_scale=1.0, mapfac=None, eps0=None, cfl=None, dt_override=None,
+              time_max=None, time_out=None, build_adjacency=True, precision="fp64"):
+    """Assemble a CaseConfig the way caseio.build_case does (caseio.py:481-598)
+    for one of ``SPECS`` or a ``WORKLOADS`` key ("C1".."C5")."""
+    if name in WORKLOADS:
+        spec_name, kw = WORKLOADS[name]
+        kw = dict(kw)
+        if dp_scale != 1.0:
+            kw["dp_scale"] = dp_scale
+        if mapfac is not None:
+            kw["mapfac"] = mapfac
+        return make_case(spec_name, eps0=eps0, cfl=cfl, dt_override=dt_override,
+                         time_max=time_max, time_out=time_out,
+                         build_adjacency=build_adjacency, precision=precision, **kw)
+    spec = SPECS[name]()
+    dp = spec["dp"] * dp_scale
+    dim = spec["dim"]
+    cfg = CaseConfig(dp=dp, coefh=spec["coefh"], cfl=spec["cfl"] if cfl is None else cfl,
+                     kernel=KernelKind(spec["kernel"]), step_algorithm=StepAlgorithm(spec["algo"]),
+                     time_max=spec["time_max"] if time_max is None else time_max,
+                     time_out=spec["time_out"] if time_out is None else time_out,
+                     dim=dim, dt_override=dt_override)
+    body_mks = {b["mk"] for b in spec["bodies"]}
+    for mk in sorted({s["mk"] for s in spec["shapes"]} - body_mks):
+        cfg.aux_geometries[mk] = _shapes_lattice(
+            [s for s in spec["shapes"] if s["mk"] == mk], dp, dim, spec["y_plane"], True)
+    for eid, (src, loc) in spec["expressions"].items():
+        cfg.expressions[eid] = ex.parse(src, loc)
+    for bspec in spec["bodies"]:
+        cards = dict(bspec["cards"])
+        if mapfac is not None:
+            cards["mapfac"] = mapfac
+        if eps0 is not None:
+            cards["pflenscale"] = eps0
+        mat = _material(cards, bspec["mk"])
+        frac = bool(cards.get("fracture", False)) and mat.model != Model.J2
+        mat.validate(frac, where=f"mk={bspec['mk']}")
+        dp_body = dp / int(round(cards.get("mapfac", 1)))
+        X = _shapes_lattice([s for s in spec["shapes"] if s["mk"] == bspec["mk"]], dp_body,
+                            dim, spec["y_plane"])
+        V0 = np.full(X.shape[0], dp_body ** 2 if dim == 2 else dp_body ** 3)
+        st = ParticleArrays.from_reference(X, V0, mat.rho0)
+        h = spec["coefh"] * dp_body * math.sqrt(dim)   # kernel_geom.py:21-27
+        body = Body(mk=bspec["mk"], state=st, material=mat, dp_body=dp_body, h=h, dim=dim,
+                    fracture=frac, notches=[Quad(points=q) for q in bspec["notches"]],
+                    nbsrange=cards.get("nbsrange"), f0=np.zeros(3))
+        for b in bspec["bcs"]:
+            bc = BoundaryCondition(kind=b["kind"], ftype=b.get("ftype", 0), mkid=b.get("mkid"),
+                                   const=tuple(b.get("const", (None, None, None))),
+                                   expr=tuple(b.get("expr", (None, None, None))))
+            if bc.mkid is not None:
+                bc.target = bc_targets(X, cfg.aux_geometries[bc.mkid], dp)
+                if bc.target.size == 0:
+                    raise CaseError(f"empty target set for mkid {bc.mkid}")
+            body.bcs.append(bc)
+        if build_adjacency:
+            from . import kernel_geom
+            body.adjacency = kernel_geom.build_adjacency(
+                X, V0, h, dim, cfg.kernel, nbsrange=body.nbsrange, dp_body=dp_body,
+                notches=body.notches, correction=body.kernel_correction)
+        cfg.bodies.append(body)
+    cfg.validate()
+    return cfg
+
+
+# ---------------------------------------------------------------------------
+# flat snapshot (numpy arrays + a JSON header)
+# ---------------------------------------------------------------------------
+
+def case_to_dict(cfg, prefix=""):
+    """Flatten a CaseConfig (either package's) into {name: ndarray}."""
+    meta = dict(dp=cfg.dp, coefh=cfg.coefh, cfl=cfg.cfl, kernel=int(cfg.kernel),
+                algo=int(cfg.step_algorithm), time_max=cfg.time_max, time_out=cfg.time_out,
+                dim=int(cfg.dim), dt_override=cfg.dt_override,
+                gravity=[float(g) for g in cfg.gravity],
+                expressions={str(k): [a.source, _locals_src(a)] for k, a in cfg.expressions.items()},
+                bodies=[])
+    out = {}
+    for bi, b in enumerate(cfg.bodies):
+        m = b.material
+        bm = dict(mk=b.mk, dp_body=b.dp_body, h=b.h, dim=b.dim, fracture=bool(b.fracture),
+                  nbsrange=b.nbsrange, kernel_correction=bool(b.kernel_correction),
+                  restrictphi_expr=b.restrictphi_expr, f0=[float(x) for x in b.f0],
+                  material=dict(rho0=m.rho0, lam=m.lam, mu=m.mu, kappa=m.kappa, model=int(m.model),
+                                beta1=m.beta1, beta2=m.beta2, Gc=m.Gc, eps0=m.eps0, s_l=m.s_l,
+                                sigma_y0=m.sigma_y0, H_hard=m.H_hard),
+                  notches=[np.asarray(q.points).tolist() for q in b.notches], bcs=[])
+        for ci, bc in enumerate(b.bcs):
+            bm["bcs"].append(dict(kind=bc.kind, ftype=bc.ftype, mkid=bc.mkid,
+                                  const=list(bc.const), expr=list(bc.expr), tst=bc.tst,
+                                  tend=None if math.isinf(bc.tend) else bc.tend,
+                                  has_target=bc.target is not None))
+            if bc.target is not None:
+                out[f"{prefix}b{bi}.bc{ci}.target"] = np.asarray(bc.target, dtype=np.int64)
+        meta["bodies"].append(bm)
+        out[f"{prefix}b{bi}.X"] = np.asarray(b.state.X)
+        out[f"{prefix}b{bi}.V0"] = np.asarray(b.state.V0)
+    out[f"{prefix}meta"] = np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8)
+    return out
+
+
+def _locals_src(ast):
+    return "; ".join(f"{k}={float(v)!r}" for k, v in ast.locals.items())
+
+
+def case_from_dict(d, prefix="", build_adjacency=False):
+    """Inverse of case_to_dict; returns this package's CaseConfig."""
+    meta = json.loads(bytes(np.asarray(d[f"{prefix}meta"], dtype=np.uint8)).decode())
+    cfg = CaseConfig(dp=meta["dp"], coefh=meta["coefh"], cfl=meta["cfl"],
+                     kernel=KernelKind(meta["kernel"]), step_algorithm=StepAlgorithm(meta["algo"]),
+                     time_max=meta["time_max"], time_out=meta["time_out"], dim=meta["dim"],
+                     gravity=np.asarray(meta["gravity"]), dt_override=meta["dt_override"])
+    for k, (src, loc) in meta["expressions"].items():
+        cfg.expressions[int(k)] = ex.parse(src, loc)
+    for bi, bm in enumerate(meta["bodies"]):
+        mm = dict(bm["material"])
+        mm["model"] = Model(mm["model"])
+        mat = MaterialParams(**mm)
+        X = np.asarray(d[f"{prefix}b{bi}.X"], dtype=np.float64)
+        V0 = np.asarray(d[f"{prefix}b{bi}.V0"], dtype=np.float64)
+        st = ParticleArrays.from_reference(X, V0, mat.rho0)
+        body = Body(mk=bm["mk"], state=st, material=mat, dp_body=bm["dp_body"], h=bm["h"],
+                    dim=bm["dim"], fracture=bm["fracture"], nbsrange=bm["nbsrange"],
+                    kernel_correction=bm["kernel_correction"],
+                    restrictphi_expr=bm["restrictphi_expr"], f0=np.asarray(bm["f0"]),
+                    notches=[Quad(points=q) for q in bm["notches"]])
+        for ci, bc in enumerate(bm["bcs"]):
+            body.bcs.append(BoundaryCondition(
+                kind=bc["kind"], ftype=bc["ftype"], mkid=bc["mkid"],
+                const=tuple(bc["const"]), expr=tuple(bc["expr"]), tst=bc["tst"],
+                tend=math.inf if bc["tend"] is None else bc["tend"],
+                target=np.asarray(d[f"{prefix}b{bi}.bc{ci}.target"]) if bc["has_target"] else None))
+        if build_adjacency:
+            from . import kernel_geom
+            body.adjacency = kernel_geom.build_adjacency(
+                X, V0, body.h, body.dim, cfg.kernel, nbsrange=body.nbsrange,
+                dp_body=body.dp_body, notches=body.notches, correction=body.kernel_correction)
+        cfg.bodies.append(body)
+    return cfg

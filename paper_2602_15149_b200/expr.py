@@ -1,0 +1,478 @@
+"""User-expression language: parser (host) and bytecode compiler for the
+device evaluator (``csrc/expr_vm.cuh``).
+
+Grammar and semantics follow the reference expression module
+(/root/reference/pkg/src/solidsph/expr.py):
+  * variables x0 y0 z0 x y z ux uy uz t dt dx (expr.py:46);
+  * functions sin cos tan cot sinh cosh tanh coth sqrt log(base 10) ln abs
+    (arity 1), pow (2), if (3, lazy) (expr.py:48-56);
+  * binary precedence or < and < comparisons < +,- < *,/ < ^ (right
+    associative); unary minus sits between * and ^ (expr.py:58-68);
+  * ``skip``/``Skip`` is legal only as the whole expression or an if-branch
+    (expr.py:264-285);
+  * ``<locals>`` are ``name=value;`` constant definitions folded at parse
+    time (expr.py:208-232).
+ASTs are the same immutable tuples the reference builds, so an ``ExprAst``
+from either package can be compiled here.
+
+Instead of walking the AST per particle on the host (the reference's masked
+numpy evaluator, expr.py:419-551), ``compile_program`` lowers an AST to a
+flat postfix program with conditional jumps; every particle lane runs it on
+the device inside the integrator kernel.  Because ``skip`` can only sit in
+tail position of an if-chain, it lowers to a terminating opcode.
+"""
+
+from __future__ import annotations
+
+import math
+import re
+from dataclasses import dataclass
+
+import numpy as np
+
+
+class ExprError(ValueError):
+    """Parse or evaluation error; carries the source offset when known."""
+
+    def __init__(self, message, offset=None):
+        if offset is not None:
+            message = f"{message} (at offset {offset})"
+        super().__init__(message)
+        self.offset = offset
+
+
+class _SkipType:
+    _one = None
+
+    def __new__(cls):
+        if cls._one is None:
+            cls._one = super().__new__(cls)
+        return cls._one
+
+    def __repr__(self):
+        return "skip"
+
+
+SKIP = _SkipType()
+
+VARIABLES = ("x0", "y0", "z0", "x", "y", "z", "ux", "uy", "uz", "t", "dt", "dx")
+ARITY = dict.fromkeys(("sin", "cos", "tan", "cot", "sinh", "cosh", "tanh",
+                       "coth", "sqrt", "log", "ln", "abs"), 1)
+ARITY.update({"pow": 2, "if": 3})
+
+# binding power of each binary operator; ^ is the only right-associative one
+_BP = {"or": 1, "and": 2, "<": 3, ">": 3, "<=": 3, ">=": 3, "==": 3, "!=": 3,
+       "+": 4, "-": 4, "*": 5, "/": 5, "^": 6}
+_NEG_BP = 5.5
+
+_LEX = re.compile(r"""
+    (?P<num>(?:\d+\.\d*|\.\d+|\d+)(?:[eE][+-]?\d+)?)
+  | (?P<name>[A-Za-z_]\w*)
+  | (?P<op><=|>=|==|!=|[-+*/^<>(),])
+  | (?P<ws>\s+)
+""", re.VERBOSE | re.ASCII)
+
+
+def _lex(text):
+    out, pos = [], 0
+    while pos < len(text):
+        m = _LEX.match(text, pos)
+        if m is None:
+            raise ExprError(f"unexpected character {text[pos]!r}", pos)
+        if m.lastgroup != "ws":
+            out.append((m.lastgroup, m.group(), pos))
+        pos = m.end()
+    out.append(("end", "", len(text)))
+    return out
+
+
+@dataclass(frozen=True)
+class ExprAst:
+    root: tuple
+    locals: dict
+    source: str
+
+    @property
+    def variables(self):
+        return frozenset(_walk_vars(self.root))
+
+    @property
+    def time_dependent(self):
+        """True when the value can change between steps (reference
+        expr.py:117-119): anything reading x/y/z, u, t or dt."""
+        return bool(self.variables & {"x", "y", "z", "ux", "uy", "uz",
+                                      "t", "dt"})
+
+
+def _walk_vars(node):
+    tag = node[0]
+    if tag == "var":
+        yield node[1]
+    elif tag == "un":
+        yield from _walk_vars(node[2])
+    elif tag == "bin":
+        yield from _walk_vars(node[2])
+        yield from _walk_vars(node[3])
+    elif tag == "call":
+        for arg in node[2]:
+            yield from _walk_vars(arg)
+    elif tag == "if":
+        for sub in node[1:]:
+            yield from _walk_vars(sub)
+
+
+class _Pratt:
+    def __init__(self, text, consts):
+        self.toks = _lex(text)
+        self.k = 0
+        self.consts = consts
+
+    def _peek(self):
+        return self.toks[self.k]
+
+    def _take(self):
+        tok = self.toks[self.k]
+        self.k += 1
+        return tok
+
+    def _need(self, text):
+        kind, val, pos = self._peek()
+        if val != text:
+            shown = val or "end of input"
+            raise ExprError(f"expected {text!r}, found {shown!r}", pos)
+        return self._take()
+
+    def whole(self):
+        tree = self.expr(0)
+        kind, val, pos = self._peek()
+        if kind != "end":
+            raise ExprError(f"unexpected trailing input {val!r}", pos)
+        return tree
+
+    def expr(self, floor):
+        lhs = self.prefix()
+        while True:
+            kind, op, _ = self._peek()
+            bp = _BP.get(op)
+            if kind == "end" or bp is None or bp < floor:
+                return lhs
+            self._take()
+            rhs = self.expr(bp if op == "^" else bp + 1)
+            lhs = ("bin", op, lhs, rhs)
+
+    def prefix(self):
+        kind, val, pos = self._take()
+        if kind == "num":
+            return ("num", float(val))
+        if val == "-":
+            inner = self.expr(_NEG_BP)
+            return ("num", -inner[1]) if inner[0] == "num" else ("un", "-", inner)
+        if val == "(":
+            inner = self.expr(0)
+            self._need(")")
+            return inner
+        if kind == "name":
+            if val in ("skip", "Skip"):
+                return ("skip",)
+            if val in ("and", "or"):
+                raise ExprError(f"operator {val!r} missing left operand", pos)
+            if self._peek()[1] == "(":
+                return self.call(val, pos)
+            if val in self.consts:
+                return ("num", self.consts[val])
+            if val in VARIABLES:
+                return ("var", val)
+            raise ExprError(f"unknown identifier {val!r}", pos)
+        raise ExprError(f"unexpected token {val or 'end of input'!r}", pos)
+
+    def call(self, name, pos):
+        want = ARITY.get(name)
+        if want is None:
+            raise ExprError(f"unknown function {name!r}", pos)
+        self._need("(")
+        args = [self.expr(0)]
+        while self._peek()[1] == ",":
+            self._take()
+            args.append(self.expr(0))
+        self._need(")")
+        if len(args) != want:
+            raise ExprError(f"function {name!r} takes {want} argument(s), "
+                            f"got {len(args)}", pos)
+        if name == "if":
+            return ("if", *args)
+        return ("call", name, tuple(args))
+
+
+def parse_locals(text, base=None):
+    """Fold ``a=1; b=a*2`` into a name -> float map (expr.py:208-232)."""
+    consts = dict(base or {})
+    for piece in (text or "").split(";"):
+        piece = piece.strip()
+        if not piece:
+            continue
+        if "=" not in piece:
+            raise ExprError(f"malformed local definition {piece!r}")
+        name, _, rhs = piece.partition("=")
+        name = name.strip()
+        if not re.fullmatch(r"[A-Za-z_][A-Za-z0-9_]*", name):
+            raise ExprError(f"invalid local name {name!r}")
+        val = eval_node(_Pratt(rhs.strip(), consts).whole(), None)
+        if val is SKIP:
+            raise ExprError(f"local {name!r} must be a number, not skip")
+        consts[name] = val
+    return consts
+
+
+def _skip_legal(node, tail):
+    tag = node[0]
+    if tag == "skip":
+        if not tail:
+            raise ExprError(
+                "`skip` is only legal as an if branch or the whole expression")
+    elif tag == "un":
+        _skip_legal(node[2], False)
+    elif tag == "bin":
+        _skip_legal(node[2], False)
+        _skip_legal(node[3], False)
+    elif tag == "call":
+        for arg in node[2]:
+            _skip_legal(arg, False)
+    elif tag == "if":
+        _skip_legal(node[1], False)
+        _skip_legal(node[2], tail)
+        _skip_legal(node[3], tail)
+
+
+def parse(source, locals_src=""):
+    """Source (+ optional locals) -> ExprAst (reference expr.py:235-242)."""
+    if not source or not source.strip():
+        raise ExprError("empty expression")
+    consts = parse_locals(locals_src)
+    root = _Pratt(source, consts).whole()
+    _skip_legal(root, True)
+    return ExprAst(root=root, locals=consts, source=source)
+
+
+# -- scalar evaluation (host; used to fold locals and for single lanes) -----
+
+def _scalar_call(name, a):
+    try:
+        x = a[0]
+        if name == "cot":
+            return math.cos(x) / math.sin(x)
+        if name == "coth":
+            return math.cosh(x) / math.sinh(x)
+        if name in ("log", "ln"):
+            if x <= 0.0:
+                raise ExprError(f"{name} of non-positive value {x!r}")
+            return math.log10(x) if name == "log" else math.log(x)
+        if name == "sqrt":
+            if x < 0.0:
+                raise ExprError(f"sqrt of negative value {x!r}")
+            return math.sqrt(x)
+        if name == "pow":
+            return math.pow(x, a[1])
+        return {"sin": math.sin, "cos": math.cos, "tan": math.tan,
+                "sinh": math.sinh, "cosh": math.cosh, "tanh": math.tanh,
+                "abs": abs}[name](x)
+    except (ValueError, ZeroDivisionError, OverflowError) as exc:
+        raise ExprError(f"domain error in {name}: {exc}") from None
+
+
+_CMP = {"<": float.__lt__, ">": float.__gt__, "<=": float.__le__,
+        ">=": float.__ge__, "==": float.__eq__, "!=": float.__ne__}
+
+
+def eval_node(node, ctx):
+    """Scalar evaluation of one AST node (reference expr.py:307-369)."""
+    tag = node[0]
+    if tag == "num":
+        return node[1]
+    if tag == "skip":
+        return SKIP
+    if tag == "var":
+        if ctx is None:
+            raise ExprError(f"variable {node[1]!r} not allowed here")
+        return float(getattr(ctx, node[1]))
+    if tag == "un":
+        val = eval_node(node[2], ctx)
+        if val is SKIP:
+            raise ExprError("skip consumed by unary '-'")
+        return -val
+    if tag == "if":
+        cond = eval_node(node[1], ctx)
+        if cond is SKIP:
+            raise ExprError("skip consumed by if condition")
+        return eval_node(node[2] if cond != 0.0 else node[3], ctx)
+    if tag == "call":
+        args = [eval_node(a, ctx) for a in node[2]]
+        if any(a is SKIP for a in args):
+            raise ExprError(f"skip consumed by function {node[1]!r}")
+        return _scalar_call(node[1], args)
+    op = node[1]
+    a = eval_node(node[2], ctx)
+    b = eval_node(node[3], ctx)
+    if a is SKIP or b is SKIP:
+        raise ExprError(f"skip consumed by operator {op!r}")
+    a, b = float(a), float(b)
+    if op == "+":
+        return a + b
+    if op == "-":
+        return a - b
+    if op == "*":
+        return a * b
+    if op == "/":
+        if b == 0.0:
+            raise ExprError("division by zero")
+        return a / b
+    if op == "^":
+        try:
+            return math.pow(a, b)
+        except (ValueError, OverflowError) as exc:
+            raise ExprError(f"domain error in '^': {exc}") from None
+    if op in _CMP:
+        return 1.0 if _CMP[op](a, b) else 0.0
+    if op == "and":
+        return 1.0 if (a != 0.0 and b != 0.0) else 0.0
+    if op == "or":
+        return 1.0 if (a != 0.0 or b != 0.0) else 0.0
+    raise ExprError(f"unknown operator {op!r}")
+
+
+@dataclass
+class EvalContext:
+    x0: float = 0.0
+    y0: float = 0.0
+    z0: float = 0.0
+    x: float = 0.0
+    y: float = 0.0
+    z: float = 0.0
+    ux: float = 0.0
+    uy: float = 0.0
+    uz: float = 0.0
+    t: float = 0.0
+    dt: float = 0.0
+    dx: float = 0.0
+
+
+def eval_expr(ast, ctx):
+    return eval_node(ast.root, ctx)
+
+
+# -- bytecode for the device evaluator --------------------------------------
+# One instruction = (opcode:int32, operand:int32).  Constants live in a
+# per-program float64 pool.  Opcode numbering is shared with
+# csrc/expr_vm.cuh (keep in sync; test_expr_compile checks the table).
+
+OP = {
+    "END": 0, "CONST": 1, "VAR": 2, "NEG": 3, "JZ": 4, "JMP": 5, "SKIP": 6,
+    "ADD": 10, "SUB": 11, "MUL": 12, "DIV": 13, "POW": 14,
+    "LT": 15, "GT": 16, "LE": 17, "GE": 18, "EQ": 19, "NE": 20,
+    "AND": 21, "OR": 22,
+    "SIN": 30, "COS": 31, "TAN": 32, "COT": 33, "SINH": 34, "COSH": 35,
+    "TANH": 36, "COTH": 37, "SQRT": 38, "LOG": 39, "LN": 40, "ABS": 41,
+    "POWF": 42,
+}
+_BIN_OP = {"+": "ADD", "-": "SUB", "*": "MUL", "/": "DIV", "^": "POW",
+           "<": "LT", ">": "GT", "<=": "LE", ">=": "GE", "==": "EQ",
+           "!=": "NE", "and": "AND", "or": "OR"}
+VAR_ID = {name: k for k, name in enumerate(VARIABLES)}
+# device error codes (ExprError messages the host re-raises)
+ERRORS = {1: "division by zero", 2: "log of non-positive value",
+          3: "ln of non-positive value", 4: "sqrt of negative value",
+          5: "domain error in pow", 6: "domain error in '^'",
+          7: "stack overflow in expression program"}
+MAX_STACK = 16
+
+
+@dataclass(frozen=True)
+class Program:
+    code: np.ndarray      # (m, 2) int32
+    consts: np.ndarray    # (c,) float64
+    depth: int            # max stack depth
+    source: str
+
+
+def compile_program(ast):
+    """Lower an ExprAst (or raw root tuple) to postfix bytecode."""
+    root = ast.root if isinstance(ast, ExprAst) else ast
+    code, consts = [], []
+    depth = [0, 0]   # current, max
+
+    def push(n=1):
+        depth[0] += n
+        depth[1] = max(depth[1], depth[0])
+
+    def emit(op, arg=0):
+        code.append([OP[op], arg])
+        return len(code) - 1
+
+    def gen(node):
+        tag = node[0]
+        if tag == "num":
+            consts.append(float(node[1]))
+            emit("CONST", len(consts) - 1)
+            push()
+        elif tag == "var":
+            emit("VAR", VAR_ID[node[1]])
+            push()
+        elif tag == "skip":
+            emit("SKIP")
+        elif tag == "un":
+            gen(node[2])
+            emit("NEG")
+        elif tag == "bin":
+            gen(node[2])
+            gen(node[3])
+            emit(_BIN_OP[node[1]])
+            depth[0] -= 1
+        elif tag == "call":
+            for arg in node[2]:
+                gen(arg)
+            emit("POWF" if node[1] == "pow" else node[1].upper())
+            depth[0] -= len(node[2]) - 1
+        elif tag == "if":
+            gen(node[1])
+            jz = emit("JZ")
+            depth[0] -= 1
+            base = depth[0]
+            gen(node[2])
+            jmp = emit("JMP")
+            depth[0] = base
+            code[jz][1] = len(code)
+            gen(node[3])
+            code[jmp][1] = len(code)
+        else:
+            raise ExprError(f"unknown node {tag!r}")
+
+    gen(root)
+    emit("END")
+    if depth[1] > MAX_STACK:
+        raise ExprError(f"expression too deep for the device evaluator "
+                        f"(stack {depth[1]} > {MAX_STACK})")
+    src = ast.source if isinstance(ast, ExprAst) else ""
+    return Program(code=np.asarray(code, dtype=np.int32).reshape(-1, 2),
+                   consts=np.asarray(consts if consts else [0.0],
+                                     dtype=np.float64),
+                   depth=depth[1], source=src)
+
+
+def pretty(ast_or_node):
+    """Fully parenthesised text that reparses to the same AST."""
+    node = ast_or_node.root if isinstance(ast_or_node, ExprAst) else ast_or_node
+    tag = node[0]
+    if tag == "num":
+        return repr(node[1])
+    if tag == "var":
+        return node[1]
+    if tag == "skip":
+        return "skip"
+    if tag == "un":
+        return f"(-{pretty(node[2])})"
+    if tag == "bin":
+        return f"({pretty(node[2])} {node[1]} {pretty(node[3])})"
+    if tag == "call":
+        return f"{node[1]}({', '.join(pretty(a) for a in node[2])})"
+    if tag == "if":
+        return f"if({pretty(node[1])}, {pretty(node[2])}, {pretty(node[3])})"
+    raise ExprError(f"unknown node {tag!r}")
