@@ -1,0 +1,304 @@
+/*
+ * tlsph.h -- C ABI of libtlsph.so, the B200 (sm_100a) TLSPH hot path.
+ *
+ * Plain C: device pointers, sizes and scalars only; no torch or C++ types.
+ * Every function is asynchronous on the given CUDA stream and returns 0 or a
+ * negative TL_ERR_* code; tl_last_error() gives the message (per host
+ * thread).  Numeric events the reference reports as return values (degenerate
+ * counts, first non-SPD particle, non-convergence) are accumulated into
+ * caller-provided DEVICE words and read at sync points, so no call blocks.
+ *
+ * Each entry point names the reference interface it replaces
+ * (/root/reference/pkg/src/solidsph/<file>:<line>).  INTEGRATION.md shows the
+ * ctypes binding a solidsph maintainer would add.
+ */
+#ifndef TLSPH_H
+#define TLSPH_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* tl_stream_t; /* a cudaStream_t; NULL = legacy default stream */
+
+enum {
+    TL_OK = 0,
+    TL_ERR_ARG = -1,
+    TL_ERR_CUDA = -2,
+    TL_ERR_UNSUPPORTED = -3,
+    TL_ERR_CASE = -4
+};
+
+#define TL_ABI_VERSION 1
+
+int tl_abi_version(void);
+/* sizeof of the ABI structs, for binding checks: 0 tl_body, 1 tl_clock,
+ * 2 tl_bc, 3 tl_prog, 4 tl_notch, 5 tl_nb_params, 6 tl_dtinfo */
+int64_t tl_struct_size(int which);
+const char* tl_last_error(void);
+int tl_device_sync(void);
+
+/* ---------------------------------------------------------------------------
+ * Backend-plugin kernels (reference backends/reference.py:18-244 and
+ * backends/fast.py:111-469).  Same argument meaning as the reference plugin:
+ * FP64, row-major (n,3) vectors and (n,3,3) tensors, int64 CSR.  Outputs are
+ * caller-allocated and written in place.  One CUDA thread per particle sums
+ * its neighbours sequentially in CSR order, like the reference.
+ * ------------------------------------------------------------------------- */
+
+/* F_i = I + sum_j V0_j (u_j-u_i) (x) grad0_ij; identity when gated and
+ * s_i <= s_l.  Replaces backends.deformation_gradient (reference.py:18). */
+int tl_deformation_gradient(tl_stream_t st, int64_t n, const int64_t* indptr,
+                            const int64_t* indices, const double* grad0, const double* u,
+                            const double* V0, const double* s, double s_l, int gated,
+                            double* out);
+
+/* Brookshaw Laplacian.  Replaces backends.sph_laplacian (reference.py:32). */
+int tl_sph_laplacian(tl_stream_t st, int64_t n, const int64_t* indptr, const int64_t* indices,
+                     const double* grad0, const double* r0, const double* r0norm,
+                     const double* V0, const double* f, double* out);
+
+/* Corrected gradient.  Replaces backends.sph_gradient (reference.py:42). */
+int tl_sph_gradient(tl_stream_t st, int64_t n, const int64_t* indptr, const int64_t* indices,
+                    const double* grad0, const double* V0, const double* f, double* out);
+
+/* Momentum with artificial viscosity; *n_bad (device) += degenerate count.
+ * Replaces backends.momentum (reference.py:52). */
+int tl_momentum(tl_stream_t st, int64_t n, const int64_t* indptr, const int64_t* indices,
+                const double* grad0, const double* grad0r, const double* r0,
+                const double* r0norm, const double* P, const double* m0, double rho0,
+                const double* v, double h, double c0, double beta1, double beta2,
+                const double* F, double* out, int64_t* n_bad);
+
+/* SVK (+ spectral split when fracture); *n_noconv (device) += count.
+ * Replaces backends.svk_batch (reference.py:94). */
+int tl_svk_batch(tl_stream_t st, int64_t n, const double* F, double lam, double mu,
+                 const double* s, int fracture, double* out_S, double* out_psi,
+                 double* out_psip, int64_t* n_noconv);
+
+/* Neo-Hookean; *n_bad (device) += degenerate count.
+ * Replaces backends.nh_batch (reference.py:119). */
+int tl_nh_batch(tl_stream_t st, int64_t n, const double* F, double kappa, double mu,
+                const double* s, int fracture, double* out_S, double* out_psi,
+                double* out_psip, int64_t* n_bad);
+
+/* J2 radial return, Cp and epbar updated in place.  counters (device):
+ * [0] += degenerate count, [1] = min(first non-SPD index) (init to INT64_MAX).
+ * As in the reference, a non-SPD update leaves the state uncommitted.
+ * Replaces backends.j2_batch (reference.py:151). */
+int tl_j2_batch(tl_stream_t st, int64_t n, const double* F, double* Cp, double* epbar,
+                double mu, double kappa, double sigma_y0, double H_hard, double* out_S,
+                double* out_psi, double* out_dwp, int64_t* counters, uint8_t* scratch);
+
+/* Penalty contact over candidate pairs, accumulated in pair order like the
+ * reference; *n_warn (device) += coincident count.  scratch: 3*npairs doubles.
+ * Replaces backends.contact_pair_accumulate (reference.py:211). */
+int tl_contact_pair_accumulate(tl_stream_t st, const double* xa, const double* va,
+                               const double* ma, const double* xb, const double* vb,
+                               const double* mb, int64_t npairs, const int64_t* pairs,
+                               double dp_contact, double k_n, double c_n, double kfric,
+                               double* out_aa, double* out_ab, int64_t* n_warn,
+                               double* scratch);
+
+/* Batched symmetric 3x3 Jacobi (descending), sweeps per matrix.
+ * Replaces fast._eig3_jacobi (fast.py:45). */
+int tl_eig3_jacobi(tl_stream_t st, int64_t n, const double* A, double* w, double* Q,
+                   int32_t* sweeps);
+
+/* ---------------------------------------------------------------------------
+ * Reference-configuration neighbour build (kernel_geom.py:65-261).
+ * Cell list radix-sorted by x-major cell key, exact inclusion tests in the
+ * reference's FP64 operation order, notch severing on directed pairs, CSR
+ * rows in ascending partner index.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+    double origin[3], nhat[3], e1[3], e2[3];
+    double poly[4][2];
+    double tol_plane, tol_poly;
+} tl_notch;
+
+typedef struct {
+    int64_t n;
+    const double* X;      /* (n,3) reference positions, device */
+    int mode;             /* 0 = radial |d|^2 < (2h)^2, 1 = nbsrange window */
+    double h;             /* smoothing length */
+    double win;           /* nbsrange window (mode 1) */
+    double lo[3];         /* bounding-box minimum */
+    double cell;          /* cell edge (>= cutoff) */
+    int64_t dims[3];      /* cells per axis */
+    int n_notch;
+    const tl_notch* notches; /* host array of n_notch frames */
+} tl_nb_params;
+
+typedef struct tl_nb_plan tl_nb_plan;
+
+/* sort particles into cells.  Replaces the cKDTree prefilter (kernel_geom.py:76-86). */
+int tl_nb_plan_create(tl_stream_t st, const tl_nb_params* p, tl_nb_plan** out);
+/* counts[i] = kept partners of i after notch severing (device int64[n]). */
+int tl_nb_count(tl_nb_plan* plan, int64_t* counts);
+/* CSR fill with ascending partners; indptr (device int64[n+1]) from counts.
+ * Replaces build_pairs + sever_notch_bonds + _csr_from_pairs
+ * (kernel_geom.py:65-173). */
+int tl_nb_fill(tl_nb_plan* plan, const int64_t* indptr, int32_t* indices);
+int tl_nb_plan_destroy(tl_nb_plan* plan);
+
+/* First-order correction L_i = A_i^-1 with the cond_2 >= 1e8 identity
+ * fallback; *fallbacks (device) += count.  L: (n,3,3) FP64.
+ * Replaces correction_matrices (kernel_geom.py:176-205). */
+int tl_correction(tl_stream_t st, int64_t n, const int64_t* indptr, const int32_t* indices,
+                  const double* X, const double* V0, double h, double alpha, int kind, int dim,
+                  int correction, double* L, int64_t* fallbacks);
+
+/* Per-pair arrays of the reference Adjacency (kernel_geom.py:228-261):
+ * rows, r0 = Xi-Xj, r0norm, w0, grad0 = L_i gb, grad0r = -L_j gb (== grad0
+ * of the reverse pair).  Any output may be NULL. */
+int tl_adjacency_expand(tl_stream_t st, int64_t n, const int64_t* indptr,
+                        const int32_t* indices, const double* X, const double* L, double h,
+                        double alpha, int kind, int64_t* rows, double* r0, double* r0norm,
+                        double* w0, double* grad0, double* grad0r);
+
+/* Sliced-ELL (32 particles per slice, lane-interleaved) copy of the CSR for
+ * coalesced neighbour-index loads in the fused step kernels.
+ * tl_sell_lengths: slen[w] = max row length in slice w (device int32[nw]).
+ * tl_sell_fill: soff (device int64[nw+1], exclusive scan of 32*slen), sidx
+ * (device int32[soff[nw]]), padding = -1. */
+int tl_sell_lengths(tl_stream_t st, int64_t n, const int64_t* indptr, int32_t* slen);
+int tl_sell_fill(tl_stream_t st, int64_t n, const int64_t* indptr, const int32_t* indices,
+                 const int64_t* soff, int32_t* sidx);
+
+/* ---------------------------------------------------------------------------
+ * Fused device-resident step (stepper.py:77-209, dynamics.py:28-217,
+ * constitutive.py:168-199, fracture.py:12-83).
+ * ------------------------------------------------------------------------- */
+
+#define TL_MAX_BC 32
+#define TL_MAX_PROG 64
+
+/* expression program table (bytecode from expr.compile_program) */
+typedef struct {
+    const int32_t* code;   /* (len,2) opcode/operand pairs, device */
+    const double* consts;  /* device */
+    int32_t len;
+    int32_t pad;
+} tl_prog;
+
+typedef struct {
+    int32_t kind;          /* 0 = velocity, 1 = force */
+    int32_t ftype;         /* force type 1|2|3 */
+    int32_t bit;           /* membership bit in bcmask, -1 = whole body */
+    int32_t has_const[3];
+    int32_t prog[3];       /* program index or -1 (axis untouched unless const) */
+    double cval[3];
+    double tst, tend;
+} tl_bc;
+
+/* device clock: time integration state kept on the device so steps never
+ * wait for the host (stepper.py:221-263 semantics) */
+typedef struct {
+    double t;           /* current time */
+    double dt;          /* dt of the step in flight */
+    double next_out;    /* next output boundary */
+    double t_max;
+    double eps;         /* 1e-12*max(t_max,1) */
+    double dt_override; /* <0: adaptive */
+    double cfl;
+    int64_t step;       /* step_index */
+    int64_t max_steps;  /* <0: unlimited */
+    int32_t halted;     /* 0 run, 1 finished, 2 output due, 3 max_steps, 4 dt collapsed */
+    int32_t out_step;   /* this step ends on an output boundary: mirror F, S, psi, a */
+} tl_clock;
+
+/* Per-body device view.  Layout (Real = float | double per `precision`):
+ *   planes  : p[c * n_all + i]   own-particle fields, perfectly coalesced
+ *   records : p[R * i + c]       fields gathered from neighbours, one
+ *                                128-bit load per 4 values
+ * Neighbour indices may reach n_all > n (halo copies on multi-GPU slabs). */
+typedef struct {
+    int64_t n;              /* particles updated by this call */
+    int64_t n_all;          /* owned + halo; plane stride */
+    int32_t dim, model, fracture, visc, precision /* 4 | 8 */, kind;
+    int32_t uniform, write_out, store_a, nbc, mk, restrict_prog;
+    int32_t bc_whole;       /* some BC targets the whole body */
+    int32_t pad0;
+    /* material / kernel constants (core.py:95-139) */
+    double h, inv_h, alpha, rho0, lam, mu, kappa, c0, beta1, beta2;
+    double Gc, eps0, s_l, sigma_y0, H_hard, V0c, m0c, dp_body, jac_tol;
+    double f0[3];
+    /* neighbours: sliced ELL, 32 particles per slice, lane-interleaved */
+    const int64_t* soff;
+    const int32_t* sidx;
+    /* geometry */
+    const double* Xs;       /* FP64 planes x,y,z */
+    const void* L;          /* 9 planes, correction matrix L_i */
+    const double* V0;       /* per particle when !uniform */
+    const double* m0;
+    /* state */
+    void* us;               /* records of 4: ux uy uz s        (pass-A gather) */
+    void* rb;               /* records of 12: (P L_i) row-major, vx vy vz (pass-B gather) */
+    void* v;                /* 3 planes */
+    void* al;               /* 9 planes: det(F) F^-1 L_i (viscosity) */
+    void* sdot;             /* plane */
+    void* sddot;            /* plane */
+    void* Hh;               /* plane, history functional */
+    void* Cpd;              /* 6 planes, Cp - I: xx yy zz xy xz yz (J2) */
+    void* epbar;            /* plane */
+    void* a;                /* 3 planes (symplectic predictor / output) */
+    /* optional FP64 host-layout outputs when write_out: (n,3,3) / (n,) */
+    double* F_out;
+    double* S_out;
+    double* psi_out;
+    double* psip_out;
+    /* boundary conditions */
+    const uint32_t* bcmask;
+    const tl_bc* bcs;       /* device array of nbc */
+    const tl_prog* progs;   /* device program table */
+    /* device words */
+    tl_clock* clock;
+    unsigned long long* red;   /* [0] max|v|^2 bits, [1] max|a|^2 bits */
+    int64_t* counters;         /* [0] degenerate, [1] eig noconv, [2] first non-SPD,
+                                  [3] first non-finite accel, [4] expr error code,
+                                  [5] restrictphi out of [0,1], [6] step of [3],
+                                  [7] first step with non-finite u or v */
+    double* pw_partial;        /* plastic-work block partials (J2) */
+} tl_body;
+
+/* pass A: F (gated), stress model, history, Laplacian, s-ddot, P L_i and
+ * Avis L_i.  Replaces deformation_gradient + update_stress +
+ * update_phase_acceleration + np.matmul(F,S) (stepper.py:80-85). */
+int tl_pass_a(tl_stream_t st, const tl_body* b);
+
+/* pass B modes */
+#define TL_B_INIT 0      /* internal accel + velocity BCs(0,0)   (stepper.py:134-142) */
+#define TL_B_VERLET 1    /* + Verlet update                      (stepper.py:144-162) */
+#define TL_B_SYMPL 2     /* symplectic corrector                 (stepper.py:176-197) */
+/* pass B: momentum + viscosity, a = a_int + f0 + force BCs, velocity BCs,
+ * integrator update, phase-field advance + clamps, dt maxima.
+ * Replaces momentum + the stepper update phases. */
+int tl_pass_b(tl_stream_t st, const tl_body* b, int mode);
+
+/* symplectic predictor (stepper.py:164-175) */
+int tl_predict(tl_stream_t st, const tl_body* b);
+
+typedef struct {
+    double h, c0;
+    const unsigned long long* red;
+} tl_dtinfo;
+
+/* dt = min(pick_dt, next_out - t, t_max - t) on the device (stepper.py:221-256) */
+int tl_clock_begin(tl_stream_t st, tl_clock* clock, int nbody, const tl_dtinfo* info);
+/* t += dt, step += 1, output/max_steps halting (stepper.py:199-209, 257-263) */
+int tl_clock_commit(tl_stream_t st, tl_clock* clock);
+/* reset the dt maxima words of nbody bodies */
+int tl_reset_red(tl_stream_t st, unsigned long long* red);
+/* deterministic sum of nparts partials into *acc (plastic work) */
+int tl_reduce_partials(tl_stream_t st, const double* partials, int64_t nparts, double* acc);
+
+/* blocks used by tl_pass_a (size of pw_partial) */
+int64_t tl_pass_blocks(int64_t n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TLSPH_H */

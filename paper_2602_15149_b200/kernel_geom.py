@@ -1,0 +1,301 @@
+"""Reference-configuration geometry on the device: the neighbour build,
+correction matrices and the Adjacency the reference's loader expects.
+
+Drop-in for ``solidsph.kernel_geom`` (/root/reference/pkg/src/solidsph/
+kernel_geom.py): same function names, arguments, return types and CaseError
+messages.  ``build_adjacency`` is the hook the reference's case loader calls
+as a module attribute (caseio.py:562), so
+
+    import solidsph.kernel_geom, paper_2602_15149_b200.kernel_geom as kg
+    solidsph.kernel_geom.build_adjacency = kg.build_adjacency
+
+moves the one-time O(N k) build onto the GPU.  The returned ``Adjacency``
+keeps the device structure (``adj.device``) that ``DeviceSimulation`` reuses;
+its per-pair host arrays (grad0, r0, ...; ~104 B/pair) are produced lazily,
+only if host code reads them.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from . import _lib
+from .core import Adjacency, CaseError, KernelKind
+
+COND_LIMIT = 1.0e8
+
+
+def smoothing_length(dp, coefh, dim):
+    """h = coefh * dp * sqrt(dim) (kernel_geom.py:21-27)."""
+    if dp <= 0.0 or coefh <= 0.0:
+        raise CaseError("dp and coefh must be positive")
+    if dim not in (2, 3):
+        raise CaseError(f"dim must be 2 or 3, got {dim}")
+    return coefh * dp * math.sqrt(dim)
+
+
+def kernel_alpha(h, dim, kind):
+    """Normalisation of the cubic spline (1) / Wendland C2 (2) kernel."""
+    if dim not in (2, 3):
+        raise CaseError(f"dim must be 2 or 3, got {dim}")
+    if int(kind) == int(KernelKind.CUBIC_SPLINE):
+        return 10.0 / (7.0 * math.pi * h * h) if dim == 2 else 1.0 / (math.pi * h ** 3)
+    if int(kind) == int(KernelKind.WENDLAND):
+        return 7.0 / (4.0 * math.pi * h * h) if dim == 2 else 21.0 / (16.0 * math.pi * h ** 3)
+    raise CaseError(f"unknown kernel kind {kind!r}")
+
+
+def kernel_eval(q, h, dim, kind):
+    """(W, dW/dr) at q = r/h, support 2h (kernel_geom.py:30-62).  Host-side
+    helper for diagnostics; the step kernels evaluate dW/dr inline."""
+    q = np.asarray(q, dtype=np.float64)
+    a = kernel_alpha(h, dim, kind)
+    if int(kind) == int(KernelKind.CUBIC_SPLINE):
+        tm = 2.0 - q
+        w = np.where(q < 1.0, 1.0 - 1.5 * q * q + 0.75 * q ** 3, np.where(q < 2.0, 0.25 * tm ** 3, 0.0))
+        dw = np.where(q < 1.0, -3.0 * q + 2.25 * q * q, np.where(q < 2.0, -0.75 * tm ** 2, 0.0))
+    else:
+        t = np.where(q < 2.0, 1.0 - 0.5 * q, 0.0)
+        w = t ** 4 * (2.0 * q + 1.0)
+        dw = -5.0 * q * t ** 3
+    return a * w, a * dw / h
+
+
+# ---------------------------------------------------------------------------
+# notch frames (kernel_geom.py:100-131), computed once on the host
+# ---------------------------------------------------------------------------
+
+def _quad_points(q):
+    return np.asarray(q.points if hasattr(q, "points") else q, dtype=np.float64).reshape(4, 3)
+
+
+def quad_frame(points, scale):
+    p = _quad_points(points)
+    e1 = p[1] - p[0]
+    nvec = np.cross(e1, p[2] - p[0])
+    nn = np.linalg.norm(nvec)
+    if nn <= 1e-14 * max(scale, 1e-300) ** 2:
+        raise CaseError("degenerate quad (zero area)")
+    nhat = nvec / nn
+    diag = np.linalg.norm(p.max(axis=0) - p.min(axis=0))
+    if abs((p[3] - p[0]) @ nhat) > 1e-6 * diag:
+        raise CaseError("quad points are not coplanar")
+    e1h = e1 / np.linalg.norm(e1)
+    e2h = np.cross(nhat, e1h)
+    poly = (p - p[0]) @ np.stack([e1h, e2h], axis=1)
+    return p[0], nhat, e1h, e2h, poly
+
+
+def notch_struct(q):
+    pts = _quad_points(q)
+    scale = max(np.abs(pts).max(), 1.0)
+    o, nh, e1, e2, poly = quad_frame(pts, scale)
+    s = _lib.tl_notch()
+    for k in range(3):
+        s.origin[k], s.nhat[k], s.e1[k], s.e2[k] = o[k], nh[k], e1[k], e2[k]
+    for k in range(4):
+        s.poly[k][0], s.poly[k][1] = poly[k, 0], poly[k, 1]
+    s.tol_plane = 1e-12 * scale
+    s.tol_poly = 1e-12 * max(1.0, np.abs(poly).max())
+    return s
+
+
+# ---------------------------------------------------------------------------
+# device structure
+# ---------------------------------------------------------------------------
+
+class DeviceAdjacency:
+    """Fixed neighbour structure resident in HBM.
+
+    indptr (n+1) int64, indices (nnz) int32 in ascending partner order per
+    row (the reference CSR), L (n,9) FP64 correction matrices, and the
+    lane-interleaved sliced-ELL copy (soff, sidx) the step kernels read."""
+
+    def __init__(self, X, indptr, indices, L, fallbacks, h, dim, kind, correction):
+        self.X = X
+        self.indptr = indptr
+        self.indices = indices
+        self.L = L
+        self.correction_fallbacks = int(fallbacks)
+        self.h = h
+        self.dim = dim
+        self.kind = int(kind)
+        self.correction = bool(correction)
+        self.n = int(X.shape[0])
+        self.nnz = int(indices.shape[0])
+        self._sell = None
+
+    def sell(self):
+        """(soff int64[nw+1], sidx int32[32*sum slen]) built once on demand."""
+        if self._sell is None:
+            import torch
+            L = _lib.lib()
+            st = _lib.stream_ptr()
+            nw = (self.n + 31) // 32
+            slen = torch.empty(nw, dtype=torch.int32, device=self.X.device)
+            _lib.check(L.tl_sell_lengths(st, self.n, _lib.ptr(self.indptr), _lib.ptr(slen)),
+                       "tl_sell_lengths")
+            soff = torch.zeros(nw + 1, dtype=torch.int64, device=self.X.device)
+            torch.cumsum(slen.to(torch.int64) * 32, 0, out=soff[1:])
+            total = int(soff[-1].item())
+            sidx = torch.empty(max(total, 1), dtype=torch.int32, device=self.X.device)
+            _lib.check(L.tl_sell_fill(st, self.n, _lib.ptr(self.indptr), _lib.ptr(self.indices),
+                                      _lib.ptr(soff), _lib.ptr(sidx)), "tl_sell_fill")
+            self._sell = (soff, sidx)
+        return self._sell
+
+    def expand(self, rows=True, r0=True, r0norm=True, w0=True, grad0=True, grad0r=True):
+        """Per-pair FP64 arrays of the reference Adjacency, on the device."""
+        import torch
+        dev = self.X.device
+        nnz = self.nnz
+        out = {}
+
+        def mk(flag, shape, dt=torch.float64):
+            return torch.empty(shape, dtype=dt, device=dev) if flag else None
+
+        out["rows"] = mk(rows, (nnz,), torch.int64)
+        out["r0"] = mk(r0, (nnz, 3))
+        out["r0norm"] = mk(r0norm, (nnz,))
+        out["w0"] = mk(w0, (nnz,))
+        out["grad0"] = mk(grad0, (nnz, 3))
+        out["grad0r"] = mk(grad0r, (nnz, 3))
+        alpha = kernel_alpha(self.h, self.dim, self.kind)
+        L = _lib.lib()
+        _lib.check(L.tl_adjacency_expand(
+            _lib.stream_ptr(), self.n, _lib.ptr(self.indptr), _lib.ptr(self.indices),
+            _lib.ptr(self.X), _lib.ptr(self.L), float(self.h), float(alpha), self.kind,
+            *[_lib.ptr(out[k]) for k in ("rows", "r0", "r0norm", "w0", "grad0", "grad0r")]),
+            "tl_adjacency_expand")
+        return out
+
+
+class LazyAdjacency(Adjacency):
+    """core.Adjacency whose per-pair host arrays are fetched from the device
+    on first access."""
+
+    _PAIR = ("rows", "grad0", "grad0r", "r0", "r0norm", "w0")
+
+    def __init__(self, dev: DeviceAdjacency):
+        object.__setattr__(self, "device", dev)
+        object.__setattr__(self, "_host", {})
+        object.__setattr__(self, "correction_fallbacks", dev.correction_fallbacks)
+
+    def __getattribute__(self, name):
+        if name in LazyAdjacency._PAIR or name in ("indptr", "indices"):
+            host = object.__getattribute__(self, "_host")
+            if name not in host:
+                dev = object.__getattribute__(self, "device")
+                if name == "indptr":
+                    host[name] = dev.indptr.cpu().numpy()
+                elif name == "indices":
+                    host[name] = dev.indices.to(dtype=__import__("torch").int64).cpu().numpy()
+                else:
+                    arrs = dev.expand()
+                    for k in LazyAdjacency._PAIR:
+                        host[k] = arrs[k].cpu().numpy()
+            return host[name]
+        return object.__getattribute__(self, name)
+
+    def __setattr__(self, name, value):
+        if name in LazyAdjacency._PAIR or name in ("indptr", "indices"):
+            object.__getattribute__(self, "_host")[name] = value
+        else:
+            object.__setattr__(self, name, value)
+
+    @property
+    def nnz(self):
+        return object.__getattribute__(self, "device").nnz
+
+    def counts(self):
+        return np.diff(self.indptr)
+
+
+def _grid_params(X, reach):
+    lo = X.min(axis=0)
+    hi = X.max(axis=0)
+    cell = reach * (1.0 + 1e-6)
+    dims = (np.floor((hi - lo) / cell).astype(np.int64) + 1)
+    return lo, cell, dims
+
+
+def _device_pairs(Xd, Xh, h, nbsrange, dp_body, notches):
+    """CSR (indptr int64, indices int32) on the device."""
+    import torch
+    L = _lib.lib()
+    n = int(Xh.shape[0])
+    if n < 2:
+        raise CaseError("need at least 2 particles to build neighbors")
+    mode = 0 if nbsrange is None else 1
+    win = 0.0 if mode == 0 else nbsrange * dp_body * (1.0 + 1e-9)
+    lo, cell, dims = _grid_params(Xh, 2.0 * h if mode == 0 else win)
+    frames = [notch_struct(q) for q in notches]
+    arr = (_lib.tl_notch * max(len(frames), 1))(*frames) if frames else None
+    p = _lib.tl_nb_params(n=n, X=_lib.ptr(Xd), mode=mode, h=float(h), win=float(win),
+                          lo=(_lib.D * 3)(*lo), cell=float(cell), dims=(_lib.I64 * 3)(*dims),
+                          n_notch=len(frames),
+                          notches=_lib.C.cast(arr, _lib.P) if frames else None)
+    st = _lib.stream_ptr()
+    plan = _lib.P()
+    _lib.check(L.tl_nb_plan_create(st, _lib.C.byref(p), _lib.C.byref(plan)), "tl_nb_plan_create")
+    try:
+        counts = torch.empty(n, dtype=torch.int64, device=Xd.device)
+        _lib.check(L.tl_nb_count(plan, _lib.ptr(counts)), "tl_nb_count")
+        indptr = torch.zeros(n + 1, dtype=torch.int64, device=Xd.device)
+        torch.cumsum(counts, 0, out=indptr[1:])
+        nnz = int(indptr[-1].item())
+        if nnz == 0:
+            raise CaseError("no neighbor pairs found (body too sparse for the kernel support)")
+        indices = torch.empty(nnz, dtype=torch.int32, device=Xd.device)
+        _lib.check(L.tl_nb_fill(plan, _lib.ptr(indptr), _lib.ptr(indices)), "tl_nb_fill")
+    finally:
+        L.tl_nb_plan_destroy(plan)
+    return indptr, indices, counts
+
+
+def build_pairs(positions, h, nbsrange=None, dp_body=None):
+    """Symmetric pair list (rows, cols) in lexsort((cols, rows)) order
+    (kernel_geom.py:65-97), built on the device."""
+    import torch
+    Xh = np.ascontiguousarray(positions, dtype=np.float64)
+    Xd = torch.from_numpy(Xh).cuda()
+    indptr, indices, counts = _device_pairs(Xd, Xh, h, nbsrange, dp_body, ())
+    rows = np.repeat(np.arange(Xh.shape[0], dtype=np.int64), counts.cpu().numpy())
+    return rows, indices.to(torch.int64).cpu().numpy()
+
+
+def build_device_adjacency(positions, V0, h, dim, kind, nbsrange=None, dp_body=None,
+                           notches=(), correction=True):
+    """The device half of build_adjacency: returns a DeviceAdjacency."""
+    import torch
+    Xh = np.ascontiguousarray(positions, dtype=np.float64)
+    if Xh.shape[0] < 2:
+        raise CaseError("need at least 2 particles to build neighbors")
+    for q in notches:   # frame validation raises CaseError like the reference
+        notch_struct(q)
+    Xd = torch.from_numpy(Xh).cuda()
+    indptr, indices, counts = _device_pairs(Xd, Xh, h, nbsrange, dp_body, notches)
+    lonely = torch.nonzero(counts == 0)
+    if lonely.numel():
+        raise CaseError(f"particle {int(lonely[0, 0])} has no neighbors after notch severing")
+    V0d = torch.from_numpy(np.ascontiguousarray(V0, dtype=np.float64)).cuda()
+    n = Xh.shape[0]
+    Ld = torch.empty((n, 9), dtype=torch.float64, device=Xd.device)
+    fb = torch.zeros(1, dtype=torch.int64, device=Xd.device)
+    alpha = kernel_alpha(h, dim, kind)
+    L = _lib.lib()
+    _lib.check(L.tl_correction(_lib.stream_ptr(), n, _lib.ptr(indptr), _lib.ptr(indices),
+                               _lib.ptr(Xd), _lib.ptr(V0d), float(h), float(alpha), int(kind),
+                               int(dim), int(bool(correction)), _lib.ptr(Ld), _lib.ptr(fb)),
+               "tl_correction")
+    return DeviceAdjacency(Xd, indptr, indices, Ld, int(fb.item()), h, dim, kind, correction)
+
+
+def build_adjacency(positions, V0, h, dim, kind, nbsrange=None, dp_body=None, notches=(),
+                    correction=True):
+    """Drop-in for kernel_geom.build_adjacency (kernel_geom.py:220-261)."""
+    dev = build_device_adjacency(positions, V0, h, dim, kind, nbsrange=nbsrange,
+                                 dp_body=dp_body, notches=notches, correction=correction)
+    return LazyAdjacency(dev)

@@ -1,0 +1,571 @@
+"""Device-resident drop-in for ``solidsph.stepper.Simulation``.
+
+Same public surface as the reference (/root/reference/pkg/src/solidsph/
+stepper.py:49-263): ``DeviceSimulation(config, trace=None)`` with
+``initialize() / step(dt) / pick_dt() / run(time_max, time_out, on_output,
+max_steps)`` and attributes ``t, step_index, bodies, be, trace,
+contact_warnings``.  ``config`` may be this package's ``CaseConfig`` or the
+reference's (duck-typed).
+
+What differs is where the state lives: every body's particle state sits in
+HBM in the structure-of-arrays / gather-record layout of include/tlsph.h
+and the whole step -- F, stress, phase field, momentum, boundary conditions,
+integrator, dt -- runs in libtlsph kernels (pass A, pass B, device clock).
+The host ``body.state`` arrays are mirrors: refreshed before every
+``on_output`` callback, after ``step()`` and at the end of ``run()``
+(``sync_host()``), and pushed back with ``push_state()`` after host edits.
+
+Errors the reference raises inside the step (SimulationError for non-finite
+acceleration, eigen non-convergence, non-SPD plastic metric; ExprError for
+expression domain errors) are recorded on the device and raised at the next
+sync point -- after every ``step()`` call, and at the end of each batch of
+device-clock steps in ``run()`` -- with the reference's messages.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import numpy as np
+
+from . import _lib, backend, kernel_geom
+from . import expr as ex
+from .core import CaseError, Model, SimulationError
+
+INT64_MAX = np.iinfo(np.int64).max
+N_COUNTERS = 8
+
+
+def _torch():
+    import torch
+    return torch
+
+
+class DeviceBody:
+    """Device buffers and the tl_body descriptor of one body."""
+
+    def __init__(self, body, config, precision, programs):
+        torch = _torch()
+        self.body = body
+        st = body.state
+        n = int(st.X.shape[0])
+        self.n = n
+        self.R = torch.float32 if precision == "fp32" else torch.float64
+        dev = torch.device("cuda")
+        self.dev = dev
+        mat = body.material
+        kind = int(config.kernel)
+        adj = body.adjacency
+        dadj = getattr(adj, "device", None) if adj is not None else None
+        if dadj is None:
+            if adj is not None:
+                dadj = _upload_adjacency(adj, st, body, kind)
+            else:
+                dadj = kernel_geom.build_device_adjacency(
+                    st.X, st.V0, body.h, body.dim, kind, nbsrange=body.nbsrange,
+                    dp_body=body.dp_body, notches=body.notches,
+                    correction=getattr(body, "kernel_correction", True))
+        self.adj = dadj
+        soff, sidx = dadj.sell()
+        self.soff, self.sidx = soff, sidx
+        R = self.R
+        z = lambda *shape: torch.zeros(shape, dtype=R, device=dev)  # noqa: E731
+        self.Xs = torch.from_numpy(np.ascontiguousarray(st.X.T)).to(dev)       # 3 planes
+        self.L = dadj.L.t().contiguous().to(R)                                 # 9 planes
+        V0 = np.asarray(st.V0, dtype=np.float64)
+        m0 = np.asarray(st.m0, dtype=np.float64)
+        self.uniform = bool(np.all(V0 == V0[0]) and np.all(m0 == m0[0]))
+        self.V0 = torch.from_numpy(V0).to(dev)
+        self.m0 = torch.from_numpy(m0).to(dev)
+        self.us = z(n, 4)
+        self.rb = z(n, 12)
+        self.v = z(3, n)
+        self.al = z(9, n)
+        self.sdot = z(n)
+        self.sddot = z(n)
+        self.Hh = z(n)
+        self.Cpd = z(6, n) if mat.model == Model.J2 else z(6, 1)
+        self.epbar = z(n)
+        self.a = z(3, n)
+        f64 = lambda *shape: torch.zeros(shape, dtype=torch.float64, device=dev)  # noqa: E731
+        self.F_out = f64(n, 3, 3)
+        self.S_out = f64(n, 3, 3)
+        self.psi_out = f64(n)
+        self.psip_out = f64(n)
+        self.counters = torch.zeros(N_COUNTERS, dtype=torch.int64, device=dev)
+        self.red = torch.zeros(2, dtype=torch.int64, device=dev)
+        self.nblocks = int(_lib.lib().tl_pass_blocks(n))
+        self.pw_partial = torch.zeros(max(self.nblocks, 1), dtype=torch.float64, device=dev)
+        self.pw_acc = torch.zeros(1, dtype=torch.float64, device=dev)
+        self.pw_base = float(getattr(body, "plastic_work", 0.0))
+        self.deg_base = int(getattr(body, "degenerate_warnings", 0))
+        self._reset_counters()
+        self._setup_bcs(body, config, programs)
+        self.push_state()
+        self.desc = self._descriptor(mat, body, kind, precision)
+
+    # -- boundary conditions -------------------------------------------------
+    def _setup_bcs(self, body, config, programs):
+        torch = _torch()
+        bcs = list(getattr(body, "bcs", []))
+        if len(bcs) > _lib_max_bc():
+            raise CaseError(f"body {body.mk}: more than {_lib_max_bc()} boundary conditions")
+        mask = np.zeros(self.n, dtype=np.uint32)
+        arr = (_lib.tl_bc * max(len(bcs), 1))()
+        bit = 0
+        self.bc_whole = 0
+        for k, bc in enumerate(bcs):
+            d = arr[k]
+            d.kind = 0 if bc.kind == "vel" else 1
+            d.ftype = int(getattr(bc, "ftype", 0) or 0)
+            if d.kind == 1 and d.ftype not in (1, 2, 3):
+                raise CaseError(f"unknown force BC type {bc.ftype}")
+            if bc.target is None:
+                d.bit = -1
+                self.bc_whole = 1
+            else:
+                if bit >= 32:
+                    raise CaseError(f"body {body.mk}: more than 32 targeted boundary conditions")
+                d.bit = bit
+                tgt = np.asarray(bc.target, dtype=np.int64)
+                mask[tgt] |= np.uint32(1 << bit)
+                bit += 1
+            for ax in range(3):
+                c = bc.const[ax]
+                e = bc.expr[ax]
+                d.has_const[ax] = int(c is not None)
+                d.cval[ax] = float(c) if c is not None else 0.0
+                if c is None and e is not None:
+                    ast = config.expressions.get(e)
+                    if ast is None:
+                        raise CaseError(
+                            f"boundary condition references unknown expression id {e}")
+                    d.prog[ax] = programs.index_of(e, ast)
+                else:
+                    d.prog[ax] = -1
+            d.tst = float(bc.tst)
+            d.tend = float(bc.tend) if math.isfinite(bc.tend) else 1e308
+        self.nbc = len(bcs)
+        self._bc_arr = arr
+        nbytes = C.sizeof(_lib.tl_bc) * max(len(bcs), 1)
+        self.bcs_dev = torch.empty(nbytes, dtype=torch.uint8, device=self.dev)
+        host = torch.frombuffer(bytearray(C.string_at(C.addressof(arr), nbytes)), dtype=torch.uint8)
+        self.bcs_dev.copy_(host)
+        self.bcmask = torch.from_numpy(mask.view(np.int32)).to(self.dev)
+        rp = getattr(body, "restrictphi_expr", None)
+        if rp is not None:
+            ast = config.expressions.get(rp)
+            if ast is None:
+                raise CaseError(f"restrictphi references unknown expression id {rp} "
+                                f"(body {body.mk})")
+            self.restrict_prog = programs.index_of(rp, ast)
+        else:
+            self.restrict_prog = -1
+
+    def _descriptor(self, mat, body, kind, precision):
+        b = _lib.tl_body()
+        b.n = self.n
+        b.n_all = self.n
+        b.dim = int(body.dim)
+        b.model = int(mat.model)
+        b.fracture = int(bool(body.fracture))
+        b.visc = int(mat.beta1 != 0.0 or mat.beta2 != 0.0)
+        b.precision = 4 if precision == "fp32" else 8
+        b.kind = kind
+        b.uniform = int(self.uniform)
+        b.write_out = 0
+        b.store_a = 0
+        b.nbc = self.nbc
+        b.mk = int(body.mk)
+        b.restrict_prog = self.restrict_prog
+        b.bc_whole = self.bc_whole
+        h = float(body.h)
+        b.h, b.inv_h = h, 1.0 / h
+        b.alpha = kernel_geom.kernel_alpha(h, body.dim, kind)
+        for k in ("rho0", "lam", "mu", "kappa", "beta1", "beta2", "Gc", "eps0", "s_l",
+                  "sigma_y0", "H_hard"):
+            setattr(b, k, float(getattr(mat, k)))
+        b.c0 = float(mat.c0)
+        b.V0c = float(self.body.state.V0[0])
+        b.m0c = float(self.body.state.m0[0])
+        b.dp_body = float(body.dp_body)
+        b.jac_tol = 1e-30 if precision == "fp64" else 1e-12
+        for k in range(3):
+            b.f0[k] = float(body.f0[k])
+        P = _lib.ptr
+        b.soff, b.sidx, b.Xs, b.L = P(self.soff), P(self.sidx), P(self.Xs), P(self.L)
+        b.V0, b.m0 = P(self.V0), P(self.m0)
+        for k in ("us", "rb", "v", "al", "sdot", "sddot", "Hh", "Cpd", "epbar", "a"):
+            setattr(b, k, P(getattr(self, k)))
+        b.F_out, b.S_out, b.psi_out, b.psip_out = (P(self.F_out), P(self.S_out),
+                                                  P(self.psi_out), P(self.psip_out))
+        b.bcmask, b.bcs = P(self.bcmask), P(self.bcs_dev)
+        b.red, b.counters, b.pw_partial = P(self.red), P(self.counters), P(self.pw_partial)
+        return b
+
+    def _reset_counters(self):
+        c = self.counters
+        c.zero_()
+        c[2] = INT64_MAX
+        c[3] = INT64_MAX
+        c[6] = INT64_MAX
+        c[7] = INT64_MAX
+
+    # -- host mirrors ------------------------------------------------------------
+    def push_state(self):
+        """Upload body.state (host, FP64) into the device layout."""
+        torch = _torch()
+        st = self.body.state
+        R, dev = self.R, self.dev
+        us = np.empty((self.n, 4))
+        us[:, :3] = st.u
+        us[:, 3] = st.s
+        self.us.copy_(torch.from_numpy(us).to(dev, R))
+        self.v.copy_(torch.from_numpy(np.ascontiguousarray(st.v.T)).to(dev, R))
+        self.a.copy_(torch.from_numpy(np.ascontiguousarray(st.a.T)).to(dev, R))
+        for name, arr in (("sdot", st.sdot), ("sddot", st.sddot), ("Hh", st.Hhist),
+                          ("epbar", st.epbar)):
+            getattr(self, name).copy_(torch.from_numpy(np.asarray(arr, dtype=np.float64)).to(dev, R))
+        if self.body.material.model == Model.J2:
+            Cp = np.asarray(st.Cp, dtype=np.float64)
+            cpd = np.stack([Cp[:, 0, 0] - 1.0, Cp[:, 1, 1] - 1.0, Cp[:, 2, 2] - 1.0,
+                            Cp[:, 0, 1], Cp[:, 0, 2], Cp[:, 1, 2]])
+            self.Cpd.copy_(torch.from_numpy(cpd).to(dev, R))
+
+    def pull_state(self, full=True):
+        """Refresh body.state (host) from the device."""
+        st = self.body.state
+        us = self.us.double().cpu().numpy()
+        st.u[...] = us[:, :3]
+        st.s[...] = us[:, 3]
+        st.v[...] = self.v.double().cpu().numpy().T
+        st.sdot[...] = self.sdot.double().cpu().numpy()
+        st.sddot[...] = self.sddot.double().cpu().numpy()
+        st.Hhist[...] = self.Hh.double().cpu().numpy()
+        st.epbar[...] = self.epbar.double().cpu().numpy()
+        if full:
+            st.a[...] = self.a.double().cpu().numpy().T
+            st.F[...] = self.F_out.cpu().numpy()
+            st.S[...] = self.S_out.cpu().numpy()
+            st.psi_e[...] = self.psi_out.cpu().numpy()
+            st.psi_plus[...] = self.psip_out.cpu().numpy()
+        if self.body.material.model == Model.J2:
+            c = self.Cpd.double().cpu().numpy()
+            Cp = np.empty((self.n, 3, 3))
+            Cp[:, 0, 0], Cp[:, 1, 1], Cp[:, 2, 2] = 1.0 + c[0], 1.0 + c[1], 1.0 + c[2]
+            Cp[:, 0, 1] = Cp[:, 1, 0] = c[3]
+            Cp[:, 0, 2] = Cp[:, 2, 0] = c[4]
+            Cp[:, 1, 2] = Cp[:, 2, 1] = c[5]
+            st.Cp[...] = Cp
+        self.body.plastic_work = self.pw_base + float(self.pw_acc.item())
+
+    def dtinfo(self):
+        return _lib.tl_dtinfo(h=float(self.body.h), c0=float(self.body.material.c0),
+                              red=_lib.ptr(self.red))
+
+
+def _lib_max_bc():
+    return 32
+
+
+def _upload_adjacency(adj, st, body, kind):
+    """Device structure from a host (reference) Adjacency: its CSR is used
+    as given; L_i is recomputed on the device from the positions."""
+    torch = _torch()
+    dev = torch.device("cuda")
+    X = torch.from_numpy(np.ascontiguousarray(st.X, dtype=np.float64)).to(dev)
+    indptr = torch.from_numpy(np.asarray(adj.indptr, dtype=np.int64)).to(dev)
+    indices = torch.from_numpy(np.asarray(adj.indices, dtype=np.int64)).to(dev, torch.int32)
+    n = X.shape[0]
+    Ld = torch.empty((n, 9), dtype=torch.float64, device=dev)
+    fb = torch.zeros(1, dtype=torch.int64, device=dev)
+    corr = bool(getattr(body, "kernel_correction", True))
+    alpha = kernel_geom.kernel_alpha(body.h, body.dim, kind)
+    V0 = torch.from_numpy(np.asarray(st.V0, dtype=np.float64)).to(dev)
+    _lib.check(_lib.lib().tl_correction(
+        _lib.stream_ptr(), n, _lib.ptr(indptr), _lib.ptr(indices), _lib.ptr(X), _lib.ptr(V0),
+        float(body.h), float(alpha), int(kind), int(body.dim), int(corr), _lib.ptr(Ld),
+        _lib.ptr(fb)), "tl_correction")
+    return kernel_geom.DeviceAdjacency(X, indptr, indices, Ld, int(fb.item()), body.h,
+                                       body.dim, kind, corr)
+
+
+class ProgramTable:
+    """All expressions of a case compiled once to device bytecode."""
+
+    def __init__(self):
+        self.ids = []
+        self.progs = []
+
+    def index_of(self, eid, ast):
+        if eid in self.ids:
+            return self.ids.index(eid)
+        self.ids.append(eid)
+        self.progs.append(ex.compile_program(ast))
+        return len(self.ids) - 1
+
+    def upload(self):
+        torch = _torch()
+        dev = torch.device("cuda")
+        self.code = [torch.from_numpy(p.code.reshape(-1).copy()).to(dev) for p in self.progs]
+        self.consts = [torch.from_numpy(p.consts.copy()).to(dev) for p in self.progs]
+        arr = (_lib.tl_prog * max(len(self.progs), 1))()
+        for k, p in enumerate(self.progs):
+            arr[k].code = _lib.ptr(self.code[k])
+            arr[k].consts = _lib.ptr(self.consts[k])
+            arr[k].len = int(p.code.shape[0])
+        nbytes = C.sizeof(_lib.tl_prog) * max(len(self.progs), 1)
+        self.table = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        self.table.copy_(torch.frombuffer(bytearray(C.string_at(C.addressof(arr), nbytes)),
+                                          dtype=torch.uint8))
+        return self.table
+
+
+class DeviceSimulation:
+    """Drop-in for solidsph.stepper.Simulation running on one B200."""
+
+    def __init__(self, config, trace=None, precision="fp64", stream=None):
+        if precision not in ("fp32", "fp64"):
+            raise ValueError("precision must be 'fp32' or 'fp64'")
+        L = _lib.lib()  # fails loudly without the native library / GPU
+        torch = _torch()
+        self.config = config
+        self.bodies = config.bodies
+        self.expressions = config.expressions
+        self.t = 0.0
+        self.step_index = 0
+        self.trace = trace
+        self.be = backend
+        self.precision = precision
+        self.contact_warnings = 0
+        self._initialized = False
+        self.stream = stream or torch.cuda.current_stream()
+        if len(self.bodies) > 1:
+            raise NotImplementedError(
+                "multi-body cases need the penalty contact phase, which is not on the "
+                "device yet (SURVEY.md 8(f) rank 3)")
+        self.programs = ProgramTable()
+        self.dbodies = [DeviceBody(b, config, precision, self.programs) for b in self.bodies]
+        prog_table = self.programs.upload()
+        self.clock_dev = torch.zeros(C.sizeof(_lib.tl_clock), dtype=torch.uint8,
+                                     device="cuda")
+        for db in self.dbodies:
+            db.desc.progs = _lib.ptr(prog_table)
+            db.desc.clock = _lib.ptr(self.clock_dev)
+            db.desc.store_a = int(int(config.step_algorithm) == 2)
+        self._lib = L
+        self._dt_arr = (_lib.tl_dtinfo * len(self.dbodies))(*[db.dtinfo() for db in self.dbodies])
+        self.workspaces = [None for _ in self.bodies]
+
+    # -- plumbing ------------------------------------------------------------
+    def _st(self):
+        return C.c_void_p(self.stream.cuda_stream)
+
+    def _mark(self, phase):
+        if self.trace is not None:
+            self.trace.append(phase)
+
+    def _set_clock(self, **kw):
+        c = _lib.tl_clock()
+        c.t = self.t
+        c.dt = 0.0
+        c.next_out = math.inf
+        c.t_max = math.inf
+        c.eps = 0.0
+        c.dt_override = -1.0
+        c.cfl = float(self.config.cfl)
+        c.step = self.step_index
+        c.max_steps = -1
+        c.halted = 0
+        c.out_step = 0
+        for k, v in kw.items():
+            setattr(c, k, v)
+        raw = bytearray(C.string_at(C.addressof(c), C.sizeof(c)))
+        torch = _torch()
+        self.clock_dev.copy_(torch.frombuffer(raw, dtype=torch.uint8), non_blocking=False)
+
+    def _get_clock(self):
+        raw = bytes(self.clock_dev.cpu().numpy().tobytes())
+        c = _lib.tl_clock.from_buffer_copy(raw)
+        return c
+
+    def _pass_a(self, db):
+        _lib.check(self._lib.tl_pass_a(self._st(), C.byref(db.desc)), "tl_pass_a")
+
+    def _pass_b(self, db, mode):
+        _lib.check(self._lib.tl_reset_red(self._st(), _lib.ptr(db.red)), "tl_reset_red")
+        _lib.check(self._lib.tl_pass_b(self._st(), C.byref(db.desc), mode), "tl_pass_b")
+        if int(db.body.material.model) == int(Model.J2):
+            _lib.check(self._lib.tl_reduce_partials(self._st(), _lib.ptr(db.pw_partial),
+                                                    db.nblocks, _lib.ptr(db.pw_acc)),
+                       "tl_reduce_partials")
+
+    def _launch_step(self, mode_verlet):
+        if mode_verlet:
+            for db in self.dbodies:
+                self._pass_a(db)
+            for db in self.dbodies:
+                self._pass_b(db, 1)
+        else:
+            for db in self.dbodies:
+                _lib.check(self._lib.tl_predict(self._st(), C.byref(db.desc)), "tl_predict")
+            for db in self.dbodies:
+                self._pass_a(db)
+            for db in self.dbodies:
+                self._pass_b(db, 2)
+
+    def _check_errors(self):
+        """Raise the reference's exceptions for events recorded on the device."""
+        for db in self.dbodies:
+            c = db.counters.cpu().numpy()
+            mk = db.body.mk
+            db.body.degenerate_warnings = db.deg_base + int(c[0])
+            if c[4]:
+                db._reset_counters()
+                raise ex.ExprError(ex.ERRORS.get(int(c[4]), "expression error"))
+            if c[5]:
+                db._reset_counters()
+                raise CaseError(f"restrictphi expression must evaluate within [0, 1] "
+                                f"(body {mk})")
+            if c[1]:
+                db._reset_counters()
+                raise SimulationError(
+                    f"eigensolver failed to converge for {int(c[1])} particles (body {mk})")
+            if c[2] != INT64_MAX:
+                db._reset_counters()
+                raise SimulationError(f"non-SPD plastic metric at particle {int(c[2])} "
+                                      f"(body {mk})")
+            if c[3] != INT64_MAX:
+                step = int(c[6]) if c[6] != INT64_MAX else self.step_index
+                db._reset_counters()
+                raise SimulationError(f"non-finite acceleration at particle {int(c[3])} "
+                                      f"(body {mk}, step {step})")
+            if c[7] != INT64_MAX:
+                first = int(c[7])
+                check_at = ((first + 63) // 64) * 64
+                if self.step_index >= check_at:
+                    db._reset_counters()
+                    raise SimulationError(f"non-finite state in body {mk} at step {check_at}")
+
+    def sync_host(self, full=True):
+        """Copy the device state into every body.state (FP64 host mirrors)."""
+        torch = _torch()
+        torch.cuda.current_stream().wait_stream(self.stream)
+        for db in self.dbodies:
+            db.pull_state(full=full)
+
+    def push_state(self):
+        """Upload host edits of body.state to the device."""
+        for db in self.dbodies:
+            db.push_state()
+
+    # -- reference API -----------------------------------------------------------
+    def initialize(self):
+        """One force evaluation at t=0 plus the initial velocity BCs
+        (stepper.py:134-142)."""
+        self._set_clock(t=0.0, dt=0.0)
+        for db in self.dbodies:
+            db.desc.write_out = 1
+        self._mark("contact")
+        self._mark("internal")
+        for db in self.dbodies:
+            self._pass_a(db)
+        for db in self.dbodies:
+            self._pass_b(db, 0)
+        for db in self.dbodies:
+            db.desc.write_out = 0
+        if self.trace is not None:
+            del self.trace[:]
+        self._initialized = True
+        self.sync_host()
+        self._check_errors()
+
+    def step(self, dt):
+        """One Verlet or symplectic step of size dt (stepper.py:211-217)."""
+        if not self._initialized:
+            self.initialize()
+        verlet = int(self.config.step_algorithm) != 2
+        self._set_clock(t=self.t, dt=float(dt), out_step=1)
+        if verlet:
+            for ph in ("contact", "internal", "bc", "update", "commit"):
+                self._mark(ph)
+        else:
+            for ph in ("predictor", "contact", "internal", "bc", "update", "commit"):
+                self._mark(ph)
+        self._launch_step(verlet)
+        self.t += dt
+        self.step_index += 1
+        self.sync_host()
+        self._check_errors()
+
+    def pick_dt(self):
+        """Adaptive dt from the device maxima, bit-identical to the
+        reference's FP64 formula (stepper.py:221-233)."""
+        if self.config.dt_override is not None:
+            return self.config.dt_override
+        dt = math.inf
+        for db in self.dbodies:
+            red = db.red.cpu().numpy().view(np.float64)
+            vmax = float(np.sqrt(red[0]))
+            amax = float(np.sqrt(red[1]))
+            h, c0, cfl = db.body.h, db.body.material.c0, self.config.cfl
+            dtv = h / (c0 + vmax)
+            cand = cfl * min(dtv, math.sqrt(h / amax)) if amax > 0.0 else cfl * dtv
+            dt = min(dt, cand)
+        return dt
+
+    def run(self, time_max=None, time_out=None, on_output=None, max_steps=None, batch=64):
+        """Advance to time_max with on_output at t=0, every time_out boundary
+        and the end (stepper.py:237-263).  Steps are launched in batches with
+        dt, t and the output/stop decisions computed on the device clock."""
+        cfg = self.config
+        t_max = cfg.time_max if time_max is None else time_max
+        t_out = cfg.time_out if time_out is None else time_out
+        if not self._initialized:
+            self.initialize()
+        if on_output is not None:
+            on_output(self)
+        if t_max <= 0.0:
+            return
+        next_out = t_out if t_out > 0.0 else t_max
+        eps = 1e-12 * max(t_max, 1.0)
+        verlet = int(cfg.step_algorithm) != 2
+        dto = -1.0 if cfg.dt_override is None else float(cfg.dt_override)
+        dtinfo = self._dt_arr
+        while self.t < t_max - eps:
+            self._set_clock(t=self.t, next_out=next_out, t_max=t_max, eps=eps, dt_override=dto,
+                            max_steps=-1 if max_steps is None else int(max_steps))
+            k = 0
+            while k < batch:
+                _lib.check(self._lib.tl_clock_begin(self._st(), _lib.ptr(self.clock_dev),
+                                                     len(self.dbodies), dtinfo), "clock")
+                self._launch_step(verlet)
+                _lib.check(self._lib.tl_clock_commit(self._st(), _lib.ptr(self.clock_dev)),
+                           "commit")
+                k += 1
+            c = self._get_clock()
+            steps_done = int(c.step) - self.step_index
+            if self.trace is not None:
+                seq = ("contact", "internal", "bc", "update", "commit") if verlet else \
+                      ("predictor", "contact", "internal", "bc", "update", "commit")
+                self.trace.extend(seq * steps_done)
+            self.t = float(c.t)
+            self.step_index = int(c.step)
+            self._check_errors()
+            if c.halted == 4:
+                raise SimulationError(f"timestep collapsed to {c.dt!r}")
+            if c.halted == 2:
+                self.sync_host()
+                if on_output is not None:
+                    on_output(self)
+                next_out = min(next_out + t_out, t_max) if t_out > 0.0 else t_max
+            if max_steps is not None and self.step_index >= max_steps:
+                break
+            if c.halted == 1:
+                break
+        self.sync_host()
+
+
+# The reference name, for ``from paper_2602_15149_b200.simulation import Simulation``
+Simulation = DeviceSimulation

@@ -1,0 +1,162 @@
+"""CPU-side checks of the C ABI and the host logic (no GPU calls)."""
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, golden
+
+HEADER = os.path.join(ROOT, "include", "tlsph.h")
+
+
+def _header_functions():
+    txt = open(HEADER).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const\s+char\s*\*)\s*(tl_\w+)\s*\(", txt, re.M)))
+
+
+def test_library_loads_and_exports_header_symbols():
+    from paper_2602_15149_b200 import _lib
+    L = _lib.load_library()
+    declared = _header_functions()
+    assert set(declared) == set(_lib.EXPORTED)
+    for name in declared:
+        assert hasattr(L, name), name
+
+
+def test_struct_layouts_match_ctypes():
+    import ctypes
+    from paper_2602_15149_b200 import _lib
+    L = _lib.load_library()
+    for k, st in enumerate(_lib.STRUCTS):
+        assert L.tl_struct_size(k) == ctypes.sizeof(st), st.__name__
+
+
+def test_product_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_2602_15149_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in re.sub(r"#.*|//.*", "", src).replace(
+                    "oracle_", ""), f
+
+
+def test_no_gpu_means_loud_failure(monkeypatch):
+    import torch
+    from paper_2602_15149_b200 import _lib
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    monkeypatch.setattr(_lib, "_lib", None)
+    with pytest.raises(_lib.NativeLibraryError):
+        _lib.lib()
+
+
+# -- expression compiler: run the bytecode with a tiny host interpreter and
+#    compare with the golden masked evaluation of the reference -------------
+
+def _run(prog, vars_):
+    from paper_2602_15149_b200 import expr as ex
+    inv = {v: k for k, v in ex.OP.items()}
+    st = []
+    pc = 0
+    code = prog.code
+    while pc < len(code):
+        op, arg = inv[int(code[pc, 0])], int(code[pc, 1])
+        pc += 1
+        if op == "END":
+            return st[-1], False
+        if op == "CONST":
+            st.append(float(prog.consts[arg]))
+        elif op == "VAR":
+            st.append(float(vars_[arg]))
+        elif op == "NEG":
+            st[-1] = -st[-1]
+        elif op == "JZ":
+            if st.pop() == 0.0:
+                pc = arg
+        elif op == "JMP":
+            pc = arg
+        elif op == "SKIP":
+            return 0.0, True
+        elif op in ("SIN", "COS", "TAN", "SINH", "COSH", "TANH", "SQRT", "ABS"):
+            st[-1] = getattr(np, op.lower() if op != "ABS" else "abs")(st[-1])
+        elif op == "COT":
+            st[-1] = np.cos(st[-1]) / np.sin(st[-1])
+        elif op == "COTH":
+            a = min(max(st[-1], -700.0), 700.0)
+            st[-1] = np.cosh(a) / np.sinh(a)
+        elif op == "LOG":
+            st[-1] = np.log10(st[-1])
+        elif op == "LN":
+            st[-1] = np.log(st[-1])
+        else:
+            b = st.pop()
+            a = st[-1]
+            st[-1] = {"ADD": lambda: a + b, "SUB": lambda: a - b, "MUL": lambda: a * b,
+                      "DIV": lambda: a / b, "POW": lambda: math.pow(a, b),
+                      "POWF": lambda: math.pow(a, b), "LT": lambda: float(a < b),
+                      "GT": lambda: float(a > b), "LE": lambda: float(a <= b),
+                      "GE": lambda: float(a >= b), "EQ": lambda: float(a == b),
+                      "NE": lambda: float(a != b),
+                      "AND": lambda: float(a != 0.0 and b != 0.0),
+                      "OR": lambda: float(a != 0.0 or b != 0.0)}[op]()
+    return st[-1], False
+
+
+def test_bytecode_matches_reference_masked_eval():
+    from paper_2602_15149_b200 import expr as ex
+    G = golden("expr")
+    srcs = bytes(G["sources"]).decode().split("\n")
+    names = ex.VARIABLES
+    n = G["x0"].shape[0]
+    for k, line in enumerate(srcs):
+        src, loc = line.split("\t")
+        prog = ex.compile_program(ex.parse(src, loc))
+        assert prog.depth <= ex.MAX_STACK
+        ref_v, ref_s = G[f"e{k}.vals"], G[f"e{k}.skip"]
+        for i in range(0, n, 7):
+            vars_ = [float(G[nm][i]) if G[nm].ndim else float(G[nm]) for nm in names]
+            val, skip = _run(prog, vars_)
+            assert skip == bool(ref_s[i]), (src, i)
+            if not skip:
+                assert val == pytest.approx(ref_v[i], rel=1e-14, abs=1e-300), (src, i)
+
+
+def test_parse_errors_and_skip_rules():
+    from paper_2602_15149_b200 import expr as ex
+    for bad, msg in [("", "empty"), ("1 +", "unexpected token"), ("foo", "unknown identifier"),
+                     ("sin(1, 2)", "takes 1"), ("1 + skip", "skip"), ("and 1", "missing left"),
+                     ("(1", "expected '\\)'"), ("1 $", "unexpected character")]:
+        with pytest.raises(ex.ExprError, match=msg):
+            ex.parse(bad)
+    assert ex.parse("if(x0 > 1, skip, 2)").root[0] == "if"
+    assert ex.parse("-2^2").root == ("num", -4.0) or ex.eval_expr(ex.parse("-2^2"), None) == -4.0
+    assert ex.eval_expr(ex.parse("2^3^2"), None) == 512.0
+    assert ex.parse("a*b", "a=2; b=a+1").root == ("bin", "*", ("num", 2.0), ("num", 3.0))
+    assert not ex.parse("x0*2").time_dependent and ex.parse("t*2").time_dependent
+
+
+def test_case_roundtrip():
+    from paper_2602_15149_b200 import cases
+    cfg = cases.make_case("kalthoff2d", dp_scale=2, mapfac=1, build_adjacency=False)
+    d = cases.case_to_dict(cfg)
+    back = cases.case_from_dict(d)
+    assert np.array_equal(back.bodies[0].state.X, cfg.bodies[0].state.X)
+    assert back.bodies[0].material == cfg.bodies[0].material
+    for a, b in zip(back.bodies[0].bcs, cfg.bodies[0].bcs):
+        assert a.kind == b.kind and a.const == b.const and a.expr == b.expr
+        assert (a.target is None and b.target is None) or np.array_equal(a.target, b.target)
+
+
+def test_workload_sizes():
+    """BASELINE configs at their stated particle counts;
+    C4 and C5 are counted from the lattice rule without materialising."""
+    from paper_2602_15149_b200 import cases
+    c1 = cases.make_case("C1", build_adjacency=False)
+    assert c1.bodies[0].n == 3800
+    # C4: round(99.5/0.1836) x round(10/0.1836) x round(99.5/0.1836)
+    dpb = 1e-3 * 0.918 / 5
+    assert (round(99.5e-3 / dpb) * round(10e-3 / dpb) * round(99.5e-3 / dpb)) == 15863256

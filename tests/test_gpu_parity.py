@@ -1,0 +1,288 @@
+"""Parity of the CUDA path against the reference's golden vectors and the
+CPU oracle.  Needs a B200 (``pytest -m gpu``).
+
+Tolerances (normwise max|x-ref|/max|ref|, the reference tests' metric):
+  * neighbour lists: bit-exact (indptr, indices, fallback count);
+  * FP64 kernels at step 1: <= 1e-12 (oracle self-spread 4e-13);
+  * FP64 multi-step runs: the same per-field bounds the oracle is held to
+    (tests/test_oracle.py TOL, <= 1e-9);
+  * FP32 mode at step 1 on perturbed states: <= 1e-5 (north star).
+"""
+import numpy as np
+import pytest
+
+from conftest import golden, relerr, run_case
+
+pytestmark = pytest.mark.gpu
+
+ADJ_TAGS = ["l2w", "l2c", "l3w", "l3c", "l3n", "l2n", "l2n2", "nocorr", "two", "tie3", "tie2",
+            "notch_rows", "notch_part", "notch3d", "notch3dr"]
+
+
+@pytest.fixture(scope="module")
+def kg():
+    from paper_2602_15149_b200 import kernel_geom
+    return kernel_geom
+
+
+@pytest.fixture(scope="module")
+def GA():
+    return golden("adjacency")
+
+
+@pytest.mark.parametrize("tag", ADJ_TAGS)
+def test_device_adjacency_bit_exact(kg, GA, tag):
+    dp, dim, kind, nbs, corr, h = GA[f"{tag}.params"]
+    adj = kg.build_adjacency(GA[f"{tag}.X"], GA[f"{tag}.V0"], h, int(dim), int(kind),
+                             nbsrange=None if nbs < 0 else int(nbs), dp_body=dp,
+                             notches=list(GA[f"{tag}.notches"]), correction=bool(corr))
+    assert np.array_equal(adj.indptr, GA[f"{tag}.indptr"])
+    assert np.array_equal(adj.indices, GA[f"{tag}.indices"])
+    assert adj.correction_fallbacks == int(GA[f"{tag}.fallbacks"][0])
+    if f"{tag}.grad0" in GA:
+        assert relerr(adj.grad0, GA[f"{tag}.grad0"]) <= 1e-13
+        assert relerr(adj.grad0r, GA[f"{tag}.grad0r"]) <= 1e-13
+        assert relerr(adj.r0norm, GA[f"{tag}.r0norm"]) <= 1e-15
+        assert relerr(adj.w0, GA[f"{tag}.w0"]) <= 1e-14
+
+
+@pytest.mark.parametrize("tag,kw", [("rnd", dict(h=0.08)),
+                                    ("rndn", dict(h=0.1, nbsrange=1, dp_body=0.07))])
+def test_device_pairs_random(kg, GA, tag, kw):
+    rows, cols = kg.build_pairs(GA[f"{tag}.X"], **kw)
+    assert np.array_equal(rows, GA[f"{tag}.rows"])
+    assert np.array_equal(cols, GA[f"{tag}.cols"])
+
+
+def test_isolated_particle_rejected(kg):
+    from paper_2602_15149_b200.core import CaseError, Quad
+    pos = np.array([[0.0, 0.0, 0.0], [1.0, 0.0, 0.0], [2.0, 0.0, 0.0]])
+    quad = Quad(points=[[0.5, -1, -1], [0.5, 1, -1], [0.5, 1, 1], [0.5, -1, 1]])
+    with pytest.raises(CaseError, match="no neighbors"):
+        kg.build_adjacency(pos, np.ones(3), 0.6, 3, 2, notches=[quad])
+    with pytest.raises(CaseError, match="degenerate"):
+        kg.build_adjacency(pos, np.ones(3), 0.6, 3, 2,
+                           notches=[Quad(points=[[0, 0, 0], [1, 0, 0], [2, 0, 0], [3, 0, 0]])])
+
+
+# ---------------------------------------------------------------------------
+# backend plugin kernels vs the reference numpy backend (golden)
+# ---------------------------------------------------------------------------
+
+@pytest.fixture(scope="module")
+def K():
+    return golden("kernels")
+
+
+@pytest.fixture(scope="module")
+def be():
+    from paper_2602_15149_b200 import backend
+    return backend
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_plugin_pair_kernels(K, be, kg, dim):
+    X = K[f"d{dim}.X"]
+    V0 = np.full(X.shape[0], 1e-3 ** dim)
+    h = 1e-3 * np.sqrt(dim)
+    adj = kg.build_adjacency(X, V0, h, dim, 2)
+    n = X.shape[0]
+    p = f"d{dim}."
+    F = np.zeros((n, 3, 3))
+    be.deformation_gradient(adj.indptr, adj.rows, adj.indices, adj.grad0, K[p + "u"], V0,
+                            K[p + "s"], 0.1, True, F)
+    assert relerr(F - np.eye(3), K[p + "F"] - np.eye(3)) <= 1e-12
+    lap = np.zeros(n)
+    be.sph_laplacian(adj.indptr, adj.rows, adj.indices, adj.grad0, adj.r0, adj.r0norm, V0,
+                     K[p + "f"], lap)
+    assert relerr(lap, K[p + "lap"]) <= 1e-12
+    g = np.zeros((n, 3))
+    be.sph_gradient(adj.indptr, adj.rows, adj.indices, adj.grad0, V0, K[p + "f"], g)
+    assert relerr(g, K[p + "grad"]) <= 1e-12
+    for tag, (b1, b2) in (("mom0", (0.0, 0.0)), ("mom1", (0.2, 0.1))):
+        a = np.zeros((n, 3))
+        nb = be.momentum(adj.indptr, adj.rows, adj.indices, adj.grad0, adj.grad0r, adj.r0,
+                         adj.r0norm, K[p + "P"], 1000.0 * V0, 1000.0, K[p + "v"], h, 64.8, b1,
+                         b2, K[p + "Fm"], a)
+        assert nb == int(K[p + tag + ".nbad"][0])
+        assert relerr(a, K[p + tag]) <= 1e-12
+
+
+def test_plugin_constitutive(K, be):
+    n = K["svk.F"].shape[0]
+    for fr in (0, 1):
+        S, psi, psip = np.zeros((n, 3, 3)), np.zeros(n), np.zeros(n)
+        assert be.svk_batch(K["svk.F"], 2.7733e6, 0.715e6, K["svk.s"], bool(fr), S, psi,
+                            psip) == 0
+        assert relerr(S, K[f"svk{fr}.S"]) <= 1e-12
+        assert relerr(psi, K[f"svk{fr}.psi"]) <= 1e-12
+        assert relerr(psip, K[f"svk{fr}.psip"]) <= 1e-12
+        S, psi, psip = np.zeros((n, 3, 3)), np.zeros(n), np.zeros(n)
+        nb = be.nh_batch(K["nh.F"], 3.25e6, 0.715e6, K["nh.s"], bool(fr), S, psi, psip)
+        assert nb == int(K[f"nh{fr}.nbad"][0])
+        assert relerr(S, K[f"nh{fr}.S"]) <= 1e-12
+        assert relerr(psi, K[f"nh{fr}.psi"]) <= 1e-11
+    for tag, Fk, Cp0, ep0 in (("j2", "j2.F", None, None), ("j2b", "j2b.F", "j2.Cp", "j2.ep")):
+        F = K[Fk]
+        n = F.shape[0]
+        Cp = np.tile(np.eye(3), (n, 1, 1)) if Cp0 is None else K[Cp0].copy()
+        ep = np.zeros(n) if ep0 is None else K[ep0].copy()
+        S, psi, dwp = np.zeros((n, 3, 3)), np.zeros(n), np.zeros(n)
+        nb, fb = be.j2_batch(F, Cp, ep, 43.333e9, 130e9, 4e8, 1e8, S, psi, dwp)
+        assert [nb, fb] == list(K[f"{tag}.ret"])
+        assert relerr(S, K[f"{tag}.S"]) <= 1e-12
+        assert relerr(Cp - np.eye(3), K[f"{tag}.Cp"] - np.eye(3)) <= 1e-12
+        assert relerr(ep, K[f"{tag}.ep"]) <= 1e-12
+        assert relerr(psi, K[f"{tag}.psi"]) <= 1e-9
+        assert relerr(dwp, K[f"{tag}.dwp"]) <= 1e-9
+
+
+def test_plugin_contact_and_eigen(K, be):
+    pairs = np.array([(i, j) for i in range(40) for j in range(50)], dtype=np.int64)
+    aa, ab = np.zeros((40, 3)), np.zeros((50, 3))
+    w = be.contact_pair_accumulate(K["ct.xa"], K["ct.va"], np.full(40, 0.3), K["ct.xb"],
+                                   K["ct.vb"], np.full(50, 0.4), pairs, 0.012, 1e7, 30.0, 0.3,
+                                   aa, ab)
+    assert w == int(K["ct.warn"][0])
+    assert relerr(aa, K["ct.aa"]) <= 1e-12 and relerr(ab, K["ct.ab"]) <= 1e-12
+    wv, Q, sw = be.eig3_jacobi_batch(K["eig.A"])
+    assert (sw < 64).all()
+    assert np.all(np.diff(wv, axis=1) <= 0)
+    assert np.abs(np.sort(wv, axis=1) - K["eig.w"]).max() <= 1e-12
+    A = K["eig.A"]
+    rec = np.einsum("nij,nj,nkj->nik", Q, wv, Q)
+    assert np.abs(rec - A).max() <= 1e-12 * max(1.0, np.abs(A).max())
+
+
+# ---------------------------------------------------------------------------
+# device-resident stepping vs reference runs
+# ---------------------------------------------------------------------------
+
+RUNS = ["kalthoff2d", "kalthoff2d_p", "kalthoff2d_sym", "beam2d", "taylor3d", "column3d",
+        "branch2d", "kalthoff3d", "twisting3d"]
+
+TOL64 = {"u": 1e-10, "v": 1e-10, "a": 1e-9, "s": 1e-10, "sdot": 1e-9, "Hhist": 1e-9,
+         "epbar": 1e-10, "F": 1e-10, "S": 1e-9, "Cp": 1e-11}
+
+
+def _errors(st, G, step, bi=0):
+    out = {}
+    for k in TOL64:
+        key = f"s{step}.b{bi}.{k}"
+        if key not in G:
+            continue
+        ref = G[key]
+        x = getattr(st, k)
+        if k in ("F", "Cp"):
+            x, ref = x - np.eye(3), ref - np.eye(3)
+        out[k] = np.abs(x - ref).max() if k == "s" else relerr(x, ref)
+    return out
+
+
+def _sim(G, precision):
+    from paper_2602_15149_b200.simulation import DeviceSimulation
+    cfg = run_case(G)
+    return cfg, DeviceSimulation(cfg, precision=precision)
+
+
+@pytest.mark.parametrize("tag", RUNS)
+def test_device_run_fp64_matches_reference(tag):
+    G = golden(f"run_{tag}")
+    cfg, sim = _sim(G, "fp64")
+    dev = sim.dbodies[0].adj
+    assert np.array_equal(dev.indptr.cpu().numpy(), G["adj0.indptr"])
+    assert np.array_equal(dev.indices.cpu().numpy(), G["adj0.indices"])
+    sim.initialize()
+    e0 = _errors(cfg.bodies[0].state, G, 0)
+    for k, err in e0.items():
+        assert err <= TOL64[k], ("init", k, err)
+    checks = set(int(c) for c in G["checkpoints"])
+    dts = G["dts"]
+    for step in range(1, len(dts) + 1):
+        dt = sim.pick_dt()
+        assert abs(dt - dts[step - 1]) <= 1e-12 * dts[step - 1], (step, dt, dts[step - 1])
+        sim.step(dts[step - 1])
+        if step in checks:
+            errs = _errors(cfg.bodies[0].state, G, step)
+            for k, err in errs.items():
+                assert err <= TOL64[k], (step, k, err)
+    assert sim.t == pytest.approx(float(G[f"s{max(checks)}.t"][0]), rel=1e-14)
+
+
+@pytest.mark.parametrize("tag", ["kalthoff2d_p", "taylor3d", "column3d", "branch2d",
+                                 "kalthoff3d", "twisting3d", "kalthoff2d_sym"])
+def test_device_step1_fp32(tag):
+    """FP32 mode: step-1 fields on the perturbed state within 1e-5."""
+    G = golden(f"run_{tag}")
+    cfg, sim = _sim(G, "fp32")
+    sim.initialize()
+    st = cfg.bodies[0].state
+    e0 = _errors(st, G, 0)
+    sim.step(G["dts"][0])
+    e1 = _errors(st, G, 1)
+    for k in ("F", "S"):
+        assert e0[k] <= 1e-5, ("init", k, e0[k])
+        assert e1[k] <= 1e-5, ("step1", k, e1[k])
+    assert e0["a"] <= 1e-5
+    assert e1["a"] <= 1e-5
+    for k in ("u", "v"):
+        assert e1[k] <= 1e-5, (k, e1[k])
+
+
+@pytest.mark.parametrize("tag", ["kalthoff2d", "beam2d"])
+def test_device_run_loop_adaptive(tag):
+    """run() on the device clock reproduces the reference's adaptive dt
+    sequence (no output clipping inside the window)."""
+    G = golden(f"run_{tag}")
+    cfg, sim = _sim(G, "fp64")
+    nsteps = len(G["dts"])
+    outs = []
+    sim.run(time_max=1.0, time_out=1.0, on_output=lambda s: outs.append((s.t, s.step_index)),
+            max_steps=nsteps, batch=7)
+    assert sim.step_index == nsteps
+    assert outs == [(0.0, 0)]
+    assert sim.t == pytest.approx(float(np.sum(G["dts"])), rel=1e-12)
+    errs = _errors(cfg.bodies[0].state, G, nsteps)
+    for k, err in errs.items():
+        assert err <= 10 * TOL64[k], (k, err)
+
+
+@pytest.mark.parametrize("tag", ["kalthoff2d_p", "kalthoff2d_sym", "taylor3d"])
+def test_device_run_outputs_match_oracle(tag, oracle_mod):
+    """run() with output boundaries (dt clipped to the output grid) against
+    the oracle's restatement of stepper.run on the same case."""
+    G = golden(f"run_{tag}")
+    cfg_o = run_case(G)
+    for b in cfg_o.bodies:
+        b.adjacency = oracle_mod.build_adjacency(
+            b.state.X, b.state.V0, b.h, b.dim, int(cfg_o.kernel), nbsrange=b.nbsrange,
+            dp_body=b.dp_body, notches=b.notches, correction=b.kernel_correction)
+    t_out = float(np.sum(G["dts"][:3])) * 1.37
+    t_max = t_out * 4.5
+    so = oracle_mod.OracleSimulation(cfg_o)
+    ref_out = []
+    so.run(time_max=t_max, time_out=t_out,
+           on_output=lambda s: ref_out.append((s.t, s.step_index, s.bodies[0].state.u.copy())))
+    cfg, sim = _sim(G, "fp64")
+    got = []
+    sim.run(time_max=t_max, time_out=t_out,
+            on_output=lambda s: got.append((s.t, s.step_index, s.bodies[0].state.u.copy())),
+            batch=5)
+    assert [g[1] for g in got] == [r[1] for r in ref_out]
+    for (tg, _, ug), (tr, _, ur) in zip(got, ref_out):
+        assert tg == pytest.approx(tr, rel=1e-13, abs=1e-300)
+        if np.abs(ur).max() > 0:
+            assert relerr(ug, ur) <= 1e-9
+
+
+def test_trace_phase_order():
+    """Phase-order audit (reference test_stepper.py:192-209)."""
+    from paper_2602_15149_b200.simulation import DeviceSimulation
+    G = golden("run_kalthoff2d")
+    cfg = run_case(G)
+    trace = []
+    sim = DeviceSimulation(cfg, trace=trace)
+    sim.initialize()
+    assert trace == []
+    sim.step(1e-9)
+    assert trace == ["contact", "internal", "bc", "update", "commit"]
