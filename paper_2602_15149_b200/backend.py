@@ -65,12 +65,23 @@ def _counter(n=1, fill=0):
     return torch.full((n,), fill, dtype=torch.int64, device="cuda")
 
 
+_keep: list = []
+
+
 def _call(name, *args):
+    """Launch and only then release the argument tensors: a device temporary
+    dropped before the launch would hand its memory to the next argument."""
     L = _lib.lib()
-    _lib.check(getattr(L, name)(_lib.stream_ptr(), *args), name)
+    try:
+        _lib.check(getattr(L, name)(_lib.stream_ptr(), *args), name)
+    finally:
+        _keep.clear()
 
 
-P = _lib.ptr
+def P(t):
+    if t is not None:
+        _keep.append(t)
+    return _lib.ptr(t)
 
 
 def deformation_gradient(indptr, rows, indices, grad0, u, V0, s, s_l, gated, out):
