@@ -1,0 +1,350 @@
+#!/usr/bin/env python3
+"""Throughput of the B200 TLSPH hot path on BASELINE.json's headline workload.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--precision fp32|fp64]
+                    [--impl ours|reference] [--config C4]
+
+Workload (default C4, BASELINE.json configs[3]): the 3D Kalthoff-Winkler
+phase-field fracture block, SVK + spectral split, nbsrange = 1 (26
+neighbours), notch through the thickness, ramp velocity BC, Verlet with
+adaptive dt -- 15,863,256 particles on one B200.  The
+initial state is the seeded "synthetic block" perturbation of SURVEY.md 8(d)
+(u ~ N(0, (2e-5 dp/1e-3)^2), v ~ N(0,1), s ~ U(0.3,1)) so every kernel
+branch does real work.  A step = one device-clock Verlet step (dt, pass A,
+pass B, commit).  value = particle-steps/s over the timed steps (CUDA
+events, max over ranks).  The ~9 GB per-step working set is far larger than
+the 126 MB L2, so no flush is needed between steps.
+
+Extra keys: roofline (dominant kernel vs measured HBM copy bandwidth,
+SURVEY.md 8(d) algorithmic bytes), cpu_baseline (the CPU oracle port, a
+bounded sample of the same case on this host's cores), e2e (public
+step()/pick_dt() API with host state mirrors every step), clocks, passes.
+
+--impl reference times the reference algorithm on the host CPU (the oracle
+port of solidsph's numba/numpy backends, oracle/; the reference itself is a
+Python package that cannot travel to the GPU box) on a bounded sample of the
+same workload and prints the same JSON line with "impl": "reference".
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "particle-steps/s, 3D phase-field fracture, 1/2/4/8 B200; % of HBM roofline"
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+TRAFFIC = os.path.join(ROOT, "profiles", "traffic.json")
+
+# canonical algorithmic bytes per particle-step, per pass,
+# 3D fracture: pass A = X(24) + L(9w) + u(3w) + s,sdot,H(3w) -> P(9w),
+# Avis(9w), H, sddot(2w) + 8 + 4k ; pass B = X(24) + L,P,Avis(27w) + v,u(6w)
+# + s,sdot,sddot(3w) -> v,u(6w), s,sdot(2w) + 8 + 4k
+def pass_bytes(w, k, dim=3, fracture=True):
+    if dim != 3 or not fracture:
+        raise NotImplementedError("bench reports the 3D fracture workload")
+    a = 24 + 9 * w + 3 * w + 3 * w + 9 * w + 9 * w + 2 * w + 8 + 4 * k
+    b = 24 + 27 * w + 6 * w + 3 * w + 6 * w + 2 * w + 8 + 4 * k
+    return a, b
+
+
+def peak_hbm():
+    try:
+        with open(PEAKS) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[2:6]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def perturb(cfg, seed=0):
+    """SURVEY.md 8(d) synthetic block state (mirrors backend_bench.py:29-34)."""
+    rng = np.random.default_rng(seed)
+    for b in cfg.bodies:
+        st = b.state
+        n = st.X.shape[0]
+        st.u[:] = rng.normal(scale=2e-5 * b.dp_body / 1e-3, size=(n, 3))
+        st.v[:] = rng.normal(scale=1.0, size=(n, 3))
+        if b.fracture:
+            st.s[:] = rng.uniform(0.3, 1.0, n)
+        if b.dim == 2:
+            st.u[:, 1] = 0.0
+            st.v[:, 1] = 0.0
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm / baseline (oracle port; test infrastructure)
+# ---------------------------------------------------------------------------
+
+CPU_SAMPLE = {"C4": dict(spec="kalthoff3d", dp_scale=0.918 * 4, mapfac=5)}
+
+
+def cpu_reference(config, steps, warmup, budget_s=25.0):
+    """Time the oracle (C/OpenMP restatement of the reference's numba
+    kernels + numpy stepper) on a bounded sample of the workload."""
+    from oracle import oracle as O
+    from paper_2602_15149_b200 import cases
+    O.build()
+    threads = os.cpu_count() or 1
+    O.set_threads(threads)
+    smp = CPU_SAMPLE[config]
+    cfg = cases.make_case(smp["spec"], dp_scale=smp["dp_scale"], mapfac=smp["mapfac"],
+                          build_adjacency=False)
+    perturb(cfg)
+    t0 = time.perf_counter()
+    for b in cfg.bodies:
+        b.adjacency = O.build_adjacency(b.state.X, b.state.V0, b.h, b.dim, int(cfg.kernel),
+                                        nbsrange=b.nbsrange, dp_body=b.dp_body,
+                                        notches=b.notches, correction=b.kernel_correction)
+    setup = time.perf_counter() - t0
+    n = sum(b.state.X.shape[0] for b in cfg.bodies)
+    sim = O.OracleSimulation(cfg)
+    sim.initialize()
+    for _ in range(max(warmup, 1)):
+        sim.step(sim.pick_dt())
+    done, t0 = 0, time.perf_counter()
+    while done < steps:
+        sim.step(sim.pick_dt())
+        done += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    el = time.perf_counter() - t0
+    k = float(np.mean(np.diff(cfg.bodies[0].adjacency.indptr)))
+    return {"value": n * done / el, "unit": "particle-steps/s", "cores": threads,
+            "kind": "port",
+            "sample": (f"{smp['spec']} dp_scale={smp['dp_scale']:.4g} mapfac={smp['mapfac']}: "
+                       f"N={n}, k={k:.1f}, {done} timed Verlet steps after {max(warmup, 1)} "
+                       f"warm-up, FP64, oracle/liboracle.so OpenMP x{threads} "
+                       f"(adjacency setup {setup:.1f}s untimed)"),
+            "steps": done, "seconds": el, "n": n}
+
+
+# ---------------------------------------------------------------------------
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--config", default="C4", choices=["C4"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        ref = cpu_reference(args.config, args.steps, args.warmup)
+        line = {"metric": METRIC, "value": ref["value"], "unit": "particle-steps/s",
+                "n_gpus": args.gpus, "steps": ref["steps"], "warmup": args.warmup,
+                "ms_per_step": 1e3 * ref["seconds"] / max(ref["steps"], 1),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic (seeded perturbed lattice state)",
+                "config": {"workload": f"{args.config} CPU sample", "sample": ref["sample"]},
+                "impl": "reference",
+                "cpu_baseline": {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "e2e": {"value": ref["value"], "unit": "particle-steps/s",
+                        "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2602_15149_b200 import cases
+    from paper_2602_15149_b200.simulation import DeviceSimulation
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://",
+                                device_id=torch.device("cuda", local))
+
+    t0 = time.perf_counter()
+    cfg = cases.make_case(args.config, lean=True, build_adjacency=False)
+    perturb(cfg, seed=rank)
+    t_case = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    sim = DeviceSimulation(cfg, precision=args.precision, mirrors=False)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t0
+    n = sum(db.n for db in sim.dbodies)
+    nnz = sum(db.adj.nnz for db in sim.dbodies)
+    k_mean = nnz / n
+    sim.initialize()
+    sim.advance(args.warmup)
+    sim.finish_advance()
+    torch.cuda.synchronize()
+
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    pass_ev = []
+    with ClockSampler(local) as clocks:
+        ev0.record(sim.stream)
+        sim.advance(args.steps, pass_events=pass_ev)
+        ev1.record(sim.stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    ta = [e[0].elapsed_time(e[1]) for e in pass_ev]
+    tb = [e[2].elapsed_time(e[3]) for e in pass_ev]
+    sim.finish_advance()
+    if world > 1:
+        tt = torch.tensor([ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+        nt = torch.tensor([n], device="cuda", dtype=torch.float64)
+        dist.all_reduce(nt)
+        n_total = float(nt.item())
+    else:
+        n_total = float(n)
+    ms_step = ms / args.steps
+    value = n_total * args.steps / (ms / 1e3)
+
+    # roofline of the dominant kernel (per-launch algorithmic bytes / event time)
+    w = 4 if args.precision == "fp32" else 8
+    ba, bb = pass_bytes(w, k_mean)
+    ma, mb = float(np.mean(ta)), float(np.mean(tb))
+    peak, peak_kind = peak_hbm()
+    dom = ("pass_b_force", bb, mb) if mb >= ma else ("pass_a_phase_field", ba, ma)
+    achieved = dom[1] * n / (dom[2] / 1e3) / 1e9
+    traffic = None
+    try:
+        with open(TRAFFIC) as f:
+            tr = json.load(f)
+        traffic = tr.get(f"{args.config}.{args.precision}.{dom[0]}")
+    except Exception:
+        pass
+    roofline = {"bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                "peak_source": f"{peak_kind} MEASURED_PEAKS.json hbm_gbs",
+                "bytes_per_particle": dom[1],
+                "step_frac": (ba + bb) * value / max(world, 1) / 1e9 / peak}
+    passes = {"pass_a_ms": ma, "pass_b_ms": mb, "bytes_a": ba, "bytes_b": bb,
+              "frac_a": ba * n / (ma / 1e3) / 1e9 / peak,
+              "frac_b": bb * n / (mb / 1e3) / 1e9 / peak}
+
+    # end to end through the public API: pick_dt() + step() with host mirrors
+    e2e = None
+    if args.e2e_steps > 0:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            dt = sim.pick_dt()
+            sim.step(dt)
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        state_bytes = n * (4 * w + 3 * w + 4 * w)   # (u,s), v, sdot, sddot, H, epbar
+        e2e = {"value": n_total * args.e2e_steps / el, "unit": "particle-steps/s",
+               "h2d_bytes_per_step": 80, "d2h_bytes_per_step": int(state_bytes + 16),
+               "api": "DeviceSimulation.pick_dt()+step(dt), host state mirror each step"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            ref = cpu_reference(args.config, 10, 1)
+            cpu = {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as exc:  # the baseline must not kill the GPU line
+            cpu = {"value": None, "error": repr(exc)}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "particle-steps/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": ms_step, "higher_is_better": True,
+                "scaling": "weak" if world > 1 else "weak", "vs_baseline": None,
+                "dtype": "f32" if args.precision == "fp32" else "f64",
+                "data": "synthetic (seeded perturbed lattice state, SURVEY.md 8(d))",
+                "config": {"workload": f"{args.config}: 3D Kalthoff-Winkler phase-field "
+                                       "fracture, SVK+spectral split, nbsrange=1, Verlet, "
+                                       "adaptive dt",
+                           "particles_per_gpu": n, "particles": int(n_total),
+                           "pairs_per_particle": k_mean,
+                           "parallelism": "replicas" if world > 1 else "single",
+                           "l2": "per-step working set >> 126 MB L2, no flush",
+                           "precision": args.precision,
+                           "setup_s": {"case": t_case, "device_build": t_setup}},
+                "roofline": roofline, "passes": passes, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": int(args.steps * (2 + 2 * len(sim.dbodies))),
+                "clocks": clocks.summary()}
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

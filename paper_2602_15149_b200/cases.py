@@ -238,7 +238,8 @@ def _material(cards, mk):
 
 
 def make_case(name, dp_scale=1.0, mapfac=None, eps0=None, cfl=None, dt_override=None,
-              time_max=None, time_out=None, build_adjacency=True, precision="fp64"):
+              time_max=None, time_out=None, build_adjacency=True, precision="fp64",
+              lean=False):
     """Assemble a CaseConfig the way caseio.build_case does (caseio.py:481-598)
     for one of ``SPECS`` or a ``WORKLOADS`` key ("C1".."C5")."""
     if name in WORKLOADS:
@@ -250,7 +251,7 @@ def make_case(name, dp_scale=1.0, mapfac=None, eps0=None, cfl=None, dt_override=
             kw["mapfac"] = mapfac
         return make_case(spec_name, eps0=eps0, cfl=cfl, dt_override=dt_override,
                          time_max=time_max, time_out=time_out,
-                         build_adjacency=build_adjacency, precision=precision, **kw)
+                         build_adjacency=build_adjacency, precision=precision, lean=lean, **kw)
     spec = SPECS[name]()
     dp = spec["dp"] * dp_scale
     dim = spec["dim"]
@@ -278,7 +279,16 @@ def make_case(name, dp_scale=1.0, mapfac=None, eps0=None, cfl=None, dt_override=
         X = _shapes_lattice([s for s in spec["shapes"] if s["mk"] == bspec["mk"]], dp_body,
                             dim, spec["y_plane"])
         V0 = np.full(X.shape[0], dp_body ** 2 if dim == 2 else dp_body ** 3)
-        st = ParticleArrays.from_reference(X, V0, mat.rho0)
+        if lean:
+            # large synthetic runs: no host (n,3,3) tensors; the device owns
+            # F / S / Cp and mirrors them only when asked
+            n = X.shape[0]
+            st = ParticleArrays(X=X, u=np.zeros((n, 3)), v=np.zeros((n, 3)), a=np.zeros((n, 3)),
+                                m0=mat.rho0 * V0, V0=V0, F=None, S=None, s=np.ones(n),
+                                sdot=np.zeros(n), sddot=np.zeros(n), Hhist=np.zeros(n), Cp=None,
+                                epbar=np.zeros(n), psi_e=np.zeros(n), psi_plus=np.zeros(n))
+        else:
+            st = ParticleArrays.from_reference(X, V0, mat.rho0)
         h = spec["coefh"] * dp_body * math.sqrt(dim)   # kernel_geom.py:21-27
         body = Body(mk=bspec["mk"], state=st, material=mat, dp_body=dp_body, h=h, dim=dim,
                     fracture=frac, notches=[Quad(points=q) for q in bspec["notches"]],

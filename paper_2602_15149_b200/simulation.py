@@ -45,8 +45,9 @@ def _torch():
 class DeviceBody:
     """Device buffers and the tl_body descriptor of one body."""
 
-    def __init__(self, body, config, precision, programs):
+    def __init__(self, body, config, precision, programs, mirrors=True):
         torch = _torch()
+        self.mirrors = mirrors
         self.body = body
         st = body.state
         n = int(st.X.shape[0])
@@ -89,10 +90,11 @@ class DeviceBody:
         self.epbar = z(n)
         self.a = z(3, n)
         f64 = lambda *shape: torch.zeros(shape, dtype=torch.float64, device=dev)  # noqa: E731
-        self.F_out = f64(n, 3, 3)
-        self.S_out = f64(n, 3, 3)
-        self.psi_out = f64(n)
-        self.psip_out = f64(n)
+        # FP64 host-layout mirrors of F, S, psi (written only on output steps)
+        self.F_out = f64(n, 3, 3) if mirrors else None
+        self.S_out = f64(n, 3, 3) if mirrors else None
+        self.psi_out = f64(n) if mirrors else None
+        self.psip_out = f64(n) if mirrors else None
         self.counters = torch.zeros(N_COUNTERS, dtype=torch.int64, device=dev)
         self.red = torch.zeros(2, dtype=torch.int64, device=dev)
         self.nblocks = int(_lib.lib().tl_pass_blocks(n))
@@ -227,7 +229,7 @@ class DeviceBody:
         for name, arr in (("sdot", st.sdot), ("sddot", st.sddot), ("Hh", st.Hhist),
                           ("epbar", st.epbar)):
             getattr(self, name).copy_(torch.from_numpy(np.asarray(arr, dtype=np.float64)).to(dev, R))
-        if self.body.material.model == Model.J2:
+        if self.body.material.model == Model.J2 and st.Cp is not None:
             Cp = np.asarray(st.Cp, dtype=np.float64)
             cpd = np.stack([Cp[:, 0, 0] - 1.0, Cp[:, 1, 1] - 1.0, Cp[:, 2, 2] - 1.0,
                             Cp[:, 0, 1], Cp[:, 0, 2], Cp[:, 1, 2]])
@@ -244,13 +246,13 @@ class DeviceBody:
         st.sddot[...] = self.sddot.double().cpu().numpy()
         st.Hhist[...] = self.Hh.double().cpu().numpy()
         st.epbar[...] = self.epbar.double().cpu().numpy()
-        if full:
+        if full and self.mirrors:
             st.a[...] = self.a.double().cpu().numpy().T
             st.F[...] = self.F_out.cpu().numpy()
             st.S[...] = self.S_out.cpu().numpy()
             st.psi_e[...] = self.psi_out.cpu().numpy()
             st.psi_plus[...] = self.psip_out.cpu().numpy()
-        if self.body.material.model == Model.J2:
+        if self.body.material.model == Model.J2 and st.Cp is not None:
             c = self.Cpd.double().cpu().numpy()
             Cp = np.empty((self.n, 3, 3))
             Cp[:, 0, 0], Cp[:, 1, 1], Cp[:, 2, 2] = 1.0 + c[0], 1.0 + c[1], 1.0 + c[2]
@@ -325,7 +327,7 @@ class ProgramTable:
 class DeviceSimulation:
     """Drop-in for solidsph.stepper.Simulation running on one B200."""
 
-    def __init__(self, config, trace=None, precision="fp64", stream=None):
+    def __init__(self, config, trace=None, precision="fp64", stream=None, mirrors=True):
         if precision not in ("fp32", "fp64"):
             raise ValueError("precision must be 'fp32' or 'fp64'")
         L = _lib.lib()  # fails loudly without the native library / GPU
@@ -346,7 +348,8 @@ class DeviceSimulation:
                 "multi-body cases need the penalty contact phase, which is not on the "
                 "device yet (SURVEY.md 8(f) rank 3)")
         self.programs = ProgramTable()
-        self.dbodies = [DeviceBody(b, config, precision, self.programs) for b in self.bodies]
+        self.dbodies = [DeviceBody(b, config, precision, self.programs, mirrors)
+                        for b in self.bodies]
         prog_table = self.programs.upload()
         self.clock_dev = torch.zeros(C.sizeof(_lib.tl_clock), dtype=torch.uint8,
                                      device="cuda")
@@ -514,6 +517,49 @@ class DeviceSimulation:
             cand = cfl * min(dtv, math.sqrt(h / amax)) if amax > 0.0 else cfl * dtv
             dt = min(dt, cand)
         return dt
+
+    def advance(self, nsteps, pass_events=None):
+        """Launch exactly ``nsteps`` device-clock steps (adaptive dt, or the
+        override) with no host synchronisation; the throughput entry point.
+        ``pass_events``: optional list that receives (ev_a0, ev_a1, ev_b0, ev_b1)
+        CUDA events around pass A and pass B of every step."""
+        if not self._initialized:
+            self.initialize()
+        cfg = self.config
+        verlet = int(cfg.step_algorithm) != 2
+        dto = -1.0 if cfg.dt_override is None else float(cfg.dt_override)
+        self._set_clock(t=self.t, next_out=math.inf, t_max=math.inf, eps=0.0, dt_override=dto)
+        torch = _torch()
+        for _ in range(nsteps):
+            _lib.check(self._lib.tl_clock_begin(self._st(), _lib.ptr(self.clock_dev),
+                                                 len(self.dbodies), self._dt_arr), "clock")
+            if pass_events is None:
+                self._launch_step(verlet)
+            else:
+                ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+                if not verlet:
+                    for db in self.dbodies:
+                        _lib.check(self._lib.tl_predict(self._st(), C.byref(db.desc)), "predict")
+                ev[0].record(self.stream)
+                for db in self.dbodies:
+                    self._pass_a(db)
+                ev[1].record(self.stream)
+                ev[2].record(self.stream)
+                for db in self.dbodies:
+                    self._pass_b(db, 1 if verlet else 2)
+                ev[3].record(self.stream)
+                pass_events.append(ev)
+            _lib.check(self._lib.tl_clock_commit(self._st(), _lib.ptr(self.clock_dev)), "commit")
+        self.step_index += nsteps
+
+    def finish_advance(self):
+        """Sync point after advance(): read the clock back, raise errors."""
+        c = self._get_clock()
+        self.t = float(c.t)
+        self.step_index = int(c.step)
+        self._check_errors()
+        if c.halted == 4:
+            raise SimulationError(f"timestep collapsed to {c.dt!r}")
 
     def run(self, time_max=None, time_out=None, on_output=None, max_steps=None, batch=64):
         """Advance to time_max with on_output at t=0, every time_out boundary
