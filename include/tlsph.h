@@ -161,12 +161,38 @@ int tl_adjacency_expand(tl_stream_t st, int64_t n, const int64_t* indptr,
 
 /* Sliced-ELL (32 particles per slice, lane-interleaved) copy of the CSR for
  * coalesced neighbour-index loads in the fused step kernels.
- * tl_sell_lengths: slen[w] = max row length in slice w (device int32[nw]).
+ * tl_sell_lengths: slen[w] = max row length in slice w rounded up to a
+ * multiple of TL_SELL_GROUP (device int32[nw]).
  * tl_sell_fill: soff (device int64[nw+1], exclusive scan of 32*slen), sidx
- * (device int32[soff[nw]]), padding = -1. */
+ * (device int32[soff[nw]]); padding slots hold the row's own index, whose
+ * pair terms vanish exactly (r0 = 0). */
+#define TL_SELL_GROUP 4
 int tl_sell_lengths(tl_stream_t st, int64_t n, const int64_t* indptr, int32_t* slen);
 int tl_sell_fill(tl_stream_t st, int64_t n, const int64_t* indptr, const int32_t* indices,
                  const int64_t* soff, int32_t* sidx);
+
+/* ---------------------------------------------------------------------------
+ * Device particle order and neighbour tiles (tiles.cu).  The step kernels
+ * run on particles sorted along a Morton curve of their cells so a CTA's
+ * neighbours are its own members plus a thin halo staged in shared memory.
+ * Rows keep ascending ORIGINAL partner order: sums match the reference's.
+ * ------------------------------------------------------------------------- */
+/* perm[p] = original index at device position p, iperm its inverse */
+int tl_reorder(tl_stream_t st, int64_t n, const double* X, const double* lo, double cell,
+               int32_t* perm, int32_t* iperm);
+int tl_csr_permute_counts(tl_stream_t st, int64_t n, const int32_t* perm, const int64_t* indptr,
+                          int64_t* counts);
+int tl_csr_permute(tl_stream_t st, int64_t n, const int32_t* perm, const int32_t* iperm,
+                   const int64_t* indptr, const int32_t* indices, const int64_t* indptr_new,
+                   int32_t* indices_new);
+/* halo of every tile of T particles (capacity nnz); tile_count[ntile];
+ * *n_halo = total (host) */
+int tl_tile_halo(tl_stream_t st, int64_t n, int32_t T, const int64_t* indptr,
+                 const int32_t* indices, int64_t nnz, int32_t* halo, int64_t* tile_count,
+                 int64_t* n_halo);
+int tl_tile_slots(tl_stream_t st, int64_t n, int32_t T, int32_t G, const int64_t* indptr,
+                  const int32_t* indices, const int64_t* hoff, const int32_t* halo,
+                  const int64_t* soff, uint16_t* slots);
 
 /* ---------------------------------------------------------------------------
  * Fused device-resident step (stepper.py:77-209, dynamics.py:28-217,
@@ -221,7 +247,7 @@ typedef struct {
     int32_t dim, model, fracture, visc, precision /* 4 | 8 */, kind;
     int32_t uniform, write_out, store_a, nbc, mk, restrict_prog;
     int32_t bc_whole;       /* some BC targets the whole body */
-    int32_t pad0;
+    int32_t unroll;         /* gather group (1 = plain loop, 2, 4); 0 = default */
     /* material / kernel constants (core.py:95-139) */
     double h, inv_h, alpha, rho0, lam, mu, kappa, c0, beta1, beta2;
     double Gc, eps0, s_l, sigma_y0, H_hard, V0c, m0c, dp_body, jac_tol;
@@ -229,6 +255,14 @@ typedef struct {
     /* neighbours: sliced ELL, 32 particles per slice, lane-interleaved */
     const int64_t* soff;
     const int32_t* sidx;
+    /* shared-memory tiles (tile > 0): CTA = `tile` consecutive particles;
+     * hoff[t]..hoff[t+1] indexes its halo particles in `halo`; slots are
+     * uint16 local indices (member p - t*tile, or tile + halo position),
+     * grouped TL_SELL_GROUP per lane, same slice offsets as sidx */
+    int32_t tile, hmax;
+    const int64_t* hoff;
+    const int32_t* halo;
+    const uint16_t* slots;
     /* geometry */
     const double* Xs;       /* FP64 planes x,y,z */
     const void* L;          /* 9 planes, correction matrix L_i */
@@ -250,6 +284,8 @@ typedef struct {
     double* S_out;
     double* psi_out;
     double* psip_out;
+    const int32_t* perm;    /* device order -> caller's particle index (NULL = identity);
+                               error words report caller indices */
     /* boundary conditions */
     const uint32_t* bcmask;
     const tl_bc* bcs;       /* device array of nbc */

@@ -12,7 +12,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtlsph.so")
+LIB_PATH = os.environ.get("TLSPH_LIB", os.path.join(HERE, "libtlsph.so"))
 ABI_VERSION = 1
 
 _lib = None
@@ -67,15 +67,17 @@ _BODY_FIELDS = [
     ("dim", I32), ("model", I32), ("fracture", I32), ("visc", I32), ("precision", I32),
     ("kind", I32),
     ("uniform", I32), ("write_out", I32), ("store_a", I32), ("nbc", I32), ("mk", I32),
-    ("restrict_prog", I32), ("bc_whole", I32), ("pad0", I32),
+    ("restrict_prog", I32), ("bc_whole", I32), ("unroll", I32),
 ]
 _BODY_FIELDS += [(k, D) for k in ("h", "inv_h", "alpha", "rho0", "lam", "mu", "kappa", "c0",
                                   "beta1", "beta2", "Gc", "eps0", "s_l", "sigma_y0", "H_hard",
                                   "V0c", "m0c", "dp_body", "jac_tol")]
 _BODY_FIELDS += [("f0", D * 3)]
-_BODY_FIELDS += [(k, P) for k in ("soff", "sidx", "Xs", "L", "V0", "m0", "us", "rb", "v", "al",
+_BODY_FIELDS += [("soff", P), ("sidx", P), ("tile", I32), ("hmax", I32), ("hoff", P),
+                 ("halo", P), ("slots", P)]
+_BODY_FIELDS += [(k, P) for k in ("Xs", "L", "V0", "m0", "us", "rb", "v", "al",
                                   "sdot", "sddot", "Hh", "Cpd", "epbar", "a", "F_out", "S_out",
-                                  "psi_out", "psip_out", "bcmask", "bcs", "progs", "clock", "red",
+                                  "psi_out", "psip_out", "perm", "bcmask", "bcs", "progs", "clock", "red",
                                   "counters", "pw_partial")]
 
 
@@ -107,6 +109,11 @@ _SIGS = {
     "tl_adjacency_expand": (INT, [P, I64, P, P, P, P, D, D, INT, P, P, P, P, P, P]),
     "tl_sell_lengths": (INT, [P, I64, P, P]),
     "tl_sell_fill": (INT, [P, I64, P, P, P, P]),
+    "tl_reorder": (INT, [P, I64, P, P, D, P, P]),
+    "tl_csr_permute_counts": (INT, [P, I64, P, P, P]),
+    "tl_csr_permute": (INT, [P, I64, P, P, P, P, P, P]),
+    "tl_tile_halo": (INT, [P, I64, I32, P, P, I64, P, P, C.POINTER(I64)]),
+    "tl_tile_slots": (INT, [P, I64, I32, I32, P, P, P, P, P, P]),
     "tl_pass_a": (INT, [P, C.POINTER(tl_body)]),
     "tl_pass_b": (INT, [P, C.POINTER(tl_body), INT]),
     "tl_predict": (INT, [P, C.POINTER(tl_body)]),

@@ -18,7 +18,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libtlsph.so")
-SOURCES = ["plugin.cu", "neighbors.cu", "step.cu"]
+SOURCES = ["plugin.cu", "neighbors.cu", "tiles.cu", "step.cu"]
 HEADERS = ["tl_common.cuh", "expr_vm.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -39,33 +39,41 @@ def needs_build():
     return any(os.path.getmtime(f) > t for f in _deps())
 
 
-def _compile(src, obj):
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+def _compile(src, obj, defines=()):
+    cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src),
+           "-o", obj]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{res.stderr}")
     return res.stderr
 
 
-def build(force=False, verbose=False):
-    if not force and not needs_build():
-        return LIB
-    objdir = os.path.join(HERE, "_obj")
+def build(force=False, verbose=False, defines=(), out=None):
+    """Compile and link.  ``defines``/``out`` build tuning variants (e.g.
+    TL_GATHER_B=2 into libtlsph_g2.so) without touching the default library."""
+    lib = out or LIB
+    if not force and not defines and not needs_build():
+        return lib
+    tag = "" if not defines else "_" + "_".join(d.replace("=", "") for d in defines)
+    objdir = os.path.join(HERE, "_obj" + tag)
     os.makedirs(objdir, exist_ok=True)
     objs = [os.path.join(objdir, s.replace(".cu", ".o")) for s in SOURCES]
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
-        logs = list(ex.map(_compile, SOURCES, objs))
+        logs = list(ex.map(lambda a: _compile(a[0], a[1], defines), zip(SOURCES, objs)))
     if verbose:
         for log in logs:
             print(log, file=sys.stderr)
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart_static"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{res.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    outs = [a[6:] for a in sys.argv[1:] if a.startswith("--out=")]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, defines=defs,
+                out=outs[0] if outs else None))

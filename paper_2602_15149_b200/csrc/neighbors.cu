@@ -361,7 +361,9 @@ __global__ void k_sell_len(int64_t n, const int64_t* __restrict__ indptr, int32_
     int len = i < n ? (int)(indptr[i + 1] - indptr[i]) : 0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) len = max(len, __shfl_xor_sync(0xffffffffu, len, o));
-    if ((threadIdx.x & 31) == 0) slen[i >> 5] = len;
+    // slices are a whole number of TL_SELL_GROUP slots so the step kernels
+    // gather neighbours in unconditional groups
+    if ((threadIdx.x & 31) == 0) slen[i >> 5] = (len + TL_SELL_GROUP - 1) / TL_SELL_GROUP * TL_SELL_GROUP;
 }
 
 __global__ void k_sell_fill(int64_t n, const int64_t* __restrict__ indptr,
@@ -376,7 +378,10 @@ __global__ void k_sell_fill(int64_t n, const int64_t* __restrict__ indptr,
     const int64_t slots = (soff[w + 1] - base) / 32;
     const int64_t b = i < n ? indptr[i] : 0;
     const int64_t len = i < n ? indptr[i + 1] - b : 0;
-    for (int64_t k = 0; k < slots; ++k) sidx[base + 32 * k + lane] = k < len ? indices[b + k] : -1;
+    // padding points at the particle itself: r0 = 0 makes every pair term
+    // vanish exactly, so the step kernels need no per-lane bounds test
+    const int32_t self = i < n ? (int32_t)i : 0;
+    for (int64_t k = 0; k < slots; ++k) sidx[base + 32 * k + lane] = k < len ? indices[b + k] : self;
 }
 
 }  // namespace

@@ -38,7 +38,18 @@ using tl::det3;
 using tl::inv3;
 using tl::mm3;
 
-constexpr int kThreads = 256;
+#ifndef TL_THREADS
+#define TL_THREADS 256
+#endif
+// neighbours gathered per group (must divide TL_SELL_GROUP)
+#ifndef TL_GATHER_A
+#define TL_GATHER_A 4
+#endif
+#ifndef TL_GATHER_B
+#define TL_GATHER_B 4
+#endif
+static_assert(TL_SELL_GROUP % TL_GATHER_A == 0 && TL_SELL_GROUP % TL_GATHER_B == 0, "gather group");
+constexpr int kThreads = TL_THREADS;
 
 __device__ __forceinline__ bool halted(const tl_body& b) {
     return b.clock != nullptr && *(volatile int32_t*)&b.clock->halted != 0;
@@ -264,17 +275,161 @@ __device__ __forceinline__ R planeR(const void* p, int64_t stride, int c, int64_
 }
 
 // ---------------------------------------------------------------------------
+// pair terms
+// ---------------------------------------------------------------------------
+template <typename R>
+using V4 = typename tl::Vec4<R>::T;
+
+// pass A pair: D += V0_j fac du (x) r0 ; M += 2 (s_i - s_j) V0_j fac / r^2 r0 r0^T
+template <typename R, int DIM, bool FRAC, int KIND>
+__device__ __forceinline__ void pair_a(R dx, R dy, R dz, const V4<R>& uj, R vj, const V4<R>& ui,
+                                       bool gated, R inv_h, R a_ih, R* D, R* M) {
+    const R r2 = dx * dx + dy * dy + dz * dz;
+    const R rs = tl::rsqrt_pos(r2);
+    const R wf = vj * tl::kernel_fac<R, KIND>(r2, rs, inv_h, a_ih);
+    if (!gated) {
+        const R du0 = wf * (uj.x - ui.x), du2 = wf * (uj.z - ui.z);
+        D[0] += du0 * dx; D[2] += du0 * dz;
+        D[6] += du2 * dx; D[8] += du2 * dz;
+        if (DIM == 3) {
+            const R du1 = wf * (uj.y - ui.y);
+            D[1] += du0 * dy; D[7] += du2 * dy;
+            D[3] += du1 * dx; D[4] += du1 * dy; D[5] += du1 * dz;
+        }
+    }
+    if (FRAC) {
+        const R c = R(2) * (ui.w - uj.w) * wf * (rs * rs);
+        const R cx = c * dx, cz = c * dz;
+        M[0] += cx * dx; M[2] += cz * dz; M[4] += cx * dz;
+        if (DIM == 3) {
+            const R cy = c * dy;
+            M[1] += cy * dy; M[3] += cx * dy; M[5] += cy * dz;
+        }
+    }
+}
+
+// pass B pair: s1 += m fac r0 ; s2 += m fac PL_j r0 ; s3 += m fac pi_ij r0
+template <typename R, int DIM, int KIND>
+__device__ __forceinline__ void pair_b(R dx, R dy, R dz, const V4<R>& q0, const V4<R>& q1,
+                                       const V4<R>& q2, R mj, R vi0, R vi1, R vi2, bool visc,
+                                       R inv_h, R a_ih, R hR, R eps_h2, R b2, R b1c0, R inv_rho,
+                                       R* s1, R* s2, R* s3) {
+    const R r2 = dx * dx + dy * dy + dz * dz;
+    const R wf = mj * tl::kernel_fac<R, KIND>(r2, tl::rsqrt_pos(r2), inv_h, a_ih);
+    R p0, p1, p2;
+    if (DIM == 3) {
+        p0 = q0.x * dx + q0.y * dy + q0.z * dz;
+        p1 = q0.w * dx + q1.x * dy + q1.y * dz;
+        p2 = q1.z * dx + q1.w * dy + q2.x * dz;
+    } else {
+        p0 = q0.x * dx + q0.z * dz;
+        p1 = R(0);
+        p2 = q1.z * dx + q2.x * dz;
+    }
+    s1[0] += wf * dx; s1[2] += wf * dz;
+    s2[0] += wf * p0; s2[2] += wf * p2;
+    if (DIM == 3) {
+        s1[1] += wf * dy;
+        s2[1] += wf * p1;
+    }
+    if (visc) {
+        const R dvr = (vi0 - q2.y) * dx + (DIM == 3 ? (vi1 - q2.z) * dy : R(0)) + (vi2 - q2.w) * dz;
+        const R Gv = hR * dvr / (r2 + eps_h2);
+        const R pw = (b2 * Gv * Gv - b1c0 * Gv) * inv_rho * wf;
+        s3[0] += pw * dx; s3[2] += pw * dz;
+        if (DIM == 3) s3[1] += pw * dy;
+    }
+}
+
+// G neighbour slots of this lane in the group-interleaved tiled layout
+template <int G>
+__device__ __forceinline__ void load_slots(const uint16_t* p, int* out) {
+    if (G == 4) {
+        const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
+        out[0] = v.x & 0xffff; out[1] = v.x >> 16; out[2] = v.y & 0xffff; out[3] = v.y >> 16;
+    } else if (G == 2) {
+        const uint32_t v = __ldg(reinterpret_cast<const uint32_t*>(p));
+        out[0] = v & 0xffff; out[1] = v >> 16;
+    } else {
+        out[0] = __ldg(p);
+    }
+}
+
+// shared-memory tile of a CTA: positions (FP32: relative to the tile
+// origin, FP64: absolute) and the gathered record of every member and halo
+// particle, staged with coalesced loads once per CTA
+template <typename R, int NREC>
+struct Tile {
+    R* x;
+    R* y;
+    R* z;
+    V4<R>* rec;   // NREC records of 4 per particle
+    R* m;         // V0 or m0 when not uniform
+    int S;
+};
+
+template <typename R, int NREC>
+__device__ __forceinline__ Tile<R, NREC> tile_layout(unsigned char* smem, int S) {
+    Tile<R, NREC> t;
+    t.S = S;
+    t.rec = reinterpret_cast<V4<R>*>(smem);
+    t.x = reinterpret_cast<R*>(t.rec + NREC * S);
+    t.y = t.x + S;
+    t.z = t.y + S;
+    t.m = t.z + S;
+    return t;
+}
+
+template <typename R, int NREC>
+__device__ __forceinline__ void stage_tile(const tl_body& b, Tile<R, NREC>& t, int64_t p0, int T,
+                                           int H, int64_t hb, const R* src, const double* mass,
+                                           bool uni, double ox, double oy, double oz) {
+    const int64_t N = b.n_all;
+    for (int s = threadIdx.x; s < T + H; s += blockDim.x) {
+        int64_t q = s < T ? p0 + s : (int64_t)b.halo[hb + s - T];
+        if (s < T && q >= b.n) q = p0;   // tail of the last tile: any valid particle
+        t.x[s] = R(b.Xs[q] - ox);
+        t.y[s] = R(b.Xs[N + q] - oy);
+        t.z[s] = R(b.Xs[2 * N + q] - oz);
+#pragma unroll
+        for (int r = 0; r < NREC; ++r) t.rec[r * t.S + s] = tl::ldg4(src + 4 * NREC * q + 4 * r);
+        if (!uni) t.m[s] = R(mass[q]);
+    }
+    __syncthreads();
+}
+
+template <typename R, int NREC>
+__host__ __device__ constexpr size_t tile_bytes(int S) {
+    return (size_t)S * (NREC * sizeof(V4<R>) + 4 * sizeof(R));
+}
+
+// ---------------------------------------------------------------------------
 // pass A
 // ---------------------------------------------------------------------------
-template <typename R, int DIM, int MODEL, bool FRAC>
+template <typename R, int DIM, int MODEL, bool FRAC, int KIND, int G, bool TILED>
 __global__ void __launch_bounds__(kThreads) k_pass_a(const tl_body b) {
+    extern __shared__ __align__(16) unsigned char smem[];
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     __shared__ double s_pw[kThreads / 32];
     double pw = 0.0;
     if (halted(b)) return;
+    const R* us = static_cast<const R*>(b.us);
+    const bool uni = b.uniform != 0;
+    // tile staging (TILED): every thread of the CTA takes part
+    Tile<R, 1> tl_;
+    double ox = 0.0, oy = 0.0, oz = 0.0;
+    if (TILED) {
+        const int64_t p0 = (int64_t)blockIdx.x * blockDim.x;
+        const int64_t hb = b.hoff[blockIdx.x];
+        const int H = (int)(b.hoff[blockIdx.x + 1] - hb);
+        if (sizeof(R) == 4) {
+            ox = b.Xs[p0]; oy = b.Xs[b.n_all + p0]; oz = b.Xs[2 * b.n_all + p0];
+        }
+        tl_ = tile_layout<R, 1>(smem, blockDim.x + H);
+        stage_tile<R, 1>(b, tl_, p0, blockDim.x, H, hb, us, b.V0, uni, ox, oy, oz);
+    }
     if (i < b.n) {
         const int64_t N = b.n_all;
-        const R* us = static_cast<const R*>(b.us);
         const int lane = (int)(i & 31);
         const int64_t w = i >> 5;
         const int64_t base = b.soff[w];
@@ -283,42 +438,56 @@ __global__ void __launch_bounds__(kThreads) k_pass_a(const tl_body b) {
         const auto ui = tl::ld4(us + 4 * i);
         const R si = ui.w;
         const bool gated = FRAC && si <= R(b.s_l);
-        const R inv_h = R(b.inv_h), alpha = R(b.alpha);
+        const R inv_h = R(b.inv_h), a_ih = R(b.alpha * b.inv_h);
         R D[9];
 #pragma unroll
         for (int q = 0; q < 9; ++q) D[q] = R(0);
         R M[6] = {R(0), R(0), R(0), R(0), R(0), R(0)};   // xx yy zz xy xz yz
-        const int32_t* sidx = b.sidx + base + lane;
-        for (int k = 0; k < len; ++k) {
-            const int32_t j = __ldg(sidx + 32 * k);
-            if (j < 0) break;
-            const R dx = R(xi - __ldg(b.Xs + j));
-            const R dy = DIM == 3 ? R(yi - __ldg(b.Xs + N + j)) : R(0);
-            const R dz = R(zi - __ldg(b.Xs + 2 * N + j));
-            const R r2 = dx * dx + dy * dy + dz * dz;
-            const R r = sqrt(r2);
-            const R fac = tl::kernel_fac(r, inv_h, alpha, b.kind);
-            const auto uj = tl::ldg4(us + 4 * (int64_t)j);
-            const R vj = b.uniform ? R(b.V0c) : R(b.V0[j]);
-            const R wf = vj * fac;
-            if (!gated) {
-                const R du0 = wf * (uj.x - ui.x), du2 = wf * (uj.z - ui.z);
-                D[0] += du0 * dx; D[2] += du0 * dz;
-                D[6] += du2 * dx; D[8] += du2 * dz;
-                if (DIM == 3) {
-                    const R du1 = wf * (uj.y - ui.y);
-                    D[1] += du0 * dy; D[7] += du2 * dy;
-                    D[3] += du1 * dx; D[4] += du1 * dy; D[5] += du1 * dz;
+        const R V0c = R(b.V0c);
+        if (TILED) {
+            const int me = threadIdx.x;
+            const R xl = tl_.x[me], yl = tl_.y[me], zl = tl_.z[me];
+            const uint16_t* sl = b.slots + base + lane * G;
+            for (int k = 0; k < len; k += G) {
+                int l[G];
+                load_slots<G>(sl + k * 32, l);
+#pragma unroll
+                for (int q = 0; q < G; ++q) {
+                    const int j = l[q];
+                    const R vj = uni ? V0c : tl_.m[j];
+                    pair_a<R, DIM, FRAC, KIND>(xl - tl_.x[j], DIM == 3 ? yl - tl_.y[j] : R(0),
+                                               zl - tl_.z[j], tl_.rec[j], vj, ui, gated, inv_h,
+                                               a_ih, D, M);
                 }
             }
-            if (FRAC) {
-                const R c = r2 > R(0) ? R(2) * (si - uj.w) * wf / r2 : R(0);
-                const R cx = c * dx, cz = c * dz;
-                M[0] += cx * dx; M[2] += cz * dz; M[4] += cx * dz;
-                if (DIM == 3) {
-                    const R cy = c * dy;
-                    M[1] += cy * dy; M[3] += cx * dy; M[5] += cy * dz;
+        } else {
+            const int32_t* sidx = b.sidx + base + lane;
+            const double* __restrict__ Xp = b.Xs;
+            const double* __restrict__ Yp = b.Xs + N;
+            const double* __restrict__ Zp = b.Xs + 2 * N;
+            // neighbours in groups of G: all index loads, then all gathers, then
+            // the math, so each warp keeps 2G independent loads in flight
+            for (int k = 0; k < len; k += G) {
+                int32_t jj[G];
+#pragma unroll
+                for (int q = 0; q < G; ++q) jj[q] = __ldg(sidx + 32 * (k + q));
+                double xj[G], yj[G], zj[G];
+                V4<R> uj[G];
+                R vj[G];
+#pragma unroll
+                for (int q = 0; q < G; ++q) {
+                    xj[q] = __ldg(Xp + jj[q]);
+                    yj[q] = DIM == 3 ? __ldg(Yp + jj[q]) : 0.0;
+                    zj[q] = __ldg(Zp + jj[q]);
+                    uj[q] = tl::ldg4(us + 4 * (int64_t)jj[q]);
+                    vj[q] = V0c;
+                    if (!uni) vj[q] = R(__ldg(b.V0 + jj[q]));
                 }
+#pragma unroll
+                for (int q = 0; q < G; ++q)
+                    pair_a<R, DIM, FRAC, KIND>(R(xi - xj[q]), DIM == 3 ? R(yi - yj[q]) : R(0),
+                                               R(zi - zj[q]), uj[q], vj[q], ui, gated, inv_h, a_ih,
+                                               D, M);
             }
         }
         // L_i (9 planes)
@@ -352,7 +521,7 @@ __global__ void __launch_bounds__(kThreads) k_pass_a(const tl_body b) {
             for (int q = 0; q < 6; ++q) Cpd[q] = double(planeR<R>(b.Cpd, N, q, i));
             double epb = double(static_cast<const R*>(b.epbar)[i]);
             bad = j2_update(Fd, Cpd, epb, b.mu, b.kappa, b.sigma_y0, b.H_hard, Sd, psid, dwp, nonspd);
-            if (nonspd) atomicMin((long long*)&b.counters[2], (long long)i);
+            if (nonspd) atomicMin((long long*)&b.counters[2], (long long)(b.perm ? b.perm[i] : i));
 #pragma unroll
             for (int q = 0; q < 6; ++q) static_cast<R*>(b.Cpd)[q * N + i] = R(Cpd[q]);
             static_cast<R*>(b.epbar)[i] = R(epb);
@@ -440,7 +609,7 @@ __global__ void __launch_bounds__(kThreads) k_pass_a(const tl_body b) {
         __syncthreads();
         if (threadIdx.x == 0) {
             double t = 0.0;
-            for (int k = 0; k < kThreads / 32; ++k) t += s_pw[k];
+            for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += s_pw[k];
             b.pw_partial[blockIdx.x] = t;
         }
     }
@@ -449,12 +618,15 @@ __global__ void __launch_bounds__(kThreads) k_pass_a(const tl_body b) {
 // ---------------------------------------------------------------------------
 // boundary conditions (dynamics.py:159-217, fracture.py:46-83)
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void make_vars(tl::ExprVars& V, double x0, double y0, double z0,
-                                          double ux, double uy, double uz, double t, double dt,
+struct D3 {
+    double x, y, z;
+};
+
+__device__ __forceinline__ void make_vars(tl::ExprVars& V, D3 X0, D3 u, double t, double dt,
                                           double dx) {
-    V.v[0] = x0; V.v[1] = y0; V.v[2] = z0;
-    V.v[3] = x0 + ux; V.v[4] = y0 + uy; V.v[5] = z0 + uz;
-    V.v[6] = ux; V.v[7] = uy; V.v[8] = uz;
+    V.v[0] = X0.x; V.v[1] = X0.y; V.v[2] = X0.z;
+    V.v[3] = X0.x + u.x; V.v[4] = X0.y + u.y; V.v[5] = X0.z + u.z;
+    V.v[6] = u.x; V.v[7] = u.y; V.v[8] = u.z;
     V.v[9] = t; V.v[10] = dt; V.v[11] = dx;
 }
 
@@ -481,10 +653,16 @@ __device__ __forceinline__ bool bc_applies(const tl_bc& c, uint32_t mask, double
     return c.bit < 0 || ((mask >> c.bit) & 1u);
 }
 
-// add force BCs active at t to acc (in file order).  Out of line so the
-// evaluator's stack frame never competes with the gather loop's registers.
-__device__ __noinline__ void force_bcs(const BcCtx b, uint32_t mask, double m0i, const tl::ExprVars& V,
-                          double t, double* acc) {
+// The BC evaluators are out of line and take / return plain values: the
+// evaluator's stack lives in their own frames and the step kernels touch no
+// local memory unless a particle actually carries a boundary condition.
+
+// acc + force BCs active at t (file order), dynamics.py:159-190
+__device__ __noinline__ D3 force_bcs(const BcCtx b, uint32_t mask, double m0i, D3 X0, D3 u,
+                                     double t, double dt, D3 acc) {
+    tl::ExprVars V;
+    make_vars(V, X0, u, t, dt, b.dp_body);
+    double a[3] = {acc.x, acc.y, acc.z};
     for (int k = 0; k < b.nbc; ++k) {
         const tl_bc c = b.bcs[k];
         if (c.kind != 1 || !bc_applies(c, mask, t)) continue;
@@ -493,21 +671,26 @@ __device__ __noinline__ void force_bcs(const BcCtx b, uint32_t mask, double m0i,
         else if (c.ftype == 2) scale = (b.dim == 3 ? b.dp_body * b.dp_body : b.dp_body) / m0i;
         for (int ax = 0; ax < 3; ++ax) {
             if (c.has_const[ax]) {
-                acc[ax] = tl::add_rn(acc[ax], tl::mul_rn(c.cval[ax], scale));
+                a[ax] = tl::add_rn(a[ax], tl::mul_rn(c.cval[ax], scale));
             } else if (c.prog[ax] >= 0) {
                 bool skip;
                 int err = 0;
                 const double val = tl::expr_eval(b.progs[c.prog[ax]], V, &skip, &err);
                 note_err(b, err);
-                acc[ax] = tl::add_rn(acc[ax], skip ? 0.0 : tl::mul_rn(val, scale));
+                a[ax] = tl::add_rn(a[ax], skip ? 0.0 : tl::mul_rn(val, scale));
             }
         }
     }
+    return D3{a[0], a[1], a[2]};
 }
 
-// overwrite velocity components from velocity BCs active at t (file order)
-__device__ __noinline__ void velocity_bcs(const BcCtx b, uint32_t mask, const tl::ExprVars& V, double t,
-                             double* vel) {
+// velocity components overwritten by velocity BCs active at t (file order),
+// dynamics.py:193-217
+__device__ __noinline__ D3 velocity_bcs(const BcCtx b, uint32_t mask, D3 X0, D3 u, double t,
+                                        double dt, D3 vin) {
+    tl::ExprVars V;
+    make_vars(V, X0, u, t, dt, b.dp_body);
+    double vel[3] = {vin.x, vin.y, vin.z};
     for (int k = 0; k < b.nbc; ++k) {
         const tl_bc c = b.bcs[k];
         if (c.kind != 0 || !bc_applies(c, mask, t)) continue;
@@ -524,27 +707,36 @@ __device__ __noinline__ void velocity_bcs(const BcCtx b, uint32_t mask, const tl
         }
     }
     if (b.dim == 2) vel[1] = 0.0;
+    return D3{vel[0], vel[1], vel[2]};
+}
+
+// restrictphi floor (fracture.py:46-63); returns the floor or -1 for skip
+__device__ __noinline__ double restrict_floor(const BcCtx b, D3 X0, D3 u, double t, double dt) {
+    tl::ExprVars V;
+    make_vars(V, X0, u, t, dt, b.dp_body);
+    bool skip;
+    int err = 0;
+    const double val = tl::expr_eval(b.progs[b.restrict_prog], V, &skip, &err);
+    note_err(b, err);
+    if (skip) return -1.0;
+    if (val < 0.0 || val > 1.0) atomicExch((unsigned long long*)&b.counters[5], 1ull);
+    return val;
 }
 
 // sdot += dtr*sddot; s += dts*sdot; clamp [0,1]; restrictphi floor
+// (stepper.py:125-130, fracture.py:66-83)
 template <typename R>
-__device__ __forceinline__ void advance_phase(const BcCtx& b, R& s, R& sd, R sdd, double dts,
-                                              double dtr, const tl::ExprVars& V) {
+__device__ __forceinline__ void advance_phase(const tl_body& b, R& s, R& sd, R sdd, double dts,
+                                              double dtr, D3 X0, D3 u, double t, double dt) {
     sd = tl::axpy_rn(sd, R(dtr), sdd);
     s = tl::axpy_rn(s, R(dts), sd);
     if (s < R(0)) { s = R(0); sd = R(0); }
     if (s > R(1)) { s = R(1); sd = R(0); }
     if (b.restrict_prog >= 0) {
-        bool skip;
-        int err = 0;
-        const double val = tl::expr_eval(b.progs[b.restrict_prog], V, &skip, &err);
-        note_err(b, err);
-        if (!skip) {
-            if (val < 0.0 || val > 1.0) atomicExch((unsigned long long*)&b.counters[5], 1ull);
-            if (double(s) < val) {
-                s = R(val);
-                sd = R(0);
-            }
+        const double fl = restrict_floor(bc_ctx(b), X0, u, t, dt);
+        if (fl >= 0.0 && double(s) < fl) {
+            s = R(fl);
+            sd = R(0);
         }
     }
 }
@@ -557,15 +749,29 @@ __device__ __forceinline__ double sq3_rn(double x, double y, double z) {
 // ---------------------------------------------------------------------------
 // pass B
 // ---------------------------------------------------------------------------
-template <typename R, int DIM, int MODE, bool FRAC>
+template <typename R, int DIM, int MODE, bool FRAC, int KIND, int G, bool TILED>
 __global__ void __launch_bounds__(kThreads) k_pass_b(const tl_body b) {
+    extern __shared__ __align__(16) unsigned char smem[];
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (halted(b)) return;
     double v2 = 0.0, a2 = 0.0;
     long long bad_acc = LLONG_MAX;
+    const R* rbp = static_cast<const R*>(b.rb);
+    const bool uni = b.uniform != 0;
+    Tile<R, 3> tl_;
+    if (TILED) {
+        const int64_t p0 = (int64_t)blockIdx.x * blockDim.x;
+        const int64_t hb = b.hoff[blockIdx.x];
+        const int H = (int)(b.hoff[blockIdx.x + 1] - hb);
+        double ox = 0.0, oy = 0.0, oz = 0.0;
+        if (sizeof(R) == 4) {
+            ox = b.Xs[p0]; oy = b.Xs[b.n_all + p0]; oz = b.Xs[2 * b.n_all + p0];
+        }
+        tl_ = tile_layout<R, 3>(smem, blockDim.x + H);
+        stage_tile<R, 3>(b, tl_, p0, blockDim.x, H, hb, rbp, b.m0, uni, ox, oy, oz);
+    }
     if (i < b.n) {
         const int64_t N = b.n_all;
-        const R* rbp = static_cast<const R*>(b.rb);
         const int lane = (int)(i & 31);
         const int64_t w = i >> 5;
         const int64_t base = b.soff[w];
@@ -575,49 +781,60 @@ __global__ void __launch_bounds__(kThreads) k_pass_b(const tl_body b) {
         const auto r1i = tl::ld4(rbp + 12 * i + 4);
         const auto r2i = tl::ld4(rbp + 12 * i + 8);
         const R vi0 = r2i.y, vi1 = r2i.z, vi2 = r2i.w;
-        const R inv_h = R(b.inv_h), alpha = R(b.alpha);
+        const R inv_h = R(b.inv_h), a_ih = R(b.alpha * b.inv_h);
         const bool visc = b.visc != 0;
         const R eps_h2 = R(0.001 * b.h * b.h);
         const R hR = R(b.h), b1c0 = R(b.beta1 * b.c0), b2 = R(b.beta2), inv_rho = R(1.0 / b.rho0);
         R s1[3] = {R(0), R(0), R(0)}, s2[3] = {R(0), R(0), R(0)}, s3[3] = {R(0), R(0), R(0)};
-        const int32_t* sidx = b.sidx + base + lane;
-        for (int k = 0; k < len; ++k) {
-            const int32_t j = __ldg(sidx + 32 * k);
-            if (j < 0) break;
-            const R dx = R(xi - __ldg(b.Xs + j));
-            const R dy = DIM == 3 ? R(yi - __ldg(b.Xs + N + j)) : R(0);
-            const R dz = R(zi - __ldg(b.Xs + 2 * N + j));
-            const R r2 = dx * dx + dy * dy + dz * dz;
-            const R fac = tl::kernel_fac(sqrt(r2), inv_h, alpha, b.kind);
-            const R* rj = rbp + 12 * (int64_t)j;
-            const auto q0 = tl::ldg4(rj);
-            const auto q1 = tl::ldg4(rj + 4);
-            const auto q2 = tl::ldg4(rj + 8);
-            const R mj = b.uniform ? R(b.m0c) : R(b.m0[j]);
-            const R wf = mj * fac;
-            // PL_j r0 (row-major PL_j = q0.x..q2.x)
-            R p0, p1, p2;
-            if (DIM == 3) {
-                p0 = q0.x * dx + q0.y * dy + q0.z * dz;
-                p1 = q0.w * dx + q1.x * dy + q1.y * dz;
-                p2 = q1.z * dx + q1.w * dy + q2.x * dz;
-            } else {
-                p0 = q0.x * dx + q0.z * dz;
-                p1 = R(0);
-                p2 = q1.z * dx + q2.x * dz;
+        const R m0c = R(b.m0c);
+        if (TILED) {
+            const int me = threadIdx.x;
+            const R xl = tl_.x[me], yl = tl_.y[me], zl = tl_.z[me];
+            const uint16_t* sl = b.slots + base + lane * G;
+            const int S = tl_.S;
+            for (int k = 0; k < len; k += G) {
+                int l[G];
+                load_slots<G>(sl + k * 32, l);
+#pragma unroll
+                for (int q = 0; q < G; ++q) {
+                    const int j = l[q];
+                    const R mj = uni ? m0c : tl_.m[j];
+                    pair_b<R, DIM, KIND>(xl - tl_.x[j], DIM == 3 ? yl - tl_.y[j] : R(0),
+                                         zl - tl_.z[j], tl_.rec[j], tl_.rec[S + j],
+                                         tl_.rec[2 * S + j], mj, vi0, vi1, vi2, visc, inv_h, a_ih,
+                                         hR, eps_h2, b2, b1c0, inv_rho, s1, s2, s3);
+                }
             }
-            s1[0] += wf * dx; s1[2] += wf * dz;
-            s2[0] += wf * p0; s2[2] += wf * p2;
-            if (DIM == 3) {
-                s1[1] += wf * dy;
-                s2[1] += wf * p1;
-            }
-            if (visc) {
-                const R dvr = (vi0 - q2.y) * dx + (DIM == 3 ? (vi1 - q2.z) * dy : R(0)) + (vi2 - q2.w) * dz;
-                const R G = hR * dvr / (r2 + eps_h2);
-                const R pw = (b2 * G * G - b1c0 * G) * inv_rho * wf;
-                s3[0] += pw * dx; s3[2] += pw * dz;
-                if (DIM == 3) s3[1] += pw * dy;
+        } else {
+            const int32_t* sidx = b.sidx + base + lane;
+            const double* __restrict__ Xp = b.Xs;
+            const double* __restrict__ Yp = b.Xs + N;
+            const double* __restrict__ Zp = b.Xs + 2 * N;
+            for (int k = 0; k < len; k += G) {
+                int32_t jj[G];
+#pragma unroll
+                for (int q = 0; q < G; ++q) jj[q] = __ldg(sidx + 32 * (k + q));
+                double xj[G], yj[G], zj[G];
+                V4<R> q0[G], q1[G], q2[G];
+                R mj[G];
+#pragma unroll
+                for (int q = 0; q < G; ++q) {
+                    xj[q] = __ldg(Xp + jj[q]);
+                    yj[q] = DIM == 3 ? __ldg(Yp + jj[q]) : 0.0;
+                    zj[q] = __ldg(Zp + jj[q]);
+                    const R* rj = rbp + 12 * (int64_t)jj[q];
+                    q0[q] = tl::ldg4(rj);
+                    q1[q] = tl::ldg4(rj + 4);
+                    q2[q] = tl::ldg4(rj + 8);
+                    mj[q] = m0c;
+                    if (!uni) mj[q] = R(__ldg(b.m0 + jj[q]));
+                }
+#pragma unroll
+                for (int q = 0; q < G; ++q)
+                    pair_b<R, DIM, KIND>(R(xi - xj[q]), DIM == 3 ? R(yi - yj[q]) : R(0),
+                                         R(zi - zj[q]), q0[q], q1[q], q2[q], mj[q], vi0, vi1, vi2,
+                                         visc, inv_h, a_ih, hR, eps_h2, b2, b1c0, inv_rho, s1, s2,
+                                         s3);
             }
         }
         // a_int = (PL_i s1 + s2)/rho0^2 - AL_i s3
@@ -641,39 +858,39 @@ __global__ void __launch_bounds__(kThreads) k_pass_b(const tl_body b) {
         const R* us = static_cast<const R*>(b.us);
         const auto ui = tl::ld4(us + 4 * i);
         const uint32_t mask = b.bcmask ? b.bcmask[i] : 0u;
+        const bool has_bc = b.nbc && (mask || b.bc_whole);
         const double t0 = b.clock ? b.clock->t : 0.0;
         const double dt = b.clock ? b.clock->dt : 0.0;
-        tl::ExprVars V;
-        const double m0i = b.uniform ? b.m0c : b.m0[i];
         const double tf = MODE == TL_B_INIT ? 0.0 : (MODE == TL_B_SYMPL ? t0 + 0.5 * dt : t0);
         const double dtf = MODE == TL_B_INIT ? 0.0 : dt;
-        make_vars(V, xi, yi, zi, double(ui.x), double(ui.y), double(ui.z), tf, dtf, b.dp_body);
-        if (b.nbc && (mask || b.bc_whole)) force_bcs(bc_ctx(b), mask, m0i, V, tf, acc);
+        const D3 X0{xi, yi, zi};
+        const D3 u0{double(ui.x), double(ui.y), double(ui.z)};
+        if (has_bc) {
+            const double m0i = b.uniform ? b.m0c : b.m0[i];
+            const D3 r = force_bcs(bc_ctx(b), mask, m0i, X0, u0, tf, dtf, D3{acc[0], acc[1], acc[2]});
+            acc[0] = r.x; acc[1] = r.y; acc[2] = r.z;
+        }
         if (DIM == 2) acc[1] = 0.0;
         if (!(isfinite(acc[0]) && isfinite(acc[1]) && isfinite(acc[2]))) {
-            bad_acc = (long long)i;
+            bad_acc = (long long)(b.perm ? b.perm[i] : i);
             if (b.clock) atomicMin((long long*)&b.counters[6], (long long)b.clock->step);
         }
         // velocity: v_i is the copy pass A put in the record
-        double vel[3] = {double(vi0), double(vi1), double(vi2)};
+        D3 vel{double(vi0), double(vi1), double(vi2)};
         R us_new[4] = {ui.x, ui.y, ui.z, ui.w};
         R* vout = static_cast<R*>(b.v);
         if (MODE == TL_B_INIT) {
-            if (b.nbc && (mask || b.bc_whole)) velocity_bcs(bc_ctx(b), mask, V, 0.0, vel);
+            if (has_bc) vel = velocity_bcs(bc_ctx(b), mask, X0, u0, 0.0, 0.0, vel);
         } else {
             const double kick = MODE == TL_B_VERLET ? dt : 0.5 * dt;
             const double t_new = t0 + dt;
             // BC phase at the force time, kick, BCs at t_new, drift
-            if (b.nbc && (mask || b.bc_whole)) velocity_bcs(bc_ctx(b), mask, V, tf, vel);
-            R vR[3];
-#pragma unroll
-            for (int a = 0; a < 3; ++a) vR[a] = tl::axpy_rn(R(vel[a]), R(kick), R(acc[a]));
-#pragma unroll
-            for (int a = 0; a < 3; ++a) vel[a] = double(vR[a]);
-            V.v[9] = t_new;
-            if (b.nbc && (mask || b.bc_whole)) velocity_bcs(bc_ctx(b), mask, V, t_new, vel);
-#pragma unroll
-            for (int a = 0; a < 3; ++a) vR[a] = R(vel[a]);
+            if (has_bc) vel = velocity_bcs(bc_ctx(b), mask, X0, u0, tf, dt, vel);
+            vel = D3{double(tl::axpy_rn(R(vel.x), R(kick), R(acc[0]))),
+                     double(tl::axpy_rn(R(vel.y), R(kick), R(acc[1]))),
+                     double(tl::axpy_rn(R(vel.z), R(kick), R(acc[2])))};
+            if (has_bc) vel = velocity_bcs(bc_ctx(b), mask, X0, u0, t_new, dt, vel);
+            const R vR[3] = {R(vel.x), R(vel.y), R(vel.z)};
             us_new[0] = tl::axpy_rn(ui.x, R(kick), vR[0]);
             us_new[1] = DIM == 3 ? tl::axpy_rn(ui.y, R(kick), vR[1]) : R(0);
             us_new[2] = tl::axpy_rn(ui.z, R(kick), vR[2]);
@@ -682,27 +899,27 @@ __global__ void __launch_bounds__(kThreads) k_pass_b(const tl_body b) {
                 R sd = sdp[i];
                 R s = ui.w;
                 const R sdd = static_cast<const R*>(b.sddot)[i];
-                tl::ExprVars Vn;
-                make_vars(Vn, xi, yi, zi, double(us_new[0]), double(us_new[1]), double(us_new[2]),
-                          t_new, dt, b.dp_body);
-                advance_phase<R>(bc_ctx(b), s, sd, sdd, kick, kick, Vn);
+                advance_phase<R>(b, s, sd, sdd, kick, kick, X0,
+                                 D3{double(us_new[0]), double(us_new[1]), double(us_new[2])},
+                                 t_new, dt);
                 us_new[3] = s;
                 sdp[i] = sd;
             }
             tl::st4(static_cast<R*>(b.us) + 4 * i, us_new[0], us_new[1], us_new[2], us_new[3]);
         }
-#pragma unroll
-        for (int a = 0; a < 3; ++a) vout[a * N + i] = R(vel[a]);
+        vout[i] = R(vel.x);
+        vout[N + i] = R(vel.y);
+        vout[2 * N + i] = R(vel.z);
         if (b.store_a || mirror_out(b)) {
             R* ap = static_cast<R*>(b.a);
 #pragma unroll
             for (int a = 0; a < 3; ++a) ap[a * N + i] = R(acc[a]);
         }
         if (MODE != TL_B_INIT && b.clock &&
-            !(isfinite(vel[0]) && isfinite(vel[1]) && isfinite(vel[2]) && isfinite(double(us_new[0])) &&
+            !(isfinite(vel.x) && isfinite(vel.y) && isfinite(vel.z) && isfinite(double(us_new[0])) &&
               isfinite(double(us_new[1])) && isfinite(double(us_new[2]))))
             atomicMin((long long*)&b.counters[7], (long long)b.clock->step + 1);
-        const double vx = double(R(vel[0])), vy = double(R(vel[1])), vz = double(R(vel[2]));
+        const double vx = double(R(vel.x)), vy = double(R(vel.y)), vz = double(R(vel.z));
         const double ax = double(R(acc[0])), ay = double(R(acc[1])), az = double(R(acc[2]));
         v2 = sq3_rn(vx, vy, vz);
         a2 = sq3_rn(ax, ay, az);
@@ -732,22 +949,20 @@ __global__ void __launch_bounds__(kThreads) k_predict(const tl_body b) {
     R* us = static_cast<R*>(b.us);
     const auto ui = tl::ld4(us + 4 * i);
     const double xi = b.Xs[i], yi = b.Xs[N + i], zi = b.Xs[2 * N + i];
-    double vel[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) vel[a] = double(tl::axpy_rn(vp[a * N + i], R(half), ap[a * N + i]));
+    D3 vel{double(tl::axpy_rn(vp[i], R(half), ap[i])), double(tl::axpy_rn(vp[N + i], R(half), ap[N + i])),
+           double(tl::axpy_rn(vp[2 * N + i], R(half), ap[2 * N + i]))};
     const uint32_t mask = b.bcmask ? b.bcmask[i] : 0u;
-    tl::ExprVars V;
-    make_vars(V, xi, yi, zi, double(ui.x), double(ui.y), double(ui.z), th, dt, b.dp_body);
-    if (b.nbc && (mask || b.bc_whole)) velocity_bcs(bc_ctx(b), mask, V, th, vel);
-    R vR[3] = {R(vel[0]), R(vel[1]), R(vel[2])};
+    const D3 X0{xi, yi, zi};
+    if (b.nbc && (mask || b.bc_whole))
+        vel = velocity_bcs(bc_ctx(b), mask, X0, D3{double(ui.x), double(ui.y), double(ui.z)}, th, dt, vel);
+    R vR[3] = {R(vel.x), R(vel.y), R(vel.z)};
     R un[4] = {tl::axpy_rn(ui.x, R(half), vR[0]), DIM == 3 ? tl::axpy_rn(ui.y, R(half), vR[1]) : R(0),
                tl::axpy_rn(ui.z, R(half), vR[2]), ui.w};
     if (FRAC) {
         R* sdp = static_cast<R*>(b.sdot);
         R sd = sdp[i], s = ui.w;
-        tl::ExprVars Vn;
-        make_vars(Vn, xi, yi, zi, double(un[0]), double(un[1]), double(un[2]), th, dt, b.dp_body);
-        advance_phase<R>(bc_ctx(b), s, sd, static_cast<const R*>(b.sddot)[i], half, half, Vn);
+        advance_phase<R>(b, s, sd, static_cast<const R*>(b.sddot)[i], half, half, X0,
+                         D3{double(un[0]), double(un[1]), double(un[2])}, th, dt);
         un[3] = s;
         sdp[i] = sd;
     }
@@ -819,34 +1034,78 @@ __global__ void k_reduce_partials(const double* p, int64_t n, double* acc) {
 // ---------------------------------------------------------------------------
 // dispatch
 // ---------------------------------------------------------------------------
-template <typename R, int DIM>
-int launch_a(cudaStream_t st, const tl_body& b) {
-    const unsigned g = tl_blocks(b.n, kThreads);
-    if (b.model == 1) {
-        if (b.fracture) k_pass_a<R, DIM, 1, true><<<g, kThreads, 0, st>>>(b);
-        else k_pass_a<R, DIM, 1, false><<<g, kThreads, 0, st>>>(b);
-    } else if (b.model == 2) {
-        if (b.fracture) k_pass_a<R, DIM, 2, true><<<g, kThreads, 0, st>>>(b);
-        else k_pass_a<R, DIM, 2, false><<<g, kThreads, 0, st>>>(b);
+// dynamic shared memory of the tiled kernels; opted in once per kernel
+template <typename K>
+int smem_opt_in(K kernel, size_t bytes) {
+    if (bytes <= 48 * 1024) return TL_OK;
+    if (bytes > 227 * 1024) {
+        tl_set_error("tile needs %zu bytes of shared memory", bytes);
+        return TL_ERR_ARG;
+    }
+    TL_TRY_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    return TL_OK;
+}
+
+template <typename R, int DIM, int MODEL, bool FRAC, int KIND>
+int launch_a_one(cudaStream_t st, const tl_body& b) {
+    constexpr int G = TL_GATHER_A;
+    if (b.tile > 0) {
+        auto kern = k_pass_a<R, DIM, MODEL, FRAC, KIND, G, true>;
+        const size_t bytes = tile_bytes<R, 1>(b.tile + b.hmax);
+        int rc = smem_opt_in(kern, bytes);
+        if (rc) return rc;
+        kern<<<tl_blocks(b.n, b.tile), b.tile, bytes, st>>>(b);
     } else {
-        k_pass_a<R, DIM, 3, false><<<g, kThreads, 0, st>>>(b);
+        k_pass_a<R, DIM, MODEL, FRAC, KIND, G, false><<<tl_blocks(b.n, kThreads), kThreads, 0, st>>>(b);
     }
     return tl_check_launch("k_pass_a");
 }
 
-template <typename R, int DIM, int MODE>
-int launch_b_mode(cudaStream_t st, const tl_body& b) {
-    const unsigned g = tl_blocks(b.n, kThreads);
-    if (b.fracture) k_pass_b<R, DIM, MODE, true><<<g, kThreads, 0, st>>>(b);
-    else k_pass_b<R, DIM, MODE, false><<<g, kThreads, 0, st>>>(b);
+template <typename R, int DIM, int KIND>
+int launch_a_k(cudaStream_t st, const tl_body& b) {
+    if (b.model == 1)
+        return b.fracture ? launch_a_one<R, DIM, 1, true, KIND>(st, b) : launch_a_one<R, DIM, 1, false, KIND>(st, b);
+    if (b.model == 2)
+        return b.fracture ? launch_a_one<R, DIM, 2, true, KIND>(st, b) : launch_a_one<R, DIM, 2, false, KIND>(st, b);
+    return launch_a_one<R, DIM, 3, false, KIND>(st, b);
+}
+
+template <typename R, int DIM>
+int launch_a(cudaStream_t st, const tl_body& b) {
+    return b.kind == 1 ? launch_a_k<R, DIM, 1>(st, b) : launch_a_k<R, DIM, 2>(st, b);
+}
+
+template <typename R, int DIM, int MODE, bool FRAC, int KIND>
+int launch_b_one(cudaStream_t st, const tl_body& b) {
+    constexpr int G = TL_GATHER_B;
+    if (b.tile > 0) {
+        auto kern = k_pass_b<R, DIM, MODE, FRAC, KIND, G, true>;
+        const size_t bytes = tile_bytes<R, 3>(b.tile + b.hmax);
+        int rc = smem_opt_in(kern, bytes);
+        if (rc) return rc;
+        kern<<<tl_blocks(b.n, b.tile), b.tile, bytes, st>>>(b);
+    } else {
+        k_pass_b<R, DIM, MODE, FRAC, KIND, G, false><<<tl_blocks(b.n, kThreads), kThreads, 0, st>>>(b);
+    }
     return tl_check_launch("k_pass_b");
+}
+
+template <typename R, int DIM, int MODE, int KIND>
+int launch_b_mode(cudaStream_t st, const tl_body& b) {
+    return b.fracture ? launch_b_one<R, DIM, MODE, true, KIND>(st, b)
+                      : launch_b_one<R, DIM, MODE, false, KIND>(st, b);
+}
+
+template <typename R, int DIM, int KIND>
+int launch_b_k(cudaStream_t st, const tl_body& b, int mode) {
+    if (mode == TL_B_INIT) return launch_b_mode<R, DIM, TL_B_INIT, KIND>(st, b);
+    if (mode == TL_B_VERLET) return launch_b_mode<R, DIM, TL_B_VERLET, KIND>(st, b);
+    return launch_b_mode<R, DIM, TL_B_SYMPL, KIND>(st, b);
 }
 
 template <typename R, int DIM>
 int launch_b(cudaStream_t st, const tl_body& b, int mode) {
-    if (mode == TL_B_INIT) return launch_b_mode<R, DIM, TL_B_INIT>(st, b);
-    if (mode == TL_B_VERLET) return launch_b_mode<R, DIM, TL_B_VERLET>(st, b);
-    return launch_b_mode<R, DIM, TL_B_SYMPL>(st, b);
+    return b.kind == 1 ? launch_b_k<R, DIM, 1>(st, b, mode) : launch_b_k<R, DIM, 2>(st, b, mode);
 }
 
 template <typename R, int DIM>

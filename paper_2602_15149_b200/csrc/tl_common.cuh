@@ -159,21 +159,25 @@ __device__ __forceinline__ int eig3_jacobi(const T* Ain, T* w, T* Q, T tol_rel) 
     return sweeps;
 }
 
-// radial kernel factor: grad_base = fac(r) * r0 with fac = (dW/dr)/r.
-// kind 1 = cubic spline, 2 = Wendland C2 (reference kernel_geom.py:30-62).
-// inv_h = 1/h; alpha = kernel normalisation.  Zero outside q < 2 and at r=0.
-template <typename T>
-__device__ __forceinline__ T kernel_fac(T r, T inv_h, T alpha, int kind) {
-    T q = r * inv_h;
+// radial kernel factor: grad_base = fac * r0 with fac = (dW/dr)/r, written
+// with rs = 1/r (0 at r = 0, so coincident pairs and the self-padding of the
+// sliced ELL contribute exactly nothing).  KIND 1 = cubic spline, 2 =
+// Wendland C2 (reference kernel_geom.py:30-62); a_ih = alpha / h.
+__device__ __forceinline__ float rsqrt_pos(float x) { return x > 0.f ? rsqrtf(x) : 0.f; }
+__device__ __forceinline__ double rsqrt_pos(double x) { return x > 0.0 ? rsqrt(x) : 0.0; }
+
+template <typename T, int KIND>
+__device__ __forceinline__ T kernel_fac(T r2, T rs, T inv_h, T a_ih) {
+    const T q = r2 * rs * inv_h;
     T dw;
-    if (kind == 2) {
-        T t = q < T(2) ? T(1) - T(0.5) * q : T(0);
+    if (KIND == 2) {
+        const T t = q < T(2) ? T(1) - T(0.5) * q : T(0);
         dw = T(-5) * q * t * t * t;
     } else {
-        T tm = T(2) - q;
+        const T tm = T(2) - q;
         dw = q < T(1) ? T(-3) * q + T(2.25) * q * q : (q < T(2) ? T(-0.75) * tm * tm : T(0));
     }
-    return r > T(0) ? alpha * dw * inv_h / r : T(0);
+    return a_ih * dw * rs;
 }
 
 // a + b*c with both roundings (no FMA contraction): the integrator updates

@@ -172,6 +172,94 @@ class DeviceAdjacency:
         return out
 
 
+class StepLayout:
+    """Device particle order and neighbour tiles for the step kernels.
+
+    perm[p] = original index of device position p (Morton order of cells of
+    about one particle, so T consecutive particles form a compact brick);
+    the CSR is renamed into that order with each row still in ascending
+    original partner order (the reference's summation order), copied to a
+    lane-interleaved sliced ELL (soff, sidx), and, when ``tile`` > 0, every
+    CTA of ``tile`` particles gets the halo list of the neighbours it does not
+    own plus uint16 shared-memory slots for each pair (tiles.cu)."""
+
+    GROUP = 4   # TL_SELL_GROUP
+
+    def __init__(self, dadj, tile=256):
+        import torch
+        L = _lib.lib()
+        st = _lib.stream_ptr()
+        dev = dadj.X.device
+        n = dadj.n
+        self.n = n
+        Xh = dadj.X
+        lo = Xh.min(dim=0).values.cpu().numpy()
+        hi = Xh.max(dim=0).values.cpu().numpy()
+        ext = hi - lo
+        active = ext > 0
+        vol = float(np.prod(ext[active])) if active.any() else 1.0
+        cell = (vol / n) ** (1.0 / max(int(active.sum()), 1)) if active.any() else 1.0
+        cell = max(cell, 1e-300)
+        self.perm = torch.empty(n, dtype=torch.int32, device=dev)
+        self.iperm = torch.empty(n, dtype=torch.int32, device=dev)
+        lo_arr = (_lib.D * 3)(*lo)
+        _lib.check(L.tl_reorder(st, n, _lib.ptr(Xh), lo_arr, float(cell), _lib.ptr(self.perm),
+                                _lib.ptr(self.iperm)), "tl_reorder")
+        counts = torch.empty(n, dtype=torch.int64, device=dev)
+        _lib.check(L.tl_csr_permute_counts(st, n, _lib.ptr(self.perm), _lib.ptr(dadj.indptr),
+                                           _lib.ptr(counts)), "tl_csr_permute_counts")
+        self.indptr = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+        torch.cumsum(counts, 0, out=self.indptr[1:])
+        self.indices = torch.empty_like(dadj.indices)
+        _lib.check(L.tl_csr_permute(st, n, _lib.ptr(self.perm), _lib.ptr(self.iperm),
+                                    _lib.ptr(dadj.indptr), _lib.ptr(dadj.indices),
+                                    _lib.ptr(self.indptr), _lib.ptr(self.indices)),
+                   "tl_csr_permute")
+        nw = (n + 31) // 32
+        slen = torch.empty(nw, dtype=torch.int32, device=dev)
+        _lib.check(L.tl_sell_lengths(st, n, _lib.ptr(self.indptr), _lib.ptr(slen)),
+                   "tl_sell_lengths")
+        self.soff = torch.zeros(nw + 1, dtype=torch.int64, device=dev)
+        torch.cumsum(slen.to(torch.int64) * 32, 0, out=self.soff[1:])
+        total = int(self.soff[-1].item())
+        self.sidx = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
+        _lib.check(L.tl_sell_fill(st, n, _lib.ptr(self.indptr), _lib.ptr(self.indices),
+                                  _lib.ptr(self.soff), _lib.ptr(self.sidx)), "tl_sell_fill")
+        self.tile = 0
+        self.hmax = 0
+        self.hoff = self.halo = self.slots = None
+        if tile and tile > 0:
+            self._build_tiles(int(tile), total)
+
+    def _build_tiles(self, T, total):
+        import torch
+        L = _lib.lib()
+        st = _lib.stream_ptr()
+        dev = self.indptr.device
+        n = self.n
+        nnz = int(self.indices.shape[0])
+        ntile = (n + T - 1) // T
+        halo = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
+        tcount = torch.zeros(ntile, dtype=torch.int64, device=dev)
+        nh = _lib.I64(0)
+        _lib.check(L.tl_tile_halo(st, n, T, _lib.ptr(self.indptr), _lib.ptr(self.indices), nnz,
+                                  _lib.ptr(halo), _lib.ptr(tcount), _lib.C.byref(nh)),
+                   "tl_tile_halo")
+        self.halo = halo[: max(int(nh.value), 1)].clone()
+        del halo
+        self.hoff = torch.zeros(ntile + 1, dtype=torch.int64, device=dev)
+        torch.cumsum(tcount, 0, out=self.hoff[1:])
+        self.hmax = int(tcount.max().item()) if ntile else 0
+        if T + self.hmax > 65535:
+            return   # slots are uint16: leave the body untiled
+        self.slots = torch.empty(max(total, 4), dtype=torch.int16, device=dev)
+        _lib.check(L.tl_tile_slots(st, n, T, self.GROUP, _lib.ptr(self.indptr),
+                                   _lib.ptr(self.indices), _lib.ptr(self.hoff),
+                                   _lib.ptr(self.halo), _lib.ptr(self.soff),
+                                   _lib.ptr(self.slots)), "tl_tile_slots")
+        self.tile = T
+
+
 class LazyAdjacency(Adjacency):
     """core.Adjacency whose per-pair host arrays are fetched from the device
     on first access."""

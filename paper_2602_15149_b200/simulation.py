@@ -26,6 +26,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 
 import numpy as np
 
@@ -35,6 +36,8 @@ from .core import CaseError, Model, SimulationError
 
 INT64_MAX = np.iinfo(np.int64).max
 N_COUNTERS = 8
+DEFAULT_TILE = 256           # particles per CTA / shared-memory tile (TLSPH_TILE overrides)
+TILE_SMEM_LIMIT = 200 * 1024  # bytes of shared memory a pass-B tile may take
 
 
 def _torch():
@@ -68,17 +71,26 @@ class DeviceBody:
                     dp_body=body.dp_body, notches=body.notches,
                     correction=getattr(body, "kernel_correction", True))
         self.adj = dadj
-        soff, sidx = dadj.sell()
-        self.soff, self.sidx = soff, sidx
+        # device particle order + neighbour tiles (kernel_geom.StepLayout)
+        tile = int(os.environ.get("TLSPH_TILE", str(DEFAULT_TILE)))
+        lay = kernel_geom.StepLayout(dadj, tile=tile)
+        rec = 64 if precision == "fp32" else 128          # pass-B bytes per staged particle
+        if lay.tile and (lay.tile + lay.hmax) * rec > TILE_SMEM_LIMIT:
+            lay.tile = 0                                   # halo too fat: gather from L2
+        self.layout = lay
+        self.perm = lay.perm
+        self.perm_h = lay.perm.cpu().numpy().astype(np.int64)
+        pl = lay.perm.long()
+        self.soff, self.sidx = lay.soff, lay.sidx
         R = self.R
         z = lambda *shape: torch.zeros(shape, dtype=R, device=dev)  # noqa: E731
-        self.Xs = torch.from_numpy(np.ascontiguousarray(st.X.T)).to(dev)       # 3 planes
-        self.L = dadj.L.t().contiguous().to(R)                                 # 9 planes
+        self.Xs = dadj.X.index_select(0, pl).t().contiguous()                 # 3 planes
+        self.L = dadj.L.index_select(0, pl).t().contiguous().to(R)             # 9 planes
         V0 = np.asarray(st.V0, dtype=np.float64)
         m0 = np.asarray(st.m0, dtype=np.float64)
         self.uniform = bool(np.all(V0 == V0[0]) and np.all(m0 == m0[0]))
-        self.V0 = torch.from_numpy(V0).to(dev)
-        self.m0 = torch.from_numpy(m0).to(dev)
+        self.V0 = torch.from_numpy(V0[self.perm_h]).to(dev)
+        self.m0 = torch.from_numpy(m0[self.perm_h]).to(dev)
         self.us = z(n, 4)
         self.rb = z(n, 12)
         self.v = z(3, n)
@@ -131,7 +143,7 @@ class DeviceBody:
                     raise CaseError(f"body {body.mk}: more than 32 targeted boundary conditions")
                 d.bit = bit
                 tgt = np.asarray(bc.target, dtype=np.int64)
-                mask[tgt] |= np.uint32(1 << bit)
+                mask[tgt] |= np.uint32(1 << bit)      # original order; permuted below
                 bit += 1
             for ax in range(3):
                 c = bc.const[ax]
@@ -154,7 +166,7 @@ class DeviceBody:
         self.bcs_dev = torch.empty(nbytes, dtype=torch.uint8, device=self.dev)
         host = torch.frombuffer(bytearray(C.string_at(C.addressof(arr), nbytes)), dtype=torch.uint8)
         self.bcs_dev.copy_(host)
-        self.bcmask = torch.from_numpy(mask.view(np.int32)).to(self.dev)
+        self.bcmask = torch.from_numpy(mask[self.perm_h].view(np.int32)).to(self.dev)
         rp = getattr(body, "restrictphi_expr", None)
         if rp is not None:
             ast = config.expressions.get(rp)
@@ -197,6 +209,11 @@ class DeviceBody:
             b.f0[k] = float(body.f0[k])
         P = _lib.ptr
         b.soff, b.sidx, b.Xs, b.L = P(self.soff), P(self.sidx), P(self.Xs), P(self.L)
+        lay = self.layout
+        b.tile, b.hmax = int(lay.tile), int(lay.hmax)
+        if lay.tile:
+            b.hoff, b.halo, b.slots = P(lay.hoff), P(lay.halo), P(lay.slots)
+        b.perm = P(self.perm)
         b.V0, b.m0 = P(self.V0), P(self.m0)
         for k in ("us", "rb", "v", "al", "sdot", "sddot", "Hh", "Cpd", "epbar", "a"):
             setattr(b, k, P(getattr(self, k)))
@@ -216,42 +233,49 @@ class DeviceBody:
 
     # -- host mirrors ------------------------------------------------------------
     def push_state(self):
-        """Upload body.state (host, FP64) into the device layout."""
+        """Upload body.state (host, FP64, original order) into the device
+        layout and order."""
         torch = _torch()
         st = self.body.state
-        R, dev = self.R, self.dev
+        R, dev, pm = self.R, self.dev, self.perm_h
         us = np.empty((self.n, 4))
-        us[:, :3] = st.u
-        us[:, 3] = st.s
+        us[:, :3] = st.u[pm]
+        us[:, 3] = st.s[pm]
         self.us.copy_(torch.from_numpy(us).to(dev, R))
-        self.v.copy_(torch.from_numpy(np.ascontiguousarray(st.v.T)).to(dev, R))
-        self.a.copy_(torch.from_numpy(np.ascontiguousarray(st.a.T)).to(dev, R))
+        self.v.copy_(torch.from_numpy(np.ascontiguousarray(st.v[pm].T)).to(dev, R))
+        self.a.copy_(torch.from_numpy(np.ascontiguousarray(st.a[pm].T)).to(dev, R))
         for name, arr in (("sdot", st.sdot), ("sddot", st.sddot), ("Hh", st.Hhist),
                           ("epbar", st.epbar)):
-            getattr(self, name).copy_(torch.from_numpy(np.asarray(arr, dtype=np.float64)).to(dev, R))
+            host = np.asarray(arr, dtype=np.float64)[pm]
+            getattr(self, name).copy_(torch.from_numpy(host).to(dev, R))
         if self.body.material.model == Model.J2 and st.Cp is not None:
-            Cp = np.asarray(st.Cp, dtype=np.float64)
+            Cp = np.asarray(st.Cp, dtype=np.float64)[pm]
             cpd = np.stack([Cp[:, 0, 0] - 1.0, Cp[:, 1, 1] - 1.0, Cp[:, 2, 2] - 1.0,
                             Cp[:, 0, 1], Cp[:, 0, 2], Cp[:, 1, 2]])
             self.Cpd.copy_(torch.from_numpy(cpd).to(dev, R))
 
     def pull_state(self, full=True):
-        """Refresh body.state (host) from the device."""
+        """Refresh body.state (host, original order) from the device."""
         st = self.body.state
+        pm = self.perm_h
+
+        def put(dst, val):
+            dst[pm] = val
+
         us = self.us.double().cpu().numpy()
-        st.u[...] = us[:, :3]
-        st.s[...] = us[:, 3]
-        st.v[...] = self.v.double().cpu().numpy().T
-        st.sdot[...] = self.sdot.double().cpu().numpy()
-        st.sddot[...] = self.sddot.double().cpu().numpy()
-        st.Hhist[...] = self.Hh.double().cpu().numpy()
-        st.epbar[...] = self.epbar.double().cpu().numpy()
+        put(st.u, us[:, :3])
+        put(st.s, us[:, 3])
+        put(st.v, self.v.double().cpu().numpy().T)
+        put(st.sdot, self.sdot.double().cpu().numpy())
+        put(st.sddot, self.sddot.double().cpu().numpy())
+        put(st.Hhist, self.Hh.double().cpu().numpy())
+        put(st.epbar, self.epbar.double().cpu().numpy())
         if full and self.mirrors:
-            st.a[...] = self.a.double().cpu().numpy().T
-            st.F[...] = self.F_out.cpu().numpy()
-            st.S[...] = self.S_out.cpu().numpy()
-            st.psi_e[...] = self.psi_out.cpu().numpy()
-            st.psi_plus[...] = self.psip_out.cpu().numpy()
+            put(st.a, self.a.double().cpu().numpy().T)
+            put(st.F, self.F_out.cpu().numpy())
+            put(st.S, self.S_out.cpu().numpy())
+            put(st.psi_e, self.psi_out.cpu().numpy())
+            put(st.psi_plus, self.psip_out.cpu().numpy())
         if self.body.material.model == Model.J2 and st.Cp is not None:
             c = self.Cpd.double().cpu().numpy()
             Cp = np.empty((self.n, 3, 3))
@@ -259,7 +283,7 @@ class DeviceBody:
             Cp[:, 0, 1] = Cp[:, 1, 0] = c[3]
             Cp[:, 0, 2] = Cp[:, 2, 0] = c[4]
             Cp[:, 1, 2] = Cp[:, 2, 1] = c[5]
-            st.Cp[...] = Cp
+            put(st.Cp, Cp)
         self.body.plastic_work = self.pw_base + float(self.pw_acc.item())
 
     def dtinfo(self):
