@@ -22,7 +22,7 @@ SOURCES = ["plugin.cu", "neighbors.cu", "tiles.cu", "step.cu"]
 HEADERS = ["tl_common.cuh", "expr_vm.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v", "-ftz=true",
          "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
 
 

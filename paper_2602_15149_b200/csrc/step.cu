@@ -48,6 +48,15 @@ using tl::mm3;
 #ifndef TL_GATHER_B
 #define TL_GATHER_B 4
 #endif
+// minimum resident CTAs per SM requested from ptxas (register budget); tuned
+// on B200 for the C4 workload: FP32 pass A 4 (64 regs), pass B 3 (80 regs);
+// FP64 pass A needs its registers (J2/eigen) and keeps 1
+#ifndef TL_MINB_A
+#define TL_MINB_A(R) (sizeof(R) == 4 ? 4 : 1)
+#endif
+#ifndef TL_MINB_B
+#define TL_MINB_B(R) 3
+#endif
 static_assert(TL_SELL_GROUP % TL_GATHER_A == 0 && TL_SELL_GROUP % TL_GATHER_B == 0, "gather group");
 constexpr int kThreads = TL_THREADS;
 
@@ -308,6 +317,9 @@ __device__ __forceinline__ void pair_a(R dx, R dy, R dz, const V4<R>& uj, R vj, 
     }
 }
 
+__device__ __forceinline__ float fdiv(float a, float b) { return __fdividef(a, b); }
+__device__ __forceinline__ double fdiv(double a, double b) { return a / b; }
+
 // pass B pair: s1 += m fac r0 ; s2 += m fac PL_j r0 ; s3 += m fac pi_ij r0
 template <typename R, int DIM, int KIND>
 __device__ __forceinline__ void pair_b(R dx, R dy, R dz, const V4<R>& q0, const V4<R>& q1,
@@ -334,7 +346,7 @@ __device__ __forceinline__ void pair_b(R dx, R dy, R dz, const V4<R>& q0, const 
     }
     if (visc) {
         const R dvr = (vi0 - q2.y) * dx + (DIM == 3 ? (vi1 - q2.z) * dy : R(0)) + (vi2 - q2.w) * dz;
-        const R Gv = hR * dvr / (r2 + eps_h2);
+        const R Gv = fdiv(hR * dvr, r2 + eps_h2);
         const R pw = (b2 * Gv * Gv - b1c0 * Gv) * inv_rho * wf;
         s3[0] += pw * dx; s3[2] += pw * dz;
         if (DIM == 3) s3[1] += pw * dy;
@@ -354,6 +366,23 @@ __device__ __forceinline__ void load_slots(const uint16_t* p, int* out) {
         out[0] = __ldg(p);
     }
 }
+
+// slot groups with the next group's load already in flight
+template <int G>
+struct SlotPipe {
+    static_assert(G == 4, "slot pipe reads TL_SELL_GROUP = 4 slots per load");
+    const uint2* p;
+    int len;
+    uint2 cur;
+    __device__ __forceinline__ SlotPipe(const uint16_t* sl, int len_) : p(reinterpret_cast<const uint2*>(sl)), len(len_) {
+        cur = len > 0 ? __ldg(p) : make_uint2(0, 0);
+    }
+    __device__ __forceinline__ void next(int k, int* out) {
+        const uint2 v = cur;
+        if (k + G < len) cur = __ldg(p + (k + G) * 8);   // 32 lanes x G slots per group
+        out[0] = v.x & 0xffff; out[1] = v.x >> 16; out[2] = v.y & 0xffff; out[3] = v.y >> 16;
+    }
+};
 
 // shared-memory tile of a CTA: positions (FP32: relative to the tile
 // origin, FP64: absolute) and the gathered record of every member and halo
@@ -407,7 +436,7 @@ __host__ __device__ constexpr size_t tile_bytes(int S) {
 // pass A
 // ---------------------------------------------------------------------------
 template <typename R, int DIM, int MODEL, bool FRAC, int KIND, int G, bool TILED>
-__global__ void __launch_bounds__(kThreads) k_pass_a(const tl_body b) {
+__global__ void __launch_bounds__(kThreads, TL_MINB_A(R)) k_pass_a(const tl_body b) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     __shared__ double s_pw[kThreads / 32];
@@ -448,9 +477,10 @@ __global__ void __launch_bounds__(kThreads) k_pass_a(const tl_body b) {
             const int me = threadIdx.x;
             const R xl = tl_.x[me], yl = tl_.y[me], zl = tl_.z[me];
             const uint16_t* sl = b.slots + base + lane * G;
+            SlotPipe<G> pipe(sl, len);
             for (int k = 0; k < len; k += G) {
                 int l[G];
-                load_slots<G>(sl + k * 32, l);
+                pipe.next(k, l);
 #pragma unroll
                 for (int q = 0; q < G; ++q) {
                     const int j = l[q];
@@ -750,7 +780,7 @@ __device__ __forceinline__ double sq3_rn(double x, double y, double z) {
 // pass B
 // ---------------------------------------------------------------------------
 template <typename R, int DIM, int MODE, bool FRAC, int KIND, int G, bool TILED>
-__global__ void __launch_bounds__(kThreads) k_pass_b(const tl_body b) {
+__global__ void __launch_bounds__(kThreads, TL_MINB_B(R)) k_pass_b(const tl_body b) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (halted(b)) return;
@@ -792,9 +822,10 @@ __global__ void __launch_bounds__(kThreads) k_pass_b(const tl_body b) {
             const R xl = tl_.x[me], yl = tl_.y[me], zl = tl_.z[me];
             const uint16_t* sl = b.slots + base + lane * G;
             const int S = tl_.S;
+            SlotPipe<G> pipe(sl, len);
             for (int k = 0; k < len; k += G) {
                 int l[G];
-                load_slots<G>(sl + k * 32, l);
+                pipe.next(k, l);
 #pragma unroll
                 for (int q = 0; q < G; ++q) {
                     const int j = l[q];

@@ -185,6 +185,23 @@ def _sim(G, precision):
     return cfg, DeviceSimulation(cfg, precision=precision)
 
 
+@pytest.mark.parametrize("tile", ["256", "0", "64"])
+@pytest.mark.parametrize("tag", ["kalthoff2d_p", "taylor3d", "kalthoff3d"])
+def test_layout_variants_agree(tag, tile, monkeypatch):
+    """Shared-memory tiles (various sizes) and the L2-gather path give the
+    same FP64 state: sums run in the same order either way."""
+    monkeypatch.setenv("TLSPH_TILE", tile)
+    G = golden(f"run_{tag}")
+    cfg, sim = _sim(G, "fp64")
+    assert sim.dbodies[0].layout.tile == int(tile)
+    sim.initialize()
+    for step in (1, 2):
+        sim.step(G["dts"][step - 1])
+    errs = _errors(cfg.bodies[0].state, G, 2)
+    for k, err in errs.items():
+        assert err <= TOL64[k], (tile, k, err)
+
+
 @pytest.mark.parametrize("tag", RUNS)
 def test_device_run_fp64_matches_reference(tag):
     G = golden(f"run_{tag}")
