@@ -75,6 +75,57 @@ __device__ __forceinline__ bool mirror_out(const tl_body& b) {
 // constitutive models on F = I + H (H-form)
 // ---------------------------------------------------------------------------
 
+// Positive part E+ of a symmetric 3x3 E (E- = E - E+), FP32 mode.
+// Closed form instead of Jacobi sweeps: eigenvalues by the trigonometric
+// (Cardano) method, then the projector of the one eigenvalue whose sign
+// differs from the other two (Sylvester: P_k = prod_{j!=k} (E - l_j I) /
+// (l_k - l_j)).  Its denominators are bounded below by |l_k| > 0, so the
+// split is well conditioned even when the two same-sign eigenvalues are
+// (nearly) equal -- the case where individual eigenvectors are not.
+__device__ __forceinline__ void positive_part(const float* E, float* Ep) {
+    const float q = (E[0] + E[4] + E[8]) * (1.f / 3.f);
+    const float p1 = E[1] * E[1] + E[2] * E[2] + E[5] * E[5];
+    const float d0 = E[0] - q, d1 = E[4] - q, d2 = E[8] - q;
+    const float p2 = d0 * d0 + d1 * d1 + d2 * d2 + 2.f * p1;
+    float l1, l2, l3;
+    if (p2 <= 0.f) {
+        l1 = l2 = l3 = q;
+    } else {
+        const float p = sqrtf(p2 * (1.f / 6.f));
+        const float ip = 1.f / p;
+        const float b0 = d0 * ip, b4 = d1 * ip, b8 = d2 * ip;
+        const float b1 = E[1] * ip, b2 = E[2] * ip, b5 = E[5] * ip;
+        const float detB = b0 * (b4 * b8 - b5 * b5) - b1 * (b1 * b8 - b5 * b2) + b2 * (b1 * b5 - b4 * b2);
+        const float r = fminf(fmaxf(0.5f * detB, -1.f), 1.f);
+        const float phi = acosf(r) * (1.f / 3.f);
+        l1 = q + 2.f * p * cosf(phi);
+        l3 = q + 2.f * p * cosf(phi + 2.0943951023931953f);
+        l2 = 3.f * q - l1 - l3;
+    }
+    if (l3 >= 0.f) {
+#pragma unroll
+        for (int k = 0; k < 9; ++k) Ep[k] = E[k];
+        return;
+    }
+    if (l1 <= 0.f) {
+#pragma unroll
+        for (int k = 0; k < 9; ++k) Ep[k] = 0.f;
+        return;
+    }
+    float E2[9];
+    tl::mm3(E, E, E2);
+    // isolated eigenvalue lk with projector (E - la I)(E - lb I) / ((lk-la)(lk-lb))
+    const bool top = l2 <= 0.f;          // l1 alone positive: E+ = l1 P1
+    const float lk = top ? l1 : l3, la = top ? l2 : l1, lb = top ? l3 : l2;
+    const float c = lk / ((lk - la) * (lk - lb));
+    const float sab = la + lb, pab = la * lb;
+    float Pk[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) Pk[k] = c * (E2[k] - sab * E[k] + ((k % 4 == 0) ? pab : 0.f));
+#pragma unroll
+    for (int k = 0; k < 9; ++k) Ep[k] = top ? Pk[k] : E[k] - Pk[k];
+}
+
 // SVK with optional spectral split (reference.py:94-116, fast.py:224-284)
 template <typename R>
 __device__ __forceinline__ int svk_update(const R* H, R lam, R mu, R s, bool fracture, R jtol,
@@ -98,9 +149,32 @@ __device__ __forceinline__ int svk_update(const R* H, R lam, R mu, R s, bool fra
         psip = R(0);
         return 0;
     }
+    const R trp = trE > R(0) ? trE : R(0), trm = trE < R(0) ? trE : R(0);
+    if (sizeof(R) == 4) {
+        float Ep[9];
+        positive_part(reinterpret_cast<const float*>(E), Ep);
+        const R s2 = s * s;
+        R fp = R(0), fm = R(0);
+#pragma unroll
+        for (int k = 0; k < 9; ++k) {
+            const R ep = R(Ep[k]), em = E[k] - R(Ep[k]);
+            fp += ep * ep;
+            fm += em * em;
+            R sp = R(2) * mu * ep, sm = R(2) * mu * em;
+            if (k % 4 == 0) {
+                sp += lam * trp;
+                sm += lam * trm;
+            }
+            S[k] = s2 * sp + sm;
+        }
+        const R pp = R(0.5) * lam * trp * trp + mu * fp;
+        const R pm = R(0.5) * lam * trm * trm + mu * fm;
+        psi = s2 * pp + pm;
+        psip = pp;
+        return 0;
+    }
     R w[3], Q[9];
     const int sw = tl::eig3_jacobi(E, w, Q, jtol);
-    const R trp = trE > R(0) ? trE : R(0), trm = trE < R(0) ? trE : R(0);
     R pp = R(0.5) * lam * trp * trp, pm = R(0.5) * lam * trm * trm;
     const R s2 = s * s;
     R lp[3], lm[3];
