@@ -195,7 +195,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--config", default="C4", choices=["C4"])
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -309,10 +309,13 @@ def main():
             sim.step(dt)
         torch.cuda.synchronize()
         el = time.perf_counter() - t0
-        state_bytes = n * (4 * w + 3 * w + 4 * w)   # (u,s), v, sdot, sddot, H, epbar
+        nb = len(sim.dbodies)
         e2e = {"value": n_total * args.e2e_steps / el, "unit": "particle-steps/s",
-               "h2d_bytes_per_step": 80, "d2h_bytes_per_step": int(state_bytes + 16),
-               "api": "DeviceSimulation.pick_dt()+step(dt), host state mirror each step"}
+               # clock struct in; dt maxima (the step's scalar result), error
+               # counters and plastic work out
+               "h2d_bytes_per_step": 80, "d2h_bytes_per_step": 16 * nb + 64 * nb + 8 * nb,
+               "api": "DeviceSimulation.pick_dt() + step(dt) per step; host state arrays "
+                      "refresh lazily on access (DeviceState)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

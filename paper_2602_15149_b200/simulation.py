@@ -53,6 +53,8 @@ class DeviceBody:
         self.mirrors = mirrors
         self.body = body
         st = body.state
+        self.host = st           # the host arrays behind body.state (see DeviceState)
+        self.dirty = False
         n = int(st.X.shape[0])
         self.n = n
         self.R = torch.float32 if precision == "fp32" else torch.float64
@@ -236,7 +238,7 @@ class DeviceBody:
         """Upload body.state (host, FP64, original order) into the device
         layout and order."""
         torch = _torch()
-        st = self.body.state
+        st = self.host
         R, dev, pm = self.R, self.dev, self.perm_h
         us = np.empty((self.n, 4))
         us[:, :3] = st.u[pm]
@@ -256,8 +258,9 @@ class DeviceBody:
 
     def pull_state(self, full=True):
         """Refresh body.state (host, original order) from the device."""
-        st = self.body.state
+        st = self.host
         pm = self.perm_h
+        self.dirty = False
 
         def put(dst, val):
             dst[pm] = val
@@ -289,6 +292,33 @@ class DeviceBody:
     def dtinfo(self):
         return _lib.tl_dtinfo(h=float(self.body.h), c0=float(self.body.material.c0),
                               red=_lib.ptr(self.red))
+
+
+class DeviceState:
+    """``body.state`` of a device-resident body.
+
+    Attribute reads of the evolving fields copy the device state into the
+    host arrays first if a step ran since the last copy, so host code (output
+    writers, tests) sees the reference's ParticleArrays contract while the
+    step loop never pays for a full-state device->host copy.  Writes go to
+    the host arrays; call ``DeviceSimulation.push_state()`` after editing
+    them in place."""
+
+    _LIVE = frozenset(("u", "v", "a", "F", "S", "s", "sdot", "sddot", "Hhist", "Cp", "epbar",
+                       "psi_e", "psi_plus", "x"))
+
+    def __init__(self, host, dbody):
+        object.__setattr__(self, "_host", host)
+        object.__setattr__(self, "_db", dbody)
+
+    def __getattr__(self, name):
+        db = object.__getattribute__(self, "_db")
+        if name in DeviceState._LIVE and db.dirty:
+            db.pull_state()
+        return getattr(object.__getattribute__(self, "_host"), name)
+
+    def __setattr__(self, name, value):
+        setattr(object.__getattribute__(self, "_host"), name, value)
 
 
 def _lib_max_bc():
@@ -364,6 +394,7 @@ class DeviceSimulation:
         self.trace = trace
         self.be = backend
         self.precision = precision
+        self.mirrors = mirrors
         self.contact_warnings = 0
         self._initialized = False
         self.stream = stream or torch.cuda.current_stream()
@@ -374,6 +405,8 @@ class DeviceSimulation:
         self.programs = ProgramTable()
         self.dbodies = [DeviceBody(b, config, precision, self.programs, mirrors)
                         for b in self.bodies]
+        for b, db in zip(self.bodies, self.dbodies):
+            b.state = DeviceState(db.host, db)
         prog_table = self.programs.upload()
         self.clock_dev = torch.zeros(C.sizeof(_lib.tl_clock), dtype=torch.uint8,
                                      device="cuda")
@@ -476,15 +509,22 @@ class DeviceSimulation:
                     raise SimulationError(f"non-finite state in body {mk} at step {check_at}")
 
     def sync_host(self, full=True):
-        """Copy the device state into every body.state (FP64 host mirrors)."""
-        torch = _torch()
-        torch.cuda.current_stream().wait_stream(self.stream)
+        """Mark the host mirrors stale: the next read of a body.state field
+        copies the device state (DeviceState); plastic work and warning
+        counters are refreshed now."""
         for db in self.dbodies:
-            db.pull_state(full=full)
+            db.dirty = True
+            db.body.plastic_work = db.pw_base + float(db.pw_acc.item())
+
+    def pull_host(self):
+        """Copy the device state into every body.state now."""
+        for db in self.dbodies:
+            db.pull_state()
 
     def push_state(self):
         """Upload host edits of body.state to the device."""
         for db in self.dbodies:
+            db.dirty = False
             db.push_state()
 
     # -- reference API -----------------------------------------------------------
@@ -513,7 +553,7 @@ class DeviceSimulation:
         if not self._initialized:
             self.initialize()
         verlet = int(self.config.step_algorithm) != 2
-        self._set_clock(t=self.t, dt=float(dt), out_step=1)
+        self._set_clock(t=self.t, dt=float(dt), out_step=int(self.mirrors))
         if verlet:
             for ph in ("contact", "internal", "bc", "update", "commit"):
                 self._mark(ph)
@@ -575,6 +615,8 @@ class DeviceSimulation:
                 pass_events.append(ev)
             _lib.check(self._lib.tl_clock_commit(self._st(), _lib.ptr(self.clock_dev)), "commit")
         self.step_index += nsteps
+        for db in self.dbodies:
+            db.dirty = True
 
     def finish_advance(self):
         """Sync point after advance(): read the clock back, raise errors."""
