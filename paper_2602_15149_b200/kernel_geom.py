@@ -185,14 +185,24 @@ class StepLayout:
 
     GROUP = 4   # TL_SELL_GROUP
 
-    def __init__(self, dadj, tile=256):
+    def __init__(self, dadj, tile=256, rows=None, halo=None):
+        """rows: adjacency rows this device owns (default all); halo: adjacency
+        ids of the off-rank particles those rows reference, in exchange order
+        (multi-GPU, see dist.py).  Device positions: owned [0, n) in Morton
+        order, then the halo block [n, n_all) in the given order."""
         import torch
         L = _lib.lib()
         st = _lib.stream_ptr()
         dev = dadj.X.device
-        n = dadj.n
+        if rows is None:
+            rows = torch.arange(dadj.n, dtype=torch.int64, device=dev)
+        rows = torch.as_tensor(rows, dtype=torch.int64, device=dev)
+        halo = (torch.zeros(0, dtype=torch.int64, device=dev) if halo is None
+                else torch.as_tensor(halo, dtype=torch.int64, device=dev))
+        n = int(rows.shape[0])
         self.n = n
-        Xh = dadj.X
+        self.n_all = n + int(halo.shape[0])
+        Xh = dadj.X.index_select(0, rows).contiguous()
         lo = Xh.min(dim=0).values.cpu().numpy()
         hi = Xh.max(dim=0).values.cpu().numpy()
         ext = hi - lo
@@ -200,21 +210,31 @@ class StepLayout:
         vol = float(np.prod(ext[active])) if active.any() else 1.0
         cell = (vol / n) ** (1.0 / max(int(active.sum()), 1)) if active.any() else 1.0
         cell = max(cell, 1e-300)
-        self.perm = torch.empty(n, dtype=torch.int32, device=dev)
-        self.iperm = torch.empty(n, dtype=torch.int32, device=dev)
+        pown = torch.empty(n, dtype=torch.int32, device=dev)
+        ipown = torch.empty(n, dtype=torch.int32, device=dev)
         lo_arr = (_lib.D * 3)(*lo)
-        _lib.check(L.tl_reorder(st, n, _lib.ptr(Xh), lo_arr, float(cell), _lib.ptr(self.perm),
-                                _lib.ptr(self.iperm)), "tl_reorder")
+        _lib.check(L.tl_reorder(st, n, _lib.ptr(Xh), lo_arr, float(cell), _lib.ptr(pown),
+                                _lib.ptr(ipown)), "tl_reorder")
+        prow = rows.index_select(0, pown.long()).to(torch.int32)     # device pos -> adj row
+        # adjacency id -> device position (owned, then halo); -1 = never referenced
+        iperm = torch.full((dadj.n,), -1, dtype=torch.int32, device=dev)
+        iperm[prow.long()] = torch.arange(n, dtype=torch.int32, device=dev)
+        if halo.numel():
+            iperm[halo] = torch.arange(n, self.n_all, dtype=torch.int32, device=dev)
+        self.perm = torch.cat([prow, halo.to(torch.int32)])          # device pos -> adj id
+        self.iperm = iperm
         counts = torch.empty(n, dtype=torch.int64, device=dev)
-        _lib.check(L.tl_csr_permute_counts(st, n, _lib.ptr(self.perm), _lib.ptr(dadj.indptr),
+        _lib.check(L.tl_csr_permute_counts(st, n, _lib.ptr(prow), _lib.ptr(dadj.indptr),
                                            _lib.ptr(counts)), "tl_csr_permute_counts")
         self.indptr = torch.zeros(n + 1, dtype=torch.int64, device=dev)
         torch.cumsum(counts, 0, out=self.indptr[1:])
-        self.indices = torch.empty_like(dadj.indices)
-        _lib.check(L.tl_csr_permute(st, n, _lib.ptr(self.perm), _lib.ptr(self.iperm),
+        self.indices = torch.empty(int(self.indptr[-1].item()), dtype=torch.int32, device=dev)
+        _lib.check(L.tl_csr_permute(st, n, _lib.ptr(prow), _lib.ptr(iperm),
                                     _lib.ptr(dadj.indptr), _lib.ptr(dadj.indices),
                                     _lib.ptr(self.indptr), _lib.ptr(self.indices)),
                    "tl_csr_permute")
+        if int(self.indices.min().item()) < 0 if self.indices.numel() else False:
+            raise ValueError("owned rows reference a particle that is neither owned nor halo")
         nw = (n + 31) // 32
         slen = torch.empty(nw, dtype=torch.int32, device=dev)
         _lib.check(L.tl_sell_lengths(st, n, _lib.ptr(self.indptr), _lib.ptr(slen)),
@@ -355,8 +375,10 @@ def build_pairs(positions, h, nbsrange=None, dp_body=None):
 
 
 def build_device_adjacency(positions, V0, h, dim, kind, nbsrange=None, dp_body=None,
-                           notches=(), correction=True):
-    """The device half of build_adjacency: returns a DeviceAdjacency."""
+                           notches=(), correction=True, required=None):
+    """The device half of build_adjacency: returns a DeviceAdjacency.
+    ``required``: optional bool mask of the rows that must have neighbours
+    (a rank's owned rows; halo-region rows at the subset edge may not)."""
     import torch
     Xh = np.ascontiguousarray(positions, dtype=np.float64)
     if Xh.shape[0] < 2:
@@ -365,7 +387,10 @@ def build_device_adjacency(positions, V0, h, dim, kind, nbsrange=None, dp_body=N
         notch_struct(q)
     Xd = torch.from_numpy(Xh).cuda()
     indptr, indices, counts = _device_pairs(Xd, Xh, h, nbsrange, dp_body, notches)
-    lonely = torch.nonzero(counts == 0)
+    empty = counts == 0
+    if required is not None:
+        empty &= torch.as_tensor(np.asarray(required, dtype=bool), device=empty.device)
+    lonely = torch.nonzero(empty)
     if lonely.numel():
         raise CaseError(f"particle {int(lonely[0, 0])} has no neighbors after notch severing")
     V0d = torch.from_numpy(np.ascontiguousarray(V0, dtype=np.float64)).cuda()

@@ -30,7 +30,7 @@ import os
 
 import numpy as np
 
-from . import _lib, backend, kernel_geom
+from . import _lib, backend, dist, kernel_geom
 from . import expr as ex
 from .core import CaseError, Model, SimulationError
 
@@ -48,61 +48,85 @@ def _torch():
 class DeviceBody:
     """Device buffers and the tl_body descriptor of one body."""
 
-    def __init__(self, body, config, precision, programs, mirrors=True):
+    def __init__(self, body, config, precision, programs, mirrors=True, part=None):
+        """part: this rank's share of the body (multi-GPU, see
+        DeviceSimulation._partition); None = the whole body on this device."""
         torch = _torch()
         self.mirrors = mirrors
         self.body = body
+        self.part = part
         st = body.state
         self.host = st           # the host arrays behind body.state (see DeviceState)
         self.dirty = False
-        n = int(st.X.shape[0])
-        self.n = n
         self.R = torch.float32 if precision == "fp32" else torch.float64
         dev = torch.device("cuda")
         self.dev = dev
         mat = body.material
         kind = int(config.kernel)
-        adj = body.adjacency
-        dadj = getattr(adj, "device", None) if adj is not None else None
-        if dadj is None:
-            if adj is not None:
-                dadj = _upload_adjacency(adj, st, body, kind)
-            else:
-                dadj = kernel_geom.build_device_adjacency(
-                    st.X, st.V0, body.h, body.dim, kind, nbsrange=body.nbsrange,
-                    dp_body=body.dp_body, notches=body.notches,
-                    correction=getattr(body, "kernel_correction", True))
+        corr = getattr(body, "kernel_correction", True)
+        if part is not None:
+            sub = part.sub
+            dadj = kernel_geom.build_device_adjacency(
+                st.X[sub], st.V0[sub], body.h, body.dim, kind, nbsrange=body.nbsrange,
+                dp_body=body.dp_body, notches=body.notches, correction=corr,
+                required=part.owned_mask)
+        else:
+            adj = body.adjacency
+            dadj = getattr(adj, "device", None) if adj is not None else None
+            if dadj is None:
+                if adj is not None:
+                    dadj = _upload_adjacency(adj, st, body, kind)
+                else:
+                    dadj = kernel_geom.build_device_adjacency(
+                        st.X, st.V0, body.h, body.dim, kind, nbsrange=body.nbsrange,
+                        dp_body=body.dp_body, notches=body.notches, correction=corr)
         self.adj = dadj
         # device particle order + neighbour tiles (kernel_geom.StepLayout)
         tile = int(os.environ.get("TLSPH_TILE", str(DEFAULT_TILE)))
-        lay = kernel_geom.StepLayout(dadj, tile=tile)
+        if part is not None:
+            part.complete(dadj)          # halo ids in exchange order (collective-free)
+            lay = kernel_geom.StepLayout(dadj, tile=tile, rows=part.owned_rows,
+                                         halo=part.halo_rows)
+        else:
+            lay = kernel_geom.StepLayout(dadj, tile=tile)
         rec = 64 if precision == "fp32" else 128          # pass-B bytes per staged particle
         if lay.tile and (lay.tile + lay.hmax) * rec > TILE_SMEM_LIMIT:
             lay.tile = 0                                   # halo too fat: gather from L2
         self.layout = lay
-        self.perm = lay.perm
-        self.perm_h = lay.perm.cpu().numpy().astype(np.int64)
+        n, n_all = lay.n, lay.n_all
+        self.n, self.n_all = n, n_all
+        self.perm = lay.perm                               # device pos -> adjacency id
         pl = lay.perm.long()
+        adj_ids = lay.perm.cpu().numpy().astype(np.int64)
+        # device position -> caller (global) particle index
+        self.gid = part.sub[adj_ids] if part is not None else adj_ids
+        self.perm_h = self.gid
+        if part is not None:
+            self.perm_global = torch.from_numpy(self.gid.astype(np.int32)).to(dev)
+        else:
+            self.perm_global = self.perm
         self.soff, self.sidx = lay.soff, lay.sidx
         R = self.R
         z = lambda *shape: torch.zeros(shape, dtype=R, device=dev)  # noqa: E731
+        # all planes use stride n_all; halo rows of own-only fields stay unused
         self.Xs = dadj.X.index_select(0, pl).t().contiguous()                 # 3 planes
         self.L = dadj.L.index_select(0, pl).t().contiguous().to(R)             # 9 planes
         V0 = np.asarray(st.V0, dtype=np.float64)
         m0 = np.asarray(st.m0, dtype=np.float64)
         self.uniform = bool(np.all(V0 == V0[0]) and np.all(m0 == m0[0]))
-        self.V0 = torch.from_numpy(V0[self.perm_h]).to(dev)
-        self.m0 = torch.from_numpy(m0[self.perm_h]).to(dev)
-        self.us = z(n, 4)
-        self.rb = z(n, 12)
-        self.v = z(3, n)
-        self.al = z(9, n)
-        self.sdot = z(n)
-        self.sddot = z(n)
-        self.Hh = z(n)
-        self.Cpd = z(6, n) if mat.model == Model.J2 else z(6, 1)
-        self.epbar = z(n)
-        self.a = z(3, n)
+        self.V0 = torch.from_numpy(V0[self.gid]).to(dev)
+        self.m0 = torch.from_numpy(m0[self.gid]).to(dev)
+        N = n_all
+        self.us = z(N, 4)
+        self.rb = z(N, 12)
+        self.v = z(3, N)
+        self.al = z(9, N)
+        self.sdot = z(N)
+        self.sddot = z(N)
+        self.Hh = z(N)
+        self.Cpd = z(6, N) if mat.model == Model.J2 else z(6, 1)
+        self.epbar = z(N)
+        self.a = z(3, N)
         f64 = lambda *shape: torch.zeros(shape, dtype=torch.float64, device=dev)  # noqa: E731
         # FP64 host-layout mirrors of F, S, psi (written only on output steps)
         self.F_out = f64(n, 3, 3) if mirrors else None
@@ -127,7 +151,7 @@ class DeviceBody:
         bcs = list(getattr(body, "bcs", []))
         if len(bcs) > _lib_max_bc():
             raise CaseError(f"body {body.mk}: more than {_lib_max_bc()} boundary conditions")
-        mask = np.zeros(self.n, dtype=np.uint32)
+        mask = np.zeros(self.host.X.shape[0], dtype=np.uint32)
         arr = (_lib.tl_bc * max(len(bcs), 1))()
         bit = 0
         self.bc_whole = 0
@@ -168,7 +192,7 @@ class DeviceBody:
         self.bcs_dev = torch.empty(nbytes, dtype=torch.uint8, device=self.dev)
         host = torch.frombuffer(bytearray(C.string_at(C.addressof(arr), nbytes)), dtype=torch.uint8)
         self.bcs_dev.copy_(host)
-        self.bcmask = torch.from_numpy(mask[self.perm_h].view(np.int32)).to(self.dev)
+        self.bcmask = torch.from_numpy(mask[self.gid].view(np.int32)).to(self.dev)
         rp = getattr(body, "restrictphi_expr", None)
         if rp is not None:
             ast = config.expressions.get(rp)
@@ -182,7 +206,7 @@ class DeviceBody:
     def _descriptor(self, mat, body, kind, precision):
         b = _lib.tl_body()
         b.n = self.n
-        b.n_all = self.n
+        b.n_all = self.n_all
         b.dim = int(body.dim)
         b.model = int(mat.model)
         b.fracture = int(bool(body.fracture))
@@ -215,7 +239,7 @@ class DeviceBody:
         b.tile, b.hmax = int(lay.tile), int(lay.hmax)
         if lay.tile:
             b.hoff, b.halo, b.slots = P(lay.hoff), P(lay.halo), P(lay.slots)
-        b.perm = P(self.perm)
+        b.perm = P(self.perm_global)
         b.V0, b.m0 = P(self.V0), P(self.m0)
         for k in ("us", "rb", "v", "al", "sdot", "sddot", "Hh", "Cpd", "epbar", "a"):
             setattr(b, k, P(getattr(self, k)))
@@ -239,8 +263,8 @@ class DeviceBody:
         layout and order."""
         torch = _torch()
         st = self.host
-        R, dev, pm = self.R, self.dev, self.perm_h
-        us = np.empty((self.n, 4))
+        R, dev, pm = self.R, self.dev, self.gid       # all n_all device rows
+        us = np.empty((self.n_all, 4))
         us[:, :3] = st.u[pm]
         us[:, 3] = st.s[pm]
         self.us.copy_(torch.from_numpy(us).to(dev, R))
@@ -259,11 +283,12 @@ class DeviceBody:
     def pull_state(self, full=True):
         """Refresh body.state (host, original order) from the device."""
         st = self.host
-        pm = self.perm_h
+        n = self.n
+        pm = self.gid[:n]                              # owned device rows only
         self.dirty = False
 
         def put(dst, val):
-            dst[pm] = val
+            dst[pm] = val[:n]
 
         us = self.us.double().cpu().numpy()
         put(st.u, us[:, :3])
@@ -280,14 +305,13 @@ class DeviceBody:
             put(st.psi_e, self.psi_out.cpu().numpy())
             put(st.psi_plus, self.psip_out.cpu().numpy())
         if self.body.material.model == Model.J2 and st.Cp is not None:
-            c = self.Cpd.double().cpu().numpy()
-            Cp = np.empty((self.n, 3, 3))
+            c = self.Cpd.double().cpu().numpy()[:, :n]
+            Cp = np.empty((n, 3, 3))
             Cp[:, 0, 0], Cp[:, 1, 1], Cp[:, 2, 2] = 1.0 + c[0], 1.0 + c[1], 1.0 + c[2]
             Cp[:, 0, 1] = Cp[:, 1, 0] = c[3]
             Cp[:, 0, 2] = Cp[:, 2, 0] = c[4]
             Cp[:, 1, 2] = Cp[:, 2, 1] = c[5]
             put(st.Cp, Cp)
-        self.body.plastic_work = self.pw_base + float(self.pw_acc.item())
 
     def dtinfo(self):
         return _lib.tl_dtinfo(h=float(self.body.h), c0=float(self.body.material.c0),
@@ -381,7 +405,8 @@ class ProgramTable:
 class DeviceSimulation:
     """Drop-in for solidsph.stepper.Simulation running on one B200."""
 
-    def __init__(self, config, trace=None, precision="fp64", stream=None, mirrors=True):
+    def __init__(self, config, trace=None, precision="fp64", stream=None, mirrors=True,
+                 group=None):
         if precision not in ("fp32", "fp64"):
             raise ValueError("precision must be 'fp32' or 'fp64'")
         L = _lib.lib()  # fails loudly without the native library / GPU
@@ -402,9 +427,25 @@ class DeviceSimulation:
             raise NotImplementedError(
                 "multi-body cases need the penalty contact phase, which is not on the "
                 "device yet (SURVEY.md 8(f) rank 3)")
+        self.group = group
+        self.world = 1
+        import torch.distributed as tdist
+        if tdist.is_available() and tdist.is_initialized():
+            self.world = tdist.get_world_size(group)
+        parts = [self._partition(b) if self.world > 1 else None for b in self.bodies]
         self.programs = ProgramTable()
-        self.dbodies = [DeviceBody(b, config, precision, self.programs, mirrors)
-                        for b in self.bodies]
+        self.dbodies = [DeviceBody(b, config, precision, self.programs, mirrors, part)
+                        for b, part in zip(self.bodies, parts)]
+        for db in self.dbodies:
+            db.exchange = None
+            if db.part is not None:
+                lay = db.layout
+                pos = lay.iperm.index_select(
+                    0, torch.from_numpy(db.part.owned_rows).to(lay.iperm.device)).cpu().numpy()
+                plan = dist.build_halo_plan(db.part.owned_gid, pos, db.part.needed_gid,
+                                            db.part.owner, group=group)
+                assert plan.n_halo == db.n_all - db.n
+                db.exchange = dist.HaloExchange(plan, "cuda", group=group)
         for b, db in zip(self.bodies, self.dbodies):
             b.state = DeviceState(db.host, db)
         prog_table = self.programs.upload()
@@ -417,6 +458,16 @@ class DeviceSimulation:
         self._lib = L
         self._dt_arr = (_lib.tl_dtinfo * len(self.dbodies))(*[db.dtinfo() for db in self.dbodies])
         self.workspaces = [None for _ in self.bodies]
+
+    def _partition(self, body):
+        """This rank's slab of ``body`` (dist.py): equal-count slabs along the
+        longest axis; the halo region extends one interaction reach."""
+        import torch.distributed as tdist
+        X = body.state.X
+        owner, axis = dist.slab_owner(X, self.world)
+        reach = (body.nbsrange * body.dp_body * (1.0 + 1e-9) if body.nbsrange is not None
+                 else 2.0 * body.h)
+        return dist.BodyPartition(X, owner, tdist.get_rank(self.group), axis, reach)
 
     # -- plumbing ------------------------------------------------------------
     def _st(self):
@@ -451,11 +502,17 @@ class DeviceSimulation:
         return c
 
     def _pass_a(self, db):
+        if db.exchange is not None:
+            db.exchange.exchange(db.us)         # halo (u, s) from the owners
         _lib.check(self._lib.tl_pass_a(self._st(), C.byref(db.desc)), "tl_pass_a")
 
     def _pass_b(self, db, mode):
+        if db.exchange is not None:
+            db.exchange.exchange(db.rb)         # halo (P L, v) from the owners
         _lib.check(self._lib.tl_reset_red(self._st(), _lib.ptr(db.red)), "tl_reset_red")
         _lib.check(self._lib.tl_pass_b(self._st(), C.byref(db.desc), mode), "tl_pass_b")
+        if db.exchange is not None:
+            dist.allreduce(db.red, "max", self.group)   # global dt maxima, exact
         if int(db.body.material.model) == int(Model.J2):
             _lib.check(self._lib.tl_reduce_partials(self._st(), _lib.ptr(db.pw_partial),
                                                     db.nblocks, _lib.ptr(db.pw_acc)),
@@ -476,7 +533,21 @@ class DeviceSimulation:
                 self._pass_b(db, 2)
 
     def _check_errors(self):
-        """Raise the reference's exceptions for events recorded on the device."""
+        """Raise the reference's exceptions for events recorded on the device.
+        Multi-GPU: every rank raises when any rank recorded an event."""
+        if self.world > 1:
+            flag = _torch().zeros(1, dtype=_torch().int64, device="cuda")
+            for db in self.dbodies:
+                c = db.counters
+                flag |= ((c[1] != 0) | (c[4] != 0) | (c[5] != 0) | (c[2] != INT64_MAX)
+                         | (c[3] != INT64_MAX)).to(flag.dtype).reshape(1)
+            dist.allreduce(flag, "max", self.group)
+            if int(flag.item()):
+                local = any(int(db.counters[k]) != v for db in self.dbodies
+                            for k, v in ((1, 0), (4, 0), (5, 0), (2, INT64_MAX),
+                                         (3, INT64_MAX)))
+                if not local:
+                    raise SimulationError("numerical error reported by another rank")
         for db in self.dbodies:
             c = db.counters.cpu().numpy()
             mk = db.body.mk
@@ -514,7 +585,10 @@ class DeviceSimulation:
         counters are refreshed now."""
         for db in self.dbodies:
             db.dirty = True
-            db.body.plastic_work = db.pw_base + float(db.pw_acc.item())
+            pw = db.pw_acc.clone()
+            if self.world > 1:
+                dist.allreduce(pw, "sum", self.group)
+            db.body.plastic_work = db.pw_base + float(pw.item())
 
     def pull_host(self):
         """Copy the device state into every body.state now."""
