@@ -75,7 +75,9 @@ __global__ void k_halo_keys(int64_t n, int T, const int64_t* __restrict__ indptr
     int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (p >= n) return;
     const int64_t tile = p / T;
-    const int64_t t0 = tile * T, t1 = t0 + T;
+    // the last tile may be partial: positions >= n are the multi-GPU halo
+    // block, never tile members
+    const int64_t t0 = tile * T, t1 = min(t0 + T, n);
     for (int64_t k = indptr[p]; k < indptr[p + 1]; ++k) {
         const int64_t q = indices[k];
         keys[k] = (q >= t0 && q < t1) ? ~0ull : ((uint64_t)tile << 32 | (uint64_t)q);
@@ -122,7 +124,7 @@ __global__ void k_slots(int64_t n, int T, int G, const int64_t* __restrict__ ind
         uint16_t s = self;
         if (k < rl) {
             const int64_t q = indices[rb + k];
-            if (q >= t0 && q < t0 + T) {
+            if (q >= t0 && q < t0 + T && q < n) {
                 s = (uint16_t)(q - t0);
             } else {
                 int64_t lo = 0, hi = hn;

@@ -1,7 +1,8 @@
 """Multi-rank device path (slabs + halo exchange) on the single available
 B200: 2 and 3 ranks share cuda:0 over gloo (halo buffers staged through the
-host).  Owned rows must be bit-identical to the single-rank device run --
-same rows, same CSR summation order, same inputs."""
+host).  FP64: owned rows must be bit-identical to the single-rank device run
+-- same rows, same CSR summation order, same inputs.  FP32:
+within 1e-5 (tile-relative coordinates round differently per tiling)."""
 import os
 import socket
 
@@ -52,6 +53,7 @@ def _worker(rank, world, port, tag, precision, out_dir):
 
 @pytest.mark.parametrize("tag,world,precision", [("kalthoff3d", 2, "fp64"),
                                                  ("kalthoff2d_p", 3, "fp64"),
+                                                 ("taylor3d", 2, "fp64"),
                                                  ("taylor3d", 2, "fp32")])
 def test_multi_rank_device_bit_identical(tag, world, precision, tmp_path):
     from paper_2602_15149_b200.simulation import DeviceSimulation
@@ -72,6 +74,17 @@ def test_multi_rank_device_bit_identical(tag, world, precision, tmp_path):
         assert d["n_halo"] > 0
         seen[g] = True
         for k in ("u", "v", "s", "S"):
-            assert np.array_equal(d[k], getattr(st, k)[g]), (r, k)
-        assert float(d["dt"]) == dt_ref
+            if precision == "fp64":
+                assert np.array_equal(d[k], getattr(st, k)[g]), (r, k)
+            else:
+                # FP32 neighbour differences are formed relative to each tile's
+                # origin, and tiles differ between the slab and the whole body:
+                # identical up to FP32 rounding of the reference coordinates
+                ref = getattr(st, k)
+                err = np.abs(d[k] - ref[g]).max() / max(np.abs(ref).max(), 1e-300)
+                assert err <= 1e-5, (r, k, err)
+        if precision == "fp64":
+            assert float(d["dt"]) == dt_ref
+        else:
+            assert abs(float(d["dt"]) - dt_ref) <= 1e-5 * dt_ref
     assert seen.all()
