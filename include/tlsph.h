@@ -31,7 +31,7 @@ enum {
     TL_ERR_CASE = -4
 };
 
-#define TL_ABI_VERSION 1
+#define TL_ABI_VERSION 2
 
 int tl_abi_version(void);
 /* sizeof of the ABI structs, for binding checks: 0 tl_body, 1 tl_clock,
@@ -190,9 +190,23 @@ int tl_csr_permute(tl_stream_t st, int64_t n, const int32_t* perm, const int32_t
 int tl_tile_halo(tl_stream_t st, int64_t n, int32_t T, const int64_t* indptr,
                  const int32_t* indices, int64_t nnz, int32_t* halo, int64_t* tile_count,
                  int64_t* n_halo);
+/* shared-memory slot of every halo entry: res = 8 puts halo particle q at a
+ * slot == q (mod 8), the residue of a member's slot, so a quarter-warp's
+ * 128-bit loads of translated neighbours avoid bank conflicts (tiles whose
+ * aligned extent exceeds cap > 0 are packed densely); res = 1 packs every
+ * tile densely.  extent[t] (device int32[ntile]) = halo slots tile t uses */
+int tl_tile_hslots(tl_stream_t st, int64_t ntile, int32_t T, int32_t res, int32_t cap,
+                   const int64_t* hoff, const int32_t* halo, uint16_t* hslot, int32_t* extent);
+/* staged position records (x, y, z, w) of every slot of every tile, in slot
+ * order from toff[t] (device int64[ntile+1]); FP32 (precision 4): relative to
+ * the tile's first member, FP64: absolute; w = per-particle weight or 0 when
+ * w == NULL.  out: device Real[4*toff[ntile]], zeroed by the caller */
+int tl_tile_pos(tl_stream_t st, int64_t n, int64_t n_all, int32_t T, int64_t ntile,
+                const int64_t* hoff, const int32_t* halo, const uint16_t* hslot, const int64_t* toff,
+                const double* X, const double* w, int32_t precision, void* out);
 int tl_tile_slots(tl_stream_t st, int64_t n, int32_t T, int32_t G, const int64_t* indptr,
                   const int32_t* indices, const int64_t* hoff, const int32_t* halo,
-                  const int64_t* soff, uint16_t* slots);
+                  const uint16_t* hslot, const int64_t* soff, uint16_t* slots);
 
 /* ---------------------------------------------------------------------------
  * Fused device-resident step (stepper.py:77-209, dynamics.py:28-217,
@@ -256,13 +270,21 @@ typedef struct {
     const int64_t* soff;
     const int32_t* sidx;
     /* shared-memory tiles (tile > 0): CTA = `tile` consecutive particles;
-     * hoff[t]..hoff[t+1] indexes its halo particles in `halo`; slots are
-     * uint16 local indices (member p - t*tile, or tile + halo position),
-     * grouped TL_SELL_GROUP per lane, same slice offsets as sidx */
+     * hoff[t]..hoff[t+1] indexes its halo particles in `halo`, staged at
+     * shared slots `hslot`; slots are uint16 local indices (member
+     * p - t*tile, or the halo entry's hslot), grouped TL_SELL_GROUP per lane,
+     * same slice offsets as sidx.  hmax = max halo slot extent over tiles;
+     * every tile uses the plane stride tile + hmax */
     int32_t tile, hmax;
     const int64_t* hoff;
     const int32_t* halo;
     const uint16_t* slots;
+    const uint16_t* hslot;
+    /* staged position records (tl_tile_pos) with V0 (pass A) and m0 (pass B)
+     * weights -- the same array when uniform; toff[t] = first record of tile t */
+    const int64_t* toff;
+    const void* tpos_a;
+    const void* tpos_b;
     /* geometry */
     const double* Xs;       /* FP64 planes x,y,z */
     const void* L;          /* 9 planes, correction matrix L_i */

@@ -13,7 +13,7 @@ import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("TLSPH_LIB", os.path.join(HERE, "libtlsph.so"))
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 _lib = None
 
@@ -74,7 +74,8 @@ _BODY_FIELDS += [(k, D) for k in ("h", "inv_h", "alpha", "rho0", "lam", "mu", "k
                                   "V0c", "m0c", "dp_body", "jac_tol")]
 _BODY_FIELDS += [("f0", D * 3)]
 _BODY_FIELDS += [("soff", P), ("sidx", P), ("tile", I32), ("hmax", I32), ("hoff", P),
-                 ("halo", P), ("slots", P)]
+                 ("halo", P), ("slots", P), ("hslot", P), ("toff", P), ("tpos_a", P),
+                 ("tpos_b", P)]
 _BODY_FIELDS += [(k, P) for k in ("Xs", "L", "V0", "m0", "us", "rb", "v", "al",
                                   "sdot", "sddot", "Hh", "Cpd", "epbar", "a", "F_out", "S_out",
                                   "psi_out", "psip_out", "perm", "bcmask", "bcs", "progs", "clock", "red",
@@ -113,7 +114,9 @@ _SIGS = {
     "tl_csr_permute_counts": (INT, [P, I64, P, P, P]),
     "tl_csr_permute": (INT, [P, I64, P, P, P, P, P, P]),
     "tl_tile_halo": (INT, [P, I64, I32, P, P, I64, P, P, C.POINTER(I64)]),
-    "tl_tile_slots": (INT, [P, I64, I32, I32, P, P, P, P, P, P]),
+    "tl_tile_hslots": (INT, [P, I64, I32, I32, I32, P, P, P, P]),
+    "tl_tile_pos": (INT, [P, I64, I64, I32, I64, P, P, P, P, P, P, I32, P]),
+    "tl_tile_slots": (INT, [P, I64, I32, I32, P, P, P, P, P, P, P]),
     "tl_pass_a": (INT, [P, C.POINTER(tl_body)]),
     "tl_pass_b": (INT, [P, C.POINTER(tl_body), INT]),
     "tl_predict": (INT, [P, C.POINTER(tl_body)]),

@@ -363,25 +363,53 @@ __device__ __forceinline__ R planeR(const void* p, int64_t stride, int c, int64_
 template <typename R>
 using V4 = typename tl::Vec4<R>::T;
 
-// pass A pair: D += V0_j fac du (x) r0 ; M += 2 (s_i - s_j) V0_j fac / r^2 r0 r0^T
+// Kernel shape.  Both passes need fac_ij = (dW/dr)/r at r = |r0_ij|; it
+// factors into a per-body constant times a shape w(r):
+//   Wendland C2 : fac = -5 alpha/h^2 * t^3,          t = max(1 - r/(2h), 0)
+//   cubic spline: fac = alpha/h * ((-3 + 2.25 q)/h   (q < 1)
+//                                  | -0.75 (2-q)^2/r (1 <= q < 2) | 0)
+// (kernel_geom.py:21-62 with q = r/h), so the pair loops carry w only and
+// the constant (with V0 / m0 when uniform) is applied once per particle.
+// r2 is floored so the self-padding entries of the neighbour slices (r0 = 0)
+// give a finite w and vanishing terms.
+template <typename R, int KIND>
+__device__ __forceinline__ R kshape(R r2, R inv_h, R& rs) {
+    rs = tl::rsqrt_floor(r2);
+    const R r = r2 * rs;
+    if (KIND == 2) {
+        const R t = fmax(R(1) - r * (R(0.5) * inv_h), R(0));
+        return t * t * t;
+    }
+    const R q = r * inv_h, tm = R(2) - q;
+    return q < R(1) ? (R(-3) + R(2.25) * q) * inv_h : (q < R(2) ? R(-0.75) * tm * tm * rs : R(0));
+}
+
+template <typename R, int KIND>
+__device__ __forceinline__ R kshape_const(const tl_body& b) {
+    return KIND == 2 ? R(-5.0 * b.alpha * b.inv_h * b.inv_h) : R(b.alpha * b.inv_h);
+}
+
+// pass A pair (w = V0_j-weighted shape):
+//   D += w (u_j - u_i) (x) r0 ;  M += (s_i - s_j) w / r^2  r0 r0^T
 template <typename R, int DIM, bool FRAC, int KIND>
-__device__ __forceinline__ void pair_a(R dx, R dy, R dz, const V4<R>& uj, R vj, const V4<R>& ui,
-                                       bool gated, R inv_h, R a_ih, R* D, R* M) {
+__device__ __forceinline__ void pair_a(R dx, R dy, R dz, const V4<R>& uj, R vj, bool uni,
+                                       const V4<R>& ui, bool gated, R inv_h, R* D, R* M) {
     const R r2 = dx * dx + dy * dy + dz * dz;
-    const R rs = tl::rsqrt_pos(r2);
-    const R wf = vj * tl::kernel_fac<R, KIND>(r2, rs, inv_h, a_ih);
+    R rs;
+    R w = kshape<R, KIND>(r2, inv_h, rs);
+    if (!uni) w *= vj;
     if (!gated) {
-        const R du0 = wf * (uj.x - ui.x), du2 = wf * (uj.z - ui.z);
+        const R du0 = w * (uj.x - ui.x), du2 = w * (uj.z - ui.z);
         D[0] += du0 * dx; D[2] += du0 * dz;
         D[6] += du2 * dx; D[8] += du2 * dz;
         if (DIM == 3) {
-            const R du1 = wf * (uj.y - ui.y);
+            const R du1 = w * (uj.y - ui.y);
             D[1] += du0 * dy; D[7] += du2 * dy;
             D[3] += du1 * dx; D[4] += du1 * dy; D[5] += du1 * dz;
         }
     }
     if (FRAC) {
-        const R c = R(2) * (ui.w - uj.w) * wf * (rs * rs);
+        const R c = (ui.w - uj.w) * (w * (rs * rs));
         const R cx = c * dx, cz = c * dz;
         M[0] += cx * dx; M[2] += cz * dz; M[4] += cx * dz;
         if (DIM == 3) {
@@ -394,36 +422,36 @@ __device__ __forceinline__ void pair_a(R dx, R dy, R dz, const V4<R>& uj, R vj, 
 __device__ __forceinline__ float fdiv(float a, float b) { return __fdividef(a, b); }
 __device__ __forceinline__ double fdiv(double a, double b) { return a / b; }
 
-// pass B pair: s1 += m fac r0 ; s2 += m fac PL_j r0 ; s3 += m fac pi_ij r0
+// pass B pair (w = m_j-weighted shape, wr = w r0):
+//   s1 += wr ;  s2 += PL_j wr ;  s3 += (B2 G'^2 - B1 G') wr
+// with G' = (v_i - v_j).r0 / (r^2 + 0.001 h^2); B2 = beta2 h^2, B1 = beta1 c0 h
 template <typename R, int DIM, int KIND>
 __device__ __forceinline__ void pair_b(R dx, R dy, R dz, const V4<R>& q0, const V4<R>& q1,
-                                       const V4<R>& q2, R mj, R vi0, R vi1, R vi2, bool visc,
-                                       R inv_h, R a_ih, R hR, R eps_h2, R b2, R b1c0, R inv_rho,
-                                       R* s1, R* s2, R* s3) {
+                                       const V4<R>& q2, R mj, bool uni, R vi0, R vi1, R vi2,
+                                       bool visc, R inv_h, R eps_h2, R B2, R B1, R* s1, R* s2,
+                                       R* s3) {
     const R r2 = dx * dx + dy * dy + dz * dz;
-    const R wf = mj * tl::kernel_fac<R, KIND>(r2, tl::rsqrt_pos(r2), inv_h, a_ih);
-    R p0, p1, p2;
+    R rs;
+    R w = kshape<R, KIND>(r2, inv_h, rs);
+    if (!uni) w *= mj;
+    const R wx = w * dx, wz = w * dz;
+    const R wy = DIM == 3 ? w * dy : R(0);
+    s1[0] += wx; s1[2] += wz;
     if (DIM == 3) {
-        p0 = q0.x * dx + q0.y * dy + q0.z * dz;
-        p1 = q0.w * dx + q1.x * dy + q1.y * dz;
-        p2 = q1.z * dx + q1.w * dy + q2.x * dz;
+        s1[1] += wy;
+        s2[0] += q0.x * wx + q0.y * wy + q0.z * wz;
+        s2[1] += q0.w * wx + q1.x * wy + q1.y * wz;
+        s2[2] += q1.z * wx + q1.w * wy + q2.x * wz;
     } else {
-        p0 = q0.x * dx + q0.z * dz;
-        p1 = R(0);
-        p2 = q1.z * dx + q2.x * dz;
-    }
-    s1[0] += wf * dx; s1[2] += wf * dz;
-    s2[0] += wf * p0; s2[2] += wf * p2;
-    if (DIM == 3) {
-        s1[1] += wf * dy;
-        s2[1] += wf * p1;
+        s2[0] += q0.x * wx + q0.z * wz;
+        s2[2] += q1.z * wx + q2.x * wz;
     }
     if (visc) {
         const R dvr = (vi0 - q2.y) * dx + (DIM == 3 ? (vi1 - q2.z) * dy : R(0)) + (vi2 - q2.w) * dz;
-        const R Gv = fdiv(hR * dvr, r2 + eps_h2);
-        const R pw = (b2 * Gv * Gv - b1c0 * Gv) * inv_rho * wf;
-        s3[0] += pw * dx; s3[2] += pw * dz;
-        if (DIM == 3) s3[1] += pw * dy;
+        const R g = fdiv(dvr, r2 + eps_h2);
+        const R pw = (B2 * g - B1) * g;
+        s3[0] += pw * wx; s3[2] += pw * wz;
+        if (DIM == 3) s3[1] += pw * wy;
     }
 }
 
@@ -458,52 +486,105 @@ struct SlotPipe {
     }
 };
 
-// shared-memory tile of a CTA: positions (FP32: relative to the tile
-// origin, FP64: absolute) and the gathered record of every member and halo
-// particle, staged with coalesced loads once per CTA
+// Shared-memory tile of a CTA.  Two arrays indexed by slot:
+//   pos[slot]             the staged position record (x, y, z, w) -- a copy of
+//                         the tile's block of tl_tile_pos records;
+//   rec[slot * NREC + r]  the NREC gathered records of the particle, stored
+//                         contiguously (48-byte FP32 pass-B records: the
+//                         stride 3 is odd, so slots distinct mod 8 still hit
+//                         distinct bank groups).
+// Members sit at slot p - p0, halo particles at their residue-aligned hslot
+// (tiles.cu k_hslots).  The capacity S = tile + hmax is the same for every
+// CTA of a launch.
 template <typename R, int NREC>
 struct Tile {
-    R* x;
-    R* y;
-    R* z;
-    V4<R>* rec;   // NREC records of 4 per particle
-    R* m;         // V0 or m0 when not uniform
-    int S;
+    V4<R>* pos;
+    V4<R>* rec;
 };
+
+template <typename R, int NREC>
+__host__ __device__ constexpr size_t tile_bytes(int S) {
+    return (size_t)S * (NREC + 1) * sizeof(V4<R>);
+}
 
 template <typename R, int NREC>
 __device__ __forceinline__ Tile<R, NREC> tile_layout(unsigned char* smem, int S) {
     Tile<R, NREC> t;
-    t.S = S;
-    t.rec = reinterpret_cast<V4<R>*>(smem);
-    t.x = reinterpret_cast<R*>(t.rec + NREC * S);
-    t.y = t.x + S;
-    t.z = t.y + S;
-    t.m = t.z + S;
+    t.pos = reinterpret_cast<V4<R>*>(smem);
+    t.rec = t.pos + S;
     return t;
 }
 
+// Stage a tile with asynchronous copies only: thread 0 arms the barrier and
+// issues two TMA bulk copies (the contiguous position block and the members'
+// records); every thread then issues 16-byte LDGSTS gathers of the halo
+// records.  No register round trip, every load of the CTA in flight at once.
 template <typename R, int NREC>
-__device__ __forceinline__ void stage_tile(const tl_body& b, Tile<R, NREC>& t, int64_t p0, int T,
-                                           int H, int64_t hb, const R* src, const double* mass,
-                                           bool uni, double ox, double oy, double oz) {
-    const int64_t N = b.n_all;
-    for (int s = threadIdx.x; s < T + H; s += blockDim.x) {
-        int64_t q = s < T ? p0 + s : (int64_t)b.halo[hb + s - T];
-        if (s < T && q >= b.n) q = p0;   // tail of the last tile: any valid particle
-        t.x[s] = R(b.Xs[q] - ox);
-        t.y[s] = R(b.Xs[N + q] - oy);
-        t.z[s] = R(b.Xs[2 * N + q] - oz);
-#pragma unroll
-        for (int r = 0; r < NREC; ++r) t.rec[r * t.S + s] = tl::ldg4(src + 4 * NREC * q + 4 * r);
-        if (!uni) t.m[s] = R(mass[q]);
+__device__ __forceinline__ void stage_tile(const tl_body& b, const Tile<R, NREC>& t, int64_t tile,
+                                           const void* tpos, const R* src, uint64_t* bar) {
+    const int T = b.tile;
+    const int64_t p0 = tile * T;
+    const int64_t hb = b.hoff[tile];
+    const int H = (int)(b.hoff[tile + 1] - hb);
+    if (threadIdx.x == 0) {
+        const int64_t nmem = min((int64_t)T, b.n - p0);
+        const int64_t r0 = b.toff[tile];
+        const uint32_t pos_bytes = (uint32_t)((b.toff[tile + 1] - r0) * sizeof(V4<R>));
+        const uint32_t mem_bytes = (uint32_t)(nmem * NREC * sizeof(V4<R>));
+        tl::mbar_init(bar, 1);
+        tl::mbar_expect_tx(bar, pos_bytes + mem_bytes);
+        tl::bulk_g2s(t.pos, static_cast<const V4<R>*>(tpos) + r0, pos_bytes, bar);
+        tl::bulk_g2s(t.rec, src + p0 * 4 * NREC, mem_bytes, bar);
     }
+    constexpr int CH = (int)(sizeof(V4<R>) / 16);   // 16-byte chunks per record
+    for (int s = threadIdx.x; s < H; s += blockDim.x) {
+        const int64_t q = b.halo[hb + s];
+        const int d = b.hslot[hb + s];
+        const char* g = reinterpret_cast<const char*>(src + q * 4 * NREC);
+        char* sm = reinterpret_cast<char*>(t.rec + (int64_t)d * NREC);
+#pragma unroll
+        for (int c = 0; c < NREC * CH; ++c) tl::cp_async16(sm + 16 * c, g + 16 * c);
+    }
+    tl::cp_async_wait_all();
     __syncthreads();
+    tl::mbar_wait(bar, 0);
 }
 
-template <typename R, int NREC>
-__host__ __device__ constexpr size_t tile_bytes(int S) {
-    return (size_t)S * (NREC * sizeof(V4<R>) + 4 * sizeof(R));
+// L2 prefetch of the tile's own-particle planes the epilogue reads after the
+// neighbour loop, issued by one thread while the tile is being staged
+template <typename T>
+__device__ __forceinline__ void prefetch_planes(const void* base, int64_t stride, int nplanes,
+                                                int64_t p0, int64_t cnt) {
+    if (!base) return;
+    const T* p = static_cast<const T*>(base);
+    for (int c = 0; c < nplanes; ++c) tl::l2_prefetch(p + c * stride + p0, cnt * sizeof(T));
+}
+
+template <typename R, int MODEL, bool FRAC>
+__device__ __forceinline__ void prefetch_own_a(const tl_body& b, int64_t p0) {
+    const int64_t cnt = min((int64_t)b.tile, b.n - p0), N = b.n_all;
+    prefetch_planes<R>(b.L, N, 9, p0, cnt);
+    prefetch_planes<R>(b.v, N, 3, p0, cnt);
+    if (FRAC) {
+        prefetch_planes<R>(b.sdot, N, 1, p0, cnt);
+        prefetch_planes<R>(b.Hh, N, 1, p0, cnt);
+    }
+    if (MODEL == 3) {
+        prefetch_planes<R>(b.Cpd, N, 6, p0, cnt);
+        prefetch_planes<R>(b.epbar, N, 1, p0, cnt);
+    }
+}
+
+template <typename R, bool FRAC>
+__device__ __forceinline__ void prefetch_own_b(const tl_body& b, int64_t p0) {
+    const int64_t cnt = min((int64_t)b.tile, b.n - p0), N = b.n_all;
+    if (b.visc) prefetch_planes<R>(b.al, N, 9, p0, cnt);
+    tl::l2_prefetch(static_cast<const R*>(b.us) + 4 * p0, cnt * 4 * sizeof(R));
+    if (FRAC) {
+        prefetch_planes<R>(b.sdot, N, 1, p0, cnt);
+        prefetch_planes<R>(b.sddot, N, 1, p0, cnt);
+    }
+    if (b.bcmask) prefetch_planes<int32_t>(b.bcmask, N, 1, p0, cnt);
 }
 
 // ---------------------------------------------------------------------------
@@ -520,16 +601,11 @@ __global__ void __launch_bounds__(kThreads, TL_MINB_A(R)) k_pass_a(const tl_body
     const bool uni = b.uniform != 0;
     // tile staging (TILED): every thread of the CTA takes part
     Tile<R, 1> tl_;
-    double ox = 0.0, oy = 0.0, oz = 0.0;
+    __shared__ uint64_t bar;
     if (TILED) {
-        const int64_t p0 = (int64_t)blockIdx.x * blockDim.x;
-        const int64_t hb = b.hoff[blockIdx.x];
-        const int H = (int)(b.hoff[blockIdx.x + 1] - hb);
-        if (sizeof(R) == 4) {
-            ox = b.Xs[p0]; oy = b.Xs[b.n_all + p0]; oz = b.Xs[2 * b.n_all + p0];
-        }
-        tl_ = tile_layout<R, 1>(smem, blockDim.x + H);
-        stage_tile<R, 1>(b, tl_, p0, blockDim.x, H, hb, us, b.V0, uni, ox, oy, oz);
+        if (threadIdx.x == 32) prefetch_own_a<R, MODEL, FRAC>(b, blockIdx.x * (int64_t)blockDim.x);
+        tl_ = tile_layout<R, 1>(smem, b.tile + b.hmax);
+        stage_tile<R, 1>(b, tl_, blockIdx.x, b.tpos_a, us, &bar);
     }
     if (i < b.n) {
         const int64_t N = b.n_all;
@@ -537,19 +613,16 @@ __global__ void __launch_bounds__(kThreads, TL_MINB_A(R)) k_pass_a(const tl_body
         const int64_t w = i >> 5;
         const int64_t base = b.soff[w];
         const int len = (int)((b.soff[w + 1] - base) >> 5);
-        const double xi = b.Xs[i], yi = b.Xs[N + i], zi = b.Xs[2 * N + i];
-        const auto ui = tl::ld4(us + 4 * i);
+        const auto ui = TILED ? tl_.rec[threadIdx.x] : tl::ld4(us + 4 * i);
         const R si = ui.w;
         const bool gated = FRAC && si <= R(b.s_l);
-        const R inv_h = R(b.inv_h), a_ih = R(b.alpha * b.inv_h);
+        const R inv_h = R(b.inv_h);
         R D[9];
 #pragma unroll
         for (int q = 0; q < 9; ++q) D[q] = R(0);
         R M[6] = {R(0), R(0), R(0), R(0), R(0), R(0)};   // xx yy zz xy xz yz
-        const R V0c = R(b.V0c);
         if (TILED) {
-            const int me = threadIdx.x;
-            const R xl = tl_.x[me], yl = tl_.y[me], zl = tl_.z[me];
+            const auto me = tl_.pos[threadIdx.x];
             const uint16_t* sl = b.slots + base + lane * G;
             SlotPipe<G> pipe(sl, len);
             for (int k = 0; k < len; k += G) {
@@ -558,13 +631,14 @@ __global__ void __launch_bounds__(kThreads, TL_MINB_A(R)) k_pass_a(const tl_body
 #pragma unroll
                 for (int q = 0; q < G; ++q) {
                     const int j = l[q];
-                    const R vj = uni ? V0c : tl_.m[j];
-                    pair_a<R, DIM, FRAC, KIND>(xl - tl_.x[j], DIM == 3 ? yl - tl_.y[j] : R(0),
-                                               zl - tl_.z[j], tl_.rec[j], vj, ui, gated, inv_h,
-                                               a_ih, D, M);
+                    const auto pj = tl_.pos[j];
+                    pair_a<R, DIM, FRAC, KIND>(me.x - pj.x, DIM == 3 ? me.y - pj.y : R(0),
+                                               me.z - pj.z, tl_.rec[j], pj.w, uni, ui, gated,
+                                               inv_h, D, M);
                 }
             }
         } else {
+            const double xi = b.Xs[i], yi = b.Xs[N + i], zi = b.Xs[2 * N + i];
             const int32_t* sidx = b.sidx + base + lane;
             const double* __restrict__ Xp = b.Xs;
             const double* __restrict__ Yp = b.Xs + N;
@@ -584,15 +658,21 @@ __global__ void __launch_bounds__(kThreads, TL_MINB_A(R)) k_pass_a(const tl_body
                     yj[q] = DIM == 3 ? __ldg(Yp + jj[q]) : 0.0;
                     zj[q] = __ldg(Zp + jj[q]);
                     uj[q] = tl::ldg4(us + 4 * (int64_t)jj[q]);
-                    vj[q] = V0c;
-                    if (!uni) vj[q] = R(__ldg(b.V0 + jj[q]));
+                    vj[q] = uni ? R(0) : R(__ldg(b.V0 + jj[q]));
                 }
 #pragma unroll
                 for (int q = 0; q < G; ++q)
                     pair_a<R, DIM, FRAC, KIND>(R(xi - xj[q]), DIM == 3 ? R(yi - yj[q]) : R(0),
-                                               R(zi - zj[q]), uj[q], vj[q], ui, gated, inv_h, a_ih,
+                                               R(zi - zj[q]), uj[q], vj[q], uni, ui, gated, inv_h,
                                                D, M);
             }
+        }
+        {   // kernel constant (and V0 when uniform), once per particle
+            const R ck = kshape_const<R, KIND>(b) * (uni ? R(b.V0c) : R(1));
+#pragma unroll
+            for (int q = 0; q < 9; ++q) D[q] *= ck;
+#pragma unroll
+            for (int q = 0; q < 6; ++q) M[q] *= R(2) * ck;
         }
         // L_i (9 planes)
         R Li[9];
@@ -863,16 +943,11 @@ __global__ void __launch_bounds__(kThreads, TL_MINB_B(R)) k_pass_b(const tl_body
     const R* rbp = static_cast<const R*>(b.rb);
     const bool uni = b.uniform != 0;
     Tile<R, 3> tl_;
+    __shared__ uint64_t bar;
     if (TILED) {
-        const int64_t p0 = (int64_t)blockIdx.x * blockDim.x;
-        const int64_t hb = b.hoff[blockIdx.x];
-        const int H = (int)(b.hoff[blockIdx.x + 1] - hb);
-        double ox = 0.0, oy = 0.0, oz = 0.0;
-        if (sizeof(R) == 4) {
-            ox = b.Xs[p0]; oy = b.Xs[b.n_all + p0]; oz = b.Xs[2 * b.n_all + p0];
-        }
-        tl_ = tile_layout<R, 3>(smem, blockDim.x + H);
-        stage_tile<R, 3>(b, tl_, p0, blockDim.x, H, hb, rbp, b.m0, uni, ox, oy, oz);
+        if (threadIdx.x == 32) prefetch_own_b<R, FRAC>(b, blockIdx.x * (int64_t)blockDim.x);
+        tl_ = tile_layout<R, 3>(smem, b.tile + b.hmax);
+        stage_tile<R, 3>(b, tl_, blockIdx.x, b.tpos_b, rbp, &bar);
     }
     if (i < b.n) {
         const int64_t N = b.n_all;
@@ -880,22 +955,19 @@ __global__ void __launch_bounds__(kThreads, TL_MINB_B(R)) k_pass_b(const tl_body
         const int64_t w = i >> 5;
         const int64_t base = b.soff[w];
         const int len = (int)((b.soff[w + 1] - base) >> 5);
-        const double xi = b.Xs[i], yi = b.Xs[N + i], zi = b.Xs[2 * N + i];
-        const auto r0i = tl::ld4(rbp + 12 * i);
-        const auto r1i = tl::ld4(rbp + 12 * i + 4);
-        const auto r2i = tl::ld4(rbp + 12 * i + 8);
+        const auto r0i = TILED ? tl_.rec[3 * threadIdx.x] : tl::ld4(rbp + 12 * i);
+        const auto r1i = TILED ? tl_.rec[3 * threadIdx.x + 1] : tl::ld4(rbp + 12 * i + 4);
+        const auto r2i = TILED ? tl_.rec[3 * threadIdx.x + 2] : tl::ld4(rbp + 12 * i + 8);
         const R vi0 = r2i.y, vi1 = r2i.z, vi2 = r2i.w;
-        const R inv_h = R(b.inv_h), a_ih = R(b.alpha * b.inv_h);
+        const R inv_h = R(b.inv_h);
         const bool visc = b.visc != 0;
         const R eps_h2 = R(0.001 * b.h * b.h);
-        const R hR = R(b.h), b1c0 = R(b.beta1 * b.c0), b2 = R(b.beta2), inv_rho = R(1.0 / b.rho0);
+        const R B1 = R(b.beta1 * b.c0 * b.h), B2 = R(b.beta2 * b.h * b.h);
+        const R inv_rho = R(1.0 / b.rho0);
         R s1[3] = {R(0), R(0), R(0)}, s2[3] = {R(0), R(0), R(0)}, s3[3] = {R(0), R(0), R(0)};
-        const R m0c = R(b.m0c);
         if (TILED) {
-            const int me = threadIdx.x;
-            const R xl = tl_.x[me], yl = tl_.y[me], zl = tl_.z[me];
+            const auto me = tl_.pos[threadIdx.x];
             const uint16_t* sl = b.slots + base + lane * G;
-            const int S = tl_.S;
             SlotPipe<G> pipe(sl, len);
             for (int k = 0; k < len; k += G) {
                 int l[G];
@@ -903,14 +975,15 @@ __global__ void __launch_bounds__(kThreads, TL_MINB_B(R)) k_pass_b(const tl_body
 #pragma unroll
                 for (int q = 0; q < G; ++q) {
                     const int j = l[q];
-                    const R mj = uni ? m0c : tl_.m[j];
-                    pair_b<R, DIM, KIND>(xl - tl_.x[j], DIM == 3 ? yl - tl_.y[j] : R(0),
-                                         zl - tl_.z[j], tl_.rec[j], tl_.rec[S + j],
-                                         tl_.rec[2 * S + j], mj, vi0, vi1, vi2, visc, inv_h, a_ih,
-                                         hR, eps_h2, b2, b1c0, inv_rho, s1, s2, s3);
+                    const auto pj = tl_.pos[j];
+                    const V4<R>* rj = tl_.rec + 3 * j;
+                    pair_b<R, DIM, KIND>(me.x - pj.x, DIM == 3 ? me.y - pj.y : R(0), me.z - pj.z,
+                                         rj[0], rj[1], rj[2], pj.w, uni, vi0, vi1, vi2, visc, inv_h,
+                                         eps_h2, B2, B1, s1, s2, s3);
                 }
             }
         } else {
+            const double xi = b.Xs[i], yi = b.Xs[N + i], zi = b.Xs[2 * N + i];
             const int32_t* sidx = b.sidx + base + lane;
             const double* __restrict__ Xp = b.Xs;
             const double* __restrict__ Yp = b.Xs + N;
@@ -931,15 +1004,22 @@ __global__ void __launch_bounds__(kThreads, TL_MINB_B(R)) k_pass_b(const tl_body
                     q0[q] = tl::ldg4(rj);
                     q1[q] = tl::ldg4(rj + 4);
                     q2[q] = tl::ldg4(rj + 8);
-                    mj[q] = m0c;
-                    if (!uni) mj[q] = R(__ldg(b.m0 + jj[q]));
+                    mj[q] = uni ? R(0) : R(__ldg(b.m0 + jj[q]));
                 }
 #pragma unroll
                 for (int q = 0; q < G; ++q)
                     pair_b<R, DIM, KIND>(R(xi - xj[q]), DIM == 3 ? R(yi - yj[q]) : R(0),
-                                         R(zi - zj[q]), q0[q], q1[q], q2[q], mj[q], vi0, vi1, vi2,
-                                         visc, inv_h, a_ih, hR, eps_h2, b2, b1c0, inv_rho, s1, s2,
-                                         s3);
+                                         R(zi - zj[q]), q0[q], q1[q], q2[q], mj[q], uni, vi0, vi1,
+                                         vi2, visc, inv_h, eps_h2, B2, B1, s1, s2, s3);
+            }
+        }
+        {   // kernel constant (and m0 when uniform), once per particle
+            const R ck = kshape_const<R, KIND>(b) * (uni ? R(b.m0c) : R(1));
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                s1[q] *= ck;
+                s2[q] *= ck;
+                s3[q] *= ck * inv_rho;
             }
         }
         // a_int = (PL_i s1 + s2)/rho0^2 - AL_i s3
@@ -968,7 +1048,9 @@ __global__ void __launch_bounds__(kThreads, TL_MINB_B(R)) k_pass_b(const tl_body
         const double dt = b.clock ? b.clock->dt : 0.0;
         const double tf = MODE == TL_B_INIT ? 0.0 : (MODE == TL_B_SYMPL ? t0 + 0.5 * dt : t0);
         const double dtf = MODE == TL_B_INIT ? 0.0 : dt;
-        const D3 X0{xi, yi, zi};
+        // reference positions only feed boundary-condition / restrictphi expressions
+        const bool need_x = has_bc || (FRAC && b.restrict_prog >= 0);
+        const D3 X0 = need_x ? D3{b.Xs[i], b.Xs[N + i], b.Xs[2 * N + i]} : D3{0.0, 0.0, 0.0};
         const D3 u0{double(ui.x), double(ui.y), double(ui.z)};
         if (has_bc) {
             const double m0i = b.uniform ? b.m0c : b.m0[i];

@@ -104,8 +104,8 @@ __global__ void k_halo_scatter(int64_t m, const uint64_t* __restrict__ keys,
 // slot(w, k, lane) at soff[w] + (k/G)*32*G + lane*G + k%G; padding = own slot
 __global__ void k_slots(int64_t n, int T, int G, const int64_t* __restrict__ indptr,
                         const int32_t* __restrict__ indices, const int64_t* __restrict__ hoff,
-                        const int32_t* __restrict__ halo, const int64_t* __restrict__ soff,
-                        uint16_t* __restrict__ slots) {
+                        const int32_t* __restrict__ halo, const uint16_t* __restrict__ hslot,
+                        const int64_t* __restrict__ soff, uint16_t* __restrict__ slots) {
     int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t nw = (n + 31) / 32;
     const int64_t w = p >> 5;
@@ -119,6 +119,7 @@ __global__ void k_slots(int64_t n, int T, int G, const int64_t* __restrict__ ind
     const int64_t rl = p < n ? indptr[p + 1] - rb : 0;
     const uint16_t self = (uint16_t)(p - t0);
     const int32_t* hs = halo + (p < n ? hoff[tile] : 0);
+    const uint16_t* hsl = hslot + (p < n ? hoff[tile] : 0);
     const int64_t hn = p < n ? hoff[tile + 1] - hoff[tile] : 0;
     for (int64_t k = 0; k < len; ++k) {
         uint16_t s = self;
@@ -132,10 +133,96 @@ __global__ void k_slots(int64_t n, int T, int G, const int64_t* __restrict__ ind
                     const int64_t m = (lo + hi) >> 1;
                     if (hs[m] < q) lo = m + 1; else hi = m;
                 }
-                s = (uint16_t)(T + lo);
+                s = hsl[lo];
             }
         }
         slots[base + (k / G) * 32 * G + lane * G + (k % G)] = s;
+    }
+}
+
+// Shared-memory slot of every halo entry of every tile.  A quarter-warp's
+// 128-bit shared loads hit distinct bank groups when the 8 slots it reads
+// are distinct mod 8.  Members sit at slot p - t0 (== p mod 8, tiles are
+// multiples of 8); giving halo particle q a slot == q (mod 8) as well,
+// T + 8*rank + (q & 7) with rank = its order within that residue class,
+// keeps a Morton-ordered warp's k-th neighbours (a translated 2x2x2 brick
+// per quarter-warp) conflict-free off the tile too.  A tile whose aligned
+// extent would exceed `cap` (> 0) is packed densely instead, so a few
+// fragmented tiles do not set the shared-memory size of every CTA; res = 1
+// packs every tile densely.  One thread per tile; extent[t] = slots used - T.
+__global__ void k_hslots(int64_t ntile, int T, int res, int cap, const int64_t* __restrict__ hoff,
+                         const int32_t* __restrict__ halo, uint16_t* __restrict__ hslot,
+                         int32_t* __restrict__ extent) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= ntile) return;
+    const int64_t k0 = hoff[t], k1 = hoff[t + 1];
+    bool aligned = res == 8;
+    if (aligned && cap > 0) {
+        int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int64_t k = k0; k < k1; ++k) {
+            const int r = halo[k] & 7;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) cnt[q] += (q == r);
+        }
+        int top = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (cnt[q]) top = max(top, 8 * (cnt[q] - 1) + q + 1);
+        aligned = top <= cap;
+    }
+    int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int top = 0;
+    for (int64_t k = k0; k < k1; ++k) {
+        int slot;
+        if (aligned) {
+            const int r = halo[k] & 7;
+            int c = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (q == r) c = cnt[q]++;
+            slot = 8 * c + r;
+        } else {
+            slot = (int)(k - k0);
+        }
+        hslot[k] = (uint16_t)(T + slot);
+        top = max(top, slot + 1);
+    }
+    extent[t] = top;
+}
+
+// Staged position record of every slot of every tile, built once: the
+// reference positions relative to the tile's first member (FP32; absolute in
+// FP64) and the particle's mass-like weight (w), in slot order, so the step
+// kernels copy a contiguous block instead of gathering FP64 planes.
+// toff[t] = first record of tile t; holes stay zero.
+template <typename R>
+__global__ void k_tile_pos(int64_t n, int64_t n_all, int T, int64_t ntile,
+                           const int64_t* __restrict__ hoff, const int32_t* __restrict__ halo,
+                           const uint16_t* __restrict__ hslot, const int64_t* __restrict__ toff,
+                           const double* __restrict__ X, const double* __restrict__ w, int rel,
+                           R* __restrict__ out) {
+    const int64_t t = blockIdx.x;
+    if (t >= ntile) return;
+    const int64_t p0 = t * T;
+    const double ox = rel ? X[p0] : 0.0, oy = rel ? X[n_all + p0] : 0.0,
+                 oz = rel ? X[2 * n_all + p0] : 0.0;
+    const int64_t k0 = hoff[t], H = hoff[t + 1] - k0;
+    R* o = out + 4 * toff[t];
+    for (int64_t s = threadIdx.x; s < T + H; s += blockDim.x) {
+        int64_t q;
+        int64_t d;
+        if (s < T) {
+            if (p0 + s >= n) continue;
+            q = p0 + s;
+            d = s;
+        } else {
+            q = halo[k0 + s - T];
+            d = hslot[k0 + s - T];
+        }
+        o[4 * d] = R(X[q] - ox);
+        o[4 * d + 1] = R(X[n_all + q] - oy);
+        o[4 * d + 2] = R(X[2 * n_all + q] - oz);
+        o[4 * d + 3] = w ? R(w[q]) : R(0);
     }
 }
 
@@ -248,12 +335,44 @@ extern "C" int tl_tile_halo(tl_stream_t st_, int64_t n, int32_t T, const int64_t
     return rc;
 }
 
+extern "C" int tl_tile_hslots(tl_stream_t st, int64_t ntile, int32_t T, int32_t res, int32_t cap,
+                              const int64_t* hoff, const int32_t* halo, uint16_t* hslot,
+                              int32_t* extent) {
+    if (ntile <= 0) return TL_OK;
+    if (res != 1 && res != 8) {
+        tl_set_error("tl_tile_hslots: res must be 1 or 8");
+        return TL_ERR_ARG;
+    }
+    if (T % 8) {
+        tl_set_error("tl_tile_hslots: tile size must be a multiple of 8");
+        return TL_ERR_ARG;
+    }
+    k_hslots<<<tl_blocks(ntile, 128), 128, 0, (cudaStream_t)st>>>(ntile, T, res, cap, hoff, halo,
+                                                                 hslot, extent);
+    return tl_check_launch("k_hslots");
+}
+
+extern "C" int tl_tile_pos(tl_stream_t st, int64_t n, int64_t n_all, int32_t T, int64_t ntile,
+                           const int64_t* hoff, const int32_t* halo, const uint16_t* hslot,
+                           const int64_t* toff, const double* X, const double* w, int32_t precision,
+                           void* out) {
+    if (ntile <= 0) return TL_OK;
+    cudaStream_t s = (cudaStream_t)st;
+    if (precision == 4)
+        k_tile_pos<float><<<(unsigned)ntile, 256, 0, s>>>(n, n_all, T, ntile, hoff, halo, hslot, toff,
+                                                          X, w, 1, (float*)out);
+    else
+        k_tile_pos<double><<<(unsigned)ntile, 256, 0, s>>>(n, n_all, T, ntile, hoff, halo, hslot, toff,
+                                                           X, w, 0, (double*)out);
+    return tl_check_launch("k_tile_pos");
+}
+
 extern "C" int tl_tile_slots(tl_stream_t st, int64_t n, int32_t T, int32_t G, const int64_t* indptr,
                              const int32_t* indices, const int64_t* hoff, const int32_t* halo,
-                             const int64_t* soff, uint16_t* slots) {
+                             const uint16_t* hslot, const int64_t* soff, uint16_t* slots) {
     if (n <= 0) return TL_OK;
     const int64_t nt = ((n + 31) / 32) * 32;
     k_slots<<<tl_blocks(nt, kThreads), kThreads, 0, (cudaStream_t)st>>>(n, T, G, indptr, indices,
-                                                                      hoff, halo, soff, slots);
+                                                                      hoff, halo, hslot, soff, slots);
     return tl_check_launch("k_slots");
 }

@@ -165,6 +165,55 @@ __device__ __forceinline__ int eig3_jacobi(const T* Ain, T* w, T* Q, T tol_rel) 
 // Wendland C2 (reference kernel_geom.py:30-62); a_ih = alpha / h.
 __device__ __forceinline__ float rsqrt_pos(float x) { return x > 0.f ? rsqrtf(x) : 0.f; }
 __device__ __forceinline__ double rsqrt_pos(double x) { return x > 0.0 ? rsqrt(x) : 0.0; }
+// --- asynchronous copies (TMA bulk, LDGSTS) and mbarriers, inline PTX ------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n"
+        " .reg .pred p;\n"
+        "TL_WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra TL_WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+// TMA 1D bulk copy global -> shared, completion counted on `bar` (16-byte
+// aligned addresses, bytes a multiple of 16)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+// 16-byte LDGSTS (L2 only)
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+// TMA bulk prefetch of [p, p + bytes) into L2 (rounded out to 16 bytes)
+__device__ __forceinline__ void l2_prefetch(const void* p, size_t bytes) {
+    const uintptr_t a = (uintptr_t)p & ~uintptr_t(15);
+    const uintptr_t e = ((uintptr_t)p + bytes + 15) & ~uintptr_t(15);
+    if (e > a)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((uint32_t)(e - a))
+                     : "memory");
+}
+
+// 1/sqrt(max(x, smallest normal)): finite for x = 0 (self-padding pairs)
+__device__ __forceinline__ float rsqrt_floor(float x) { return rsqrtf(fmaxf(x, 1.17549435e-38f)); }
+__device__ __forceinline__ double rsqrt_floor(double x) { return rsqrt(fmax(x, 2.2250738585072014e-308)); }
 
 template <typename T, int KIND>
 __device__ __forceinline__ T kernel_fac(T r2, T rs, T inv_h, T a_ih) {

@@ -19,6 +19,8 @@ from __future__ import annotations
 
 import math
 
+import os
+
 import numpy as np
 
 from . import _lib
@@ -184,6 +186,7 @@ class StepLayout:
     own plus uint16 shared-memory slots for each pair (tiles.cu)."""
 
     GROUP = 4   # TL_SELL_GROUP
+    RESIDUE = int(os.environ.get("TLSPH_HALO_RESIDUE", "8"))   # 8 = bank-aligned halo slots
 
     def __init__(self, dadj, tile=256, rows=None, halo=None):
         """rows: adjacency rows this device owns (default all); halo: adjacency
@@ -247,7 +250,7 @@ class StepLayout:
                                   _lib.ptr(self.soff), _lib.ptr(self.sidx)), "tl_sell_fill")
         self.tile = 0
         self.hmax = 0
-        self.hoff = self.halo = self.slots = None
+        self.hoff = self.halo = self.slots = self.hslot = self.toff = None
         if tile and tile > 0:
             self._build_tiles(int(tile), total)
 
@@ -269,15 +272,45 @@ class StepLayout:
         del halo
         self.hoff = torch.zeros(ntile + 1, dtype=torch.int64, device=dev)
         torch.cumsum(tcount, 0, out=self.hoff[1:])
-        self.hmax = int(tcount.max().item()) if ntile else 0
-        if T + self.hmax > 65535:
+        if T + 8 * int(tcount.max().item() if ntile else 0) > 65535:
             return   # slots are uint16: leave the body untiled
+        # shared-memory slot of every halo entry (bank-conflict-free residues;
+        # tiles that would outgrow 1.1x the densest halo are packed densely)
+        self.hslot = torch.empty(max(int(self.halo.shape[0]), 1), dtype=torch.int16, device=dev)
+        extent = torch.zeros(max(ntile, 1), dtype=torch.int32, device=dev)
+        hdense = int(tcount.max().item()) if ntile else 0
+        cap = ((int(1.1 * hdense) + 7) // 8) * 8
+        _lib.check(L.tl_tile_hslots(st, ntile, T, self.RESIDUE, cap, _lib.ptr(self.hoff),
+                                    _lib.ptr(self.halo), _lib.ptr(self.hslot), _lib.ptr(extent)),
+                   "tl_tile_hslots")
+        self.hmax = int(extent.max().item()) if ntile else 0
+        # staged position records: tile t owns records [toff[t], toff[t+1])
+        self.toff = torch.zeros(ntile + 1, dtype=torch.int64, device=dev)
+        torch.cumsum(extent[:ntile].to(torch.int64) + T, 0, out=self.toff[1:])
         self.slots = torch.empty(max(total, 4), dtype=torch.int16, device=dev)
         _lib.check(L.tl_tile_slots(st, n, T, self.GROUP, _lib.ptr(self.indptr),
                                    _lib.ptr(self.indices), _lib.ptr(self.hoff),
-                                   _lib.ptr(self.halo), _lib.ptr(self.soff),
+                                   _lib.ptr(self.halo), _lib.ptr(self.hslot), _lib.ptr(self.soff),
                                    _lib.ptr(self.slots)), "tl_tile_slots")
         self.tile = T
+
+
+    def positions(self, Xs, weight=None, precision="fp32"):
+        """Staged position records (x, y, z, w) of every tile slot
+        (tl_tile_pos): Xs = 3 device FP64 planes of stride n_all in device
+        order; weight = per-particle device FP64 (V0 or m0) or None."""
+        import torch
+        if not self.tile:
+            return None
+        R = torch.float32 if precision == "fp32" else torch.float64
+        ntile = int(self.hoff.shape[0]) - 1
+        out = torch.zeros((int(self.toff[-1].item()), 4), dtype=R, device=Xs.device)
+        _lib.check(_lib.lib().tl_tile_pos(
+            _lib.stream_ptr(), self.n, self.n_all, self.tile, ntile, _lib.ptr(self.hoff),
+            _lib.ptr(self.halo), _lib.ptr(self.hslot), _lib.ptr(self.toff), _lib.ptr(Xs),
+            _lib.ptr(weight) if weight is not None else None, 4 if precision == "fp32" else 8,
+            _lib.ptr(out)), "tl_tile_pos")
+        return out
 
 
 class LazyAdjacency(Adjacency):

@@ -133,6 +133,13 @@ class DeviceBody:
         self.S_out = f64(n, 3, 3) if mirrors else None
         self.psi_out = f64(n) if mirrors else None
         self.psip_out = f64(n) if mirrors else None
+        # staged tile positions with the pass-A (V0) and pass-B (m0) weights
+        if lay.tile:
+            self.tpos_a = lay.positions(self.Xs, None if self.uniform else self.V0, precision)
+            self.tpos_b = (self.tpos_a if self.uniform
+                           else lay.positions(self.Xs, self.m0, precision))
+        else:
+            self.tpos_a = self.tpos_b = None
         self.counters = torch.zeros(N_COUNTERS, dtype=torch.int64, device=dev)
         self.red = torch.zeros(2, dtype=torch.int64, device=dev)
         self.nblocks = int(_lib.lib().tl_pass_blocks(n))
@@ -238,7 +245,9 @@ class DeviceBody:
         lay = self.layout
         b.tile, b.hmax = int(lay.tile), int(lay.hmax)
         if lay.tile:
-            b.hoff, b.halo, b.slots = P(lay.hoff), P(lay.halo), P(lay.slots)
+            b.hoff, b.halo, b.slots, b.hslot = (P(lay.hoff), P(lay.halo), P(lay.slots),
+                                                P(lay.hslot))
+            b.toff, b.tpos_a, b.tpos_b = P(lay.toff), P(self.tpos_a), P(self.tpos_b)
         b.perm = P(self.perm_global)
         b.V0, b.m0 = P(self.V0), P(self.m0)
         for k in ("us", "rb", "v", "al", "sdot", "sddot", "Hh", "Cpd", "epbar", "a"):
