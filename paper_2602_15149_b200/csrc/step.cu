@@ -469,24 +469,20 @@ __device__ __forceinline__ void load_slots(const uint16_t* p, int* out) {
     }
 }
 
-// slot groups with the next group's load already in flight
+// G slots of this lane's next neighbour group: from the CTA's staged slot
+// block (shared) or, when a body's slot table is too large to stage
+// (slmax == 0, e.g. radial 3D stencils), straight from global memory
 template <int G>
-struct SlotPipe {
-    static_assert(G == 4, "slot pipe reads TL_SELL_GROUP = 4 slots per load");
-    const uint2* p;
-    int len;
-    uint2 cur;
-    __device__ __forceinline__ SlotPipe(const uint16_t* sl, int len_) : p(reinterpret_cast<const uint2*>(sl)), len(len_) {
-        cur = len > 0 ? __ldg(p) : make_uint2(0, 0);
-    }
-    __device__ __forceinline__ void next(int k, int* out) {
-        const uint2 v = cur;
-        if (k + G < len) cur = __ldg(p + (k + G) * 8);   // 32 lanes x G slots per group
-        out[0] = v.x & 0xffff; out[1] = v.x >> 16; out[2] = v.y & 0xffff; out[3] = v.y >> 16;
-    }
-};
+__device__ __forceinline__ void next_slots(bool staged, const uint16_t* sp, const uint16_t* gp,
+                                           int k, int* out) {
+    static_assert(G == 4, "slot groups are TL_SELL_GROUP = 4 wide");
+    const uint2 v = staged ? *reinterpret_cast<const uint2*>(sp + k * 32)
+                           : __ldg(reinterpret_cast<const uint2*>(gp + k * 32));
+    out[0] = v.x & 0xffff; out[1] = v.x >> 16; out[2] = v.y & 0xffff; out[3] = v.y >> 16;
+}
 
-// Shared-memory tile of a CTA.  Two arrays indexed by slot:
+// Shared-memory tile of a CTA.  Two arrays indexed by slot, then the CTA's
+// block of the neighbour-slot table:
 //   pos[slot]             the staged position record (x, y, z, w) -- a copy of
 //                         the tile's block of tl_tile_pos records;
 //   rec[slot * NREC + r]  the NREC gathered records of the particle, stored
@@ -500,11 +496,12 @@ template <typename R, int NREC>
 struct Tile {
     V4<R>* pos;
     V4<R>* rec;
+    uint16_t* slots;   // the CTA's block of the slot table (its warps' slices)
 };
 
 template <typename R, int NREC>
-__host__ __device__ constexpr size_t tile_bytes(int S) {
-    return (size_t)S * (NREC + 1) * sizeof(V4<R>);
+__host__ __device__ constexpr size_t tile_bytes(int S, int slmax) {
+    return (size_t)S * (NREC + 1) * sizeof(V4<R>) + (size_t)slmax * sizeof(uint16_t);
 }
 
 template <typename R, int NREC>
@@ -512,13 +509,15 @@ __device__ __forceinline__ Tile<R, NREC> tile_layout(unsigned char* smem, int S)
     Tile<R, NREC> t;
     t.pos = reinterpret_cast<V4<R>*>(smem);
     t.rec = t.pos + S;
+    t.slots = reinterpret_cast<uint16_t*>(t.rec + (size_t)S * NREC);
     return t;
 }
 
 // Stage a tile with asynchronous copies only: thread 0 arms the barrier and
-// issues two TMA bulk copies (the contiguous position block and the members'
-// records); every thread then issues 16-byte LDGSTS gathers of the halo
-// records.  No register round trip, every load of the CTA in flight at once.
+// issues three TMA bulk copies (the contiguous position block, the members'
+// records, the CTA's neighbour-slot block); every thread then issues 16-byte
+// LDGSTS gathers of the halo records.  No register round trip, every load of
+// the CTA in flight at once.
 template <typename R, int NREC>
 __device__ __forceinline__ void stage_tile(const tl_body& b, const Tile<R, NREC>& t, int64_t tile,
                                            const void* tpos, const R* src, uint64_t* bar) {
@@ -531,10 +530,14 @@ __device__ __forceinline__ void stage_tile(const tl_body& b, const Tile<R, NREC>
         const int64_t r0 = b.toff[tile];
         const uint32_t pos_bytes = (uint32_t)((b.toff[tile + 1] - r0) * sizeof(V4<R>));
         const uint32_t mem_bytes = (uint32_t)(nmem * NREC * sizeof(V4<R>));
+        const int64_t w0 = p0 >> 5, w1 = min(w0 + T / 32, (b.n + 31) >> 5);
+        const uint32_t sl_bytes =
+            b.slmax > 0 ? (uint32_t)((b.soff[w1] - b.soff[w0]) * sizeof(uint16_t)) : 0u;
         tl::mbar_init(bar, 1);
-        tl::mbar_expect_tx(bar, pos_bytes + mem_bytes);
+        tl::mbar_expect_tx(bar, pos_bytes + mem_bytes + sl_bytes);
         tl::bulk_g2s(t.pos, static_cast<const V4<R>*>(tpos) + r0, pos_bytes, bar);
         tl::bulk_g2s(t.rec, src + p0 * 4 * NREC, mem_bytes, bar);
+        if (sl_bytes) tl::bulk_g2s(t.slots, b.slots + b.soff[w0], sl_bytes, bar);
     }
     constexpr int CH = (int)(sizeof(V4<R>) / 16);   // 16-byte chunks per record
     for (int s = threadIdx.x; s < H; s += blockDim.x) {
@@ -623,11 +626,14 @@ __global__ void __launch_bounds__(kThreads, TL_MINB_A(R)) k_pass_a(const tl_body
         R M[6] = {R(0), R(0), R(0), R(0), R(0), R(0)};   // xx yy zz xy xz yz
         if (TILED) {
             const auto me = tl_.pos[threadIdx.x];
-            const uint16_t* sl = b.slots + base + lane * G;
-            SlotPipe<G> pipe(sl, len);
+            // this warp's slice within the CTA's staged slot block
+            const bool staged = b.slmax > 0;
+            const uint16_t* sl = tl_.slots + (base - b.soff[(blockIdx.x * (int64_t)blockDim.x) >> 5]) +
+                                 lane * G;
+            const uint16_t* slg = b.slots + base + lane * G;
             for (int k = 0; k < len; k += G) {
                 int l[G];
-                pipe.next(k, l);
+                next_slots<G>(staged, sl, slg, k, l);
 #pragma unroll
                 for (int q = 0; q < G; ++q) {
                     const int j = l[q];
@@ -967,11 +973,14 @@ __global__ void __launch_bounds__(kThreads, TL_MINB_B(R)) k_pass_b(const tl_body
         R s1[3] = {R(0), R(0), R(0)}, s2[3] = {R(0), R(0), R(0)}, s3[3] = {R(0), R(0), R(0)};
         if (TILED) {
             const auto me = tl_.pos[threadIdx.x];
-            const uint16_t* sl = b.slots + base + lane * G;
-            SlotPipe<G> pipe(sl, len);
+            // this warp's slice within the CTA's staged slot block
+            const bool staged = b.slmax > 0;
+            const uint16_t* sl = tl_.slots + (base - b.soff[(blockIdx.x * (int64_t)blockDim.x) >> 5]) +
+                                 lane * G;
+            const uint16_t* slg = b.slots + base + lane * G;
             for (int k = 0; k < len; k += G) {
                 int l[G];
-                pipe.next(k, l);
+                next_slots<G>(staged, sl, slg, k, l);
 #pragma unroll
                 for (int q = 0; q < G; ++q) {
                     const int j = l[q];
@@ -1238,7 +1247,7 @@ int launch_a_one(cudaStream_t st, const tl_body& b) {
     constexpr int G = TL_GATHER_A;
     if (b.tile > 0) {
         auto kern = k_pass_a<R, DIM, MODEL, FRAC, KIND, G, true>;
-        const size_t bytes = tile_bytes<R, 1>(b.tile + b.hmax);
+        const size_t bytes = tile_bytes<R, 1>(b.tile + b.hmax, b.slmax);
         int rc = smem_opt_in(kern, bytes);
         if (rc) return rc;
         kern<<<tl_blocks(b.n, b.tile), b.tile, bytes, st>>>(b);
@@ -1267,7 +1276,7 @@ int launch_b_one(cudaStream_t st, const tl_body& b) {
     constexpr int G = TL_GATHER_B;
     if (b.tile > 0) {
         auto kern = k_pass_b<R, DIM, MODE, FRAC, KIND, G, true>;
-        const size_t bytes = tile_bytes<R, 3>(b.tile + b.hmax);
+        const size_t bytes = tile_bytes<R, 3>(b.tile + b.hmax, b.slmax);
         int rc = smem_opt_in(kern, bytes);
         if (rc) return rc;
         kern<<<tl_blocks(b.n, b.tile), b.tile, bytes, st>>>(b);

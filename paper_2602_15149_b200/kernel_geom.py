@@ -250,6 +250,7 @@ class StepLayout:
                                   _lib.ptr(self.soff), _lib.ptr(self.sidx)), "tl_sell_fill")
         self.tile = 0
         self.hmax = 0
+        self.slmax = 0
         self.hoff = self.halo = self.slots = self.hslot = self.toff = None
         if tile and tile > 0:
             self._build_tiles(int(tile), total)
@@ -287,6 +288,11 @@ class StepLayout:
         # staged position records: tile t owns records [toff[t], toff[t+1])
         self.toff = torch.zeros(ntile + 1, dtype=torch.int64, device=dev)
         torch.cumsum(extent[:ntile].to(torch.int64) + T, 0, out=self.toff[1:])
+        # slot-table entries of each tile (its warps' slices), staged per CTA
+        nw = (n + 31) // 32
+        wb = torch.arange(0, ntile + 1, device=dev, dtype=torch.int64) * (T // 32)
+        wb.clamp_(max=nw)
+        self.slmax = int((self.soff[wb[1:]] - self.soff[wb[:-1]]).max().item()) if ntile else 0
         self.slots = torch.empty(max(total, 4), dtype=torch.int16, device=dev)
         _lib.check(L.tl_tile_slots(st, n, T, self.GROUP, _lib.ptr(self.indptr),
                                    _lib.ptr(self.indices), _lib.ptr(self.hoff),

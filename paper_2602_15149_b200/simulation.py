@@ -92,6 +92,8 @@ class DeviceBody:
         rec = 64 if precision == "fp32" else 128          # pass-B bytes per staged particle
         if lay.tile and (lay.tile + lay.hmax) * rec > TILE_SMEM_LIMIT:
             lay.tile = 0                                   # halo too fat: gather from L2
+        if lay.tile and (lay.tile + lay.hmax) * rec + 2 * lay.slmax > TILE_SMEM_LIMIT:
+            lay.slmax = 0                                  # slot table read from global memory
         self.layout = lay
         n, n_all = lay.n, lay.n_all
         self.n, self.n_all = n, n_all
@@ -243,7 +245,7 @@ class DeviceBody:
         P = _lib.ptr
         b.soff, b.sidx, b.Xs, b.L = P(self.soff), P(self.sidx), P(self.Xs), P(self.L)
         lay = self.layout
-        b.tile, b.hmax = int(lay.tile), int(lay.hmax)
+        b.tile, b.hmax, b.slmax = int(lay.tile), int(lay.hmax), int(lay.slmax)
         if lay.tile:
             b.hoff, b.halo, b.slots, b.hslot = (P(lay.hoff), P(lay.halo), P(lay.slots),
                                                 P(lay.hslot))
