@@ -439,12 +439,12 @@ __device__ __forceinline__ void pair_b(R dx, R dy, R dz, const V4<R>& q0, const 
     s1[0] += wx; s1[2] += wz;
     if (DIM == 3) {
         s1[1] += wy;
-        s2[0] += q0.x * wx + q0.y * wy + q0.z * wz;
-        s2[1] += q0.w * wx + q1.x * wy + q1.y * wz;
-        s2[2] += q1.z * wx + q1.w * wy + q2.x * wz;
+        s2[0] = fma(q0.z, wz, fma(q0.y, wy, fma(q0.x, wx, s2[0])));
+        s2[1] = fma(q1.y, wz, fma(q1.x, wy, fma(q0.w, wx, s2[1])));
+        s2[2] = fma(q2.x, wz, fma(q1.w, wy, fma(q1.z, wx, s2[2])));
     } else {
-        s2[0] += q0.x * wx + q0.z * wz;
-        s2[2] += q1.z * wx + q2.x * wz;
+        s2[0] = fma(q0.z, wz, fma(q0.x, wx, s2[0]));
+        s2[2] = fma(q2.x, wz, fma(q1.z, wx, s2[2]));
     }
     if (visc) {
         const R dvr = (vi0 - q2.y) * dx + (DIM == 3 ? (vi1 - q2.z) * dy : R(0)) + (vi2 - q2.w) * dz;
@@ -540,7 +540,15 @@ __device__ __forceinline__ void stage_tile(const tl_body& b, const Tile<R, NREC>
         if (sl_bytes) tl::bulk_g2s(t.slots, b.slots + b.soff[w0], sl_bytes, bar);
     }
     constexpr int CH = (int)(sizeof(V4<R>) / 16);   // 16-byte chunks per record
+#ifdef TL_EXP_NO_HALO
+    for (int s = threadIdx.x; s < H; s += blockDim.x) {   // timing experiment: no gathers
+        const int d = b.hslot[hb + s];
+        for (int r = 0; r < NREC; ++r) t.rec[(int64_t)d * NREC + r] = V4<R>{};
+    }
+    for (int s = threadIdx.x; s < 0; s += blockDim.x) {
+#else
     for (int s = threadIdx.x; s < H; s += blockDim.x) {
+#endif
         const int64_t q = b.halo[hb + s];
         const int d = b.hslot[hb + s];
         const char* g = reinterpret_cast<const char*>(src + q * 4 * NREC);
@@ -596,7 +604,12 @@ __device__ __forceinline__ void prefetch_own_b(const tl_body& b, int64_t p0) {
 template <typename R, int DIM, int MODEL, bool FRAC, int KIND, int G, bool TILED>
 __global__ void __launch_bounds__(kThreads, TL_MINB_A(R)) k_pass_a(const tl_body b) {
     extern __shared__ __align__(16) unsigned char smem[];
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    // a CTA of blockDim.x threads owns blockDim.x consecutive particles (TILED:
+    // one shared tile of b.tile == blockDim.x particles); one particle per
+    // thread -- larger tiles looped over by 256 threads measured slower
+    // (shared memory per CTA cuts residency)
+    const int64_t p0 = blockIdx.x * (int64_t)blockDim.x;
+    constexpr int P = 1;
     __shared__ double s_pw[kThreads / 32];
     double pw = 0.0;
     if (halted(b)) return;
@@ -606,189 +619,193 @@ __global__ void __launch_bounds__(kThreads, TL_MINB_A(R)) k_pass_a(const tl_body
     Tile<R, 1> tl_;
     __shared__ uint64_t bar;
     if (TILED) {
-        if (threadIdx.x == 32) prefetch_own_a<R, MODEL, FRAC>(b, blockIdx.x * (int64_t)blockDim.x);
+        if (threadIdx.x == 32) prefetch_own_a<R, MODEL, FRAC>(b, p0);
         tl_ = tile_layout<R, 1>(smem, b.tile + b.hmax);
         stage_tile<R, 1>(b, tl_, blockIdx.x, b.tpos_a, us, &bar);
     }
-    if (i < b.n) {
-        const int64_t N = b.n_all;
-        const int lane = (int)(i & 31);
-        const int64_t w = i >> 5;
-        const int64_t base = b.soff[w];
-        const int len = (int)((b.soff[w + 1] - base) >> 5);
-        const auto ui = TILED ? tl_.rec[threadIdx.x] : tl::ld4(us + 4 * i);
-        const R si = ui.w;
-        const bool gated = FRAC && si <= R(b.s_l);
-        const R inv_h = R(b.inv_h);
-        R D[9];
-#pragma unroll
-        for (int q = 0; q < 9; ++q) D[q] = R(0);
-        R M[6] = {R(0), R(0), R(0), R(0), R(0), R(0)};   // xx yy zz xy xz yz
-        if (TILED) {
-            const auto me = tl_.pos[threadIdx.x];
-            // this warp's slice within the CTA's staged slot block
-            const bool staged = b.slmax > 0;
-            const uint16_t* sl = tl_.slots + (base - b.soff[(blockIdx.x * (int64_t)blockDim.x) >> 5]) +
-                                 lane * G;
-            const uint16_t* slg = b.slots + base + lane * G;
-            for (int k = 0; k < len; k += G) {
-                int l[G];
-                next_slots<G>(staged, sl, slg, k, l);
-#pragma unroll
-                for (int q = 0; q < G; ++q) {
-                    const int j = l[q];
-                    const auto pj = tl_.pos[j];
-                    pair_a<R, DIM, FRAC, KIND>(me.x - pj.x, DIM == 3 ? me.y - pj.y : R(0),
-                                               me.z - pj.z, tl_.rec[j], pj.w, uni, ui, gated,
-                                               inv_h, D, M);
+    for (int sub = 0; sub < P; ++sub) {
+        const int ms = sub * (int)blockDim.x + (int)threadIdx.x;   // member slot
+        const int64_t i = p0 + ms;
+        if (i < b.n) {
+            const int64_t N = b.n_all;
+            const int lane = (int)(i & 31);
+            const int64_t w = i >> 5;
+            const int64_t base = b.soff[w];
+            const int len = (int)((b.soff[w + 1] - base) >> 5);
+            const auto ui = TILED ? tl_.rec[ms] : tl::ld4(us + 4 * i);
+            const R si = ui.w;
+            const bool gated = FRAC && si <= R(b.s_l);
+            const R inv_h = R(b.inv_h);
+            R D[9];
+    #pragma unroll
+            for (int q = 0; q < 9; ++q) D[q] = R(0);
+            R M[6] = {R(0), R(0), R(0), R(0), R(0), R(0)};   // xx yy zz xy xz yz
+            if (TILED) {
+                const auto me = tl_.pos[ms];
+                // this warp's slice within the CTA's staged slot block
+                const bool staged = b.slmax > 0;
+                const uint16_t* sl = tl_.slots + (base - b.soff[p0 >> 5]) +
+                                     lane * G;
+                const uint16_t* slg = b.slots + base + lane * G;
+                for (int k = 0; k < len; k += G) {
+                    int l[G];
+                    next_slots<G>(staged, sl, slg, k, l);
+    #pragma unroll
+                    for (int q = 0; q < G; ++q) {
+                        const int j = l[q];
+                        const auto pj = tl_.pos[j];
+                        pair_a<R, DIM, FRAC, KIND>(me.x - pj.x, DIM == 3 ? me.y - pj.y : R(0),
+                                                   me.z - pj.z, tl_.rec[j], pj.w, uni, ui, gated,
+                                                   inv_h, D, M);
+                    }
                 }
-            }
-        } else {
-            const double xi = b.Xs[i], yi = b.Xs[N + i], zi = b.Xs[2 * N + i];
-            const int32_t* sidx = b.sidx + base + lane;
-            const double* __restrict__ Xp = b.Xs;
-            const double* __restrict__ Yp = b.Xs + N;
-            const double* __restrict__ Zp = b.Xs + 2 * N;
-            // neighbours in groups of G: all index loads, then all gathers, then
-            // the math, so each warp keeps 2G independent loads in flight
-            for (int k = 0; k < len; k += G) {
-                int32_t jj[G];
-#pragma unroll
-                for (int q = 0; q < G; ++q) jj[q] = __ldg(sidx + 32 * (k + q));
-                double xj[G], yj[G], zj[G];
-                V4<R> uj[G];
-                R vj[G];
-#pragma unroll
-                for (int q = 0; q < G; ++q) {
-                    xj[q] = __ldg(Xp + jj[q]);
-                    yj[q] = DIM == 3 ? __ldg(Yp + jj[q]) : 0.0;
-                    zj[q] = __ldg(Zp + jj[q]);
-                    uj[q] = tl::ldg4(us + 4 * (int64_t)jj[q]);
-                    vj[q] = uni ? R(0) : R(__ldg(b.V0 + jj[q]));
-                }
-#pragma unroll
-                for (int q = 0; q < G; ++q)
-                    pair_a<R, DIM, FRAC, KIND>(R(xi - xj[q]), DIM == 3 ? R(yi - yj[q]) : R(0),
-                                               R(zi - zj[q]), uj[q], vj[q], uni, ui, gated, inv_h,
-                                               D, M);
-            }
-        }
-        {   // kernel constant (and V0 when uniform), once per particle
-            const R ck = kshape_const<R, KIND>(b) * (uni ? R(b.V0c) : R(1));
-#pragma unroll
-            for (int q = 0; q < 9; ++q) D[q] *= ck;
-#pragma unroll
-            for (int q = 0; q < 6; ++q) M[q] *= R(2) * ck;
-        }
-        // L_i (9 planes)
-        R Li[9];
-#pragma unroll
-        for (int q = 0; q < 9; ++q) Li[q] = planeR<R>(b.L, N, q, i);
-        // H = F - I = D L^T
-        R Hm[9];
-#pragma unroll
-        for (int r = 0; r < 3; ++r)
-#pragma unroll
-            for (int c = 0; c < 3; ++c)
-                Hm[3 * r + c] = D[3 * r] * Li[3 * c] + D[3 * r + 1] * Li[3 * c + 1] + D[3 * r + 2] * Li[3 * c + 2];
-        if (gated) {
-#pragma unroll
-            for (int q = 0; q < 9; ++q) Hm[q] = R(0);
-        }
-        // constitutive update
-        R S[9], psi = R(0), psip = R(0);
-        int bad = 0, noconv = 0;
-        if (MODEL == 1) {
-            noconv = svk_update<R>(Hm, R(b.lam), R(b.mu), si, FRAC, R(b.jac_tol), S, psi, psip);
-        } else if (MODEL == 2) {
-            bad = nh_update<R>(Hm, R(b.kappa), R(b.mu), si, FRAC, S, psi, psip);
-        } else {
-            double Fd[9], Cpd[6], Sd[9], psid, dwp;
-            bool nonspd;
-#pragma unroll
-            for (int q = 0; q < 9; ++q) Fd[q] = double(Hm[q]) + ((q % 4 == 0) ? 1.0 : 0.0);
-#pragma unroll
-            for (int q = 0; q < 6; ++q) Cpd[q] = double(planeR<R>(b.Cpd, N, q, i));
-            double epb = double(static_cast<const R*>(b.epbar)[i]);
-            bad = j2_update(Fd, Cpd, epb, b.mu, b.kappa, b.sigma_y0, b.H_hard, Sd, psid, dwp, nonspd);
-            if (nonspd) atomicMin((long long*)&b.counters[2], (long long)(b.perm ? b.perm[i] : i));
-#pragma unroll
-            for (int q = 0; q < 6; ++q) static_cast<R*>(b.Cpd)[q * N + i] = R(Cpd[q]);
-            static_cast<R*>(b.epbar)[i] = R(epb);
-#pragma unroll
-            for (int q = 0; q < 9; ++q) S[q] = R(Sd[q]);
-            psi = R(psid);
-            psip = R(0);
-            pw = dwp * (b.uniform ? b.V0c : b.V0[i]);
-        }
-        // phase field: history, Laplacian, s-ddot (fracture.py:12-43)
-        if (FRAC) {
-            R* Hh = static_cast<R*>(b.Hh);
-            const R Hn = fmax(psip, Hh[i]);
-            Hh[i] = Hn;
-            const R lap = Li[0] * M[0] + Li[4] * M[1] + Li[8] * M[2] + (Li[1] + Li[3]) * M[3] +
-                          (Li[2] + Li[6]) * M[4] + (Li[5] + Li[7]) * M[5];
-            const R eps0 = R(b.eps0), Gc = R(b.Gc), c0 = R(b.c0);
-            const R ratio = Hn / Gc;
-            const R damp = R(2) * sqrt(R(4) * eps0 * ratio + R(1)) / c0;
-            const R sd = static_cast<const R*>(b.sdot)[i];
-            static_cast<R*>(b.sddot)[i] =
-                (c0 * c0 / (R(2) * eps0)) *
-                (R(2) * eps0 * lap + (R(1) - si) / (R(2) * eps0) - damp * sd - R(2) * si * ratio);
-        }
-        // P = F S = S + H S ; PL = P L_i
-        R P[9], PL[9];
-#pragma unroll
-        for (int r = 0; r < 3; ++r)
-#pragma unroll
-            for (int c = 0; c < 3; ++c)
-                P[3 * r + c] = S[3 * r + c] + (Hm[3 * r] * S[c] + Hm[3 * r + 1] * S[3 + c] + Hm[3 * r + 2] * S[6 + c]);
-        mm3(P, Li, PL);
-        // viscosity tensor: det(F) F^-1 = adj(F), zero when det F <= J_MIN
-        R* al = static_cast<R*>(b.al);
-        if (b.visc) {
-            R Fm[9], A[9];
-#pragma unroll
-            for (int q = 0; q < 9; ++q) Fm[q] = Hm[q] + ((q % 4 == 0) ? R(1) : R(0));
-            const R J = R(1) + jm1_of(Hm);
-            if (J > R(TL_J_MIN)) {
-                R adj[9];
-                adj[0] = Fm[4] * Fm[8] - Fm[5] * Fm[7];
-                adj[1] = Fm[2] * Fm[7] - Fm[1] * Fm[8];
-                adj[2] = Fm[1] * Fm[5] - Fm[2] * Fm[4];
-                adj[3] = Fm[5] * Fm[6] - Fm[3] * Fm[8];
-                adj[4] = Fm[0] * Fm[8] - Fm[2] * Fm[6];
-                adj[5] = Fm[2] * Fm[3] - Fm[0] * Fm[5];
-                adj[6] = Fm[3] * Fm[7] - Fm[4] * Fm[6];
-                adj[7] = Fm[1] * Fm[6] - Fm[0] * Fm[7];
-                adj[8] = Fm[0] * Fm[4] - Fm[1] * Fm[3];
-                mm3(adj, Li, A);
             } else {
-#pragma unroll
-                for (int q = 0; q < 9; ++q) A[q] = R(0);
-                bad += 1;
+                const double xi = b.Xs[i], yi = b.Xs[N + i], zi = b.Xs[2 * N + i];
+                const int32_t* sidx = b.sidx + base + lane;
+                const double* __restrict__ Xp = b.Xs;
+                const double* __restrict__ Yp = b.Xs + N;
+                const double* __restrict__ Zp = b.Xs + 2 * N;
+                // neighbours in groups of G: all index loads, then all gathers, then
+                // the math, so each warp keeps 2G independent loads in flight
+                for (int k = 0; k < len; k += G) {
+                    int32_t jj[G];
+    #pragma unroll
+                    for (int q = 0; q < G; ++q) jj[q] = __ldg(sidx + 32 * (k + q));
+                    double xj[G], yj[G], zj[G];
+                    V4<R> uj[G];
+                    R vj[G];
+    #pragma unroll
+                    for (int q = 0; q < G; ++q) {
+                        xj[q] = __ldg(Xp + jj[q]);
+                        yj[q] = DIM == 3 ? __ldg(Yp + jj[q]) : 0.0;
+                        zj[q] = __ldg(Zp + jj[q]);
+                        uj[q] = tl::ldg4(us + 4 * (int64_t)jj[q]);
+                        vj[q] = uni ? R(0) : R(__ldg(b.V0 + jj[q]));
+                    }
+    #pragma unroll
+                    for (int q = 0; q < G; ++q)
+                        pair_a<R, DIM, FRAC, KIND>(R(xi - xj[q]), DIM == 3 ? R(yi - yj[q]) : R(0),
+                                                   R(zi - zj[q]), uj[q], vj[q], uni, ui, gated, inv_h,
+                                                   D, M);
+                }
             }
-#pragma unroll
-            for (int q = 0; q < 9; ++q) al[q * N + i] = A[q];
-        }
-        // pass-B gather record: PL (9) + v (3)
-        const R* vv = static_cast<const R*>(b.v);
-        R* rb = static_cast<R*>(b.rb) + 12 * i;
-        tl::st4(rb, PL[0], PL[1], PL[2], PL[3]);
-        tl::st4(rb + 4, PL[4], PL[5], PL[6], PL[7]);
-        tl::st4(rb + 8, PL[8], vv[i], vv[N + i], vv[2 * N + i]);
-        if (mirror_out(b)) {
-#pragma unroll
-            for (int q = 0; q < 9; ++q) {
-                b.F_out[9 * i + q] = double(Hm[q]) + ((q % 4 == 0) ? 1.0 : 0.0);
-                b.S_out[9 * i + q] = double(S[q]);
+            {   // kernel constant (and V0 when uniform), once per particle
+                const R ck = kshape_const<R, KIND>(b) * (uni ? R(b.V0c) : R(1));
+    #pragma unroll
+                for (int q = 0; q < 9; ++q) D[q] *= ck;
+    #pragma unroll
+                for (int q = 0; q < 6; ++q) M[q] *= R(2) * ck;
             }
-            b.psi_out[i] = double(psi);
-            b.psip_out[i] = double(psip);
-        }
-        if (bad || noconv) {
-            if (bad) atomicAdd((unsigned long long*)&b.counters[0], (unsigned long long)bad);
-            if (noconv) atomicAdd((unsigned long long*)&b.counters[1], 1ull);
+            // L_i (9 planes)
+            R Li[9];
+    #pragma unroll
+            for (int q = 0; q < 9; ++q) Li[q] = planeR<R>(b.L, N, q, i);
+            // H = F - I = D L^T
+            R Hm[9];
+    #pragma unroll
+            for (int r = 0; r < 3; ++r)
+    #pragma unroll
+                for (int c = 0; c < 3; ++c)
+                    Hm[3 * r + c] = D[3 * r] * Li[3 * c] + D[3 * r + 1] * Li[3 * c + 1] + D[3 * r + 2] * Li[3 * c + 2];
+            if (gated) {
+    #pragma unroll
+                for (int q = 0; q < 9; ++q) Hm[q] = R(0);
+            }
+            // constitutive update
+            R S[9], psi = R(0), psip = R(0);
+            int bad = 0, noconv = 0;
+            if (MODEL == 1) {
+                noconv = svk_update<R>(Hm, R(b.lam), R(b.mu), si, FRAC, R(b.jac_tol), S, psi, psip);
+            } else if (MODEL == 2) {
+                bad = nh_update<R>(Hm, R(b.kappa), R(b.mu), si, FRAC, S, psi, psip);
+            } else {
+                double Fd[9], Cpd[6], Sd[9], psid, dwp;
+                bool nonspd;
+    #pragma unroll
+                for (int q = 0; q < 9; ++q) Fd[q] = double(Hm[q]) + ((q % 4 == 0) ? 1.0 : 0.0);
+    #pragma unroll
+                for (int q = 0; q < 6; ++q) Cpd[q] = double(planeR<R>(b.Cpd, N, q, i));
+                double epb = double(static_cast<const R*>(b.epbar)[i]);
+                bad = j2_update(Fd, Cpd, epb, b.mu, b.kappa, b.sigma_y0, b.H_hard, Sd, psid, dwp, nonspd);
+                if (nonspd) atomicMin((long long*)&b.counters[2], (long long)(b.perm ? b.perm[i] : i));
+    #pragma unroll
+                for (int q = 0; q < 6; ++q) static_cast<R*>(b.Cpd)[q * N + i] = R(Cpd[q]);
+                static_cast<R*>(b.epbar)[i] = R(epb);
+    #pragma unroll
+                for (int q = 0; q < 9; ++q) S[q] = R(Sd[q]);
+                psi = R(psid);
+                psip = R(0);
+                pw = dwp * (b.uniform ? b.V0c : b.V0[i]);
+            }
+            // phase field: history, Laplacian, s-ddot (fracture.py:12-43)
+            if (FRAC) {
+                R* Hh = static_cast<R*>(b.Hh);
+                const R Hn = fmax(psip, Hh[i]);
+                Hh[i] = Hn;
+                const R lap = Li[0] * M[0] + Li[4] * M[1] + Li[8] * M[2] + (Li[1] + Li[3]) * M[3] +
+                              (Li[2] + Li[6]) * M[4] + (Li[5] + Li[7]) * M[5];
+                const R eps0 = R(b.eps0), Gc = R(b.Gc), c0 = R(b.c0);
+                const R ratio = Hn / Gc;
+                const R damp = R(2) * sqrt(R(4) * eps0 * ratio + R(1)) / c0;
+                const R sd = static_cast<const R*>(b.sdot)[i];
+                static_cast<R*>(b.sddot)[i] =
+                    (c0 * c0 / (R(2) * eps0)) *
+                    (R(2) * eps0 * lap + (R(1) - si) / (R(2) * eps0) - damp * sd - R(2) * si * ratio);
+            }
+            // P = F S = S + H S ; PL = P L_i
+            R P[9], PL[9];
+    #pragma unroll
+            for (int r = 0; r < 3; ++r)
+    #pragma unroll
+                for (int c = 0; c < 3; ++c)
+                    P[3 * r + c] = S[3 * r + c] + (Hm[3 * r] * S[c] + Hm[3 * r + 1] * S[3 + c] + Hm[3 * r + 2] * S[6 + c]);
+            mm3(P, Li, PL);
+            // viscosity tensor: det(F) F^-1 = adj(F), zero when det F <= J_MIN
+            R* al = static_cast<R*>(b.al);
+            if (b.visc) {
+                R Fm[9], A[9];
+    #pragma unroll
+                for (int q = 0; q < 9; ++q) Fm[q] = Hm[q] + ((q % 4 == 0) ? R(1) : R(0));
+                const R J = R(1) + jm1_of(Hm);
+                if (J > R(TL_J_MIN)) {
+                    R adj[9];
+                    adj[0] = Fm[4] * Fm[8] - Fm[5] * Fm[7];
+                    adj[1] = Fm[2] * Fm[7] - Fm[1] * Fm[8];
+                    adj[2] = Fm[1] * Fm[5] - Fm[2] * Fm[4];
+                    adj[3] = Fm[5] * Fm[6] - Fm[3] * Fm[8];
+                    adj[4] = Fm[0] * Fm[8] - Fm[2] * Fm[6];
+                    adj[5] = Fm[2] * Fm[3] - Fm[0] * Fm[5];
+                    adj[6] = Fm[3] * Fm[7] - Fm[4] * Fm[6];
+                    adj[7] = Fm[1] * Fm[6] - Fm[0] * Fm[7];
+                    adj[8] = Fm[0] * Fm[4] - Fm[1] * Fm[3];
+                    mm3(adj, Li, A);
+                } else {
+    #pragma unroll
+                    for (int q = 0; q < 9; ++q) A[q] = R(0);
+                    bad += 1;
+                }
+    #pragma unroll
+                for (int q = 0; q < 9; ++q) al[q * N + i] = A[q];
+            }
+            // pass-B gather record: PL (9) + v (3)
+            const R* vv = static_cast<const R*>(b.v);
+            R* rb = static_cast<R*>(b.rb) + 12 * i;
+            tl::st4(rb, PL[0], PL[1], PL[2], PL[3]);
+            tl::st4(rb + 4, PL[4], PL[5], PL[6], PL[7]);
+            tl::st4(rb + 8, PL[8], vv[i], vv[N + i], vv[2 * N + i]);
+            if (mirror_out(b)) {
+    #pragma unroll
+                for (int q = 0; q < 9; ++q) {
+                    b.F_out[9 * i + q] = double(Hm[q]) + ((q % 4 == 0) ? 1.0 : 0.0);
+                    b.S_out[9 * i + q] = double(S[q]);
+                }
+                b.psi_out[i] = double(psi);
+                b.psip_out[i] = double(psip);
+            }
+            if (bad || noconv) {
+                if (bad) atomicAdd((unsigned long long*)&b.counters[0], (unsigned long long)bad);
+                if (noconv) atomicAdd((unsigned long long*)&b.counters[1], 1ull);
+            }
         }
     }
     if (MODEL == 3) {
@@ -915,14 +932,14 @@ __device__ __noinline__ double restrict_floor(const BcCtx b, D3 X0, D3 u, double
 
 // sdot += dtr*sddot; s += dts*sdot; clamp [0,1]; restrictphi floor
 // (stepper.py:125-130, fracture.py:66-83)
-template <typename R>
+template <typename R, bool RESTRICT = true>
 __device__ __forceinline__ void advance_phase(const tl_body& b, R& s, R& sd, R sdd, double dts,
                                               double dtr, D3 X0, D3 u, double t, double dt) {
     sd = tl::axpy_rn(sd, R(dtr), sdd);
     s = tl::axpy_rn(s, R(dts), sd);
     if (s < R(0)) { s = R(0); sd = R(0); }
     if (s > R(1)) { s = R(1); sd = R(0); }
-    if (b.restrict_prog >= 0) {
+    if (RESTRICT && b.restrict_prog >= 0) {
         const double fl = restrict_floor(bc_ctx(b), X0, u, t, dt);
         if (fl >= 0.0 && double(s) < fl) {
             s = R(fl);
@@ -936,13 +953,119 @@ __device__ __forceinline__ double sq3_rn(double x, double y, double z) {
     return __dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(z, z)), __dmul_rn(y, y));
 }
 
+// Per-particle update after the force sum (stepper.py:86-130, dynamics.py:138-217,
+// fracture.py:46-83): f0 and force BCs, the acceleration check, velocity BCs,
+// the Verlet / symplectic kick and drift, the phase-field advance; writes
+// v, u|s, sdot (and a when asked) and returns the dt maxima and the first
+// non-finite particle.  BC = false is the common path: no boundary
+// conditions and no restrictphi expression apply to this particle.
+struct EpiOut {
+    double v2, a2;
+    long long bad;
+};
+
+template <typename R, int DIM, int MODE, bool FRAC, bool BC>
+__device__ __forceinline__ EpiOut epi_body(const tl_body& b, int64_t i, uint32_t mask, double ax0,
+                                           double ay0, double az0, R vi0, R vi1, R vi2) {
+    EpiOut o{0.0, 0.0, LLONG_MAX};
+    const int64_t N = b.n_all;
+    double acc[3] = {ax0, ay0, az0};
+    // a = a_int + f0 + force BCs ; 2D a_y = 0  (stepper.py:86-95)
+    acc[0] = tl::add_rn(acc[0], b.f0[0]);
+    acc[1] = tl::add_rn(acc[1], b.f0[1]);
+    acc[2] = tl::add_rn(acc[2], b.f0[2]);
+    const R* us = static_cast<const R*>(b.us);
+    const auto ui = tl::ld4(us + 4 * i);
+    const bool has_bc = BC && b.nbc && (mask || b.bc_whole);
+    const double t0 = b.clock ? b.clock->t : 0.0;
+    const double dt = b.clock ? b.clock->dt : 0.0;
+    const double tf = MODE == TL_B_INIT ? 0.0 : (MODE == TL_B_SYMPL ? t0 + 0.5 * dt : t0);
+    const double dtf = MODE == TL_B_INIT ? 0.0 : dt;
+    // reference positions only feed boundary-condition / restrictphi expressions
+    const bool need_x = has_bc || (BC && FRAC && b.restrict_prog >= 0);
+    const D3 X0 = need_x ? D3{b.Xs[i], b.Xs[N + i], b.Xs[2 * N + i]} : D3{0.0, 0.0, 0.0};
+    const D3 u0{double(ui.x), double(ui.y), double(ui.z)};
+    if (has_bc) {
+        const double m0i = b.uniform ? b.m0c : b.m0[i];
+        const D3 r = force_bcs(bc_ctx(b), mask, m0i, X0, u0, tf, dtf, D3{acc[0], acc[1], acc[2]});
+        acc[0] = r.x; acc[1] = r.y; acc[2] = r.z;
+    }
+    if (DIM == 2) acc[1] = 0.0;
+    if (!(isfinite(acc[0]) && isfinite(acc[1]) && isfinite(acc[2]))) {
+        o.bad = (long long)(b.perm ? b.perm[i] : i);
+        if (b.clock) atomicMin((long long*)&b.counters[6], (long long)b.clock->step);
+    }
+    // velocity: v_i is the copy pass A put in the record
+    D3 vel{double(vi0), double(vi1), double(vi2)};
+    R us_new[4] = {ui.x, ui.y, ui.z, ui.w};
+    R* vout = static_cast<R*>(b.v);
+    if (MODE == TL_B_INIT) {
+        if (has_bc) vel = velocity_bcs(bc_ctx(b), mask, X0, u0, 0.0, 0.0, vel);
+    } else {
+        const double kick = MODE == TL_B_VERLET ? dt : 0.5 * dt;
+        const double t_new = t0 + dt;
+        // BC phase at the force time, kick, BCs at t_new, drift
+        if (has_bc) vel = velocity_bcs(bc_ctx(b), mask, X0, u0, tf, dt, vel);
+        vel = D3{double(tl::axpy_rn(R(vel.x), R(kick), R(acc[0]))),
+                 double(tl::axpy_rn(R(vel.y), R(kick), R(acc[1]))),
+                 double(tl::axpy_rn(R(vel.z), R(kick), R(acc[2])))};
+        if (has_bc) vel = velocity_bcs(bc_ctx(b), mask, X0, u0, t_new, dt, vel);
+        const R vR[3] = {R(vel.x), R(vel.y), R(vel.z)};
+        us_new[0] = tl::axpy_rn(ui.x, R(kick), vR[0]);
+        us_new[1] = DIM == 3 ? tl::axpy_rn(ui.y, R(kick), vR[1]) : R(0);
+        us_new[2] = tl::axpy_rn(ui.z, R(kick), vR[2]);
+        if (FRAC) {
+            R* sdp = static_cast<R*>(b.sdot);
+            R sd = sdp[i];
+            R s = ui.w;
+            const R sdd = static_cast<const R*>(b.sddot)[i];
+            advance_phase<R, BC>(b, s, sd, sdd, kick, kick, X0,
+                             D3{double(us_new[0]), double(us_new[1]), double(us_new[2])},
+                             t_new, dt);
+            us_new[3] = s;
+            sdp[i] = sd;
+        }
+        tl::st4(static_cast<R*>(b.us) + 4 * i, us_new[0], us_new[1], us_new[2], us_new[3]);
+    }
+    vout[i] = R(vel.x);
+    vout[N + i] = R(vel.y);
+    vout[2 * N + i] = R(vel.z);
+    if (b.store_a || mirror_out(b)) {
+        R* ap = static_cast<R*>(b.a);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) ap[a * N + i] = R(acc[a]);
+    }
+    if (MODE != TL_B_INIT && b.clock &&
+        !(isfinite(vel.x) && isfinite(vel.y) && isfinite(vel.z) && isfinite(double(us_new[0])) &&
+          isfinite(double(us_new[1])) && isfinite(double(us_new[2]))))
+        atomicMin((long long*)&b.counters[7], (long long)b.clock->step + 1);
+    const double vx = double(R(vel.x)), vy = double(R(vel.y)), vz = double(R(vel.z));
+    const double ax = double(R(acc[0])), ay = double(R(acc[1])), az = double(R(acc[2]));
+    o.v2 = sq3_rn(vx, vy, vz);
+    o.a2 = sq3_rn(ax, ay, az);
+    if (!(o.a2 == o.a2)) o.a2 = 0.0;  // NaN is reported through counters[3]
+    if (!(o.v2 == o.v2)) o.v2 = 0.0;  // and through counters[7]
+    return o;
+}
+
+template <typename R, int DIM, int MODE, bool FRAC>
+__device__ __noinline__ EpiOut epi_slow(const tl_body* b, int64_t i, uint32_t mask, double ax,
+                                        double ay, double az, R vi0, R vi1, R vi2) {
+    return epi_body<R, DIM, MODE, FRAC, true>(*b, i, mask, ax, ay, az, vi0, vi1, vi2);
+}
+
 // ---------------------------------------------------------------------------
 // pass B
 // ---------------------------------------------------------------------------
 template <typename R, int DIM, int MODE, bool FRAC, int KIND, int G, bool TILED>
-__global__ void __launch_bounds__(kThreads, TL_MINB_B(R)) k_pass_b(const tl_body b) {
+__global__ void __launch_bounds__(kThreads, TL_MINB_B(R)) k_pass_b(const __grid_constant__ tl_body b) {
     extern __shared__ __align__(16) unsigned char smem[];
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    // a CTA of blockDim.x threads owns blockDim.x consecutive particles (TILED:
+    // one shared tile of b.tile == blockDim.x particles); one particle per
+    // thread -- larger tiles looped over by 256 threads measured slower
+    // (shared memory per CTA cuts residency)
+    const int64_t p0 = blockIdx.x * (int64_t)blockDim.x;
+    constexpr int P = 1;
     if (halted(b)) return;
     double v2 = 0.0, a2 = 0.0;
     long long bad_acc = LLONG_MAX;
@@ -951,175 +1074,117 @@ __global__ void __launch_bounds__(kThreads, TL_MINB_B(R)) k_pass_b(const tl_body
     Tile<R, 3> tl_;
     __shared__ uint64_t bar;
     if (TILED) {
-        if (threadIdx.x == 32) prefetch_own_b<R, FRAC>(b, blockIdx.x * (int64_t)blockDim.x);
+        if (threadIdx.x == 32) prefetch_own_b<R, FRAC>(b, p0);
         tl_ = tile_layout<R, 3>(smem, b.tile + b.hmax);
         stage_tile<R, 3>(b, tl_, blockIdx.x, b.tpos_b, rbp, &bar);
     }
-    if (i < b.n) {
-        const int64_t N = b.n_all;
-        const int lane = (int)(i & 31);
-        const int64_t w = i >> 5;
-        const int64_t base = b.soff[w];
-        const int len = (int)((b.soff[w + 1] - base) >> 5);
-        const auto r0i = TILED ? tl_.rec[3 * threadIdx.x] : tl::ld4(rbp + 12 * i);
-        const auto r1i = TILED ? tl_.rec[3 * threadIdx.x + 1] : tl::ld4(rbp + 12 * i + 4);
-        const auto r2i = TILED ? tl_.rec[3 * threadIdx.x + 2] : tl::ld4(rbp + 12 * i + 8);
-        const R vi0 = r2i.y, vi1 = r2i.z, vi2 = r2i.w;
-        const R inv_h = R(b.inv_h);
-        const bool visc = b.visc != 0;
-        const R eps_h2 = R(0.001 * b.h * b.h);
-        const R B1 = R(b.beta1 * b.c0 * b.h), B2 = R(b.beta2 * b.h * b.h);
-        const R inv_rho = R(1.0 / b.rho0);
-        R s1[3] = {R(0), R(0), R(0)}, s2[3] = {R(0), R(0), R(0)}, s3[3] = {R(0), R(0), R(0)};
-        if (TILED) {
-            const auto me = tl_.pos[threadIdx.x];
-            // this warp's slice within the CTA's staged slot block
-            const bool staged = b.slmax > 0;
-            const uint16_t* sl = tl_.slots + (base - b.soff[(blockIdx.x * (int64_t)blockDim.x) >> 5]) +
-                                 lane * G;
-            const uint16_t* slg = b.slots + base + lane * G;
-            for (int k = 0; k < len; k += G) {
-                int l[G];
-                next_slots<G>(staged, sl, slg, k, l);
-#pragma unroll
-                for (int q = 0; q < G; ++q) {
-                    const int j = l[q];
-                    const auto pj = tl_.pos[j];
-                    const V4<R>* rj = tl_.rec + 3 * j;
-                    pair_b<R, DIM, KIND>(me.x - pj.x, DIM == 3 ? me.y - pj.y : R(0), me.z - pj.z,
-                                         rj[0], rj[1], rj[2], pj.w, uni, vi0, vi1, vi2, visc, inv_h,
-                                         eps_h2, B2, B1, s1, s2, s3);
+    for (int sub = 0; sub < P; ++sub) {
+        const int ms = sub * (int)blockDim.x + (int)threadIdx.x;   // member slot
+        const int64_t i = p0 + ms;
+        if (i < b.n) {
+            const int64_t N = b.n_all;
+            const int lane = (int)(i & 31);
+            const int64_t w = i >> 5;
+            const int64_t base = b.soff[w];
+            const int len = (int)((b.soff[w + 1] - base) >> 5);
+            // own record: v_i now, P L_i after the neighbour loop (fewer live registers)
+            const auto r2i = TILED ? tl_.rec[3 * ms + 2] : tl::ld4(rbp + 12 * i + 8);
+            const R vi0 = r2i.y, vi1 = r2i.z, vi2 = r2i.w;
+            const R inv_h = R(b.inv_h);
+            const bool visc = b.visc != 0;
+            const R eps_h2 = R(0.001 * b.h * b.h);
+            const R B1 = R(b.beta1 * b.c0 * b.h), B2 = R(b.beta2 * b.h * b.h);
+            const R inv_rho = R(1.0 / b.rho0);
+            R s1[3] = {R(0), R(0), R(0)}, s2[3] = {R(0), R(0), R(0)}, s3[3] = {R(0), R(0), R(0)};
+            if (TILED) {
+                const auto me = tl_.pos[ms];
+                // this warp's slice within the CTA's staged slot block
+                const bool staged = b.slmax > 0;
+                const uint16_t* sl = tl_.slots + (base - b.soff[p0 >> 5]) +
+                                     lane * G;
+                const uint16_t* slg = b.slots + base + lane * G;
+                for (int k = 0; k < len; k += G) {
+                    int l[G];
+                    next_slots<G>(staged, sl, slg, k, l);
+    #pragma unroll
+                    for (int q = 0; q < G; ++q) {
+                        const int j = l[q];
+                        const auto pj = tl_.pos[j];
+                        const V4<R>* rj = tl_.rec + 3 * j;
+                        pair_b<R, DIM, KIND>(me.x - pj.x, DIM == 3 ? me.y - pj.y : R(0), me.z - pj.z,
+                                             rj[0], rj[1], rj[2], pj.w, uni, vi0, vi1, vi2, visc, inv_h,
+                                             eps_h2, B2, B1, s1, s2, s3);
+                    }
+                }
+            } else {
+                const double xi = b.Xs[i], yi = b.Xs[N + i], zi = b.Xs[2 * N + i];
+                const int32_t* sidx = b.sidx + base + lane;
+                const double* __restrict__ Xp = b.Xs;
+                const double* __restrict__ Yp = b.Xs + N;
+                const double* __restrict__ Zp = b.Xs + 2 * N;
+                for (int k = 0; k < len; k += G) {
+                    int32_t jj[G];
+    #pragma unroll
+                    for (int q = 0; q < G; ++q) jj[q] = __ldg(sidx + 32 * (k + q));
+                    double xj[G], yj[G], zj[G];
+                    V4<R> q0[G], q1[G], q2[G];
+                    R mj[G];
+    #pragma unroll
+                    for (int q = 0; q < G; ++q) {
+                        xj[q] = __ldg(Xp + jj[q]);
+                        yj[q] = DIM == 3 ? __ldg(Yp + jj[q]) : 0.0;
+                        zj[q] = __ldg(Zp + jj[q]);
+                        const R* rj = rbp + 12 * (int64_t)jj[q];
+                        q0[q] = tl::ldg4(rj);
+                        q1[q] = tl::ldg4(rj + 4);
+                        q2[q] = tl::ldg4(rj + 8);
+                        mj[q] = uni ? R(0) : R(__ldg(b.m0 + jj[q]));
+                    }
+    #pragma unroll
+                    for (int q = 0; q < G; ++q)
+                        pair_b<R, DIM, KIND>(R(xi - xj[q]), DIM == 3 ? R(yi - yj[q]) : R(0),
+                                             R(zi - zj[q]), q0[q], q1[q], q2[q], mj[q], uni, vi0, vi1,
+                                             vi2, visc, inv_h, eps_h2, B2, B1, s1, s2, s3);
                 }
             }
-        } else {
-            const double xi = b.Xs[i], yi = b.Xs[N + i], zi = b.Xs[2 * N + i];
-            const int32_t* sidx = b.sidx + base + lane;
-            const double* __restrict__ Xp = b.Xs;
-            const double* __restrict__ Yp = b.Xs + N;
-            const double* __restrict__ Zp = b.Xs + 2 * N;
-            for (int k = 0; k < len; k += G) {
-                int32_t jj[G];
-#pragma unroll
-                for (int q = 0; q < G; ++q) jj[q] = __ldg(sidx + 32 * (k + q));
-                double xj[G], yj[G], zj[G];
-                V4<R> q0[G], q1[G], q2[G];
-                R mj[G];
-#pragma unroll
-                for (int q = 0; q < G; ++q) {
-                    xj[q] = __ldg(Xp + jj[q]);
-                    yj[q] = DIM == 3 ? __ldg(Yp + jj[q]) : 0.0;
-                    zj[q] = __ldg(Zp + jj[q]);
-                    const R* rj = rbp + 12 * (int64_t)jj[q];
-                    q0[q] = tl::ldg4(rj);
-                    q1[q] = tl::ldg4(rj + 4);
-                    q2[q] = tl::ldg4(rj + 8);
-                    mj[q] = uni ? R(0) : R(__ldg(b.m0 + jj[q]));
+            {   // kernel constant (and m0 when uniform), once per particle
+                const R ck = kshape_const<R, KIND>(b) * (uni ? R(b.m0c) : R(1));
+    #pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    s1[q] *= ck;
+                    s2[q] *= ck;
+                    s3[q] *= ck * inv_rho;
                 }
-#pragma unroll
-                for (int q = 0; q < G; ++q)
-                    pair_b<R, DIM, KIND>(R(xi - xj[q]), DIM == 3 ? R(yi - yj[q]) : R(0),
-                                         R(zi - zj[q]), q0[q], q1[q], q2[q], mj[q], uni, vi0, vi1,
-                                         vi2, visc, inv_h, eps_h2, B2, B1, s1, s2, s3);
             }
-        }
-        {   // kernel constant (and m0 when uniform), once per particle
-            const R ck = kshape_const<R, KIND>(b) * (uni ? R(b.m0c) : R(1));
-#pragma unroll
-            for (int q = 0; q < 3; ++q) {
-                s1[q] *= ck;
-                s2[q] *= ck;
-                s3[q] *= ck * inv_rho;
+            // a_int = (PL_i s1 + s2)/rho0^2 - AL_i s3
+            const auto r0i = TILED ? tl_.rec[3 * ms] : tl::ld4(rbp + 12 * i);
+            const auto r1i = TILED ? tl_.rec[3 * ms + 1] : tl::ld4(rbp + 12 * i + 4);
+            const R PLi[9] = {r0i.x, r0i.y, r0i.z, r0i.w, r1i.x, r1i.y, r1i.z, r1i.w, r2i.x};
+            const R inv_rho2 = inv_rho * inv_rho;
+            double acc[3];
+    #pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                R t = (PLi[3 * a] * s1[0] + PLi[3 * a + 1] * s1[1] + PLi[3 * a + 2] * s1[2] + s2[a]) * inv_rho2;
+                if (visc) {
+                    const R* al = static_cast<const R*>(b.al);
+                    t -= al[(3 * a) * N + i] * s3[0] + al[(3 * a + 1) * N + i] * s3[1] +
+                         al[(3 * a + 2) * N + i] * s3[2];
+                }
+                acc[a] = double(t);
             }
+            // the rest of the particle's update: boundary conditions / restrictphi
+            // expressions only on the (rare) particles that carry them, out of
+            // line, so the common path holds no call frame
+            const uint32_t mask = b.bcmask ? b.bcmask[i] : 0u;
+            const bool slow = (b.nbc && (mask || b.bc_whole)) || (FRAC && b.restrict_prog >= 0);
+            const EpiOut o = slow ? epi_slow<R, DIM, MODE, FRAC>(&b, i, mask, acc[0], acc[1], acc[2],
+                                                                 vi0, vi1, vi2)
+                                  : epi_body<R, DIM, MODE, FRAC, false>(b, i, mask, acc[0], acc[1],
+                                                                        acc[2], vi0, vi1, vi2);
+            v2 = fmax(v2, o.v2);
+            a2 = fmax(a2, o.a2);
+            bad_acc = min(bad_acc, o.bad);
         }
-        // a_int = (PL_i s1 + s2)/rho0^2 - AL_i s3
-        const R PLi[9] = {r0i.x, r0i.y, r0i.z, r0i.w, r1i.x, r1i.y, r1i.z, r1i.w, r2i.x};
-        const R inv_rho2 = inv_rho * inv_rho;
-        double acc[3];
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            R t = (PLi[3 * a] * s1[0] + PLi[3 * a + 1] * s1[1] + PLi[3 * a + 2] * s1[2] + s2[a]) * inv_rho2;
-            if (visc) {
-                const R* al = static_cast<const R*>(b.al);
-                t -= al[(3 * a) * N + i] * s3[0] + al[(3 * a + 1) * N + i] * s3[1] +
-                     al[(3 * a + 2) * N + i] * s3[2];
-            }
-            acc[a] = double(t);
-        }
-        // a = a_int + f0 + force BCs ; 2D a_y = 0  (stepper.py:86-95)
-        acc[0] = tl::add_rn(acc[0], b.f0[0]);
-        acc[1] = tl::add_rn(acc[1], b.f0[1]);
-        acc[2] = tl::add_rn(acc[2], b.f0[2]);
-        const R* us = static_cast<const R*>(b.us);
-        const auto ui = tl::ld4(us + 4 * i);
-        const uint32_t mask = b.bcmask ? b.bcmask[i] : 0u;
-        const bool has_bc = b.nbc && (mask || b.bc_whole);
-        const double t0 = b.clock ? b.clock->t : 0.0;
-        const double dt = b.clock ? b.clock->dt : 0.0;
-        const double tf = MODE == TL_B_INIT ? 0.0 : (MODE == TL_B_SYMPL ? t0 + 0.5 * dt : t0);
-        const double dtf = MODE == TL_B_INIT ? 0.0 : dt;
-        // reference positions only feed boundary-condition / restrictphi expressions
-        const bool need_x = has_bc || (FRAC && b.restrict_prog >= 0);
-        const D3 X0 = need_x ? D3{b.Xs[i], b.Xs[N + i], b.Xs[2 * N + i]} : D3{0.0, 0.0, 0.0};
-        const D3 u0{double(ui.x), double(ui.y), double(ui.z)};
-        if (has_bc) {
-            const double m0i = b.uniform ? b.m0c : b.m0[i];
-            const D3 r = force_bcs(bc_ctx(b), mask, m0i, X0, u0, tf, dtf, D3{acc[0], acc[1], acc[2]});
-            acc[0] = r.x; acc[1] = r.y; acc[2] = r.z;
-        }
-        if (DIM == 2) acc[1] = 0.0;
-        if (!(isfinite(acc[0]) && isfinite(acc[1]) && isfinite(acc[2]))) {
-            bad_acc = (long long)(b.perm ? b.perm[i] : i);
-            if (b.clock) atomicMin((long long*)&b.counters[6], (long long)b.clock->step);
-        }
-        // velocity: v_i is the copy pass A put in the record
-        D3 vel{double(vi0), double(vi1), double(vi2)};
-        R us_new[4] = {ui.x, ui.y, ui.z, ui.w};
-        R* vout = static_cast<R*>(b.v);
-        if (MODE == TL_B_INIT) {
-            if (has_bc) vel = velocity_bcs(bc_ctx(b), mask, X0, u0, 0.0, 0.0, vel);
-        } else {
-            const double kick = MODE == TL_B_VERLET ? dt : 0.5 * dt;
-            const double t_new = t0 + dt;
-            // BC phase at the force time, kick, BCs at t_new, drift
-            if (has_bc) vel = velocity_bcs(bc_ctx(b), mask, X0, u0, tf, dt, vel);
-            vel = D3{double(tl::axpy_rn(R(vel.x), R(kick), R(acc[0]))),
-                     double(tl::axpy_rn(R(vel.y), R(kick), R(acc[1]))),
-                     double(tl::axpy_rn(R(vel.z), R(kick), R(acc[2])))};
-            if (has_bc) vel = velocity_bcs(bc_ctx(b), mask, X0, u0, t_new, dt, vel);
-            const R vR[3] = {R(vel.x), R(vel.y), R(vel.z)};
-            us_new[0] = tl::axpy_rn(ui.x, R(kick), vR[0]);
-            us_new[1] = DIM == 3 ? tl::axpy_rn(ui.y, R(kick), vR[1]) : R(0);
-            us_new[2] = tl::axpy_rn(ui.z, R(kick), vR[2]);
-            if (FRAC) {
-                R* sdp = static_cast<R*>(b.sdot);
-                R sd = sdp[i];
-                R s = ui.w;
-                const R sdd = static_cast<const R*>(b.sddot)[i];
-                advance_phase<R>(b, s, sd, sdd, kick, kick, X0,
-                                 D3{double(us_new[0]), double(us_new[1]), double(us_new[2])},
-                                 t_new, dt);
-                us_new[3] = s;
-                sdp[i] = sd;
-            }
-            tl::st4(static_cast<R*>(b.us) + 4 * i, us_new[0], us_new[1], us_new[2], us_new[3]);
-        }
-        vout[i] = R(vel.x);
-        vout[N + i] = R(vel.y);
-        vout[2 * N + i] = R(vel.z);
-        if (b.store_a || mirror_out(b)) {
-            R* ap = static_cast<R*>(b.a);
-#pragma unroll
-            for (int a = 0; a < 3; ++a) ap[a * N + i] = R(acc[a]);
-        }
-        if (MODE != TL_B_INIT && b.clock &&
-            !(isfinite(vel.x) && isfinite(vel.y) && isfinite(vel.z) && isfinite(double(us_new[0])) &&
-              isfinite(double(us_new[1])) && isfinite(double(us_new[2]))))
-            atomicMin((long long*)&b.counters[7], (long long)b.clock->step + 1);
-        const double vx = double(R(vel.x)), vy = double(R(vel.y)), vz = double(R(vel.z));
-        const double ax = double(R(acc[0])), ay = double(R(acc[1])), az = double(R(acc[2]));
-        v2 = sq3_rn(vx, vy, vz);
-        a2 = sq3_rn(ax, ay, az);
-        if (!(a2 == a2)) a2 = 0.0;  // NaN is reported through counters[3]
     }
     v2 = tl::warp_max(v2);
     a2 = tl::warp_max(a2);

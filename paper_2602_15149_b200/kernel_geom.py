@@ -253,6 +253,8 @@ class StepLayout:
         self.slmax = 0
         self.hoff = self.halo = self.slots = self.hslot = self.toff = None
         if tile and tile > 0:
+            if tile % 32 or tile > 256:
+                raise ValueError(f"tile size {tile}: a multiple of 32, at most 256")
             self._build_tiles(int(tile), total)
 
     def _build_tiles(self, T, total):

@@ -36,7 +36,9 @@ from .core import CaseError, Model, SimulationError
 
 INT64_MAX = np.iinfo(np.int64).max
 N_COUNTERS = 8
-DEFAULT_TILE = 256           # particles per CTA / shared-memory tile (TLSPH_TILE overrides)
+# particles per CTA / shared-memory tile, one per thread (TLSPH_TILE overrides;
+# a multiple of 32, at most 256)
+DEFAULT_TILE = {"fp32": 256, "fp64": 256}
 TILE_SMEM_LIMIT = 200 * 1024  # bytes of shared memory a pass-B tile may take
 
 
@@ -82,7 +84,7 @@ class DeviceBody:
                         dp_body=body.dp_body, notches=body.notches, correction=corr)
         self.adj = dadj
         # device particle order + neighbour tiles (kernel_geom.StepLayout)
-        tile = int(os.environ.get("TLSPH_TILE", str(DEFAULT_TILE)))
+        tile = int(os.environ.get("TLSPH_TILE", str(DEFAULT_TILE[precision])))
         if part is not None:
             part.complete(dadj)          # halo ids in exchange order (collective-free)
             lay = kernel_geom.StepLayout(dadj, tile=tile, rows=part.owned_rows,

@@ -185,7 +185,7 @@ def _sim(G, precision):
     return cfg, DeviceSimulation(cfg, precision=precision)
 
 
-@pytest.mark.parametrize("tile", ["256", "0", "64"])
+@pytest.mark.parametrize("tile", ["256", "0", "64", "128"])
 @pytest.mark.parametrize("tag", ["kalthoff2d_p", "taylor3d", "kalthoff3d"])
 def test_layout_variants_agree(tag, tile, monkeypatch):
     """Shared-memory tiles (various sizes) and the L2-gather path give the
