@@ -31,7 +31,7 @@ enum {
     TL_ERR_CASE = -4
 };
 
-#define TL_ABI_VERSION 3
+#define TL_ABI_VERSION 4
 
 int tl_abi_version(void);
 /* sizeof of the ABI structs, for binding checks: 0 tl_body, 1 tl_clock,
@@ -204,9 +204,12 @@ int tl_tile_hslots(tl_stream_t st, int64_t ntile, int32_t T, int32_t res, int32_
 int tl_tile_pos(tl_stream_t st, int64_t n, int64_t n_all, int32_t T, int64_t ntile,
                 const int64_t* hoff, const int32_t* halo, const uint16_t* hslot, const int64_t* toff,
                 const double* X, const double* w, int32_t precision, void* out);
-int tl_tile_slots(tl_stream_t st, int64_t n, int32_t T, int32_t G, const int64_t* indptr,
-                  const int32_t* indices, const int64_t* hoff, const int32_t* halo,
-                  const uint16_t* hslot, const int64_t* soff, uint16_t* slots);
+/* per-pair shared-memory slots of the tiled step kernels, stored as
+ * slot << shift (shift 4: the byte offset of the slot's FP32 position
+ * record; FP64 records are two such units) */
+int tl_tile_slots(tl_stream_t st, int64_t n, int32_t T, int32_t G, int32_t shift,
+                  const int64_t* indptr, const int32_t* indices, const int64_t* hoff,
+                  const int32_t* halo, const uint16_t* hslot, const int64_t* soff, uint16_t* slots);
 
 /* ---------------------------------------------------------------------------
  * Fused device-resident step (stepper.py:77-209, dynamics.py:28-217,

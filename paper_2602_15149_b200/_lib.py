@@ -13,7 +13,7 @@ import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("TLSPH_LIB", os.path.join(HERE, "libtlsph.so"))
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 _lib = None
 
@@ -116,7 +116,7 @@ _SIGS = {
     "tl_tile_halo": (INT, [P, I64, I32, P, P, I64, P, P, C.POINTER(I64)]),
     "tl_tile_hslots": (INT, [P, I64, I32, I32, I32, P, P, P, P]),
     "tl_tile_pos": (INT, [P, I64, I64, I32, I64, P, P, P, P, P, P, I32, P]),
-    "tl_tile_slots": (INT, [P, I64, I32, I32, P, P, P, P, P, P, P]),
+    "tl_tile_slots": (INT, [P, I64, I32, I32, I32, P, P, P, P, P, P, P]),
     "tl_pass_a": (INT, [P, C.POINTER(tl_body)]),
     "tl_pass_b": (INT, [P, C.POINTER(tl_body), INT]),
     "tl_predict": (INT, [P, C.POINTER(tl_body)]),

@@ -55,9 +55,10 @@ using tl::mm3;
 #define TL_MINB_A(R) (sizeof(R) == 4 ? 4 : 1)
 #endif
 #ifndef TL_MINB_B
-#define TL_MINB_B(R) 3
+#define TL_MINB_B(R) 4
 #endif
 static_assert(TL_SELL_GROUP % TL_GATHER_A == 0 && TL_SELL_GROUP % TL_GATHER_B == 0, "gather group");
+static_assert(TL_SELL_GROUP == 4, "tiled neighbour loops read 4 slots per group");
 constexpr int kThreads = TL_THREADS;
 
 __device__ __forceinline__ bool halted(const tl_body& b) {
@@ -398,12 +399,13 @@ __device__ __forceinline__ void pair_a(R dx, R dy, R dz, const V4<R>& uj, R vj, 
     R rs;
     R w = kshape<R, KIND>(r2, inv_h, rs);
     if (!uni) w *= vj;
-    if (!gated) {
-        const R du0 = w * (uj.x - ui.x), du2 = w * (uj.z - ui.z);
+    {   // F = I on gated particles (s_i <= s_l): a select, not a branch per pair
+        const R wg = gated ? R(0) : w;
+        const R du0 = wg * (uj.x - ui.x), du2 = wg * (uj.z - ui.z);
         D[0] += du0 * dx; D[2] += du0 * dz;
         D[6] += du2 * dx; D[8] += du2 * dz;
         if (DIM == 3) {
-            const R du1 = w * (uj.y - ui.y);
+            const R du1 = wg * (uj.y - ui.y);
             D[1] += du0 * dy; D[7] += du2 * dy;
             D[3] += du1 * dx; D[4] += du1 * dy; D[5] += du1 * dz;
         }
@@ -469,16 +471,83 @@ __device__ __forceinline__ void load_slots(const uint16_t* p, int* out) {
     }
 }
 
-// G slots of this lane's next neighbour group: from the CTA's staged slot
-// block (shared) or, when a body's slot table is too large to stage
-// (slmax == 0, e.g. radial 3D stencils), straight from global memory
-template <int G>
-__device__ __forceinline__ void next_slots(bool staged, const uint16_t* sp, const uint16_t* gp,
-                                           int k, int* out) {
-    static_assert(G == 4, "slot groups are TL_SELL_GROUP = 4 wide");
-    const uint2 v = staged ? *reinterpret_cast<const uint2*>(sp + k * 32)
-                           : __ldg(reinterpret_cast<const uint2*>(gp + k * 32));
-    out[0] = v.x & 0xffff; out[1] = v.x >> 16; out[2] = v.y & 0xffff; out[3] = v.y >> 16;
+// explicit 32-bit shared-memory loads (slot byte offsets + per-CTA bases)
+template <typename R>
+__device__ __forceinline__ V4<R> lds4(uint32_t a);
+template <>
+__device__ __forceinline__ float4 lds4<float>(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(a));
+    return v;
+}
+template <>
+__device__ __forceinline__ double4 lds4<double>(uint32_t a) {
+    double4 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%4];\n\tld.shared.v2.f64 {%2, %3}, [%4+16];"
+                 : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+                 : "r"(a));
+    return v;
+}
+
+// the 4 slot byte offsets of this lane's neighbour group k (staged in
+// shared memory, or from global memory for oversized slot tables)
+template <bool STAGED>
+__device__ __forceinline__ uint2 slot_group(uint32_t sl_sh, const uint16_t* sl_g, int k) {
+    if (STAGED) {
+        uint2 v;
+        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(sl_sh + 64u * k));
+        return v;
+    }
+    return __ldg(reinterpret_cast<const uint2*>(sl_g + 32 * k));
+}
+
+// Neighbour loops over a staged tile.  Slots are slot * 16: the byte offset
+// of the neighbour's FP32 position record (FP64 records are twice as wide);
+// the gathered record sits at the same offset (pass A, one record) or
+// three times it (pass B, three records).
+// UNI (uniform V0 / m0) and STAGED (slot table in shared memory) are
+// compile-time so the loop body has no per-pair predicates or branches.
+template <typename R, int DIM, bool FRAC, int KIND, bool UNI, bool STAGED>
+__device__ __forceinline__ void loop_a(uint32_t pos_sh, uint32_t rec_sh, uint32_t sl_sh,
+                                       const uint16_t* sl_g, int len, const V4<R>& me,
+                                       const V4<R>& ui, bool gated, R inv_h, R* D, R* M) {
+    for (int k = 0; k < len; k += 4) {
+        const uint2 v = slot_group<STAGED>(sl_sh, sl_g, k);
+        constexpr uint32_t U = sizeof(V4<R>) / 16;   // 16-byte units per record
+        const uint32_t off[4] = {U * (v.x & 0xffffu), U * (v.x >> 16), U * (v.y & 0xffffu),
+                                 U * (v.y >> 16)};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const V4<R> pj = lds4<R>(pos_sh + off[q]);
+            const V4<R> uj = lds4<R>(rec_sh + off[q]);
+            pair_a<R, DIM, FRAC, KIND>(me.x - pj.x, DIM == 3 ? me.y - pj.y : R(0), me.z - pj.z, uj,
+                                       pj.w, UNI, ui, gated, inv_h, D, M);
+        }
+    }
+}
+
+template <typename R, int DIM, int KIND, bool UNI, bool STAGED>
+__device__ __forceinline__ void loop_b(uint32_t pos_sh, uint32_t rec_sh, uint32_t sl_sh,
+                                       const uint16_t* sl_g, int len, const V4<R>& me, R vi0, R vi1,
+                                       R vi2, bool visc, R inv_h, R eps_h2, R B2, R B1, R* s1, R* s2,
+                                       R* s3) {
+    for (int k = 0; k < len; k += 4) {
+        const uint2 v = slot_group<STAGED>(sl_sh, sl_g, k);
+        constexpr uint32_t U = sizeof(V4<R>) / 16;   // 16-byte units per record
+        const uint32_t off[4] = {U * (v.x & 0xffffu), U * (v.x >> 16), U * (v.y & 0xffffu),
+                                 U * (v.y >> 16)};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const V4<R> pj = lds4<R>(pos_sh + off[q]);
+            const uint32_t ra = rec_sh + 3u * off[q];
+            pair_b<R, DIM, KIND>(me.x - pj.x, DIM == 3 ? me.y - pj.y : R(0), me.z - pj.z,
+                                 lds4<R>(ra), lds4<R>(ra + sizeof(V4<R>)),
+                                 lds4<R>(ra + 2 * sizeof(V4<R>)), pj.w, UNI, vi0, vi1, vi2, visc,
+                                 inv_h, eps_h2, B2, B1, s1, s2, s3);
+        }
+    }
 }
 
 // Shared-memory tile of a CTA.  Two arrays indexed by slot, then the CTA's
@@ -641,24 +710,19 @@ __global__ void __launch_bounds__(kThreads, TL_MINB_A(R)) k_pass_a(const tl_body
             for (int q = 0; q < 9; ++q) D[q] = R(0);
             R M[6] = {R(0), R(0), R(0), R(0), R(0), R(0)};   // xx yy zz xy xz yz
             if (TILED) {
-                const auto me = tl_.pos[ms];
-                // this warp's slice within the CTA's staged slot block
-                const bool staged = b.slmax > 0;
-                const uint16_t* sl = tl_.slots + (base - b.soff[p0 >> 5]) +
-                                     lane * G;
+                const V4<R> me = tl_.pos[ms];
+                const uint32_t pos_sh = tl::smem_u32(tl_.pos), rec_sh = tl::smem_u32(tl_.rec);
+                const uint32_t sl_sh = tl::smem_u32(tl_.slots + (base - b.soff[p0 >> 5]) + lane * G);
                 const uint16_t* slg = b.slots + base + lane * G;
-                for (int k = 0; k < len; k += G) {
-                    int l[G];
-                    next_slots<G>(staged, sl, slg, k, l);
-    #pragma unroll
-                    for (int q = 0; q < G; ++q) {
-                        const int j = l[q];
-                        const auto pj = tl_.pos[j];
-                        pair_a<R, DIM, FRAC, KIND>(me.x - pj.x, DIM == 3 ? me.y - pj.y : R(0),
-                                                   me.z - pj.z, tl_.rec[j], pj.w, uni, ui, gated,
-                                                   inv_h, D, M);
-                    }
+                const bool staged = b.slmax > 0;
+#define TL_LOOP_A(U, ST)                                                                           \
+    loop_a<R, DIM, FRAC, KIND, U, ST>(pos_sh, rec_sh, sl_sh, slg, len, me, ui, gated, inv_h, D, M)
+                if (uni) {
+                    if (staged) TL_LOOP_A(true, true); else TL_LOOP_A(true, false);
+                } else {
+                    if (staged) TL_LOOP_A(false, true); else TL_LOOP_A(false, false);
                 }
+#undef TL_LOOP_A
             } else {
                 const double xi = b.Xs[i], yi = b.Xs[N + i], zi = b.Xs[2 * N + i];
                 const int32_t* sidx = b.sidx + base + lane;
@@ -1097,25 +1161,20 @@ __global__ void __launch_bounds__(kThreads, TL_MINB_B(R)) k_pass_b(const __grid_
             const R inv_rho = R(1.0 / b.rho0);
             R s1[3] = {R(0), R(0), R(0)}, s2[3] = {R(0), R(0), R(0)}, s3[3] = {R(0), R(0), R(0)};
             if (TILED) {
-                const auto me = tl_.pos[ms];
-                // this warp's slice within the CTA's staged slot block
-                const bool staged = b.slmax > 0;
-                const uint16_t* sl = tl_.slots + (base - b.soff[p0 >> 5]) +
-                                     lane * G;
+                const V4<R> me = tl_.pos[ms];
+                const uint32_t pos_sh = tl::smem_u32(tl_.pos), rec_sh = tl::smem_u32(tl_.rec);
+                const uint32_t sl_sh = tl::smem_u32(tl_.slots + (base - b.soff[p0 >> 5]) + lane * G);
                 const uint16_t* slg = b.slots + base + lane * G;
-                for (int k = 0; k < len; k += G) {
-                    int l[G];
-                    next_slots<G>(staged, sl, slg, k, l);
-    #pragma unroll
-                    for (int q = 0; q < G; ++q) {
-                        const int j = l[q];
-                        const auto pj = tl_.pos[j];
-                        const V4<R>* rj = tl_.rec + 3 * j;
-                        pair_b<R, DIM, KIND>(me.x - pj.x, DIM == 3 ? me.y - pj.y : R(0), me.z - pj.z,
-                                             rj[0], rj[1], rj[2], pj.w, uni, vi0, vi1, vi2, visc, inv_h,
-                                             eps_h2, B2, B1, s1, s2, s3);
-                    }
+                const bool staged = b.slmax > 0;
+#define TL_LOOP_B(U, ST)                                                                           \
+    loop_b<R, DIM, KIND, U, ST>(pos_sh, rec_sh, sl_sh, slg, len, me, vi0, vi1, vi2, visc, inv_h,  \
+                                eps_h2, B2, B1, s1, s2, s3)
+                if (uni) {
+                    if (staged) TL_LOOP_B(true, true); else TL_LOOP_B(true, false);
+                } else {
+                    if (staged) TL_LOOP_B(false, true); else TL_LOOP_B(false, false);
                 }
+#undef TL_LOOP_B
             } else {
                 const double xi = b.Xs[i], yi = b.Xs[N + i], zi = b.Xs[2 * N + i];
                 const int32_t* sidx = b.sidx + base + lane;

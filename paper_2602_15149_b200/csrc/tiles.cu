@@ -102,7 +102,7 @@ __global__ void k_halo_scatter(int64_t m, const uint64_t* __restrict__ keys,
 
 // local slot of every pair, in the group-interleaved sliced layout:
 // slot(w, k, lane) at soff[w] + (k/G)*32*G + lane*G + k%G; padding = own slot
-__global__ void k_slots(int64_t n, int T, int G, const int64_t* __restrict__ indptr,
+__global__ void k_slots(int64_t n, int T, int G, int shift, const int64_t* __restrict__ indptr,
                         const int32_t* __restrict__ indices, const int64_t* __restrict__ hoff,
                         const int32_t* __restrict__ halo, const uint16_t* __restrict__ hslot,
                         const int64_t* __restrict__ soff, uint16_t* __restrict__ slots) {
@@ -136,7 +136,7 @@ __global__ void k_slots(int64_t n, int T, int G, const int64_t* __restrict__ ind
                 s = hsl[lo];
             }
         }
-        slots[base + (k / G) * 32 * G + lane * G + (k % G)] = s;
+        slots[base + (k / G) * 32 * G + lane * G + (k % G)] = (uint16_t)(s << shift);
     }
 }
 
@@ -367,12 +367,17 @@ extern "C" int tl_tile_pos(tl_stream_t st, int64_t n, int64_t n_all, int32_t T, 
     return tl_check_launch("k_tile_pos");
 }
 
-extern "C" int tl_tile_slots(tl_stream_t st, int64_t n, int32_t T, int32_t G, const int64_t* indptr,
-                             const int32_t* indices, const int64_t* hoff, const int32_t* halo,
-                             const uint16_t* hslot, const int64_t* soff, uint16_t* slots) {
+extern "C" int tl_tile_slots(tl_stream_t st, int64_t n, int32_t T, int32_t G, int32_t shift,
+                             const int64_t* indptr, const int32_t* indices, const int64_t* hoff,
+                             const int32_t* halo, const uint16_t* hslot, const int64_t* soff,
+                             uint16_t* slots) {
     if (n <= 0) return TL_OK;
+    if (shift < 0 || shift > 8) {
+        tl_set_error("tl_tile_slots: shift out of range");
+        return TL_ERR_ARG;
+    }
     const int64_t nt = ((n + 31) / 32) * 32;
-    k_slots<<<tl_blocks(nt, kThreads), kThreads, 0, (cudaStream_t)st>>>(n, T, G, indptr, indices,
+    k_slots<<<tl_blocks(nt, kThreads), kThreads, 0, (cudaStream_t)st>>>(n, T, G, shift, indptr, indices,
                                                                       hoff, halo, hslot, soff, slots);
     return tl_check_launch("k_slots");
 }

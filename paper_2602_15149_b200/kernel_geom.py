@@ -188,7 +188,7 @@ class StepLayout:
     GROUP = 4   # TL_SELL_GROUP
     RESIDUE = int(os.environ.get("TLSPH_HALO_RESIDUE", "8"))   # 8 = bank-aligned halo slots
 
-    def __init__(self, dadj, tile=256, rows=None, halo=None):
+    def __init__(self, dadj, tile=256, rows=None, halo=None, precision="fp64"):
         """rows: adjacency rows this device owns (default all); halo: adjacency
         ids of the off-rank particles those rows reference, in exchange order
         (multi-GPU, see dist.py).  Device positions: owned [0, n) in Morton
@@ -252,6 +252,8 @@ class StepLayout:
         self.hmax = 0
         self.slmax = 0
         self.hoff = self.halo = self.slots = self.hslot = self.toff = None
+        # slots hold slot * 16 (16-byte units; FP64 records are two units)
+        self.slot_shift = 4
         if tile and tile > 0:
             if tile % 32 or tile > 256:
                 raise ValueError(f"tile size {tile}: a multiple of 32, at most 256")
@@ -276,7 +278,7 @@ class StepLayout:
         self.hoff = torch.zeros(ntile + 1, dtype=torch.int64, device=dev)
         torch.cumsum(tcount, 0, out=self.hoff[1:])
         if T + 8 * int(tcount.max().item() if ntile else 0) > 65535:
-            return   # slots are uint16: leave the body untiled
+            return   # slot indices are uint16: leave the body untiled
         # shared-memory slot of every halo entry (bank-conflict-free residues;
         # tiles that would outgrow 1.1x the densest halo are packed densely)
         self.hslot = torch.empty(max(int(self.halo.shape[0]), 1), dtype=torch.int16, device=dev)
@@ -296,7 +298,11 @@ class StepLayout:
         wb.clamp_(max=nw)
         self.slmax = int((self.soff[wb[1:]] - self.soff[wb[:-1]]).max().item()) if ntile else 0
         self.slots = torch.empty(max(total, 4), dtype=torch.int16, device=dev)
-        _lib.check(L.tl_tile_slots(st, n, T, self.GROUP, _lib.ptr(self.indptr),
+        if (T + self.hmax) << self.slot_shift > 65535:
+            self.hoff = self.halo = self.hslot = self.toff = None
+            self.hmax = 0
+            return   # slot byte offsets are uint16: leave the body untiled
+        _lib.check(L.tl_tile_slots(st, n, T, self.GROUP, self.slot_shift, _lib.ptr(self.indptr),
                                    _lib.ptr(self.indices), _lib.ptr(self.hoff),
                                    _lib.ptr(self.halo), _lib.ptr(self.hslot), _lib.ptr(self.soff),
                                    _lib.ptr(self.slots)), "tl_tile_slots")

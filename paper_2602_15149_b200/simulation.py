@@ -88,13 +88,14 @@ class DeviceBody:
         if part is not None:
             part.complete(dadj)          # halo ids in exchange order (collective-free)
             lay = kernel_geom.StepLayout(dadj, tile=tile, rows=part.owned_rows,
-                                         halo=part.halo_rows)
+                                         halo=part.halo_rows, precision=precision)
         else:
-            lay = kernel_geom.StepLayout(dadj, tile=tile)
+            lay = kernel_geom.StepLayout(dadj, tile=tile, precision=precision)
         rec = 64 if precision == "fp32" else 128          # pass-B bytes per staged particle
         if lay.tile and (lay.tile + lay.hmax) * rec > TILE_SMEM_LIMIT:
             lay.tile = 0                                   # halo too fat: gather from L2
-        if lay.tile and (lay.tile + lay.hmax) * rec + 2 * lay.slmax > TILE_SMEM_LIMIT:
+        if lay.tile and ((lay.tile + lay.hmax) * rec + 2 * lay.slmax > TILE_SMEM_LIMIT
+                         or os.environ.get("TLSPH_SLOT_STAGE", "1") == "0"):
             lay.slmax = 0                                  # slot table read from global memory
         self.layout = lay
         n, n_all = lay.n, lay.n_all
