@@ -1,7 +1,8 @@
 """Key metrics + top stall reasons of every kernel in an .ncu-rep.
-usage: python tools/ncu_report.py report.ncu-rep"""
+usage: python tools/ncu_report.py report.ncu-rep [--json out.json]"""
 import csv
 import io
+import json
 import subprocess
 import sys
 
@@ -23,17 +24,26 @@ def main():
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     h = rows[0]
+    summary = {}
     for r in rows[2:]:
-        print(r[h.index('Kernel Name')][:70])
+        name = r[h.index('Kernel Name')]
+        print(name[:70])
+        d = {}
         for k in KEYS:
             if k in h:
                 print(f"   {k:62s} {r[h.index(k)]} {rows[1][h.index(k)]}")
+                d[k] = f"{r[h.index(k)]} {rows[1][h.index(k)]}".strip()
         st = [(k.replace('smsp__average_warps_issue_stalled_', '').replace(
             '_per_issue_active.ratio', ''), float(r[i])) for i, k in enumerate(h)
             if k.startswith('smsp__average_warps_issue_stalled') and
             k.endswith('per_issue_active.ratio') and r[i]]
         st.sort(key=lambda x: -x[1])
         print("   stalls", [(a, round(b, 2)) for a, b in st[:7]])
+        d["top_stalls_per_issue"] = {a: round(b, 2) for a, b in st[:7]}
+        summary[name] = d
+    if "--json" in sys.argv:
+        with open(sys.argv[sys.argv.index("--json") + 1], "w") as f:
+            json.dump(summary, f, indent=1)
 
 
 if __name__ == "__main__":
