@@ -528,11 +528,10 @@ __device__ __forceinline__ void loop_a(uint32_t pos_sh, uint32_t rec_sh, uint32_
     }
 }
 
-template <typename R, int DIM, int KIND, bool UNI, bool STAGED>
+template <typename R, int DIM, int KIND, bool UNI, bool STAGED, bool VISC>
 __device__ __forceinline__ void loop_b(uint32_t pos_sh, uint32_t rec_sh, uint32_t sl_sh,
                                        const uint16_t* sl_g, int len, const V4<R>& me, R vi0, R vi1,
-                                       R vi2, bool visc, R inv_h, R eps_h2, R B2, R B1, R* s1, R* s2,
-                                       R* s3) {
+                                       R vi2, R inv_h, R eps_h2, R B2, R B1, R* s1, R* s2, R* s3) {
     for (int k = 0; k < len; k += 4) {
         const uint2 v = slot_group<STAGED>(sl_sh, sl_g, k);
         constexpr uint32_t U = sizeof(V4<R>) / 16;   // 16-byte units per record
@@ -544,7 +543,7 @@ __device__ __forceinline__ void loop_b(uint32_t pos_sh, uint32_t rec_sh, uint32_
             const uint32_t ra = rec_sh + 3u * off[q];
             pair_b<R, DIM, KIND>(me.x - pj.x, DIM == 3 ? me.y - pj.y : R(0), me.z - pj.z,
                                  lds4<R>(ra), lds4<R>(ra + sizeof(V4<R>)),
-                                 lds4<R>(ra + 2 * sizeof(V4<R>)), pj.w, UNI, vi0, vi1, vi2, visc,
+                                 lds4<R>(ra + 2 * sizeof(V4<R>)), pj.w, UNI, vi0, vi1, vi2, VISC,
                                  inv_h, eps_h2, B2, B1, s1, s2, s3);
         }
     }
@@ -1166,14 +1165,17 @@ __global__ void __launch_bounds__(kThreads, TL_MINB_B(R)) k_pass_b(const __grid_
                 const uint32_t sl_sh = tl::smem_u32(tl_.slots + (base - b.soff[p0 >> 5]) + lane * G);
                 const uint16_t* slg = b.slots + base + lane * G;
                 const bool staged = b.slmax > 0;
-#define TL_LOOP_B(U, ST)                                                                           \
-    loop_b<R, DIM, KIND, U, ST>(pos_sh, rec_sh, sl_sh, slg, len, me, vi0, vi1, vi2, visc, inv_h,  \
-                                eps_h2, B2, B1, s1, s2, s3)
+#define TL_LOOP_B(U, ST, V)                                                                        \
+    loop_b<R, DIM, KIND, U, ST, V>(pos_sh, rec_sh, sl_sh, slg, len, me, vi0, vi1, vi2, inv_h,     \
+                                   eps_h2, B2, B1, s1, s2, s3)
+#define TL_LOOP_B2(U, ST)                                                                          \
+    if (visc) TL_LOOP_B(U, ST, true); else TL_LOOP_B(U, ST, false)
                 if (uni) {
-                    if (staged) TL_LOOP_B(true, true); else TL_LOOP_B(true, false);
+                    if (staged) { TL_LOOP_B2(true, true); } else { TL_LOOP_B2(true, false); }
                 } else {
-                    if (staged) TL_LOOP_B(false, true); else TL_LOOP_B(false, false);
+                    if (staged) { TL_LOOP_B2(false, true); } else { TL_LOOP_B2(false, false); }
                 }
+#undef TL_LOOP_B2
 #undef TL_LOOP_B
             } else {
                 const double xi = b.Xs[i], yi = b.Xs[N + i], zi = b.Xs[2 * N + i];

@@ -280,11 +280,11 @@ class StepLayout:
         if T + 8 * int(tcount.max().item() if ntile else 0) > 65535:
             return   # slot indices are uint16: leave the body untiled
         # shared-memory slot of every halo entry (bank-conflict-free residues;
-        # tiles that would outgrow 1.1x the densest halo are packed densely)
+        # tiles that would outgrow the densest dense halo are packed densely)
         self.hslot = torch.empty(max(int(self.halo.shape[0]), 1), dtype=torch.int16, device=dev)
         extent = torch.zeros(max(ntile, 1), dtype=torch.int32, device=dev)
         hdense = int(tcount.max().item()) if ntile else 0
-        cap = ((int(1.1 * hdense) + 7) // 8) * 8
+        cap = ((int(float(os.environ.get("TLSPH_HALO_CAP", "1.0")) * hdense) + 7) // 8) * 8
         _lib.check(L.tl_tile_hslots(st, ntile, T, self.RESIDUE, cap, _lib.ptr(self.hoff),
                                     _lib.ptr(self.halo), _lib.ptr(self.hslot), _lib.ptr(extent)),
                    "tl_tile_hslots")
