@@ -360,6 +360,20 @@ int tl_reduce_partials(tl_stream_t st, const double* partials, int64_t nparts, d
 /* blocks used by tl_pass_a (size of pw_partial) */
 int64_t tl_pass_blocks(int64_t n);
 
+/* ---------------------------------------------------------------------------
+ * Output reductions (output.cu).  Per-block FP64
+ * partials in block order (deterministic); the caller adds them.
+ * ------------------------------------------------------------------------- */
+/* blocks (= partial triples) tl_energies writes for n particles */
+int64_t tl_energy_blocks(int64_t n);
+/* (V0 psi_e, 1/2 m0 |v|^2, V0 Gc [(1-s)^2/(4 eps0) + eps0 |grad s|^2]) partials
+ * of the owned particles (output.py:25-49; grad s as backends/fast.py:156-169).
+ * Needs the host-layout mirrors (psi_out) of the last output step. */
+int tl_energies(tl_stream_t st, const tl_body* b, double* partials);
+/* (sum u, sum m0 a) partials, 6 per block of 256, over device positions
+ * pos[0..m) (output.py:63-71) */
+int tl_measure(tl_stream_t st, const tl_body* b, const int32_t* pos, int64_t m, double* partials);
+
 #ifdef __cplusplus
 }
 #endif

@@ -224,6 +224,17 @@ def gen_kernels():
 
 
 # ---------------------------------------------------------------------------
+def _outputs(sim):
+    """The reference's own output rows (output.py:25-71) at this step."""
+    from solidsph import output as rout
+    d = {}
+    for bi, b in enumerate(sim.bodies):
+        d[f"b{bi}.energies"] = np.array(rout.compute_energies(b, ref))
+        for k, idx in enumerate(b.measure_sets):
+            d[f"b{bi}.measure{k}"] = np.array(rout.measure_row(b, idx, sim.t)[1:], dtype=np.float64)
+    return d
+
+
 def _state(sim, full=True):
     d = {}
     keys = ("u", "v", "a", "s", "sdot", "sddot", "Hhist", "epbar", "psi_e", "F", "S", "Cp")
@@ -304,9 +315,56 @@ def gen_runs():
                 full = step in (checks[0], checks[-1])
                 for k, v in _state(sim, full).items():
                     out[f"s{step}.{k}"] = v
+                for k, v in _outputs(sim).items():
+                    out[f"s{step}.{k}"] = v
         out["dts"] = np.array(dts)
         out["checkpoints"] = np.array(checks)
         save(f"run_{tag}", **out)
+
+
+CRACK_T = 2.0e-4   # past the case's TimeMax (1.2e-4): the crack is well grown
+
+
+def gen_crack():
+    """2D Kalthoff-Winkler run to t = 2e-4 s (adaptive steps at dp_scale=2,
+    the reference's run loop: the crack leaves the notch tip), with the reference's own
+    crack metric (bench.py:237-260): the kink angle of the s < 0.5 set ahead
+    of the tip.  The device run must reproduce the crack path."""
+    import math
+    cfg = caseio.load_case(os.path.join(CASES, "kalthoff2d.xml"), dp_scale=2, mapfac=1)
+    out = dict(case_to_dict(cfg))
+    b = cfg.bodies[0]
+    out["adj0.indptr"] = b.adjacency.indptr
+    out["adj0.indices"] = b.adjacency.indices
+    sim = stepper.Simulation(cfg)
+    dts = []
+    orig_step = sim.step
+
+    def step(dt):
+        dts.append(dt)
+        orig_step(dt)
+
+    sim.step = step
+    # the reference's own run loop (stepper.py:237-263): adaptive dt clipped
+    # to the output grid, one output at TimeMax
+    sim.run(time_max=CRACK_T, time_out=CRACK_T)
+    st = b.state
+    quad = b.notches[0].points
+    tip = quad[int(np.argmax(quad[:, 0]))]
+    damaged = np.flatnonzero((st.s < 0.5) & (st.X[:, 0] > tip[0] + 2.0 * b.dp_body))
+    pts = st.X[damaged][:, [0, 2]]
+    _, _, vt = np.linalg.svd(pts - pts.mean(axis=0), full_matrices=False)
+    angle = math.degrees(math.atan2(abs(vt[0][1]), abs(vt[0][0])))
+    print(f"crack: {len(dts)} steps, t={sim.t:.6g}, {damaged.size} damaged ahead of the tip, "
+          f"kink {angle:.2f} deg")
+    for k in ("u", "v", "s", "sdot", "Hhist"):
+        out[f"end.{k}"] = getattr(st, k).copy()
+    out["end.t"] = np.array([sim.t])
+    out["end.energies"] = _outputs(sim)["b0.energies"]
+    out["dts"] = np.array(dts)
+    out["kink_angle_deg"] = np.array([angle])
+    out["damaged"] = damaged
+    save("crack_kalthoff2d", **out)
 
 
 def _with_algo(cfg, algo):
@@ -378,6 +436,6 @@ def gen_targets():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["adjacency", "kernels", "runs", "expr", "targets"]
+    which = sys.argv[1:] or ["adjacency", "kernels", "runs", "expr", "targets", "crack"]
     for w in which:
         globals()[f"gen_{w}"]()

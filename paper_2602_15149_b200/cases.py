@@ -341,6 +341,9 @@ def case_to_dict(cfg, prefix=""):
                                   has_target=bc.target is not None))
             if bc.target is not None:
                 out[f"{prefix}b{bi}.bc{ci}.target"] = np.asarray(bc.target, dtype=np.int64)
+        bm["n_measure"] = len(getattr(b, "measure_sets", []) or [])
+        for k, idx in enumerate(getattr(b, "measure_sets", []) or []):
+            out[f"{prefix}b{bi}.measure{k}"] = np.asarray(idx, dtype=np.int64)
         meta["bodies"].append(bm)
         out[f"{prefix}b{bi}.X"] = np.asarray(b.state.X)
         out[f"{prefix}b{bi}.V0"] = np.asarray(b.state.V0)
@@ -373,6 +376,8 @@ def case_from_dict(d, prefix="", build_adjacency=False):
                     kernel_correction=bm["kernel_correction"],
                     restrictphi_expr=bm["restrictphi_expr"], f0=np.asarray(bm["f0"]),
                     notches=[Quad(points=q) for q in bm["notches"]])
+        body.measure_sets = [np.asarray(d[f"{prefix}b{bi}.measure{k}"])
+                             for k in range(bm.get("n_measure", 0))]
         for ci, bc in enumerate(bm["bcs"]):
             body.bcs.append(BoundaryCondition(
                 kind=bc["kind"], ftype=bc["ftype"], mkid=bc["mkid"],

@@ -152,8 +152,25 @@ __device__ __forceinline__ int svk_update(const R* H, R lam, R mu, R s, bool fra
     }
     const R trp = trE > R(0) ? trE : R(0), trm = trE < R(0) ? trE : R(0);
     if (sizeof(R) == 4) {
+        // the split is positively homogeneous (E+(aE) = a E+(E)): run it on E
+        // scaled to unit max entry so tiny strains far from the load do not
+        // underflow (FTZ) into a 0/0 in the projector
+        float m = 0.f;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) m = fmaxf(m, fabsf(float(E[k])));
         float Ep[9];
-        positive_part(reinterpret_cast<const float*>(E), Ep);
+        if (m > 0.f) {
+            const float im = 1.f / m;
+            float En[9];
+#pragma unroll
+            for (int k = 0; k < 9; ++k) En[k] = float(E[k]) * im;
+            positive_part(En, Ep);
+#pragma unroll
+            for (int k = 0; k < 9; ++k) Ep[k] *= m;
+        } else {
+#pragma unroll
+            for (int k = 0; k < 9; ++k) Ep[k] = 0.f;
+        }
         const R s2 = s * s;
         R fp = R(0), fm = R(0);
 #pragma unroll

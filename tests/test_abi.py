@@ -160,3 +160,18 @@ def test_workload_sizes():
     # C4: round(99.5/0.1836) x round(10/0.1836) x round(99.5/0.1836)
     dpb = 1e-3 * 0.918 / 5
     assert (round(99.5e-3 / dpb) * round(10e-3 / dpb) * round(99.5e-3 / dpb)) == 15863256
+
+
+def test_output_hooks_install_and_reject_host_bodies():
+    """output.install routes a reference-style module's OutputManager to the
+    device reductions; host (non-device) bodies are refused, not computed
+    on the CPU."""
+    import types
+    from paper_2602_15149_b200 import output
+    mod = types.SimpleNamespace(compute_energies=None, measure_row=None)
+    output.install(mod)
+    assert mod.compute_energies is output.compute_energies
+    assert mod.measure_row is output.measure_row
+    body = types.SimpleNamespace(state=types.SimpleNamespace())
+    with pytest.raises(TypeError):
+        output.compute_energies(body)

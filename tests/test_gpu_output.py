@@ -1,0 +1,157 @@
+"""Device output rows and long-run behaviour against the reference's own
+numbers (tests/golden, oracle/gen_golden.py):
+
+* output.compute_energies / measure_row (output.py:25-71) on the device,
+  FP64, at the golden checkpoints;
+* the 2D Kalthoff-Winkler crack path: 2010 adaptive device-clock steps to
+  t = 2e-4 s, damaged set and kink angle as the reference's bench metric
+  (bench.py:237-260), FP64 and FP32;
+* FP32 drift after N steps against the FP64 reference.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from conftest import golden, relerr, run_case
+
+pytestmark = pytest.mark.gpu
+
+# energies: sums of up to 1e4 terms in a different order than numpy's dot
+ENERGY_RTOL = 1e-10
+
+
+def _device(G, precision="fp64"):
+    from paper_2602_15149_b200.simulation import DeviceSimulation
+    cfg = run_case(G)
+    return cfg, DeviceSimulation(cfg, precision=precision)
+
+
+@pytest.mark.parametrize("tag", ["kalthoff2d_p", "taylor3d", "beam2d", "kalthoff3d", "branch2d"])
+def test_device_energies_match_reference(tag):
+    from paper_2602_15149_b200 import output
+    G = golden(f"run_{tag}")
+    cfg, sim = _device(G)
+    sim.initialize()
+    body = cfg.bodies[0]
+    checks = [int(c) for c in G["checkpoints"]]
+    for step in range(1, checks[-1] + 1):
+        sim.step(G["dts"][step - 1])
+        if step in checks:
+            got = np.array(output.compute_energies(body, sim.be))
+            ref = G[f"s{step}.b0.energies"]
+            scale = max(np.abs(ref).max(), 1e-300)
+            for k in range(4):
+                assert abs(got[k] - ref[k]) <= ENERGY_RTOL * max(abs(ref[k]), 1e-6 * scale), \
+                    (step, k, got[k], ref[k])
+
+
+@pytest.mark.parametrize("tag", ["kalthoff2d_p", "taylor3d"])
+def test_device_measure_row(tag):
+    """measure_row over an arbitrary particle set: mean u and sum m0*a, as
+    the reference formula applied to the reference state."""
+    from paper_2602_15149_b200 import output
+    G = golden(f"run_{tag}")
+    cfg, sim = _device(G)
+    sim.initialize()
+    body = cfg.bodies[0]
+    n = body.state.X.shape[0]
+    idx = np.arange(3, n, 7)
+    last = int(G["checkpoints"][-1])
+    for step in range(1, last + 1):
+        sim.step(G["dts"][step - 1])
+    row = output.measure_row(body, idx, sim.t)
+    u = G[f"s{last}.b0.u"]
+    a = G[f"s{last}.b0.a"]
+    m0 = np.full(n, float(body.state.m0[0])) if np.all(body.state.m0 == body.state.m0[0]) \
+        else np.asarray(body.state.m0)
+    u_avg = u[idx].mean(axis=0)
+    f_tot = (m0[idx, None] * a[idx]).sum(axis=0)
+    assert row[7] == idx.size and row[0] == sim.t
+    assert relerr(np.array(row[1:4]), u_avg) <= 1e-9
+    assert relerr(np.array(row[4:7]), f_tot) <= 1e-9
+    assert output.measure_row(body, np.array([], dtype=np.int64), sim.t)[7] == 0
+
+
+def _crack(X, s, tip, dp):
+    """The reference's crack metric (bench.py:237-260): the s < 0.5 set ahead
+    of the notch tip and the kink angle of its principal direction."""
+    damaged = np.flatnonzero((s < 0.5) & (X[:, 0] > tip[0] + 2.0 * dp))
+    pts = X[damaged][:, [0, 2]]
+    _, _, vt = np.linalg.svd(pts - pts.mean(axis=0), full_matrices=False)
+    return damaged, math.degrees(math.atan2(abs(vt[0][1]), abs(vt[0][0])))
+
+
+# This coarse Kalthoff run is chaotic: the phase field hits its clamps every
+# few steps and rounding-level differences grow to O(1) in s.  Measured in the
+# build container with the reference algorithm itself (the oracle, which
+# matches the numpy reference to 1e-12 over the 2010 steps), six runs whose
+# initial u differ by 1e-22 m end apart by: u up to 4.2e-3 relative, damaged
+# count 12-16, kink angle 24.5-27 deg (two outliers at 73 and 81), centroid
+# of the damaged set up to 3.1 dp, crack tip column identical in all runs,
+# strain energy +-0.8 %, kinetic +-0.37 %, fracture -1.4 % .. +5.7 %
+# (10 runs).  The reference's numba
+# backend against its numpy backend: u 1.7e-3, fracture energy 0.26 %.  The
+# device run is held to that ensemble's spread (with margin) -- what crack
+# path agreement can mean for this case -- and must grow the crack from the
+# notch along the reference's line (centroid and crack tip of the damaged
+# set).
+CRACK_TOL = dict(count=(10, 22), centroid=4.0, tip=2.0, u=1e-2,
+                 energy=(0.02, 0.01, 0.08))   # strain, kinetic, fracture
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_crack_path_matches_reference(precision):
+    """2D Kalthoff run (device clock, adaptive dt, 2010 steps, the
+    reference's run loop): the crack leaves the notch along the reference's
+    path."""
+    from paper_2602_15149_b200 import output
+    tol = CRACK_TOL
+    G = golden("crack_kalthoff2d")
+    cfg, sim = _device(G, precision)
+    body = cfg.bodies[0]
+    t_end = float(G["end.t"][0])
+    sim.run(time_max=t_end, time_out=t_end)
+    assert sim.step_index == G["dts"].shape[0]
+    assert abs(sim.t - t_end) <= 1e-12 * t_end
+    st = body.state
+    X, dp = st.X, body.dp_body
+    quad = body.notches[0].points
+    tip = quad[int(np.argmax(quad[:, 0]))]
+    damaged, angle = _crack(X, st.s, tip, dp)
+    ref = G["damaged"]
+    print(precision, f"damaged {damaged.size} vs {ref.size}, kink {angle:.2f} vs "
+          f"{float(G['kink_angle_deg'][0]):.2f} deg")
+    assert tol["count"][0] <= damaged.size <= tol["count"][1]
+    cen = X[damaged][:, [0, 2]].mean(axis=0) - X[ref][:, [0, 2]].mean(axis=0)
+    assert np.linalg.norm(cen) <= tol["centroid"] * dp
+    assert abs(X[damaged, 0].max() - X[ref, 0].max()) <= tol["tip"] * dp
+    assert relerr(st.u, G["end.u"]) <= tol["u"]
+    e = output.compute_energies(body, sim.be)
+    for k in range(3):
+        ref_e = float(G["end.energies"][k])
+        assert abs(e[k] - ref_e) <= tol["energy"][k] * abs(ref_e), (k, e[k], ref_e)
+
+
+# FP32 drift against the FP64 reference after the golden run length
+# (normwise max|x - ref| / max|ref|; H = F - I for F)
+FP32_DRIFT = {"u": 2e-5, "v": 2e-4, "S": 2e-4}
+
+
+@pytest.mark.parametrize("tag", ["kalthoff2d_p", "beam2d", "taylor3d", "kalthoff3d", "column3d"])
+def test_fp32_drift_after_n_steps(tag):
+    G = golden(f"run_{tag}")
+    cfg, sim = _device(G, "fp32")
+    sim.initialize()
+    last = int(G["checkpoints"][-1])
+    for step in range(1, last + 1):
+        sim.step(G["dts"][step - 1])
+    st = cfg.bodies[0].state
+    errs = {k: relerr(getattr(st, k), G[f"s{last}.b0.{k}"]) for k in FP32_DRIFT}
+    if cfg.bodies[0].fracture:
+        errs["s_abs"] = float(np.abs(st.s - G[f"s{last}.b0.s"]).max())
+    print(tag, last, "steps FP32 drift", {k: f"{v:.2e}" for k, v in errs.items()})
+    for k, tol in FP32_DRIFT.items():
+        assert errs[k] <= tol, (k, errs[k])
+    if "s_abs" in errs:
+        assert errs["s_abs"] <= 1e-4
