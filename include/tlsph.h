@@ -31,7 +31,7 @@ enum {
     TL_ERR_CASE = -4
 };
 
-#define TL_ABI_VERSION 4
+#define TL_ABI_VERSION 5
 
 int tl_abi_version(void);
 /* sizeof of the ABI structs, for binding checks: 0 tl_body, 1 tl_clock,
@@ -269,9 +269,11 @@ typedef struct {
     double h, inv_h, alpha, rho0, lam, mu, kappa, c0, beta1, beta2;
     double Gc, eps0, s_l, sigma_y0, H_hard, V0c, m0c, dp_body, jac_tol;
     double f0[3];
-    /* neighbours: sliced ELL, 32 particles per slice, lane-interleaved */
+    /* neighbours: sliced ELL, 32 particles per slice, lane-interleaved;
+     * wlen[w] = longest real row of slice w (slices are padded to 4) */
     const int64_t* soff;
     const int32_t* sidx;
+    const int32_t* wlen;
     /* shared-memory tiles (tile > 0): CTA = `tile` consecutive particles;
      * hoff[t]..hoff[t+1] indexes its halo particles in `halo`, staged at
      * shared slots `hslot`; slots are uint16 local indices (member

@@ -395,7 +395,12 @@ __device__ __forceinline__ R kshape(R r2, R inv_h, R& rs) {
     rs = tl::rsqrt_floor(r2);
     const R r = r2 * rs;
     if (KIND == 2) {
-        const R t = fmax(R(1) - r * (R(0.5) * inv_h), R(0));
+        // neighbours lie inside the support (r < 2h, decided in FP64 at the
+        // build), so t > 0; FP32 rounding near r = 2h can leave t ~ -1e-7,
+        // whose t^3 ~ -1e-21 is below the mode's resolution -- the clamp is
+        // kept only in FP64
+        R t = R(1) - r * (R(0.5) * inv_h);
+        if (sizeof(R) == 8) t = fmax(t, R(0));
         return t * t * t;
     }
     const R q = r * inv_h, tm = R(2) - q;
@@ -407,32 +412,32 @@ __device__ __forceinline__ R kshape_const(const tl_body& b) {
     return KIND == 2 ? R(-5.0 * b.alpha * b.inv_h * b.inv_h) : R(b.alpha * b.inv_h);
 }
 
-// pass A pair (w = V0_j-weighted shape):
-//   D += w (u_j - u_i) (x) r0 ;  M += (s_i - s_j) w / r^2  r0 r0^T
+// pass A pair (w = V0_j-weighted shape, wr = w r0):
+//   D += (u_j - u_i) (x) wr ;  M += (s_i - s_j) / r^2  wr (x) r0
+// (gated particles, s_i <= s_l, get F = I after the loop)
 template <typename R, int DIM, bool FRAC, int KIND>
 __device__ __forceinline__ void pair_a(R dx, R dy, R dz, const V4<R>& uj, R vj, bool uni,
-                                       const V4<R>& ui, bool gated, R inv_h, R* D, R* M) {
+                                       const V4<R>& ui, R inv_h, R* D, R* M) {
     const R r2 = dx * dx + dy * dy + dz * dz;
     R rs;
     R w = kshape<R, KIND>(r2, inv_h, rs);
     if (!uni) w *= vj;
-    {   // F = I on gated particles (s_i <= s_l): a select, not a branch per pair
-        const R wg = gated ? R(0) : w;
-        const R du0 = wg * (uj.x - ui.x), du2 = wg * (uj.z - ui.z);
-        D[0] += du0 * dx; D[2] += du0 * dz;
-        D[6] += du2 * dx; D[8] += du2 * dz;
-        if (DIM == 3) {
-            const R du1 = wg * (uj.y - ui.y);
-            D[1] += du0 * dy; D[7] += du2 * dy;
-            D[3] += du1 * dx; D[4] += du1 * dy; D[5] += du1 * dz;
-        }
+    const R wx = w * dx, wz = w * dz;
+    const R du0 = uj.x - ui.x, du2 = uj.z - ui.z;
+    D[0] += du0 * wx; D[2] += du0 * wz;
+    D[6] += du2 * wx; D[8] += du2 * wz;
+    const R wy = DIM == 3 ? w * dy : R(0);
+    if (DIM == 3) {
+        const R du1 = uj.y - ui.y;
+        D[1] += du0 * wy; D[7] += du2 * wy;
+        D[3] += du1 * wx; D[4] += du1 * wy; D[5] += du1 * wz;
     }
     if (FRAC) {
-        const R c = (ui.w - uj.w) * (w * (rs * rs));
-        const R cx = c * dx, cz = c * dz;
+        const R c = (ui.w - uj.w) * (rs * rs);
+        const R cx = c * wx, cz = c * wz;
         M[0] += cx * dx; M[2] += cz * dz; M[4] += cx * dz;
         if (DIM == 3) {
-            const R cy = c * dy;
+            const R cy = c * wy;
             M[1] += cy * dy; M[3] += cx * dy; M[5] += cy * dz;
         }
     }
@@ -526,22 +531,33 @@ __device__ __forceinline__ uint2 slot_group(uint32_t sl_sh, const uint16_t* sl_g
 // three times it (pass B, three records).
 // UNI (uniform V0 / m0) and STAGED (slot table in shared memory) are
 // compile-time so the loop body has no per-pair predicates or branches.
+// A warp's slices are padded to a multiple of 4 (slot groups); `len` is
+// the warp's real longest row, so the last group runs only len % 4 pairs.
 template <typename R, int DIM, bool FRAC, int KIND, bool UNI, bool STAGED>
 __device__ __forceinline__ void loop_a(uint32_t pos_sh, uint32_t rec_sh, uint32_t sl_sh,
                                        const uint16_t* sl_g, int len, const V4<R>& me,
-                                       const V4<R>& ui, bool gated, R inv_h, R* D, R* M) {
-    for (int k = 0; k < len; k += 4) {
+                                       const V4<R>& ui, R inv_h, R* D, R* M) {
+    constexpr uint32_t U = sizeof(V4<R>) / 16;   // 16-byte units per record
+    auto pair = [&](uint32_t o) {
+        const V4<R> pj = lds4<R>(pos_sh + o);
+        const V4<R> uj = lds4<R>(rec_sh + o);
+        pair_a<R, DIM, FRAC, KIND>(me.x - pj.x, DIM == 3 ? me.y - pj.y : R(0), me.z - pj.z, uj, pj.w,
+                                   UNI, ui, inv_h, D, M);
+    };
+    const int full = len & ~3;
+    int k = 0;
+    for (; k < full; k += 4) {
         const uint2 v = slot_group<STAGED>(sl_sh, sl_g, k);
-        constexpr uint32_t U = sizeof(V4<R>) / 16;   // 16-byte units per record
-        const uint32_t off[4] = {U * (v.x & 0xffffu), U * (v.x >> 16), U * (v.y & 0xffffu),
-                                 U * (v.y >> 16)};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const V4<R> pj = lds4<R>(pos_sh + off[q]);
-            const V4<R> uj = lds4<R>(rec_sh + off[q]);
-            pair_a<R, DIM, FRAC, KIND>(me.x - pj.x, DIM == 3 ? me.y - pj.y : R(0), me.z - pj.z, uj,
-                                       pj.w, UNI, ui, gated, inv_h, D, M);
-        }
+        pair(U * (v.x & 0xffffu));
+        pair(U * (v.x >> 16));
+        pair(U * (v.y & 0xffffu));
+        pair(U * (v.y >> 16));
+    }
+    if (len & 3) {
+        const uint2 v = slot_group<STAGED>(sl_sh, sl_g, k);
+        pair(U * (v.x & 0xffffu));
+        if ((len & 3) > 1) pair(U * (v.x >> 16));
+        if ((len & 3) > 2) pair(U * (v.y & 0xffffu));
     }
 }
 
@@ -549,20 +565,28 @@ template <typename R, int DIM, int KIND, bool UNI, bool STAGED, bool VISC>
 __device__ __forceinline__ void loop_b(uint32_t pos_sh, uint32_t rec_sh, uint32_t sl_sh,
                                        const uint16_t* sl_g, int len, const V4<R>& me, R vi0, R vi1,
                                        R vi2, R inv_h, R eps_h2, R B2, R B1, R* s1, R* s2, R* s3) {
-    for (int k = 0; k < len; k += 4) {
+    constexpr uint32_t U = sizeof(V4<R>) / 16;
+    auto pair = [&](uint32_t o) {
+        const V4<R> pj = lds4<R>(pos_sh + o);
+        const uint32_t ra = rec_sh + 3u * o;
+        pair_b<R, DIM, KIND>(me.x - pj.x, DIM == 3 ? me.y - pj.y : R(0), me.z - pj.z, lds4<R>(ra),
+                             lds4<R>(ra + sizeof(V4<R>)), lds4<R>(ra + 2 * sizeof(V4<R>)), pj.w, UNI,
+                             vi0, vi1, vi2, VISC, inv_h, eps_h2, B2, B1, s1, s2, s3);
+    };
+    const int full = len & ~3;
+    int k = 0;
+    for (; k < full; k += 4) {
         const uint2 v = slot_group<STAGED>(sl_sh, sl_g, k);
-        constexpr uint32_t U = sizeof(V4<R>) / 16;   // 16-byte units per record
-        const uint32_t off[4] = {U * (v.x & 0xffffu), U * (v.x >> 16), U * (v.y & 0xffffu),
-                                 U * (v.y >> 16)};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const V4<R> pj = lds4<R>(pos_sh + off[q]);
-            const uint32_t ra = rec_sh + 3u * off[q];
-            pair_b<R, DIM, KIND>(me.x - pj.x, DIM == 3 ? me.y - pj.y : R(0), me.z - pj.z,
-                                 lds4<R>(ra), lds4<R>(ra + sizeof(V4<R>)),
-                                 lds4<R>(ra + 2 * sizeof(V4<R>)), pj.w, UNI, vi0, vi1, vi2, VISC,
-                                 inv_h, eps_h2, B2, B1, s1, s2, s3);
-        }
+        pair(U * (v.x & 0xffffu));
+        pair(U * (v.x >> 16));
+        pair(U * (v.y & 0xffffu));
+        pair(U * (v.y >> 16));
+    }
+    if (len & 3) {
+        const uint2 v = slot_group<STAGED>(sl_sh, sl_g, k);
+        pair(U * (v.x & 0xffffu));
+        if ((len & 3) > 1) pair(U * (v.x >> 16));
+        if ((len & 3) > 2) pair(U * (v.y & 0xffffu));
     }
 }
 
@@ -731,8 +755,9 @@ __global__ void __launch_bounds__(kThreads, TL_MINB_A(R)) k_pass_a(const tl_body
                 const uint32_t sl_sh = tl::smem_u32(tl_.slots + (base - b.soff[p0 >> 5]) + lane * G);
                 const uint16_t* slg = b.slots + base + lane * G;
                 const bool staged = b.slmax > 0;
+                const int lenr = b.wlen ? (int)b.wlen[w] : len;   // real longest row
 #define TL_LOOP_A(U, ST)                                                                           \
-    loop_a<R, DIM, FRAC, KIND, U, ST>(pos_sh, rec_sh, sl_sh, slg, len, me, ui, gated, inv_h, D, M)
+    loop_a<R, DIM, FRAC, KIND, U, ST>(pos_sh, rec_sh, sl_sh, slg, lenr, me, ui, inv_h, D, M)
                 if (uni) {
                     if (staged) TL_LOOP_A(true, true); else TL_LOOP_A(true, false);
                 } else {
@@ -765,7 +790,7 @@ __global__ void __launch_bounds__(kThreads, TL_MINB_A(R)) k_pass_a(const tl_body
     #pragma unroll
                     for (int q = 0; q < G; ++q)
                         pair_a<R, DIM, FRAC, KIND>(R(xi - xj[q]), DIM == 3 ? R(yi - yj[q]) : R(0),
-                                                   R(zi - zj[q]), uj[q], vj[q], uni, ui, gated, inv_h,
+                                                   R(zi - zj[q]), uj[q], vj[q], uni, ui, inv_h,
                                                    D, M);
                 }
             }
@@ -1182,8 +1207,9 @@ __global__ void __launch_bounds__(kThreads, TL_MINB_B(R)) k_pass_b(const __grid_
                 const uint32_t sl_sh = tl::smem_u32(tl_.slots + (base - b.soff[p0 >> 5]) + lane * G);
                 const uint16_t* slg = b.slots + base + lane * G;
                 const bool staged = b.slmax > 0;
+                const int lenr = b.wlen ? (int)b.wlen[w] : len;   // real longest row
 #define TL_LOOP_B(U, ST, V)                                                                        \
-    loop_b<R, DIM, KIND, U, ST, V>(pos_sh, rec_sh, sl_sh, slg, len, me, vi0, vi1, vi2, inv_h,     \
+    loop_b<R, DIM, KIND, U, ST, V>(pos_sh, rec_sh, sl_sh, slg, lenr, me, vi0, vi1, vi2, inv_h,    \
                                    eps_h2, B2, B1, s1, s2, s3)
 #define TL_LOOP_B2(U, ST)                                                                          \
     if (visc) TL_LOOP_B(U, ST, true); else TL_LOOP_B(U, ST, false)

@@ -242,6 +242,10 @@ class StepLayout:
         slen = torch.empty(nw, dtype=torch.int32, device=dev)
         _lib.check(L.tl_sell_lengths(st, n, _lib.ptr(self.indptr), _lib.ptr(slen)),
                    "tl_sell_lengths")
+        # longest real row of every slice (the slice itself is padded to 4)
+        rl = torch.zeros(nw * 32, dtype=torch.int32, device=dev)
+        rl[:n] = (self.indptr[1:] - self.indptr[:-1]).to(torch.int32)
+        self.wlen = rl.view(nw, 32).amax(dim=1).contiguous()
         self.soff = torch.zeros(nw + 1, dtype=torch.int64, device=dev)
         torch.cumsum(slen.to(torch.int64) * 32, 0, out=self.soff[1:])
         total = int(self.soff[-1].item())
