@@ -198,6 +198,9 @@ def main():
     ap.add_argument("--config", default="C4", choices=["C4"])
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: ranks may share one GPU (halo buffers staged through the host; "
+                         "a plumbing check, not a throughput number)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -227,10 +230,13 @@ def main():
     from paper_2602_15149_b200 import cases
     from paper_2602_15149_b200.simulation import DeviceSimulation
 
-    torch.cuda.set_device(local)
+    torch.cuda.set_device(local % max(torch.cuda.device_count(), 1))
     if world > 1:
-        dist.init_process_group("nccl", init_method="env://",
-                                device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", init_method="env://",
+                                    device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo", init_method="env://")
 
     t0 = time.perf_counter()
     cfg = cases.make_case(args.config, lean=True, build_adjacency=False)
@@ -241,7 +247,7 @@ def main():
     torch.cuda.synchronize()
     t_setup = time.perf_counter() - t0
     n = sum(db.n for db in sim.dbodies)
-    nnz = sum(db.adj.nnz for db in sim.dbodies)
+    nnz = sum(int(db.layout.indptr[-1].item()) for db in sim.dbodies)   # owned rows
     k_mean = nnz / n
     sim.initialize()
     sim.advance(args.warmup)
@@ -268,10 +274,11 @@ def main():
     tb = [e[2].elapsed_time(e[3]) for e in pass_ev]
     sim.finish_advance()
     if world > 1:
-        tt = torch.tensor([ms], device="cuda")
+        cdev = "cuda" if args.dist_backend == "nccl" else "cpu"
+        tt = torch.tensor([ms], device=cdev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
-        nt = torch.tensor([n], device="cuda", dtype=torch.float64)
+        nt = torch.tensor([n], device=cdev, dtype=torch.float64)
         dist.all_reduce(nt)
         n_total = float(nt.item())
     else:
@@ -340,8 +347,8 @@ def main():
                                        "adaptive dt",
                            "particles_per_gpu": n, "particles": int(n_total),
                            "pairs_per_particle": k_mean,
-                           "parallelism": (f"slab{world} (halo exchange over NCCL)" if world > 1
-                                           else "single"),
+                           "parallelism": (f"slab{world} (halo exchange over "
+                                           f"{args.dist_backend})" if world > 1 else "single"),
                            "l2": "per-step working set >> 126 MB L2, no flush",
                            "precision": args.precision,
                            "setup_s": {"case": t_case, "device_build": t_setup}},
