@@ -13,13 +13,16 @@ initial state is the seeded "synthetic block" perturbation of SURVEY.md 8(d)
 branch does real work.  A step = one device-clock Verlet step (dt, pass A,
 pass B, commit).  value = particle-steps/s over the timed steps (CUDA
 events, max over ranks).  --gpus N (torchrun) partitions the same 15.9 M
-particles into N slabs with halo exchange (strong scaling).  The ~9 GB per-step working set is far larger than
-the 126 MB L2, so no flush is needed between steps.
+particles into N slabs with halo exchange (strong scaling, SURVEY.md
+8(e)).  The ~9 GB per-step working set is far larger than the 126 MB L2, so
+no flush is needed between steps.
 
 Extra keys: roofline (dominant kernel vs measured HBM copy bandwidth,
 SURVEY.md 8(d) algorithmic bytes), cpu_baseline (the CPU oracle port, a
-bounded sample of the same case on this host's cores), e2e (public
-step()/pick_dt() API with host state mirrors every step), clocks, passes.
+bounded sample of the same case on this host's cores), e2e (the public
+Simulation.run() API: device-clock batches of 64 steps, one host round trip
+per batch; per_step_api = pick_dt() + step() with a round trip per step),
+clocks, passes.
 
 --impl reference times the reference algorithm on the host CPU (the oracle
 port of solidsph's numba/numpy backends, oracle/; the reference itself is a
@@ -196,7 +199,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--config", default="C4", choices=["C4"])
-    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: ranks may share one GPU (halo buffers staged through the host; "
@@ -309,23 +312,37 @@ def main():
               "frac_a": ba * n / (ma / 1e3) / 1e9 / peak,
               "frac_b": bb * n / (mb / 1e3) / 1e9 / peak}
 
-    # end to end through the public API: pick_dt() + step() with host mirrors
+    # end to end through the public API (stepper.Simulation's): run() -- the
+    # throughput entry point, device-clock batches of 64 steps with one host
+    # round trip per batch -- and pick_dt() + step() with a round trip per step
     e2e = None
     if args.e2e_steps > 0:
+        import math as _m
+        nb = len(sim.dbodies)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        for _ in range(args.e2e_steps):
-            dt = sim.pick_dt()
-            sim.step(dt)
+        sim.run(time_max=1e30, time_out=1e30, max_steps=sim.step_index + args.e2e_steps)
         torch.cuda.synchronize()
         el = time.perf_counter() - t0
-        nb = len(sim.dbodies)
+        batches = _m.ceil(args.e2e_steps / 64)
         e2e = {"value": n_total * args.e2e_steps / el, "unit": "particle-steps/s",
-               # clock struct in; dt maxima (the step's scalar result), error
-               # counters and plastic work out
-               "h2d_bytes_per_step": 80, "d2h_bytes_per_step": 16 * nb + 64 * nb + 8 * nb,
-               "api": "DeviceSimulation.pick_dt() + step(dt) per step; host state arrays "
-                      "refresh lazily on access (DeviceState)"}
+               # per batch: clock struct in; clock, error counters, plastic work out
+               "h2d_bytes_per_step": 80 * batches / args.e2e_steps,
+               "d2h_bytes_per_step": (80 + 72 * nb) * batches / args.e2e_steps,
+               "steps": args.e2e_steps,
+               "api": "DeviceSimulation.run(max_steps=...) (the reference's Simulation.run); "
+                      "host state arrays refresh lazily on access (DeviceState)"}
+        k = min(args.e2e_steps, 32)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(k):
+            sim.step(sim.pick_dt())
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        e2e["per_step_api"] = {"value": n_total * k / el, "steps": k,
+                               "api": "pick_dt() + step(dt), one host round trip per step",
+                               "h2d_bytes_per_step": 80,
+                               "d2h_bytes_per_step": 16 * nb + 64 * nb + 8 * nb}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
