@@ -31,7 +31,7 @@ enum {
     TL_ERR_CASE = -4
 };
 
-#define TL_ABI_VERSION 5
+#define TL_ABI_VERSION 6
 
 int tl_abi_version(void);
 /* sizeof of the ABI structs, for binding checks: 0 tl_body, 1 tl_clock,
@@ -296,6 +296,8 @@ typedef struct {
     const void* L;          /* 9 planes, correction matrix L_i */
     const double* V0;       /* per particle when !uniform */
     const double* m0;
+    /* contact acceleration (3 FP64 planes, stride n_all) added before f0, or NULL */
+    const double* ac;
     /* state */
     void* us;               /* records of 4: ux uy uz s        (pass-A gather) */
     void* rb;               /* records of 12: (P L_i) row-major, vx vy vz (pass-B gather) */
@@ -375,6 +377,32 @@ int tl_energies(tl_stream_t st, const tl_body* b, double* partials);
 /* (sum u, sum m0 a) partials, 6 per block of 256, over device positions
  * pos[0..m) (output.py:63-71) */
 int tl_measure(tl_stream_t st, const tl_body* b, const int32_t* pos, int64_t m, double* partials);
+
+/* ---------------------------------------------------------------------------
+ * Penalty contact between two bodies (contact.cu; dynamics.py:81-135,
+ * backends/fast.py:426-469).  Current positions x = X + u, velocities v.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+    int64_t n, n_all;       /* owned particles; plane stride */
+    int32_t precision;      /* 4 | 8: Real of us / v */
+    int32_t uniform;        /* m0 == m0c for every particle */
+    double m0c;
+    const double* Xs;       /* 3 FP64 planes (device order) */
+    const void* us;         /* records (ux uy uz s) */
+    const void* v;          /* 3 planes */
+    const double* m0;       /* per particle when !uniform */
+    const int32_t* perm;    /* device position -> original index (summation order) */
+} tl_contact_side;
+/* scratch bytes tl_contact_pair needs (cell grid of at most cell_cap cells) */
+int tl_contact_workspace_bytes(int64_t n_a, int64_t n_b, int64_t cell_cap, int64_t* bytes);
+/* accumulate the contact accelerations of the pair (a, b) into acc_a / acc_b
+ * (3 FP64 planes each, stride n_all, NOT cleared): each particle adds its
+ * partners' terms in ascending original partner index, the reference's
+ * order.  counters[0] += near-coincident pairs (the reference's n_warn),
+ * counters[1] += candidates dropped over TL_CONTACT_CAP (must stay 0). */
+int tl_contact_pair(tl_stream_t st, const tl_contact_side* a, const tl_contact_side* b, int dim,
+                    double dpc, double k_n, double c_n, double kfric, int64_t cell_cap, void* work,
+                    int64_t work_bytes, double* acc_a, double* acc_b, unsigned long long* counters);
 
 #ifdef __cplusplus
 }

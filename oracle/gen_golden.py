@@ -290,6 +290,8 @@ def gen_runs():
         ("kalthoff3d", lambda: caseio.build_case(_kalthoff3d_raw(), dp_scale=6, mapfac=2), 36,
          10, (1, 2, 10)),
         ("twisting3d", lambda: L(C("twisting3d.xml"), dp_scale=4), 37, 10, (1, 10)),
+        # two J2 bodies, penalty contact from step 1 (_touching)
+        ("flyer2d", lambda: _touching(L(C("flyer2d.xml"), dp_scale=2)), None, 30, (1, 2, 30)),
     ]
     for tag, make, seed, steps, checks in runs:
         cfg = make()
@@ -365,6 +367,18 @@ def gen_crack():
     out["kink_angle_deg"] = np.array([angle])
     out["damaged"] = damaged
     save("crack_kalthoff2d", **out)
+
+
+def _touching(cfg):
+    """flyer2d with the upper body displaced (u, a rigid shift) so its lowest
+    layer sits 0.6 dp_contact above the plate: contact acts from step 1."""
+    up, low = cfg.bodies[0], cfg.bodies[1]
+    if up.state.X[:, 2].min() < low.state.X[:, 2].min():
+        up, low = low, up
+    dpc = 0.5 * (up.dp_body + low.dp_body)
+    shift = (up.state.X[:, 2].min() - low.state.X[:, 2].max()) - 0.6 * dpc
+    up.state.u[:, 2] = -shift
+    return cfg
 
 
 def _with_algo(cfg, algo):

@@ -13,7 +13,7 @@ import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("TLSPH_LIB", os.path.join(HERE, "libtlsph.so"))
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 _lib = None
 
@@ -76,7 +76,7 @@ _BODY_FIELDS += [("f0", D * 3)]
 _BODY_FIELDS += [("soff", P), ("sidx", P), ("wlen", P), ("tile", I32), ("hmax", I32), ("slmax", I32), ("pad_", I32), ("hoff", P),
                  ("halo", P), ("slots", P), ("hslot", P), ("toff", P), ("tpos_a", P),
                  ("tpos_b", P)]
-_BODY_FIELDS += [(k, P) for k in ("Xs", "L", "V0", "m0", "us", "rb", "v", "al",
+_BODY_FIELDS += [(k, P) for k in ("Xs", "L", "V0", "m0", "ac", "us", "rb", "v", "al",
                                   "sdot", "sddot", "Hh", "Cpd", "epbar", "a", "F_out", "S_out",
                                   "psi_out", "psip_out", "perm", "bcmask", "bcs", "progs", "clock", "red",
                                   "counters", "pw_partial")]
@@ -86,7 +86,12 @@ class tl_body(C.Structure):
     _fields_ = _BODY_FIELDS
 
 
-STRUCTS = (tl_body, tl_clock, tl_bc, tl_prog, tl_notch, tl_nb_params, tl_dtinfo)
+class tl_contact_side(C.Structure):
+    _fields_ = [("n", I64), ("n_all", I64), ("precision", I32), ("uniform", I32), ("m0c", D),
+                ("Xs", P), ("us", P), ("v", P), ("m0", P), ("perm", P)]
+
+
+STRUCTS = (tl_body, tl_clock, tl_bc, tl_prog, tl_notch, tl_nb_params, tl_dtinfo, tl_contact_side)
 
 _SIGS = {
     "tl_abi_version": (INT, []),
@@ -128,6 +133,9 @@ _SIGS = {
     "tl_energy_blocks": (I64, [I64]),
     "tl_energies": (INT, [P, C.POINTER(tl_body), P]),
     "tl_measure": (INT, [P, C.POINTER(tl_body), P, I64, P]),
+    "tl_contact_workspace_bytes": (INT, [I64, I64, I64, C.POINTER(I64)]),
+    "tl_contact_pair": (INT, [P, C.POINTER(tl_contact_side), C.POINTER(tl_contact_side), INT, D, D,
+                              D, D, I64, P, I64, P, P, P]),
 }
 
 EXPORTED = tuple(_SIGS)

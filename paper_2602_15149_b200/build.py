@@ -18,7 +18,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libtlsph.so")
-SOURCES = ["plugin.cu", "neighbors.cu", "tiles.cu", "step.cu", "output.cu"]
+SOURCES = ["plugin.cu", "neighbors.cu", "tiles.cu", "step.cu", "output.cu", "contact.cu"]
 HEADERS = ["tl_common.cuh", "expr_vm.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

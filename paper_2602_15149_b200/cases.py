@@ -322,6 +322,7 @@ def case_to_dict(cfg, prefix=""):
                 algo=int(cfg.step_algorithm), time_max=cfg.time_max, time_out=cfg.time_out,
                 dim=int(cfg.dim), dt_override=cfg.dt_override,
                 gravity=[float(g) for g in cfg.gravity],
+                contcoeff=float(getattr(cfg, "contcoeff", 1.0)),
                 expressions={str(k): [a.source, _locals_src(a)] for k, a in cfg.expressions.items()},
                 bodies=[])
     out = {}
@@ -332,7 +333,9 @@ def case_to_dict(cfg, prefix=""):
                   restrictphi_expr=b.restrictphi_expr, f0=[float(x) for x in b.f0],
                   material=dict(rho0=m.rho0, lam=m.lam, mu=m.mu, kappa=m.kappa, model=int(m.model),
                                 beta1=m.beta1, beta2=m.beta2, Gc=m.Gc, eps0=m.eps0, s_l=m.s_l,
-                                sigma_y0=m.sigma_y0, H_hard=m.H_hard),
+                                sigma_y0=m.sigma_y0, H_hard=m.H_hard,
+                                restcoef=float(getattr(m, "restcoef", 1.0)),
+                                kfric=float(getattr(m, "kfric", 0.0))),
                   notches=[np.asarray(q.points).tolist() for q in b.notches], bcs=[])
         for ci, bc in enumerate(b.bcs):
             bm["bcs"].append(dict(kind=bc.kind, ftype=bc.ftype, mkid=bc.mkid,
@@ -361,7 +364,8 @@ def case_from_dict(d, prefix="", build_adjacency=False):
     cfg = CaseConfig(dp=meta["dp"], coefh=meta["coefh"], cfl=meta["cfl"],
                      kernel=KernelKind(meta["kernel"]), step_algorithm=StepAlgorithm(meta["algo"]),
                      time_max=meta["time_max"], time_out=meta["time_out"], dim=meta["dim"],
-                     gravity=np.asarray(meta["gravity"]), dt_override=meta["dt_override"])
+                     gravity=np.asarray(meta["gravity"]), dt_override=meta["dt_override"],
+                     contcoeff=meta.get("contcoeff", 1.0))
     for k, (src, loc) in meta["expressions"].items():
         cfg.expressions[int(k)] = ex.parse(src, loc)
     for bi, bm in enumerate(meta["bodies"]):

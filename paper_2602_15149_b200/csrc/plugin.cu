@@ -41,6 +41,7 @@ extern "C" int64_t tl_struct_size(int which) {
         case 4: return (int64_t)sizeof(tl_notch);
         case 5: return (int64_t)sizeof(tl_nb_params);
         case 6: return (int64_t)sizeof(tl_dtinfo);
+        case 7: return (int64_t)sizeof(tl_contact_side);
         default: return -1;
     }
 }

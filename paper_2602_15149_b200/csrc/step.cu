@@ -1079,7 +1079,12 @@ __device__ __forceinline__ EpiOut epi_body(const tl_body& b, int64_t i, uint32_t
     EpiOut o{0.0, 0.0, LLONG_MAX};
     const int64_t N = b.n_all;
     double acc[3] = {ax0, ay0, az0};
-    // a = a_int + f0 + force BCs ; 2D a_y = 0  (stepper.py:86-95)
+    // a = (a_int + a_contact) + f0 + force BCs ; 2D a_y = 0  (stepper.py:86-95)
+    if (b.ac) {
+        acc[0] = tl::add_rn(acc[0], b.ac[i]);
+        acc[1] = tl::add_rn(acc[1], b.ac[N + i]);
+        acc[2] = tl::add_rn(acc[2], b.ac[2 * N + i]);
+    }
     acc[0] = tl::add_rn(acc[0], b.f0[0]);
     acc[1] = tl::add_rn(acc[1], b.f0[1]);
     acc[2] = tl::add_rn(acc[2], b.f0[2]);

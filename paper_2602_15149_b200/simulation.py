@@ -438,15 +438,13 @@ class DeviceSimulation:
         self.contact_warnings = 0
         self._initialized = False
         self.stream = stream or torch.cuda.current_stream()
-        if len(self.bodies) > 1:
-            raise NotImplementedError(
-                "multi-body cases need the penalty contact phase, which is not on the "
-                "device yet (SURVEY.md 8(f) rank 3)")
         self.group = group
         self.world = 1
         import torch.distributed as tdist
         if tdist.is_available() and tdist.is_initialized():
             self.world = tdist.get_world_size(group)
+        if len(self.bodies) > 1 and self.world > 1:
+            raise NotImplementedError("multi-body (contact) cases run on one GPU")
         parts = [self._partition(b) if self.world > 1 else None for b in self.bodies]
         self.programs = ProgramTable()
         self.dbodies = [DeviceBody(b, config, precision, self.programs, mirrors, part)
@@ -463,6 +461,7 @@ class DeviceSimulation:
                 db.exchange = dist.HaloExchange(plan, "cuda", group=group)
         for b, db in zip(self.bodies, self.dbodies):
             b.state = DeviceState(db.host, db)
+        self._setup_contact(torch)
         prog_table = self.programs.upload()
         self.clock_dev = torch.zeros(C.sizeof(_lib.tl_clock), dtype=torch.uint8,
                                      device="cuda")
@@ -473,6 +472,66 @@ class DeviceSimulation:
         self._lib = L
         self._dt_arr = (_lib.tl_dtinfo * len(self.dbodies))(*[db.dtinfo() for db in self.dbodies])
         self.workspaces = [None for _ in self.bodies]
+
+    # -- penalty contact (dynamics.py:81-135) --------------------------------
+    CONTACT_CELLS = 1 << 20      # cell-grid capacity of one body pair
+
+    def _setup_contact(self, torch):
+        """Per body pair, the reference's contact constants (dynamics.py:
+        106-122) and a device workspace; per body, the contact-acceleration
+        planes pass B adds before f0."""
+        from .core import youngs_from_lame, damping_ratio
+        self.contact_pairs = []
+        self.contact_counters = None
+        if len(self.dbodies) < 2:
+            return
+        contcoeff = float(getattr(self.config, "contcoeff", 1.0))
+        for db in self.dbodies:
+            db.ac = torch.zeros((3, db.n_all), dtype=torch.float64, device=db.dev)
+            db.desc.ac = _lib.ptr(db.ac)
+            s = _lib.tl_contact_side()
+            s.n, s.n_all = db.n, db.n_all
+            s.precision = 4 if db.R == torch.float32 else 8
+            s.uniform, s.m0c = int(db.uniform), float(db.body.state.m0[0])
+            s.Xs, s.us, s.v, s.m0, s.perm = (_lib.ptr(db.Xs), _lib.ptr(db.us), _lib.ptr(db.v),
+                                             _lib.ptr(db.m0), _lib.ptr(db.perm_global))
+            db.contact_side = s
+        L = _lib.lib()
+        for ia in range(len(self.dbodies)):
+            for ib in range(ia + 1, len(self.dbodies)):
+                a, b = self.bodies[ia], self.bodies[ib]
+                dpc = 0.5 * (a.dp_body + b.dp_body)
+                Ea = youngs_from_lame(a.material.lam, a.material.mu)[0]
+                Eb = youngs_from_lame(b.material.lam, b.material.mu)[0]
+                k_n = contcoeff * min(Ea, Eb) * dpc
+                ma = float(np.mean(a.state.m0))
+                mb = float(np.mean(b.state.m0))
+                m_eff = ma * mb / (ma + mb)
+                zeta = damping_ratio(min(a.material.restcoef, b.material.restcoef))
+                c_n = 2.0 * zeta * math.sqrt(k_n * m_eff)
+                kfric = 0.5 * (a.material.kfric + b.material.kfric)
+                nbytes = _lib.I64(0)
+                _lib.check(L.tl_contact_workspace_bytes(self.dbodies[ia].n, self.dbodies[ib].n,
+                                                        self.CONTACT_CELLS, C.byref(nbytes)),
+                           "tl_contact_workspace_bytes")
+                work = torch.empty(int(nbytes.value), dtype=torch.uint8, device="cuda")
+                self.contact_pairs.append((ia, ib, dpc, k_n, c_n, kfric, work))
+        self.contact_counters = torch.zeros(2, dtype=torch.int64, device="cuda")
+
+    def _contact(self):
+        """Contact accelerations from x = X + u, v at the start of the force
+        evaluation (pass A leaves u and v untouched)."""
+        if not self.contact_pairs:
+            return
+        for db in self.dbodies:
+            db.ac.zero_()
+        dim = int(self.bodies[0].dim)
+        for ia, ib, dpc, k_n, c_n, kfric, work in self.contact_pairs:
+            A, B = self.dbodies[ia], self.dbodies[ib]
+            _lib.check(self._lib.tl_contact_pair(
+                self._st(), C.byref(A.contact_side), C.byref(B.contact_side), dim, dpc, k_n, c_n,
+                kfric, self.CONTACT_CELLS, _lib.ptr(work), int(work.numel()), _lib.ptr(A.ac),
+                _lib.ptr(B.ac), _lib.ptr(self.contact_counters)), "tl_contact_pair")
 
     def _partition(self, body):
         """This rank's slab of ``body`` (dist.py): equal-count slabs along the
@@ -537,6 +596,7 @@ class DeviceSimulation:
         if mode_verlet:
             for db in self.dbodies:
                 self._pass_a(db)
+            self._contact()
             for db in self.dbodies:
                 self._pass_b(db, 1)
         else:
@@ -544,12 +604,19 @@ class DeviceSimulation:
                 _lib.check(self._lib.tl_predict(self._st(), C.byref(db.desc)), "tl_predict")
             for db in self.dbodies:
                 self._pass_a(db)
+            self._contact()
             for db in self.dbodies:
                 self._pass_b(db, 2)
 
     def _check_errors(self):
         """Raise the reference's exceptions for events recorded on the device.
         Multi-GPU: every rank raises when any rank recorded an event."""
+        if self.contact_counters is not None:
+            cc = self.contact_counters.cpu().numpy()
+            self.contact_warnings = int(cc[0])
+            if cc[1]:
+                raise SimulationError(f"contact: {int(cc[1])} candidate pairs over the per-particle "
+                                      f"capacity (TL_CONTACT_CAP)")
         if self.world > 1:
             flag = _torch().zeros(1, dtype=_torch().int64, device="cuda")
             for db in self.dbodies:
@@ -627,6 +694,7 @@ class DeviceSimulation:
         self._mark("internal")
         for db in self.dbodies:
             self._pass_a(db)
+        self._contact()
         for db in self.dbodies:
             self._pass_b(db, 0)
         for db in self.dbodies:
@@ -696,6 +764,7 @@ class DeviceSimulation:
                 ev[0].record(self.stream)
                 for db in self.dbodies:
                     self._pass_a(db)
+                self._contact()
                 ev[1].record(self.stream)
                 ev[2].record(self.stream)
                 for db in self.dbodies:

@@ -303,3 +303,34 @@ def test_trace_phase_order():
     assert trace == []
     sim.step(1e-9)
     assert trace == ["contact", "internal", "bc", "update", "commit"]
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_device_contact_run_matches_reference(precision):
+    """Two J2 bodies in penalty contact from step 1 (flyer2d, csrc/contact.cu):
+    every body's fields against the reference run (numpy backend, which
+    accumulates each particle's contact pairs in the same order)."""
+    G = golden("run_flyer2d")
+    cfg, sim = _sim(G, precision)
+    assert len(cfg.bodies) == 2
+    sim.initialize()
+    checks = set(int(c) for c in G["checkpoints"])
+    dts = G["dts"]
+    for step in range(1, len(dts) + 1):
+        if precision == "fp64":
+            dt = sim.pick_dt()
+            assert abs(dt - dts[step - 1]) <= 1e-12 * dts[step - 1], (step, dt, dts[step - 1])
+        sim.step(dts[step - 1])
+        if step in checks:
+            for bi in range(2):
+                errs = _errors(cfg.bodies[bi].state, G, step, bi)
+                print(precision, step, bi, {k: f"{v:.1e}" for k, v in errs.items()})
+                for k, err in errs.items():
+                    # FP32: plastic strain and metric grow from the excess over the yield
+                    # stress, so its relative error is the stress error
+                    # divided by how far past yield the particle is
+                    tol = TOL64[k] if precision == "fp64" else (2e-3 if k in ("epbar", "Cp") else 3e-4)
+                    assert err <= tol, (precision, step, bi, k, err)
+    # contact acts: the bodies' touching layers decelerate
+    assert np.abs(G["s1.b0.a"]).max() > 1e6
+    assert sim.contact_warnings == 0
