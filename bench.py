@@ -50,15 +50,20 @@ METRIC = "particle-steps/s, 3D phase-field fracture, 1/2/4/8 B200; % of HBM roof
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 TRAFFIC = os.path.join(ROOT, "profiles", "traffic.json")
 
-# canonical algorithmic bytes per particle-step, per pass,
-# 3D fracture: pass A = X(24) + L(9w) + u(3w) + s,sdot,H(3w) -> P(9w),
-# Avis(9w), H, sddot(2w) + 8 + 4k ; pass B = X(24) + L,P,Avis(27w) + v,u(6w)
-# + s,sdot,sddot(3w) -> v,u(6w), s,sdot(2w) + 8 + 4k
-def pass_bytes(w, k, dim=3, fracture=True):
-    if dim != 3 or not fracture:
-        raise NotImplementedError("bench reports the 3D fracture workload")
-    a = 24 + 9 * w + 3 * w + 3 * w + 9 * w + 9 * w + 2 * w + 8 + 4 * k
-    b = 24 + 27 * w + 6 * w + 3 * w + 6 * w + 2 * w + 8 + 4 * k
+# canonical algorithmic bytes per particle-step, per pass
+# (w = bytes per Real).  3D: pass A reads X(24) + L(9w) + u(3w)
+# [+ s, sdot, H (3w)] [+ Cp, epbar (7w)] and writes P(9w) + Avis(9w)
+# [+ H, sddot (2w)] [+ Cp, epbar (7w)]; pass B reads X(24) + L, P, Avis (27w)
+# + v, u (6w) [+ s, sdot, sddot (3w)] and writes v, u (6w) [+ s, sdot (2w)];
+# each + 8 + 4k (indptr, int32 neighbour indices).  2D: X 16 B, tensors 4w,
+# vectors 2w.  3D fracture FP32: 172 + 4k and 208 + 4k (C4: 585 B per step).
+def pass_bytes(w, k, dim=3, fracture=True, j2=False):
+    t, v, x = (9, 3, 24) if dim == 3 else (4, 2, 16)
+    fa = 3 * w if fracture else 0
+    fw = 2 * w if fracture else 0
+    jr = (t - 3 + 1) * w if j2 else 0          # Cp (symmetric) + epbar
+    a = x + t * w + v * w + fa + jr + t * w + t * w + fw + jr + 8 + 4 * k
+    b = x + 3 * t * w + 2 * v * w + fa + 2 * v * w + fw + 8 + 4 * k
     return a, b
 
 
@@ -147,6 +152,13 @@ def perturb(cfg, seed=0):
 # ---------------------------------------------------------------------------
 
 CPU_SAMPLE = {"C4": dict(spec="kalthoff3d", dp_scale=0.918 * 4, mapfac=5)}
+WORKLOAD_NAMES = {
+    "C1": "C1: 2D elastic cantilever plate (beam2d), SVK, radial, Verlet, adaptive dt",
+    "C2": "C2: 3D elastic column (column3d), Neo-Hookean, radial (k~160), adaptive dt",
+    "C3": "C3: 3D Taylor bar impact (taylor3d), J2 finite-strain plasticity, radial, adaptive dt",
+    "C4": "C4: 3D Kalthoff-Winkler phase-field fracture, SVK+spectral split, nbsrange=1, "
+          "Verlet, adaptive dt",
+    "C5": "C5: 2D crack-branching plate (branch2d), SVK+PF AT2, nbsrange=1, adaptive dt"}
 
 
 def cpu_reference(config, steps, warmup, budget_s=25.0):
@@ -198,7 +210,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
-    ap.add_argument("--config", default="C4", choices=["C4"])
+    ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4", "C5"],
+                    help="BASELINE.json configs: C4 is the headline; the others are extra "
+                         "measurements (no CPU baseline sample)")
     ap.add_argument("--e2e-steps", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
@@ -242,7 +256,8 @@ def main():
             dist.init_process_group("gloo", init_method="env://")
 
     t0 = time.perf_counter()
-    cfg = cases.make_case(args.config, lean=True, build_adjacency=False)
+    cfg = cases.make_case(args.config, lean=True, build_adjacency=False,
+                          lenient_targets=args.config == "C5")
     perturb(cfg, seed=0)      # one global state; ranks own slabs of it
     t_case = time.perf_counter() - t0
     t0 = time.perf_counter()
@@ -291,7 +306,9 @@ def main():
 
     # roofline of the dominant kernel (per-launch algorithmic bytes / event time)
     w = 4 if args.precision == "fp32" else 8
-    ba, bb = pass_bytes(w, k_mean)
+    b0 = cfg.bodies[0]
+    ba, bb = pass_bytes(w, k_mean, dim=int(b0.dim), fracture=bool(b0.fracture),
+                        j2=int(b0.material.model) == 3)
     ma, mb = float(np.mean(ta)), float(np.mean(tb))
     peak, peak_kind = peak_hbm()
     dom = ("pass_b_force", bb, mb) if mb >= ma else ("pass_a_phase_field", ba, ma)
@@ -345,7 +362,7 @@ def main():
                                "d2h_bytes_per_step": 16 * nb + 64 * nb + 8 * nb}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config in CPU_SAMPLE:
         try:
             ref = cpu_reference(args.config, 10, 1)
             cpu = {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")}
@@ -359,9 +376,7 @@ def main():
                 "scaling": "strong", "vs_baseline": None,
                 "dtype": "f32" if args.precision == "fp32" else "f64",
                 "data": "synthetic (seeded perturbed lattice state, SURVEY.md 8(d))",
-                "config": {"workload": f"{args.config}: 3D Kalthoff-Winkler phase-field "
-                                       "fracture, SVK+spectral split, nbsrange=1, Verlet, "
-                                       "adaptive dt",
+                "config": {"workload": WORKLOAD_NAMES[args.config],
                            "particles_per_gpu": n, "particles": int(n_total),
                            "pairs_per_particle": k_mean,
                            "parallelism": (f"slab{world} (halo exchange over "

@@ -361,7 +361,8 @@ int tl_reset_red(tl_stream_t st, unsigned long long* red);
 /* deterministic sum of nparts partials into *acc (plastic work) */
 int tl_reduce_partials(tl_stream_t st, const double* partials, int64_t nparts, double* acc);
 
-/* blocks used by tl_pass_a (size of pw_partial) */
+/* CTAs of an untiled tl_pass_a (256 particles each); a tiled launch has
+ * ceil(n / tile).  pw_partial needs one double per CTA. */
 int64_t tl_pass_blocks(int64_t n);
 
 /* ---------------------------------------------------------------------------

@@ -221,6 +221,8 @@ WORKLOADS = {
     "C2": ("column3d", dict(mapfac=5)),                              # N = 1,022,625
     "C3": ("taylor3d", dict(dp_scale=0.32)),                          # N = 3,977,160
     "C4": ("kalthoff3d", dict(dp_scale=0.918, mapfac=5)),            # N = 15,863,256
+    # C5: the shipped branch2d force-BC boxes are thinner than dp at this scale
+    # (the reference's loader rejects it); built with lenient_targets=True
     "C5": ("branch2d", dict(dp_scale=0.0893, mapfac=2)),             # N = 128,135,336
 }
 
@@ -237,9 +239,20 @@ def _material(cards, mk):
         H_hard=cards.get("hardening", 0.0))
 
 
+def _near_boxes(X, boxes, dp):
+    """Particles closer than dp to any of the axis-aligned boxes."""
+    hit = np.zeros(X.shape[0], dtype=bool)
+    for sh in boxes:
+        lo = np.asarray(sh["point"], dtype=np.float64)
+        hi = lo + np.asarray(sh["size"], dtype=np.float64)
+        d = np.maximum(np.maximum(lo - X, X - hi), 0.0)
+        hit |= np.sqrt((d * d).sum(axis=1)) < dp
+    return np.flatnonzero(hit).astype(np.int64)
+
+
 def make_case(name, dp_scale=1.0, mapfac=None, eps0=None, cfl=None, dt_override=None,
               time_max=None, time_out=None, build_adjacency=True, precision="fp64",
-              lean=False):
+              lean=False, lenient_targets=False):
     """Assemble a CaseConfig the way caseio.build_case does (caseio.py:481-598)
     for one of ``SPECS`` or a ``WORKLOADS`` key ("C1".."C5")."""
     if name in WORKLOADS:
@@ -251,7 +264,8 @@ def make_case(name, dp_scale=1.0, mapfac=None, eps0=None, cfl=None, dt_override=
             kw["mapfac"] = mapfac
         return make_case(spec_name, eps0=eps0, cfl=cfl, dt_override=dt_override,
                          time_max=time_max, time_out=time_out,
-                         build_adjacency=build_adjacency, precision=precision, lean=lean, **kw)
+                         build_adjacency=build_adjacency, precision=precision, lean=lean,
+                         lenient_targets=lenient_targets, **kw)
     spec = SPECS[name]()
     dp = spec["dp"] * dp_scale
     dim = spec["dim"]
@@ -299,6 +313,12 @@ def make_case(name, dp_scale=1.0, mapfac=None, eps0=None, cfl=None, dt_override=
                                    expr=tuple(b.get("expr", (None, None, None))))
             if bc.mkid is not None:
                 bc.target = bc_targets(X, cfg.aux_geometries[bc.mkid], dp)
+                if bc.target.size == 0 and lenient_targets:
+                    # the aux box is thinner than dp, so its lattice is empty
+                    # (the reference's loader rejects such scales): target the
+                    # particles within dp of the box itself
+                    boxes = [sh for sh in spec["shapes"] if sh["mk"] == bc.mkid]
+                    bc.target = _near_boxes(X, boxes, dp)
                 if bc.target.size == 0:
                     raise CaseError(f"empty target set for mkid {bc.mkid}")
             body.bcs.append(bc)

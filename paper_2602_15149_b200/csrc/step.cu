@@ -1369,11 +1369,12 @@ __global__ void k_clock_begin(tl_clock* c, DtInfos info) {
             const double amax = sqrt(__longlong_as_double((long long)info.d[k].red[1]));
             const double dtv = info.d[k].h / (info.d[k].c0 + vmax);
             double cand = amax > 0.0 ? c->cfl * fmin(dtv, sqrt(info.d[k].h / amax)) : c->cfl * dtv;
-            dt = fmin(dt, cand);
+            // a NaN maximum (non-finite state) must stop the clock, not vanish in fmin
+            dt = (isnan(cand) || cand < dt) ? cand : dt;
         }
     }
     dt = fmin(fmin(dt, c->next_out - c->t), c->t_max - c->t);
-    if (!(dt > 0.0)) {
+    if (!(dt > 0.0) || isinf(dt)) {
         c->halted = 4;
         c->dt = dt;
         return;

@@ -147,7 +147,11 @@ class DeviceBody:
             self.tpos_a = self.tpos_b = None
         self.counters = torch.zeros(N_COUNTERS, dtype=torch.int64, device=dev)
         self.red = torch.zeros(2, dtype=torch.int64, device=dev)
+        # one plastic-work partial per pass-A CTA: tiled launches use CTAs of
+        # `tile` particles, untiled ones of 256 (tl_pass_blocks)
         self.nblocks = int(_lib.lib().tl_pass_blocks(n))
+        if lay.tile:
+            self.nblocks = max(self.nblocks, (n + lay.tile - 1) // lay.tile)
         self.pw_partial = torch.zeros(max(self.nblocks, 1), dtype=torch.float64, device=dev)
         self.pw_acc = torch.zeros(1, dtype=torch.float64, device=dev)
         self.pw_base = float(getattr(body, "plastic_work", 0.0))
