@@ -240,14 +240,16 @@ def _material(cards, mk):
 
 
 def _near_boxes(X, boxes, dp):
-    """Particles closer than dp to any of the axis-aligned boxes."""
-    hit = np.zeros(X.shape[0], dtype=bool)
+    """The particle layer nearest to the axis-aligned boxes: particles within
+    dp of the closest particle-to-box distance (scale-free stand-in for the
+    loader's 'within dp of the auxiliary lattice' rule)."""
+    dist = np.full(X.shape[0], np.inf)
     for sh in boxes:
         lo = np.asarray(sh["point"], dtype=np.float64)
         hi = lo + np.asarray(sh["size"], dtype=np.float64)
         d = np.maximum(np.maximum(lo - X, X - hi), 0.0)
-        hit |= np.sqrt((d * d).sum(axis=1)) < dp
-    return np.flatnonzero(hit).astype(np.int64)
+        dist = np.minimum(dist, np.sqrt((d * d).sum(axis=1)))
+    return np.flatnonzero(dist < dist.min() + dp).astype(np.int64)
 
 
 def make_case(name, dp_scale=1.0, mapfac=None, eps0=None, cfl=None, dt_override=None,
@@ -314,11 +316,12 @@ def make_case(name, dp_scale=1.0, mapfac=None, eps0=None, cfl=None, dt_override=
             if bc.mkid is not None:
                 bc.target = bc_targets(X, cfg.aux_geometries[bc.mkid], dp)
                 if bc.target.size == 0 and lenient_targets:
-                    # the aux box is thinner than dp, so its lattice is empty
-                    # (the reference's loader rejects such scales): target the
-                    # particles within dp of the box itself
+                    # the aux box is thinner than dp (or off the body by more
+                    # than dp), so its lattice finds nothing -- the
+                    # reference's loader rejects such scales: target the
+                    # particle layer nearest to the box itself
                     boxes = [sh for sh in spec["shapes"] if sh["mk"] == bc.mkid]
-                    bc.target = _near_boxes(X, boxes, dp)
+                    bc.target = _near_boxes(X, boxes, 0.5 * dp_body)
                 if bc.target.size == 0:
                     raise CaseError(f"empty target set for mkid {bc.mkid}")
             body.bcs.append(bc)
