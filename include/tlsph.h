@@ -31,7 +31,7 @@ enum {
     TL_ERR_CASE = -4
 };
 
-#define TL_ABI_VERSION 6
+#define TL_ABI_VERSION 7
 
 int tl_abi_version(void);
 /* sizeof of the ABI structs, for binding checks: 0 tl_body, 1 tl_clock,
@@ -286,6 +286,10 @@ typedef struct {
     const int32_t* halo;
     const uint16_t* slots;
     const uint16_t* hslot;
+    /* tile list (multi-GPU split launches): when non-NULL, a tiled pass runs
+     * tiles tlist[tbase .. tbase + tcount) instead of all tiles */
+    const int32_t* tlist;
+    int64_t tbase, tcount;
     /* staged position records (tl_tile_pos) with V0 (pass A) and m0 (pass B)
      * weights -- the same array when uniform; toff[t] = first record of tile t */
     const int64_t* toff;

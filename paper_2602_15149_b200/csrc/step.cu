@@ -674,6 +674,13 @@ __device__ __forceinline__ void stage_tile(const tl_body& b, const Tile<R, NREC>
     tl::mbar_wait(bar, 0);
 }
 
+// Tile of this CTA.  Multi-GPU slabs launch a tiled pass in two parts -- the
+// tiles that read no halo rows while the halo exchange is in flight, then
+// the rest -- through the tile list tlist[tbase + blockIdx.x].
+__device__ __forceinline__ int64_t tile_of(const tl_body& b, bool tiled) {
+    return (tiled && b.tlist) ? (int64_t)b.tlist[b.tbase + blockIdx.x] : (int64_t)blockIdx.x;
+}
+
 // L2 prefetch of the tile's own-particle planes the epilogue reads after the
 // neighbour loop, issued by one thread while the tile is being staged
 template <typename T>
@@ -721,7 +728,8 @@ __global__ void __launch_bounds__(kThreads, TL_MINB_A(R)) k_pass_a(const tl_body
     // one shared tile of b.tile == blockDim.x particles); one particle per
     // thread -- larger tiles looped over by 256 threads measured slower
     // (shared memory per CTA cuts residency)
-    const int64_t p0 = blockIdx.x * (int64_t)blockDim.x;
+    const int64_t tb = tile_of(b, TILED);
+    const int64_t p0 = tb * (int64_t)blockDim.x;
     constexpr int P = 1;
     __shared__ double s_pw[kThreads / 32];
     double pw = 0.0;
@@ -734,7 +742,7 @@ __global__ void __launch_bounds__(kThreads, TL_MINB_A(R)) k_pass_a(const tl_body
     if (TILED) {
         if (threadIdx.x == 32) prefetch_own_a<R, MODEL, FRAC>(b, p0);
         tl_ = tile_layout<R, 1>(smem, b.tile + b.hmax);
-        stage_tile<R, 1>(b, tl_, blockIdx.x, b.tpos_a, us, &bar);
+        stage_tile<R, 1>(b, tl_, tb, b.tpos_a, us, &bar);
     }
     for (int sub = 0; sub < P; ++sub) {
         const int ms = sub * (int)blockDim.x + (int)threadIdx.x;   // member slot
@@ -926,7 +934,7 @@ __global__ void __launch_bounds__(kThreads, TL_MINB_A(R)) k_pass_a(const tl_body
         if (threadIdx.x == 0) {
             double t = 0.0;
             for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += s_pw[k];
-            b.pw_partial[blockIdx.x] = t;
+            b.pw_partial[tb] = t;
         }
     }
 }
@@ -1178,7 +1186,8 @@ __global__ void __launch_bounds__(kThreads, TL_MINB_B(R)) k_pass_b(const __grid_
     // one shared tile of b.tile == blockDim.x particles); one particle per
     // thread -- larger tiles looped over by 256 threads measured slower
     // (shared memory per CTA cuts residency)
-    const int64_t p0 = blockIdx.x * (int64_t)blockDim.x;
+    const int64_t tb = tile_of(b, TILED);
+    const int64_t p0 = tb * (int64_t)blockDim.x;
     constexpr int P = 1;
     if (halted(b)) return;
     double v2 = 0.0, a2 = 0.0;
@@ -1190,7 +1199,7 @@ __global__ void __launch_bounds__(kThreads, TL_MINB_B(R)) k_pass_b(const __grid_
     if (TILED) {
         if (threadIdx.x == 32) prefetch_own_b<R, FRAC>(b, p0);
         tl_ = tile_layout<R, 3>(smem, b.tile + b.hmax);
-        stage_tile<R, 3>(b, tl_, blockIdx.x, b.tpos_b, rbp, &bar);
+        stage_tile<R, 3>(b, tl_, tb, b.tpos_b, rbp, &bar);
     }
     for (int sub = 0; sub < P; ++sub) {
         const int ms = sub * (int)blockDim.x + (int)threadIdx.x;   // member slot
@@ -1429,7 +1438,7 @@ int launch_a_one(cudaStream_t st, const tl_body& b) {
         const size_t bytes = tile_bytes<R, 1>(b.tile + b.hmax, b.slmax);
         int rc = smem_opt_in(kern, bytes);
         if (rc) return rc;
-        kern<<<tl_blocks(b.n, b.tile), b.tile, bytes, st>>>(b);
+        kern<<<b.tlist ? (unsigned)b.tcount : tl_blocks(b.n, b.tile), b.tile, bytes, st>>>(b);
     } else {
         k_pass_a<R, DIM, MODEL, FRAC, KIND, G, false><<<tl_blocks(b.n, kThreads), kThreads, 0, st>>>(b);
     }
@@ -1458,7 +1467,7 @@ int launch_b_one(cudaStream_t st, const tl_body& b) {
         const size_t bytes = tile_bytes<R, 3>(b.tile + b.hmax, b.slmax);
         int rc = smem_opt_in(kern, bytes);
         if (rc) return rc;
-        kern<<<tl_blocks(b.n, b.tile), b.tile, bytes, st>>>(b);
+        kern<<<b.tlist ? (unsigned)b.tcount : tl_blocks(b.n, b.tile), b.tile, bytes, st>>>(b);
     } else {
         k_pass_b<R, DIM, MODE, FRAC, KIND, G, false><<<tl_blocks(b.n, kThreads), kThreads, 0, st>>>(b);
     }

@@ -313,6 +313,24 @@ class StepLayout:
         self.tile = T
 
 
+    def split_tiles(self):
+        """Multi-GPU launch order: (tile list, number of interior tiles).
+        Interior tiles read no halo row (device position >= n) and can run
+        while the halo exchange is in flight; the rest follow it."""
+        import torch
+        if not self.tile or self.n_all == self.n:
+            return None, 0
+        ntile = int(self.hoff.shape[0]) - 1
+        counts = self.hoff[1:] - self.hoff[:-1]
+        owner = torch.repeat_interleave(torch.arange(ntile, device=counts.device), counts)
+        hal = self.halo[: owner.shape[0]].long()
+        boundary = torch.zeros(ntile, dtype=torch.bool, device=counts.device)
+        boundary[owner[hal >= self.n]] = True
+        interior = torch.nonzero(~boundary).flatten()
+        border = torch.nonzero(boundary).flatten()
+        tlist = torch.cat([interior, border]).to(torch.int32).contiguous()
+        return tlist, int(interior.shape[0])
+
     def positions(self, Xs, weight=None, precision="fp32"):
         """Staged position records (x, y, z, w) of every tile slot
         (tl_tile_pos): Xs = 3 device FP64 planes of stride n_all in device

@@ -145,6 +145,8 @@ class DeviceBody:
                            else lay.positions(self.Xs, self.m0, precision))
         else:
             self.tpos_a = self.tpos_b = None
+        # multi-GPU: interior tiles first (they overlap the halo exchange)
+        self.tlist, self.n_interior = lay.split_tiles() if part is not None else (None, 0)
         self.counters = torch.zeros(N_COUNTERS, dtype=torch.int64, device=dev)
         self.red = torch.zeros(2, dtype=torch.int64, device=dev)
         # one plastic-work partial per pass-A CTA: tiled launches use CTAs of
@@ -463,6 +465,7 @@ class DeviceSimulation:
                                             db.part.owner, group=group)
                 assert plan.n_halo == db.n_all - db.n
                 db.exchange = dist.HaloExchange(plan, "cuda", group=group)
+                db.comm_stream = torch.cuda.Stream()
         for b, db in zip(self.bodies, self.dbodies):
             b.state = DeviceState(db.host, db)
         self._setup_contact(torch)
@@ -579,16 +582,52 @@ class DeviceSimulation:
         c = _lib.tl_clock.from_buffer_copy(raw)
         return c
 
+    def _exchange_and_launch(self, db, buf, launch):
+        """Fill the halo rows of ``buf`` from their owners and run a pass.
+        Tiled slabs overlap the two: the exchange runs on a side stream while
+        the interior tiles (no halo reads) compute, then the boundary tiles
+        run once the halo has landed."""
+        if db.exchange is None:
+            launch()
+            return
+        if db.tlist is None:
+            db.exchange.exchange(buf)
+            launch()
+            return
+        torch = _torch()
+        ready = torch.cuda.Event()
+        ready.record(self.stream)              # buf's owned rows are final
+        side = db.comm_stream
+        with torch.cuda.stream(side):
+            side.wait_event(ready)
+            db.exchange.exchange(buf)
+            done = torch.cuda.Event()
+            done.record(side)
+        d = db.desc
+        d.tlist = _lib.ptr(db.tlist)
+        nt = int(db.tlist.shape[0])
+        try:
+            if db.n_interior:
+                d.tbase, d.tcount = 0, db.n_interior
+                launch()
+            self.stream.wait_event(done)
+            if nt > db.n_interior:
+                d.tbase, d.tcount = db.n_interior, nt - db.n_interior
+                launch()
+        finally:
+            d.tlist, d.tbase, d.tcount = None, 0, 0
+
     def _pass_a(self, db):
-        if db.exchange is not None:
-            db.exchange.exchange(db.us)         # halo (u, s) from the owners
-        _lib.check(self._lib.tl_pass_a(self._st(), C.byref(db.desc)), "tl_pass_a")
+        self._exchange_and_launch(          # halo (u, s) from the owners
+            db, db.us,
+            lambda: _lib.check(self._lib.tl_pass_a(self._st(), C.byref(db.desc)), "tl_pass_a"))
 
     def _pass_b(self, db, mode):
-        if db.exchange is not None:
-            db.exchange.exchange(db.rb)         # halo (P L, v) from the owners
         _lib.check(self._lib.tl_reset_red(self._st(), _lib.ptr(db.red)), "tl_reset_red")
-        _lib.check(self._lib.tl_pass_b(self._st(), C.byref(db.desc), mode), "tl_pass_b")
+        self._exchange_and_launch(          # halo (P L, v) from the owners
+            db, db.rb,
+            lambda: _lib.check(self._lib.tl_pass_b(self._st(), C.byref(db.desc), mode),
+                               "tl_pass_b"))
         if db.exchange is not None:
             dist.allreduce(db.red, "max", self.group)   # global dt maxima, exact
         if int(db.body.material.model) == int(Model.J2):
