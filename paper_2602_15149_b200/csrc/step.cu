@@ -653,15 +653,7 @@ __device__ __forceinline__ void stage_tile(const tl_body& b, const Tile<R, NREC>
         if (sl_bytes) tl::bulk_g2s(t.slots, b.slots + b.soff[w0], sl_bytes, bar);
     }
     constexpr int CH = (int)(sizeof(V4<R>) / 16);   // 16-byte chunks per record
-#ifdef TL_EXP_NO_HALO
-    for (int s = threadIdx.x; s < H; s += blockDim.x) {   // timing experiment: no gathers
-        const int d = b.hslot[hb + s];
-        for (int r = 0; r < NREC; ++r) t.rec[(int64_t)d * NREC + r] = V4<R>{};
-    }
-    for (int s = threadIdx.x; s < 0; s += blockDim.x) {
-#else
     for (int s = threadIdx.x; s < H; s += blockDim.x) {
-#endif
         const int64_t q = b.halo[hb + s];
         const int d = b.hslot[hb + s];
         const char* g = reinterpret_cast<const char*>(src + q * 4 * NREC);
@@ -730,7 +722,6 @@ __global__ void __launch_bounds__(kThreads, TL_MINB_A(R)) k_pass_a(const tl_body
     // (shared memory per CTA cuts residency)
     const int64_t tb = tile_of(b, TILED);
     const int64_t p0 = tb * (int64_t)blockDim.x;
-    constexpr int P = 1;
     __shared__ double s_pw[kThreads / 32];
     double pw = 0.0;
     if (halted(b)) return;
@@ -744,185 +735,183 @@ __global__ void __launch_bounds__(kThreads, TL_MINB_A(R)) k_pass_a(const tl_body
         tl_ = tile_layout<R, 1>(smem, b.tile + b.hmax);
         stage_tile<R, 1>(b, tl_, tb, b.tpos_a, us, &bar);
     }
-    for (int sub = 0; sub < P; ++sub) {
-        const int ms = sub * (int)blockDim.x + (int)threadIdx.x;   // member slot
-        const int64_t i = p0 + ms;
-        if (i < b.n) {
-            const int64_t N = b.n_all;
-            const int lane = (int)(i & 31);
-            const int64_t w = i >> 5;
-            const int64_t base = b.soff[w];
-            const int len = (int)((b.soff[w + 1] - base) >> 5);
-            const auto ui = TILED ? tl_.rec[ms] : tl::ld4(us + 4 * i);
-            const R si = ui.w;
-            const bool gated = FRAC && si <= R(b.s_l);
-            const R inv_h = R(b.inv_h);
-            R D[9];
-    #pragma unroll
-            for (int q = 0; q < 9; ++q) D[q] = R(0);
-            R M[6] = {R(0), R(0), R(0), R(0), R(0), R(0)};   // xx yy zz xy xz yz
-            if (TILED) {
-                const V4<R> me = tl_.pos[ms];
-                const uint32_t pos_sh = tl::smem_u32(tl_.pos), rec_sh = tl::smem_u32(tl_.rec);
-                const uint32_t sl_sh = tl::smem_u32(tl_.slots + (base - b.soff[p0 >> 5]) + lane * G);
-                const uint16_t* slg = b.slots + base + lane * G;
-                const bool staged = b.slmax > 0;
-                const int lenr = b.wlen ? (int)b.wlen[w] : len;   // real longest row
+    const int ms = (int)threadIdx.x;   // member slot
+    const int64_t i = p0 + ms;
+    if (i < b.n) {
+        const int64_t N = b.n_all;
+        const int lane = (int)(i & 31);
+        const int64_t w = i >> 5;
+        const int64_t base = b.soff[w];
+        const int len = (int)((b.soff[w + 1] - base) >> 5);
+        const auto ui = TILED ? tl_.rec[ms] : tl::ld4(us + 4 * i);
+        const R si = ui.w;
+        const bool gated = FRAC && si <= R(b.s_l);
+        const R inv_h = R(b.inv_h);
+        R D[9];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) D[q] = R(0);
+        R M[6] = {R(0), R(0), R(0), R(0), R(0), R(0)};   // xx yy zz xy xz yz
+        if (TILED) {
+            const V4<R> me = tl_.pos[ms];
+            const uint32_t pos_sh = tl::smem_u32(tl_.pos), rec_sh = tl::smem_u32(tl_.rec);
+            const uint32_t sl_sh = tl::smem_u32(tl_.slots + (base - b.soff[p0 >> 5]) + lane * G);
+            const uint16_t* slg = b.slots + base + lane * G;
+            const bool staged = b.slmax > 0;
+            const int lenr = b.wlen ? (int)b.wlen[w] : len;   // real longest row
 #define TL_LOOP_A(U, ST)                                                                           \
-    loop_a<R, DIM, FRAC, KIND, U, ST>(pos_sh, rec_sh, sl_sh, slg, lenr, me, ui, inv_h, D, M)
-                if (uni) {
-                    if (staged) TL_LOOP_A(true, true); else TL_LOOP_A(true, false);
-                } else {
-                    if (staged) TL_LOOP_A(false, true); else TL_LOOP_A(false, false);
-                }
+loop_a<R, DIM, FRAC, KIND, U, ST>(pos_sh, rec_sh, sl_sh, slg, lenr, me, ui, inv_h, D, M)
+            if (uni) {
+                if (staged) TL_LOOP_A(true, true); else TL_LOOP_A(true, false);
+            } else {
+                if (staged) TL_LOOP_A(false, true); else TL_LOOP_A(false, false);
+            }
 #undef TL_LOOP_A
+        } else {
+            const double xi = b.Xs[i], yi = b.Xs[N + i], zi = b.Xs[2 * N + i];
+            const int32_t* sidx = b.sidx + base + lane;
+            const double* __restrict__ Xp = b.Xs;
+            const double* __restrict__ Yp = b.Xs + N;
+            const double* __restrict__ Zp = b.Xs + 2 * N;
+            // neighbours in groups of G: all index loads, then all gathers, then
+            // the math, so each warp keeps 2G independent loads in flight
+            for (int k = 0; k < len; k += G) {
+                int32_t jj[G];
+#pragma unroll
+                for (int q = 0; q < G; ++q) jj[q] = __ldg(sidx + 32 * (k + q));
+                double xj[G], yj[G], zj[G];
+                V4<R> uj[G];
+                R vj[G];
+#pragma unroll
+                for (int q = 0; q < G; ++q) {
+                    xj[q] = __ldg(Xp + jj[q]);
+                    yj[q] = DIM == 3 ? __ldg(Yp + jj[q]) : 0.0;
+                    zj[q] = __ldg(Zp + jj[q]);
+                    uj[q] = tl::ldg4(us + 4 * (int64_t)jj[q]);
+                    vj[q] = uni ? R(0) : R(__ldg(b.V0 + jj[q]));
+                }
+#pragma unroll
+                for (int q = 0; q < G; ++q)
+                    pair_a<R, DIM, FRAC, KIND>(R(xi - xj[q]), DIM == 3 ? R(yi - yj[q]) : R(0),
+                                               R(zi - zj[q]), uj[q], vj[q], uni, ui, inv_h,
+                                               D, M);
+            }
+        }
+        {   // kernel constant (and V0 when uniform), once per particle
+            const R ck = kshape_const<R, KIND>(b) * (uni ? R(b.V0c) : R(1));
+#pragma unroll
+            for (int q = 0; q < 9; ++q) D[q] *= ck;
+#pragma unroll
+            for (int q = 0; q < 6; ++q) M[q] *= R(2) * ck;
+        }
+        // L_i (9 planes)
+        R Li[9];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) Li[q] = planeR<R>(b.L, N, q, i);
+        // H = F - I = D L^T
+        R Hm[9];
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+                Hm[3 * r + c] = D[3 * r] * Li[3 * c] + D[3 * r + 1] * Li[3 * c + 1] + D[3 * r + 2] * Li[3 * c + 2];
+        if (gated) {
+#pragma unroll
+            for (int q = 0; q < 9; ++q) Hm[q] = R(0);
+        }
+        // constitutive update
+        R S[9], psi = R(0), psip = R(0);
+        int bad = 0, noconv = 0;
+        if (MODEL == 1) {
+            noconv = svk_update<R>(Hm, R(b.lam), R(b.mu), si, FRAC, R(b.jac_tol), S, psi, psip);
+        } else if (MODEL == 2) {
+            bad = nh_update<R>(Hm, R(b.kappa), R(b.mu), si, FRAC, S, psi, psip);
+        } else {
+            double Fd[9], Cpd[6], Sd[9], psid, dwp;
+            bool nonspd;
+#pragma unroll
+            for (int q = 0; q < 9; ++q) Fd[q] = double(Hm[q]) + ((q % 4 == 0) ? 1.0 : 0.0);
+#pragma unroll
+            for (int q = 0; q < 6; ++q) Cpd[q] = double(planeR<R>(b.Cpd, N, q, i));
+            double epb = double(static_cast<const R*>(b.epbar)[i]);
+            bad = j2_update(Fd, Cpd, epb, b.mu, b.kappa, b.sigma_y0, b.H_hard, Sd, psid, dwp, nonspd);
+            if (nonspd) atomicMin((long long*)&b.counters[2], (long long)(b.perm ? b.perm[i] : i));
+#pragma unroll
+            for (int q = 0; q < 6; ++q) static_cast<R*>(b.Cpd)[q * N + i] = R(Cpd[q]);
+            static_cast<R*>(b.epbar)[i] = R(epb);
+#pragma unroll
+            for (int q = 0; q < 9; ++q) S[q] = R(Sd[q]);
+            psi = R(psid);
+            psip = R(0);
+            pw = dwp * (b.uniform ? b.V0c : b.V0[i]);
+        }
+        // phase field: history, Laplacian, s-ddot (fracture.py:12-43)
+        if (FRAC) {
+            R* Hh = static_cast<R*>(b.Hh);
+            const R Hn = fmax(psip, Hh[i]);
+            Hh[i] = Hn;
+            const R lap = Li[0] * M[0] + Li[4] * M[1] + Li[8] * M[2] + (Li[1] + Li[3]) * M[3] +
+                          (Li[2] + Li[6]) * M[4] + (Li[5] + Li[7]) * M[5];
+            const R eps0 = R(b.eps0), Gc = R(b.Gc), c0 = R(b.c0);
+            const R ratio = Hn / Gc;
+            const R damp = R(2) * sqrt(R(4) * eps0 * ratio + R(1)) / c0;
+            const R sd = static_cast<const R*>(b.sdot)[i];
+            static_cast<R*>(b.sddot)[i] =
+                (c0 * c0 / (R(2) * eps0)) *
+                (R(2) * eps0 * lap + (R(1) - si) / (R(2) * eps0) - damp * sd - R(2) * si * ratio);
+        }
+        // P = F S = S + H S ; PL = P L_i
+        R P[9], PL[9];
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+                P[3 * r + c] = S[3 * r + c] + (Hm[3 * r] * S[c] + Hm[3 * r + 1] * S[3 + c] + Hm[3 * r + 2] * S[6 + c]);
+        mm3(P, Li, PL);
+        // viscosity tensor: det(F) F^-1 = adj(F), zero when det F <= J_MIN
+        R* al = static_cast<R*>(b.al);
+        if (b.visc) {
+            R Fm[9], A[9];
+#pragma unroll
+            for (int q = 0; q < 9; ++q) Fm[q] = Hm[q] + ((q % 4 == 0) ? R(1) : R(0));
+            const R J = R(1) + jm1_of(Hm);
+            if (J > R(TL_J_MIN)) {
+                R adj[9];
+                adj[0] = Fm[4] * Fm[8] - Fm[5] * Fm[7];
+                adj[1] = Fm[2] * Fm[7] - Fm[1] * Fm[8];
+                adj[2] = Fm[1] * Fm[5] - Fm[2] * Fm[4];
+                adj[3] = Fm[5] * Fm[6] - Fm[3] * Fm[8];
+                adj[4] = Fm[0] * Fm[8] - Fm[2] * Fm[6];
+                adj[5] = Fm[2] * Fm[3] - Fm[0] * Fm[5];
+                adj[6] = Fm[3] * Fm[7] - Fm[4] * Fm[6];
+                adj[7] = Fm[1] * Fm[6] - Fm[0] * Fm[7];
+                adj[8] = Fm[0] * Fm[4] - Fm[1] * Fm[3];
+                mm3(adj, Li, A);
             } else {
-                const double xi = b.Xs[i], yi = b.Xs[N + i], zi = b.Xs[2 * N + i];
-                const int32_t* sidx = b.sidx + base + lane;
-                const double* __restrict__ Xp = b.Xs;
-                const double* __restrict__ Yp = b.Xs + N;
-                const double* __restrict__ Zp = b.Xs + 2 * N;
-                // neighbours in groups of G: all index loads, then all gathers, then
-                // the math, so each warp keeps 2G independent loads in flight
-                for (int k = 0; k < len; k += G) {
-                    int32_t jj[G];
-    #pragma unroll
-                    for (int q = 0; q < G; ++q) jj[q] = __ldg(sidx + 32 * (k + q));
-                    double xj[G], yj[G], zj[G];
-                    V4<R> uj[G];
-                    R vj[G];
-    #pragma unroll
-                    for (int q = 0; q < G; ++q) {
-                        xj[q] = __ldg(Xp + jj[q]);
-                        yj[q] = DIM == 3 ? __ldg(Yp + jj[q]) : 0.0;
-                        zj[q] = __ldg(Zp + jj[q]);
-                        uj[q] = tl::ldg4(us + 4 * (int64_t)jj[q]);
-                        vj[q] = uni ? R(0) : R(__ldg(b.V0 + jj[q]));
-                    }
-    #pragma unroll
-                    for (int q = 0; q < G; ++q)
-                        pair_a<R, DIM, FRAC, KIND>(R(xi - xj[q]), DIM == 3 ? R(yi - yj[q]) : R(0),
-                                                   R(zi - zj[q]), uj[q], vj[q], uni, ui, inv_h,
-                                                   D, M);
-                }
+#pragma unroll
+                for (int q = 0; q < 9; ++q) A[q] = R(0);
+                bad += 1;
             }
-            {   // kernel constant (and V0 when uniform), once per particle
-                const R ck = kshape_const<R, KIND>(b) * (uni ? R(b.V0c) : R(1));
-    #pragma unroll
-                for (int q = 0; q < 9; ++q) D[q] *= ck;
-    #pragma unroll
-                for (int q = 0; q < 6; ++q) M[q] *= R(2) * ck;
+#pragma unroll
+            for (int q = 0; q < 9; ++q) al[q * N + i] = A[q];
+        }
+        // pass-B gather record: PL (9) + v (3)
+        const R* vv = static_cast<const R*>(b.v);
+        R* rb = static_cast<R*>(b.rb) + 12 * i;
+        tl::st4(rb, PL[0], PL[1], PL[2], PL[3]);
+        tl::st4(rb + 4, PL[4], PL[5], PL[6], PL[7]);
+        tl::st4(rb + 8, PL[8], vv[i], vv[N + i], vv[2 * N + i]);
+        if (mirror_out(b)) {
+#pragma unroll
+            for (int q = 0; q < 9; ++q) {
+                b.F_out[9 * i + q] = double(Hm[q]) + ((q % 4 == 0) ? 1.0 : 0.0);
+                b.S_out[9 * i + q] = double(S[q]);
             }
-            // L_i (9 planes)
-            R Li[9];
-    #pragma unroll
-            for (int q = 0; q < 9; ++q) Li[q] = planeR<R>(b.L, N, q, i);
-            // H = F - I = D L^T
-            R Hm[9];
-    #pragma unroll
-            for (int r = 0; r < 3; ++r)
-    #pragma unroll
-                for (int c = 0; c < 3; ++c)
-                    Hm[3 * r + c] = D[3 * r] * Li[3 * c] + D[3 * r + 1] * Li[3 * c + 1] + D[3 * r + 2] * Li[3 * c + 2];
-            if (gated) {
-    #pragma unroll
-                for (int q = 0; q < 9; ++q) Hm[q] = R(0);
-            }
-            // constitutive update
-            R S[9], psi = R(0), psip = R(0);
-            int bad = 0, noconv = 0;
-            if (MODEL == 1) {
-                noconv = svk_update<R>(Hm, R(b.lam), R(b.mu), si, FRAC, R(b.jac_tol), S, psi, psip);
-            } else if (MODEL == 2) {
-                bad = nh_update<R>(Hm, R(b.kappa), R(b.mu), si, FRAC, S, psi, psip);
-            } else {
-                double Fd[9], Cpd[6], Sd[9], psid, dwp;
-                bool nonspd;
-    #pragma unroll
-                for (int q = 0; q < 9; ++q) Fd[q] = double(Hm[q]) + ((q % 4 == 0) ? 1.0 : 0.0);
-    #pragma unroll
-                for (int q = 0; q < 6; ++q) Cpd[q] = double(planeR<R>(b.Cpd, N, q, i));
-                double epb = double(static_cast<const R*>(b.epbar)[i]);
-                bad = j2_update(Fd, Cpd, epb, b.mu, b.kappa, b.sigma_y0, b.H_hard, Sd, psid, dwp, nonspd);
-                if (nonspd) atomicMin((long long*)&b.counters[2], (long long)(b.perm ? b.perm[i] : i));
-    #pragma unroll
-                for (int q = 0; q < 6; ++q) static_cast<R*>(b.Cpd)[q * N + i] = R(Cpd[q]);
-                static_cast<R*>(b.epbar)[i] = R(epb);
-    #pragma unroll
-                for (int q = 0; q < 9; ++q) S[q] = R(Sd[q]);
-                psi = R(psid);
-                psip = R(0);
-                pw = dwp * (b.uniform ? b.V0c : b.V0[i]);
-            }
-            // phase field: history, Laplacian, s-ddot (fracture.py:12-43)
-            if (FRAC) {
-                R* Hh = static_cast<R*>(b.Hh);
-                const R Hn = fmax(psip, Hh[i]);
-                Hh[i] = Hn;
-                const R lap = Li[0] * M[0] + Li[4] * M[1] + Li[8] * M[2] + (Li[1] + Li[3]) * M[3] +
-                              (Li[2] + Li[6]) * M[4] + (Li[5] + Li[7]) * M[5];
-                const R eps0 = R(b.eps0), Gc = R(b.Gc), c0 = R(b.c0);
-                const R ratio = Hn / Gc;
-                const R damp = R(2) * sqrt(R(4) * eps0 * ratio + R(1)) / c0;
-                const R sd = static_cast<const R*>(b.sdot)[i];
-                static_cast<R*>(b.sddot)[i] =
-                    (c0 * c0 / (R(2) * eps0)) *
-                    (R(2) * eps0 * lap + (R(1) - si) / (R(2) * eps0) - damp * sd - R(2) * si * ratio);
-            }
-            // P = F S = S + H S ; PL = P L_i
-            R P[9], PL[9];
-    #pragma unroll
-            for (int r = 0; r < 3; ++r)
-    #pragma unroll
-                for (int c = 0; c < 3; ++c)
-                    P[3 * r + c] = S[3 * r + c] + (Hm[3 * r] * S[c] + Hm[3 * r + 1] * S[3 + c] + Hm[3 * r + 2] * S[6 + c]);
-            mm3(P, Li, PL);
-            // viscosity tensor: det(F) F^-1 = adj(F), zero when det F <= J_MIN
-            R* al = static_cast<R*>(b.al);
-            if (b.visc) {
-                R Fm[9], A[9];
-    #pragma unroll
-                for (int q = 0; q < 9; ++q) Fm[q] = Hm[q] + ((q % 4 == 0) ? R(1) : R(0));
-                const R J = R(1) + jm1_of(Hm);
-                if (J > R(TL_J_MIN)) {
-                    R adj[9];
-                    adj[0] = Fm[4] * Fm[8] - Fm[5] * Fm[7];
-                    adj[1] = Fm[2] * Fm[7] - Fm[1] * Fm[8];
-                    adj[2] = Fm[1] * Fm[5] - Fm[2] * Fm[4];
-                    adj[3] = Fm[5] * Fm[6] - Fm[3] * Fm[8];
-                    adj[4] = Fm[0] * Fm[8] - Fm[2] * Fm[6];
-                    adj[5] = Fm[2] * Fm[3] - Fm[0] * Fm[5];
-                    adj[6] = Fm[3] * Fm[7] - Fm[4] * Fm[6];
-                    adj[7] = Fm[1] * Fm[6] - Fm[0] * Fm[7];
-                    adj[8] = Fm[0] * Fm[4] - Fm[1] * Fm[3];
-                    mm3(adj, Li, A);
-                } else {
-    #pragma unroll
-                    for (int q = 0; q < 9; ++q) A[q] = R(0);
-                    bad += 1;
-                }
-    #pragma unroll
-                for (int q = 0; q < 9; ++q) al[q * N + i] = A[q];
-            }
-            // pass-B gather record: PL (9) + v (3)
-            const R* vv = static_cast<const R*>(b.v);
-            R* rb = static_cast<R*>(b.rb) + 12 * i;
-            tl::st4(rb, PL[0], PL[1], PL[2], PL[3]);
-            tl::st4(rb + 4, PL[4], PL[5], PL[6], PL[7]);
-            tl::st4(rb + 8, PL[8], vv[i], vv[N + i], vv[2 * N + i]);
-            if (mirror_out(b)) {
-    #pragma unroll
-                for (int q = 0; q < 9; ++q) {
-                    b.F_out[9 * i + q] = double(Hm[q]) + ((q % 4 == 0) ? 1.0 : 0.0);
-                    b.S_out[9 * i + q] = double(S[q]);
-                }
-                b.psi_out[i] = double(psi);
-                b.psip_out[i] = double(psip);
-            }
-            if (bad || noconv) {
-                if (bad) atomicAdd((unsigned long long*)&b.counters[0], (unsigned long long)bad);
-                if (noconv) atomicAdd((unsigned long long*)&b.counters[1], 1ull);
-            }
+            b.psi_out[i] = double(psi);
+            b.psip_out[i] = double(psip);
+        }
+        if (bad || noconv) {
+            if (bad) atomicAdd((unsigned long long*)&b.counters[0], (unsigned long long)bad);
+            if (noconv) atomicAdd((unsigned long long*)&b.counters[1], 1ull);
         }
     }
     if (MODEL == 3) {
@@ -1188,7 +1177,6 @@ __global__ void __launch_bounds__(kThreads, TL_MINB_B(R)) k_pass_b(const __grid_
     // (shared memory per CTA cuts residency)
     const int64_t tb = tile_of(b, TILED);
     const int64_t p0 = tb * (int64_t)blockDim.x;
-    constexpr int P = 1;
     if (halted(b)) return;
     double v2 = 0.0, a2 = 0.0;
     long long bad_acc = LLONG_MAX;
@@ -1201,112 +1189,110 @@ __global__ void __launch_bounds__(kThreads, TL_MINB_B(R)) k_pass_b(const __grid_
         tl_ = tile_layout<R, 3>(smem, b.tile + b.hmax);
         stage_tile<R, 3>(b, tl_, tb, b.tpos_b, rbp, &bar);
     }
-    for (int sub = 0; sub < P; ++sub) {
-        const int ms = sub * (int)blockDim.x + (int)threadIdx.x;   // member slot
-        const int64_t i = p0 + ms;
-        if (i < b.n) {
-            const int64_t N = b.n_all;
-            const int lane = (int)(i & 31);
-            const int64_t w = i >> 5;
-            const int64_t base = b.soff[w];
-            const int len = (int)((b.soff[w + 1] - base) >> 5);
-            // own record: v_i now, P L_i after the neighbour loop (fewer live registers)
-            const auto r2i = TILED ? tl_.rec[3 * ms + 2] : tl::ld4(rbp + 12 * i + 8);
-            const R vi0 = r2i.y, vi1 = r2i.z, vi2 = r2i.w;
-            const R inv_h = R(b.inv_h);
-            const bool visc = b.visc != 0;
-            const R eps_h2 = R(0.001 * b.h * b.h);
-            const R B1 = R(b.beta1 * b.c0 * b.h), B2 = R(b.beta2 * b.h * b.h);
-            const R inv_rho = R(1.0 / b.rho0);
-            R s1[3] = {R(0), R(0), R(0)}, s2[3] = {R(0), R(0), R(0)}, s3[3] = {R(0), R(0), R(0)};
-            if (TILED) {
-                const V4<R> me = tl_.pos[ms];
-                const uint32_t pos_sh = tl::smem_u32(tl_.pos), rec_sh = tl::smem_u32(tl_.rec);
-                const uint32_t sl_sh = tl::smem_u32(tl_.slots + (base - b.soff[p0 >> 5]) + lane * G);
-                const uint16_t* slg = b.slots + base + lane * G;
-                const bool staged = b.slmax > 0;
-                const int lenr = b.wlen ? (int)b.wlen[w] : len;   // real longest row
+    const int ms = (int)threadIdx.x;   // member slot
+    const int64_t i = p0 + ms;
+    if (i < b.n) {
+        const int64_t N = b.n_all;
+        const int lane = (int)(i & 31);
+        const int64_t w = i >> 5;
+        const int64_t base = b.soff[w];
+        const int len = (int)((b.soff[w + 1] - base) >> 5);
+        // own record: v_i now, P L_i after the neighbour loop (fewer live registers)
+        const auto r2i = TILED ? tl_.rec[3 * ms + 2] : tl::ld4(rbp + 12 * i + 8);
+        const R vi0 = r2i.y, vi1 = r2i.z, vi2 = r2i.w;
+        const R inv_h = R(b.inv_h);
+        const bool visc = b.visc != 0;
+        const R eps_h2 = R(0.001 * b.h * b.h);
+        const R B1 = R(b.beta1 * b.c0 * b.h), B2 = R(b.beta2 * b.h * b.h);
+        const R inv_rho = R(1.0 / b.rho0);
+        R s1[3] = {R(0), R(0), R(0)}, s2[3] = {R(0), R(0), R(0)}, s3[3] = {R(0), R(0), R(0)};
+        if (TILED) {
+            const V4<R> me = tl_.pos[ms];
+            const uint32_t pos_sh = tl::smem_u32(tl_.pos), rec_sh = tl::smem_u32(tl_.rec);
+            const uint32_t sl_sh = tl::smem_u32(tl_.slots + (base - b.soff[p0 >> 5]) + lane * G);
+            const uint16_t* slg = b.slots + base + lane * G;
+            const bool staged = b.slmax > 0;
+            const int lenr = b.wlen ? (int)b.wlen[w] : len;   // real longest row
 #define TL_LOOP_B(U, ST, V)                                                                        \
-    loop_b<R, DIM, KIND, U, ST, V>(pos_sh, rec_sh, sl_sh, slg, lenr, me, vi0, vi1, vi2, inv_h,    \
-                                   eps_h2, B2, B1, s1, s2, s3)
+loop_b<R, DIM, KIND, U, ST, V>(pos_sh, rec_sh, sl_sh, slg, lenr, me, vi0, vi1, vi2, inv_h,    \
+                               eps_h2, B2, B1, s1, s2, s3)
 #define TL_LOOP_B2(U, ST)                                                                          \
-    if (visc) TL_LOOP_B(U, ST, true); else TL_LOOP_B(U, ST, false)
-                if (uni) {
-                    if (staged) { TL_LOOP_B2(true, true); } else { TL_LOOP_B2(true, false); }
-                } else {
-                    if (staged) { TL_LOOP_B2(false, true); } else { TL_LOOP_B2(false, false); }
-                }
+if (visc) TL_LOOP_B(U, ST, true); else TL_LOOP_B(U, ST, false)
+            if (uni) {
+                if (staged) { TL_LOOP_B2(true, true); } else { TL_LOOP_B2(true, false); }
+            } else {
+                if (staged) { TL_LOOP_B2(false, true); } else { TL_LOOP_B2(false, false); }
+            }
 #undef TL_LOOP_B2
 #undef TL_LOOP_B
-            } else {
-                const double xi = b.Xs[i], yi = b.Xs[N + i], zi = b.Xs[2 * N + i];
-                const int32_t* sidx = b.sidx + base + lane;
-                const double* __restrict__ Xp = b.Xs;
-                const double* __restrict__ Yp = b.Xs + N;
-                const double* __restrict__ Zp = b.Xs + 2 * N;
-                for (int k = 0; k < len; k += G) {
-                    int32_t jj[G];
-    #pragma unroll
-                    for (int q = 0; q < G; ++q) jj[q] = __ldg(sidx + 32 * (k + q));
-                    double xj[G], yj[G], zj[G];
-                    V4<R> q0[G], q1[G], q2[G];
-                    R mj[G];
-    #pragma unroll
-                    for (int q = 0; q < G; ++q) {
-                        xj[q] = __ldg(Xp + jj[q]);
-                        yj[q] = DIM == 3 ? __ldg(Yp + jj[q]) : 0.0;
-                        zj[q] = __ldg(Zp + jj[q]);
-                        const R* rj = rbp + 12 * (int64_t)jj[q];
-                        q0[q] = tl::ldg4(rj);
-                        q1[q] = tl::ldg4(rj + 4);
-                        q2[q] = tl::ldg4(rj + 8);
-                        mj[q] = uni ? R(0) : R(__ldg(b.m0 + jj[q]));
-                    }
-    #pragma unroll
-                    for (int q = 0; q < G; ++q)
-                        pair_b<R, DIM, KIND>(R(xi - xj[q]), DIM == 3 ? R(yi - yj[q]) : R(0),
-                                             R(zi - zj[q]), q0[q], q1[q], q2[q], mj[q], uni, vi0, vi1,
-                                             vi2, visc, inv_h, eps_h2, B2, B1, s1, s2, s3);
+        } else {
+            const double xi = b.Xs[i], yi = b.Xs[N + i], zi = b.Xs[2 * N + i];
+            const int32_t* sidx = b.sidx + base + lane;
+            const double* __restrict__ Xp = b.Xs;
+            const double* __restrict__ Yp = b.Xs + N;
+            const double* __restrict__ Zp = b.Xs + 2 * N;
+            for (int k = 0; k < len; k += G) {
+                int32_t jj[G];
+#pragma unroll
+                for (int q = 0; q < G; ++q) jj[q] = __ldg(sidx + 32 * (k + q));
+                double xj[G], yj[G], zj[G];
+                V4<R> q0[G], q1[G], q2[G];
+                R mj[G];
+#pragma unroll
+                for (int q = 0; q < G; ++q) {
+                    xj[q] = __ldg(Xp + jj[q]);
+                    yj[q] = DIM == 3 ? __ldg(Yp + jj[q]) : 0.0;
+                    zj[q] = __ldg(Zp + jj[q]);
+                    const R* rj = rbp + 12 * (int64_t)jj[q];
+                    q0[q] = tl::ldg4(rj);
+                    q1[q] = tl::ldg4(rj + 4);
+                    q2[q] = tl::ldg4(rj + 8);
+                    mj[q] = uni ? R(0) : R(__ldg(b.m0 + jj[q]));
                 }
+#pragma unroll
+                for (int q = 0; q < G; ++q)
+                    pair_b<R, DIM, KIND>(R(xi - xj[q]), DIM == 3 ? R(yi - yj[q]) : R(0),
+                                         R(zi - zj[q]), q0[q], q1[q], q2[q], mj[q], uni, vi0, vi1,
+                                         vi2, visc, inv_h, eps_h2, B2, B1, s1, s2, s3);
             }
-            {   // kernel constant (and m0 when uniform), once per particle
-                const R ck = kshape_const<R, KIND>(b) * (uni ? R(b.m0c) : R(1));
-    #pragma unroll
-                for (int q = 0; q < 3; ++q) {
-                    s1[q] *= ck;
-                    s2[q] *= ck;
-                    s3[q] *= ck * inv_rho;
-                }
-            }
-            // a_int = (PL_i s1 + s2)/rho0^2 - AL_i s3
-            const auto r0i = TILED ? tl_.rec[3 * ms] : tl::ld4(rbp + 12 * i);
-            const auto r1i = TILED ? tl_.rec[3 * ms + 1] : tl::ld4(rbp + 12 * i + 4);
-            const R PLi[9] = {r0i.x, r0i.y, r0i.z, r0i.w, r1i.x, r1i.y, r1i.z, r1i.w, r2i.x};
-            const R inv_rho2 = inv_rho * inv_rho;
-            double acc[3];
-    #pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                R t = (PLi[3 * a] * s1[0] + PLi[3 * a + 1] * s1[1] + PLi[3 * a + 2] * s1[2] + s2[a]) * inv_rho2;
-                if (visc) {
-                    const R* al = static_cast<const R*>(b.al);
-                    t -= al[(3 * a) * N + i] * s3[0] + al[(3 * a + 1) * N + i] * s3[1] +
-                         al[(3 * a + 2) * N + i] * s3[2];
-                }
-                acc[a] = double(t);
-            }
-            // the rest of the particle's update: boundary conditions / restrictphi
-            // expressions only on the (rare) particles that carry them, out of
-            // line, so the common path holds no call frame
-            const uint32_t mask = b.bcmask ? b.bcmask[i] : 0u;
-            const bool slow = (b.nbc && (mask || b.bc_whole)) || (FRAC && b.restrict_prog >= 0);
-            const EpiOut o = slow ? epi_slow<R, DIM, MODE, FRAC>(&b, i, mask, acc[0], acc[1], acc[2],
-                                                                 vi0, vi1, vi2)
-                                  : epi_body<R, DIM, MODE, FRAC, false>(b, i, mask, acc[0], acc[1],
-                                                                        acc[2], vi0, vi1, vi2);
-            v2 = fmax(v2, o.v2);
-            a2 = fmax(a2, o.a2);
-            bad_acc = min(bad_acc, o.bad);
         }
+        {   // kernel constant (and m0 when uniform), once per particle
+            const R ck = kshape_const<R, KIND>(b) * (uni ? R(b.m0c) : R(1));
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                s1[q] *= ck;
+                s2[q] *= ck;
+                s3[q] *= ck * inv_rho;
+            }
+        }
+        // a_int = (PL_i s1 + s2)/rho0^2 - AL_i s3
+        const auto r0i = TILED ? tl_.rec[3 * ms] : tl::ld4(rbp + 12 * i);
+        const auto r1i = TILED ? tl_.rec[3 * ms + 1] : tl::ld4(rbp + 12 * i + 4);
+        const R PLi[9] = {r0i.x, r0i.y, r0i.z, r0i.w, r1i.x, r1i.y, r1i.z, r1i.w, r2i.x};
+        const R inv_rho2 = inv_rho * inv_rho;
+        double acc[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            R t = (PLi[3 * a] * s1[0] + PLi[3 * a + 1] * s1[1] + PLi[3 * a + 2] * s1[2] + s2[a]) * inv_rho2;
+            if (visc) {
+                const R* al = static_cast<const R*>(b.al);
+                t -= al[(3 * a) * N + i] * s3[0] + al[(3 * a + 1) * N + i] * s3[1] +
+                     al[(3 * a + 2) * N + i] * s3[2];
+            }
+            acc[a] = double(t);
+        }
+        // the rest of the particle's update: boundary conditions / restrictphi
+        // expressions only on the (rare) particles that carry them, out of
+        // line, so the common path holds no call frame
+        const uint32_t mask = b.bcmask ? b.bcmask[i] : 0u;
+        const bool slow = (b.nbc && (mask || b.bc_whole)) || (FRAC && b.restrict_prog >= 0);
+        const EpiOut o = slow ? epi_slow<R, DIM, MODE, FRAC>(&b, i, mask, acc[0], acc[1], acc[2],
+                                                             vi0, vi1, vi2)
+                              : epi_body<R, DIM, MODE, FRAC, false>(b, i, mask, acc[0], acc[1],
+                                                                    acc[2], vi0, vi1, vi2);
+        v2 = fmax(v2, o.v2);
+        a2 = fmax(a2, o.a2);
+        bad_acc = min(bad_acc, o.bad);
     }
     v2 = tl::warp_max(v2);
     a2 = tl::warp_max(a2);
