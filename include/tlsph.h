@@ -31,7 +31,7 @@ enum {
     TL_ERR_CASE = -4
 };
 
-#define TL_ABI_VERSION 7
+#define TL_ABI_VERSION 8
 
 int tl_abi_version(void);
 /* sizeof of the ABI structs, for binding checks: 0 tl_body, 1 tl_clock,
@@ -268,6 +268,7 @@ typedef struct {
     /* material / kernel constants (core.py:95-139) */
     double h, inv_h, alpha, rho0, lam, mu, kappa, c0, beta1, beta2;
     double Gc, eps0, s_l, sigma_y0, H_hard, V0c, m0c, dp_body, jac_tol;
+    double inv_Gc, inv_eps0, inv_c0;   /* reciprocals (no per-particle divisions) */
     double f0[3];
     /* neighbours: sliced ELL, 32 particles per slice, lane-interleaved;
      * wlen[w] = longest real row of slice w (slices are padded to 4) */

@@ -93,7 +93,7 @@ __device__ __forceinline__ void positive_part(const float* E, float* Ep) {
         l1 = l2 = l3 = q;
     } else {
         const float p = sqrtf(p2 * (1.f / 6.f));
-        const float ip = 1.f / p;
+        const float ip = __fdividef(1.f, p);
         const float b0 = d0 * ip, b4 = d1 * ip, b8 = d2 * ip;
         const float b1 = E[1] * ip, b2 = E[2] * ip, b5 = E[5] * ip;
         const float detB = b0 * (b4 * b8 - b5 * b5) - b1 * (b1 * b8 - b5 * b2) + b2 * (b1 * b5 - b4 * b2);
@@ -122,7 +122,7 @@ __device__ __forceinline__ void positive_part(const float* E, float* Ep) {
     // isolated eigenvalue lk with projector (E - la I)(E - lb I) / ((lk-la)(lk-lb))
     const bool top = l2 <= 0.f;          // l1 alone positive: E+ = l1 P1
     const float lk = top ? l1 : l3, la = top ? l2 : l1, lb = top ? l3 : l2;
-    const float c = lk / ((lk - la) * (lk - lb));
+    const float c = __fdividef(lk, (lk - la) * (lk - lb));
     const float sab = la + lb, pab = la * lb;
     float Pk[9];
 #pragma unroll
@@ -164,7 +164,7 @@ __device__ __forceinline__ int svk_update(const R* H, R lam, R mu, R s, bool fra
         for (int k = 0; k < 9; ++k) m = fmaxf(m, fabsf(float(E[k])));
         float Ep[9];
         if (m > 0.f) {
-            const float im = 1.f / m;
+            const float im = __fdividef(1.f, m);
             float En[9];
 #pragma unroll
             for (int k = 0; k < 9; ++k) En[k] = float(E[k]) * im;
@@ -851,13 +851,14 @@ loop_a<R, DIM, FRAC, KIND, U, ST>(pos_sh, rec_sh, sl_sh, slg, lenr, me, ui, inv_
             Hh[i] = Hn;
             const R lap = Li[0] * M[0] + Li[4] * M[1] + Li[8] * M[2] + (Li[1] + Li[3]) * M[3] +
                           (Li[2] + Li[6]) * M[4] + (Li[5] + Li[7]) * M[5];
-            const R eps0 = R(b.eps0), Gc = R(b.Gc), c0 = R(b.c0);
-            const R ratio = Hn / Gc;
-            const R damp = R(2) * sqrt(R(4) * eps0 * ratio + R(1)) / c0;
+            // fracture.py:25-32 with the divisions as host-side reciprocals
+            const R eps0 = R(b.eps0), c0 = R(b.c0), ieps = R(b.inv_eps0);
+            const R ratio = Hn * R(b.inv_Gc);
+            const R damp = R(2) * sqrt(R(4) * eps0 * ratio + R(1)) * R(b.inv_c0);
             const R sd = static_cast<const R*>(b.sdot)[i];
             static_cast<R*>(b.sddot)[i] =
-                (c0 * c0 / (R(2) * eps0)) *
-                (R(2) * eps0 * lap + (R(1) - si) / (R(2) * eps0) - damp * sd - R(2) * si * ratio);
+                (R(0.5) * c0 * c0 * ieps) *
+                (R(2) * eps0 * lap + R(0.5) * (R(1) - si) * ieps - damp * sd - R(2) * si * ratio);
         }
         // P = F S = S + H S ; PL = P L_i
         R P[9], PL[9];

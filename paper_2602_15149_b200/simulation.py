@@ -245,6 +245,9 @@ class DeviceBody:
                   "sigma_y0", "H_hard"):
             setattr(b, k, float(getattr(mat, k)))
         b.c0 = float(mat.c0)
+        b.inv_Gc = 1.0 / b.Gc if b.Gc else 0.0
+        b.inv_eps0 = 1.0 / b.eps0 if b.eps0 else 0.0
+        b.inv_c0 = 1.0 / b.c0 if b.c0 else 0.0
         b.V0c = float(self.body.state.V0[0])
         b.m0c = float(self.body.state.m0[0])
         b.dp_body = float(body.dp_body)
