@@ -83,10 +83,11 @@ __device__ __forceinline__ bool mirror_out(const tl_body& b) {
 // (l_k - l_j)).  Its denominators are bounded below by |l_k| > 0, so the
 // split is well conditioned even when the two same-sign eigenvalues are
 // (nearly) equal -- the case where individual eigenvectors are not.
-__device__ __forceinline__ void positive_part(const float* E, float* Ep) {
-    const float q = (E[0] + E[4] + E[8]) * (1.f / 3.f);
-    const float p1 = E[1] * E[1] + E[2] * E[2] + E[5] * E[5];
-    const float d0 = E[0] - q, d1 = E[4] - q, d2 = E[8] - q;
+// Symmetric storage e = (xx, yy, zz, xy, xz, yz).
+__device__ __forceinline__ void positive_part_sym(const float* e, float* ep) {
+    const float q = (e[0] + e[1] + e[2]) * (1.f / 3.f);
+    const float p1 = e[3] * e[3] + e[4] * e[4] + e[5] * e[5];
+    const float d0 = e[0] - q, d1 = e[1] - q, d2 = e[2] - q;
     const float p2 = d0 * d0 + d1 * d1 + d2 * d2 + 2.f * p1;
     float l1, l2, l3;
     if (p2 <= 0.f) {
@@ -95,12 +96,12 @@ __device__ __forceinline__ void positive_part(const float* E, float* Ep) {
         const float p = sqrtf(p2 * (1.f / 6.f));
         const float ip = __fdividef(1.f, p);
         const float b0 = d0 * ip, b4 = d1 * ip, b8 = d2 * ip;
-        const float b1 = E[1] * ip, b2 = E[2] * ip, b5 = E[5] * ip;
+        const float b1 = e[3] * ip, b2 = e[4] * ip, b5 = e[5] * ip;
         const float detB = b0 * (b4 * b8 - b5 * b5) - b1 * (b1 * b8 - b5 * b2) + b2 * (b1 * b5 - b4 * b2);
         const float r = fminf(fmaxf(0.5f * detB, -1.f), 1.f);
         const float phi = acosf(r) * (1.f / 3.f);   // in [0, pi/3]
         // cos(phi + 2pi/3) = -cos(phi)/2 - sqrt(3)/2 sin(phi); MUFU sin/cos
-        // (abs. error ~4e-7 on [0, pi/3]; E is scaled to unit max entry)
+        // (abs. error ~4e-7 on [0, pi/3]; e is scaled to unit max entry)
         float sp, cp;
         __sincosf(phi, &sp, &cp);
         l1 = q + 2.f * p * cp;
@@ -109,26 +110,89 @@ __device__ __forceinline__ void positive_part(const float* E, float* Ep) {
     }
     if (l3 >= 0.f) {
 #pragma unroll
-        for (int k = 0; k < 9; ++k) Ep[k] = E[k];
+        for (int k = 0; k < 6; ++k) ep[k] = e[k];
         return;
     }
     if (l1 <= 0.f) {
 #pragma unroll
-        for (int k = 0; k < 9; ++k) Ep[k] = 0.f;
+        for (int k = 0; k < 6; ++k) ep[k] = 0.f;
         return;
     }
-    float E2[9];
-    tl::mm3(E, E, E2);
+    const float e2[6] = {e[0] * e[0] + e[3] * e[3] + e[4] * e[4],
+                         e[3] * e[3] + e[1] * e[1] + e[5] * e[5],
+                         e[4] * e[4] + e[5] * e[5] + e[2] * e[2],
+                         e[0] * e[3] + e[3] * e[1] + e[4] * e[5],
+                         e[0] * e[4] + e[3] * e[5] + e[4] * e[2],
+                         e[3] * e[4] + e[1] * e[5] + e[5] * e[2]};
     // isolated eigenvalue lk with projector (E - la I)(E - lb I) / ((lk-la)(lk-lb))
     const bool top = l2 <= 0.f;          // l1 alone positive: E+ = l1 P1
     const float lk = top ? l1 : l3, la = top ? l2 : l1, lb = top ? l3 : l2;
     const float c = __fdividef(lk, (lk - la) * (lk - lb));
     const float sab = la + lb, pab = la * lb;
-    float Pk[9];
 #pragma unroll
-    for (int k = 0; k < 9; ++k) Pk[k] = c * (E2[k] - sab * E[k] + ((k % 4 == 0) ? pab : 0.f));
+    for (int k = 0; k < 6; ++k) {
+        const float pk = c * (e2[k] - sab * e[k] + (k < 3 ? pab : 0.f));
+        ep[k] = top ? pk : e[k] - pk;
+    }
+}
+
+// FP32 SVK + spectral split on symmetric storage (reference.py:94-116):
+// E = (H + H^T + H^T H)/2, E+ by the closed form, S = s^2 S+ + S-
+__device__ __forceinline__ void svk_split_f32(const float* H, float lam, float mu, float s, float* S,
+                                              float& psi, float& psip) {
+    // (r, c) of the symmetric components xx, yy, zz, xy, xz, yz
+    constexpr int RR[6] = {0, 1, 2, 0, 0, 1}, CC[6] = {0, 1, 2, 1, 2, 2};
+    float e[6];
 #pragma unroll
-    for (int k = 0; k < 9; ++k) Ep[k] = top ? Pk[k] : E[k] - Pk[k];
+    for (int k = 0; k < 6; ++k) {
+        const int r = RR[k], c = CC[k];
+        e[k] = 0.5f * (H[3 * r + c] + H[3 * c + r] +
+                       (H[r] * H[c] + H[3 + r] * H[3 + c] + H[6 + r] * H[6 + c]));
+    }
+    const float trE = e[0] + e[1] + e[2];
+    const float trp = trE > 0.f ? trE : 0.f, trm = trE < 0.f ? trE : 0.f;
+    // the split is positively homogeneous (E+(aE) = a E+(E)): run it on E
+    // scaled to unit max entry so tiny strains far from the load do not
+    // underflow (FTZ) into a 0/0 in the projector
+    float m = 0.f;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) m = fmaxf(m, fabsf(e[k]));
+    float ep[6];
+    if (m > 0.f) {
+        const float im = __fdividef(1.f, m);
+        float en[6];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) en[k] = e[k] * im;
+        positive_part_sym(en, ep);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) ep[k] *= m;
+    } else {
+#pragma unroll
+        for (int k = 0; k < 6; ++k) ep[k] = 0.f;
+    }
+    const float s2 = s * s;
+    float fp = 0.f, fm = 0.f, Ss[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+        const float a = ep[k], b = e[k] - ep[k];
+        const float wgt = k < 3 ? 1.f : 2.f;     // off-diagonals count twice in E:E
+        fp += wgt * a * a;
+        fm += wgt * b * b;
+        float sp = 2.f * mu * a, sm = 2.f * mu * b;
+        if (k < 3) {
+            sp += lam * trp;
+            sm += lam * trm;
+        }
+        Ss[k] = s2 * sp + sm;
+    }
+    S[0] = Ss[0]; S[4] = Ss[1]; S[8] = Ss[2];
+    S[1] = S[3] = Ss[3];
+    S[2] = S[6] = Ss[4];
+    S[5] = S[7] = Ss[5];
+    const float pp = 0.5f * lam * trp * trp + mu * fp;
+    const float pm = 0.5f * lam * trm * trm + mu * fm;
+    psi = s2 * pp + pm;
+    psip = pp;
 }
 
 // SVK with optional spectral split (reference.py:94-116, fast.py:224-284)
@@ -156,43 +220,9 @@ __device__ __forceinline__ int svk_update(const R* H, R lam, R mu, R s, bool fra
     }
     const R trp = trE > R(0) ? trE : R(0), trm = trE < R(0) ? trE : R(0);
     if (sizeof(R) == 4) {
-        // the split is positively homogeneous (E+(aE) = a E+(E)): run it on E
-        // scaled to unit max entry so tiny strains far from the load do not
-        // underflow (FTZ) into a 0/0 in the projector
-        float m = 0.f;
-#pragma unroll
-        for (int k = 0; k < 9; ++k) m = fmaxf(m, fabsf(float(E[k])));
-        float Ep[9];
-        if (m > 0.f) {
-            const float im = __fdividef(1.f, m);
-            float En[9];
-#pragma unroll
-            for (int k = 0; k < 9; ++k) En[k] = float(E[k]) * im;
-            positive_part(En, Ep);
-#pragma unroll
-            for (int k = 0; k < 9; ++k) Ep[k] *= m;
-        } else {
-#pragma unroll
-            for (int k = 0; k < 9; ++k) Ep[k] = 0.f;
-        }
-        const R s2 = s * s;
-        R fp = R(0), fm = R(0);
-#pragma unroll
-        for (int k = 0; k < 9; ++k) {
-            const R ep = R(Ep[k]), em = E[k] - R(Ep[k]);
-            fp += ep * ep;
-            fm += em * em;
-            R sp = R(2) * mu * ep, sm = R(2) * mu * em;
-            if (k % 4 == 0) {
-                sp += lam * trp;
-                sm += lam * trm;
-            }
-            S[k] = s2 * sp + sm;
-        }
-        const R pp = R(0.5) * lam * trp * trp + mu * fp;
-        const R pm = R(0.5) * lam * trm * trm + mu * fm;
-        psi = s2 * pp + pm;
-        psip = pp;
+        svk_split_f32(reinterpret_cast<const float*>(H), float(lam), float(mu), float(s),
+                      reinterpret_cast<float*>(S), reinterpret_cast<float&>(psi),
+                      reinterpret_cast<float&>(psip));
         return 0;
     }
     R w[3], Q[9];
