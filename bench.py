@@ -215,6 +215,8 @@ def main():
                          "measurements (no CPU baseline sample)")
     ap.add_argument("--e2e-steps", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dp-scale", type=float, default=1.0,
+                    help="multiply the config's particle spacing (profiling at reduced size)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: ranks may share one GPU (halo buffers staged through the host; "
                          "a plumbing check, not a throughput number)")
@@ -256,8 +258,10 @@ def main():
             dist.init_process_group("gloo", init_method="env://")
 
     t0 = time.perf_counter()
+    base_scale = cases.WORKLOADS[args.config][1].get("dp_scale", 1.0)
     cfg = cases.make_case(args.config, lean=True, build_adjacency=False,
-                          lenient_targets=args.config == "C5")
+                          lenient_targets=args.config == "C5",
+                          dp_scale=base_scale * args.dp_scale)
     perturb(cfg, seed=0)      # one global state; ranks own slabs of it
     t_case = time.perf_counter() - t0
     t0 = time.perf_counter()

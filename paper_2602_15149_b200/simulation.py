@@ -145,6 +145,13 @@ class DeviceBody:
                            else lay.positions(self.Xs, self.m0, precision))
         else:
             self.tpos_a = self.tpos_b = None
+        # pass B tiling: with few neighbours per particle (2D stencils) a tile's
+        # short compute cannot hide its staging latency, and the L2-gather
+        # pass B measured faster on B200 (C5: 1.75 vs 2.45 ms); pass A keeps
+        # its tiles either way.  TLSPH_TILE_B=0/1 overrides.
+        env_b = os.environ.get("TLSPH_TILE_B")
+        self.tile_b = bool(lay.tile) and (int(env_b) != 0 if env_b is not None
+                                          else int(body.dim) == 3)
         # multi-GPU: interior tiles first (they overlap the halo exchange)
         self.tlist, self.n_interior = lay.split_tiles() if part is not None else (None, 0)
         self.counters = torch.zeros(N_COUNTERS, dtype=torch.int64, device=dev)
@@ -620,6 +627,11 @@ class DeviceSimulation:
         finally:
             d.tlist, d.tbase, d.tcount = None, 0, 0
 
+    def _exchange_plain(self, db, buf, launch):
+        if db.exchange is not None:
+            db.exchange.exchange(buf)
+        launch()
+
     def _pass_a(self, db):
         self._exchange_and_launch(          # halo (u, s) from the owners
             db, db.us,
@@ -627,10 +639,23 @@ class DeviceSimulation:
 
     def _pass_b(self, db, mode):
         _lib.check(self._lib.tl_reset_red(self._st(), _lib.ptr(db.red)), "tl_reset_red")
-        self._exchange_and_launch(          # halo (P L, v) from the owners
-            db, db.rb,
-            lambda: _lib.check(self._lib.tl_pass_b(self._st(), C.byref(db.desc), mode),
-                               "tl_pass_b"))
+
+        def launch():
+            d = db.desc
+            if db.tile_b:
+                _lib.check(self._lib.tl_pass_b(self._st(), C.byref(d), mode), "tl_pass_b")
+                return
+            tile, tl = d.tile, d.tlist        # L2-gather pass B (see DeviceBody)
+            d.tile, d.tlist = 0, None
+            try:
+                _lib.check(self._lib.tl_pass_b(self._st(), C.byref(d), mode), "tl_pass_b")
+            finally:
+                d.tile, d.tlist = tile, tl
+
+        if db.tile_b:
+            self._exchange_and_launch(db, db.rb, launch)   # halo (P L, v) from the owners
+        else:
+            self._exchange_plain(db, db.rb, launch)        # no tile split: exchange first
         if db.exchange is not None:
             dist.allreduce(db.red, "max", self.group)   # global dt maxima, exact
         if int(db.body.material.model) == int(Model.J2):
