@@ -152,6 +152,13 @@ class DeviceBody:
         env_b = os.environ.get("TLSPH_TILE_B")
         self.tile_b = bool(lay.tile) and (int(env_b) != 0 if env_b is not None
                                           else int(body.dim) == 3)
+        # pass A tiling: radial 3D stencils (k ~ 165) stage ~13 halo records
+        # per member and fit one CTA per SM; their pass A gathers faster from
+        # L2 (C2: 0.60 vs 0.68 ms, C3: 3.0 vs 3.55 ms).  TLSPH_TILE_A overrides.
+        env_a = os.environ.get("TLSPH_TILE_A")
+        k_mean = float(lay.indptr[-1].item()) / max(n, 1)
+        self.tile_a = bool(lay.tile) and (int(env_a) != 0 if env_a is not None
+                                          else k_mean <= 64.0)
         # multi-GPU: interior tiles first (they overlap the halo exchange)
         self.tlist, self.n_interior = lay.split_tiles() if part is not None else (None, 0)
         self.counters = torch.zeros(N_COUNTERS, dtype=torch.int64, device=dev)
@@ -633,9 +640,22 @@ class DeviceSimulation:
         launch()
 
     def _pass_a(self, db):
-        self._exchange_and_launch(          # halo (u, s) from the owners
-            db, db.us,
-            lambda: _lib.check(self._lib.tl_pass_a(self._st(), C.byref(db.desc)), "tl_pass_a"))
+        def launch():
+            d = db.desc
+            if db.tile_a:
+                _lib.check(self._lib.tl_pass_a(self._st(), C.byref(d)), "tl_pass_a")
+                return
+            tile, tl = d.tile, d.tlist        # L2-gather pass A (see DeviceBody)
+            d.tile, d.tlist = 0, None
+            try:
+                _lib.check(self._lib.tl_pass_a(self._st(), C.byref(d)), "tl_pass_a")
+            finally:
+                d.tile, d.tlist = tile, tl
+
+        if db.tile_a:
+            self._exchange_and_launch(db, db.us, launch)   # halo (u, s) from the owners
+        else:
+            self._exchange_plain(db, db.us, launch)
 
     def _pass_b(self, db, mode):
         _lib.check(self._lib.tl_reset_red(self._st(), _lib.ptr(db.red)), "tl_reset_red")

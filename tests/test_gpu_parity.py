@@ -191,9 +191,12 @@ def test_layout_variants_agree(tag, tile, monkeypatch):
     """Shared-memory tiles (various sizes) and the L2-gather path give the
     same FP64 state: sums run in the same order either way."""
     monkeypatch.setenv("TLSPH_TILE", tile)
+    monkeypatch.setenv("TLSPH_TILE_A", "1")    # both passes tiled whatever the stencil
+    monkeypatch.setenv("TLSPH_TILE_B", "1")
     G = golden(f"run_{tag}")
     cfg, sim = _sim(G, "fp64")
     assert sim.dbodies[0].layout.tile == int(tile)
+    assert sim.dbodies[0].tile_a == (int(tile) > 0) and sim.dbodies[0].tile_b == (int(tile) > 0)
     sim.initialize()
     for step in (1, 2):
         sim.step(G["dts"][step - 1])
