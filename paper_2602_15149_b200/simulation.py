@@ -38,7 +38,7 @@ INT64_MAX = np.iinfo(np.int64).max
 N_COUNTERS = 8
 # particles per CTA / shared-memory tile, one per thread (TLSPH_TILE overrides;
 # a multiple of 32, at most 256)
-DEFAULT_TILE = {"fp32": 160, "fp64": 256}   # measured on B200 (C4): 160 best in FP32
+DEFAULT_TILE = {"fp32": 160, "fp64": 160}   # measured on B200 (C4): 160 best in both modes
 TILE_SMEM_LIMIT = 200 * 1024  # bytes of shared memory a pass-B tile may take
 
 
