@@ -49,9 +49,10 @@ using tl::mm3;
 #ifndef TL_GATHER_B
 #define TL_GATHER_B 4
 #endif
-// minimum resident CTAs per SM requested from ptxas (register budget); tuned
-// on B200 for the C4 workload: FP32 pass A 4 (64 regs), pass B 3 (80 regs);
-// FP64 pass A needs its registers (J2/eigen) and keeps 1
+// minimum resident CTAs per SM requested from ptxas (register budget, for
+// 256-thread launch bounds); tuned on B200 for the C4 workload: FP32 pass A
+// and pass B 4 (64 registers; 48 spills and measured slower); FP64 pass A
+// needs its registers (J2/eigen) and keeps 1
 #ifndef TL_MINB_A
 #define TL_MINB_A(R) (sizeof(R) == 4 ? 4 : 1)
 #endif
@@ -511,20 +512,6 @@ __device__ __forceinline__ void pair_b(R dx, R dy, R dz, const V4<R>& q0, const 
         const R pw = (B2 * g - B1) * g;
         s3[0] += pw * wx; s3[2] += pw * wz;
         if (DIM == 3) s3[1] += pw * wy;
-    }
-}
-
-// G neighbour slots of this lane in the group-interleaved tiled layout
-template <int G>
-__device__ __forceinline__ void load_slots(const uint16_t* p, int* out) {
-    if (G == 4) {
-        const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
-        out[0] = v.x & 0xffff; out[1] = v.x >> 16; out[2] = v.y & 0xffff; out[3] = v.y >> 16;
-    } else if (G == 2) {
-        const uint32_t v = __ldg(reinterpret_cast<const uint32_t*>(p));
-        out[0] = v & 0xffff; out[1] = v >> 16;
-    } else {
-        out[0] = __ldg(p);
     }
 }
 
