@@ -84,7 +84,10 @@ class DeviceBody:
                         dp_body=body.dp_body, notches=body.notches, correction=corr)
         self.adj = dadj
         # device particle order + neighbour tiles (kernel_geom.StepLayout)
-        tile = int(os.environ.get("TLSPH_TILE", str(DEFAULT_TILE[precision])))
+        tile = DEFAULT_TILE[precision]
+        if int(body.dim) == 2:
+            tile = 128    # 2D stencils: thin 1-deep halos, measured best for pass A (C5)
+        tile = int(os.environ.get("TLSPH_TILE", str(tile)))
         if part is not None:
             part.complete(dadj)          # halo ids in exchange order (collective-free)
             lay = kernel_geom.StepLayout(dadj, tile=tile, rows=part.owned_rows,
