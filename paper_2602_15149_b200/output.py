@@ -57,6 +57,10 @@ def compute_energies(body, be=None, grad_buf=None):
     if db.psi_out is None:
         raise ValueError("energies need the stress mirrors: construct the simulation "
                          "with mirrors=True")
+    if db.body.fracture and getattr(db, "exchange", None) is not None:
+        # the fracture energy's grad s reads halo s, last exchanged before pass A:
+        # refresh the halo rows from their owners (collective)
+        db.exchange.exchange(db.us)
     L = _lib.lib()
     nb = int(L.tl_energy_blocks(db.n))
     part = torch.empty((nb, 3), dtype=torch.float64, device=db.dev)

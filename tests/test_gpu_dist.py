@@ -45,8 +45,12 @@ def _worker(rank, world, port, tag, precision, out_dir):
     st = cfg.bodies[0].state
     g = db.gid[:db.n]
     dt_next = sim.pick_dt()
+    from paper_2602_15149_b200 import output
+    energies = np.array(output.compute_energies(cfg.bodies[0], sim.be))   # collective
+    idx = np.arange(0, st.X.shape[0], 5)
+    mrow = np.array(output.measure_row(cfg.bodies[0], idx, sim.t)[1:7])  # collective
     np.savez(os.path.join(out_dir, f"r{rank}.npz"), gid=g, u=st.u[g], v=st.v[g], s=st.s[g],
-             S=st.S[g], n_halo=db.n_all - db.n, dt=dt_next)
+             S=st.S[g], n_halo=db.n_all - db.n, dt=dt_next, energies=energies, mrow=mrow)
     dist.barrier()
     dist.destroy_process_group()
 
@@ -67,6 +71,10 @@ def test_multi_rank_device_bit_identical(tag, world, precision, tmp_path):
         sim.step(G["dts"][k])
     st = cfg.bodies[0].state
     dt_ref = sim.pick_dt()
+    from paper_2602_15149_b200 import output
+    e_ref = np.array(output.compute_energies(cfg.bodies[0], sim.be))
+    m_ref = np.array(output.measure_row(cfg.bodies[0], np.arange(0, st.X.shape[0], 5),
+                                        sim.t)[1:7])
     seen = np.zeros(st.X.shape[0], dtype=bool)
     for r in range(world):
         d = np.load(tmp_path / f"r{r}.npz")
@@ -87,4 +95,11 @@ def test_multi_rank_device_bit_identical(tag, world, precision, tmp_path):
             assert float(d["dt"]) == dt_ref
         else:
             assert abs(float(d["dt"]) - dt_ref) <= 1e-5 * dt_ref
+        # output reductions over the slabs (per-rank fsum, then an all-reduce):
+        # a different summation order than one GPU
+        tol = 1e-12 if precision == "fp64" else 1e-5
+        scale = max(np.abs(e_ref).max(), 1e-300)
+        assert np.abs(d["energies"] - e_ref).max() <= tol * scale, (d["energies"], e_ref)
+        mscale = max(np.abs(m_ref).max(), 1e-300)
+        assert np.abs(d["mrow"] - m_ref).max() <= tol * mscale, (d["mrow"], m_ref)
     assert seen.all()
