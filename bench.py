@@ -285,16 +285,22 @@ def main():
     with ClockSampler(local) as clocks:
         torch.cuda.nvtx.range_push("timed")      # ncu --nvtx --nvtx-include timed/
         ev0.record(sim.stream)
-        sim.advance(args.steps, pass_events=pass_ev)
+        sim.advance(args.steps)
         ev1.record(sim.stream)
         torch.cuda.synchronize()
         torch.cuda.nvtx.range_pop()
     if world > 1:
         dist.barrier()
     ms = ev0.elapsed_time(ev1)
+    sim.finish_advance()
+    # per-pass kernel times for the roofline: a further short run with events
+    # around each pass (which launches the passes back to back, without the
+    # single-GPU pass overlap of the timed steps)
+    sim.advance(min(args.steps, 20), pass_events=pass_ev)
+    torch.cuda.synchronize()
+    sim.finish_advance()
     ta = [e[0].elapsed_time(e[1]) for e in pass_ev]
     tb = [e[2].elapsed_time(e[3]) for e in pass_ev]
-    sim.finish_advance()
     if world > 1:
         cdev = "cuda" if args.dist_backend == "nccl" else "cpu"
         tt = torch.tensor([ms], device=cdev)
