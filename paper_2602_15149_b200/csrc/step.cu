@@ -57,7 +57,7 @@ using tl::mm3;
 #define TL_MINB_A(R) (sizeof(R) == 4 ? 4 : 1)
 #endif
 #ifndef TL_MINB_B
-#define TL_MINB_B(R) 4
+#define TL_MINB_B(R) (sizeof(R) == 4 ? 4 : 2)
 #endif
 static_assert(TL_SELL_GROUP % TL_GATHER_A == 0 && TL_SELL_GROUP % TL_GATHER_B == 0, "gather group");
 static_assert(TL_SELL_GROUP == 4, "tiled neighbour loops read 4 slots per group");
