@@ -51,10 +51,10 @@ using tl::mm3;
 #endif
 // minimum resident CTAs per SM requested from ptxas (register budget, for
 // 256-thread launch bounds); tuned on B200 for the C4 workload: FP32 pass A
-// and pass B 4 (64 registers; 48 spills and measured slower); FP64 pass A
-// needs its registers (J2/eigen) and keeps 1
+// and pass B 4 (64 registers; 48 spills and measured slower); FP64 2 (128
+// registers: 64 spilled 2 KB in pass B, 136 in pass A left it at 3 CTAs/SM)
 #ifndef TL_MINB_A
-#define TL_MINB_A(R) (sizeof(R) == 4 ? 4 : 1)
+#define TL_MINB_A(R) (sizeof(R) == 4 ? 4 : 2)
 #endif
 #ifndef TL_MINB_B
 #define TL_MINB_B(R) (sizeof(R) == 4 ? 4 : 2)
