@@ -31,7 +31,7 @@ enum {
     TL_ERR_CASE = -4
 };
 
-#define TL_ABI_VERSION 8
+#define TL_ABI_VERSION 9
 
 int tl_abi_version(void);
 /* sizeof of the ABI structs, for binding checks: 0 tl_body, 1 tl_clock,
@@ -282,7 +282,9 @@ typedef struct {
      * same slice offsets as sidx.  hmax = max halo slot extent over tiles;
      * every tile uses the plane stride tile + hmax */
     int32_t tile, hmax;
-    int32_t slmax, pad_;    /* max slot-table entries of one tile (its warps' slices) */
+    int32_t slmax;          /* max slot-table entries of one tile (its warps' slices) */
+    int32_t bsplit;         /* tiled FP32 3D pass B: 1, or 4 threads per member, each
+                               summing a quarter of the row (high-k stencils) */
     const int64_t* hoff;
     const int32_t* halo;
     const uint16_t* slots;

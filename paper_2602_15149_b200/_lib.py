@@ -13,7 +13,7 @@ import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("TLSPH_LIB", os.path.join(HERE, "libtlsph.so"))
-ABI_VERSION = 8
+ABI_VERSION = 9
 
 _lib = None
 
@@ -74,7 +74,7 @@ _BODY_FIELDS += [(k, D) for k in ("h", "inv_h", "alpha", "rho0", "lam", "mu", "k
                                   "V0c", "m0c", "dp_body", "jac_tol", "inv_Gc", "inv_eps0",
                                   "inv_c0")]
 _BODY_FIELDS += [("f0", D * 3)]
-_BODY_FIELDS += [("soff", P), ("sidx", P), ("wlen", P), ("tile", I32), ("hmax", I32), ("slmax", I32), ("pad_", I32), ("hoff", P),
+_BODY_FIELDS += [("soff", P), ("sidx", P), ("wlen", P), ("tile", I32), ("hmax", I32), ("slmax", I32), ("bsplit", I32), ("hoff", P),
                  ("halo", P), ("slots", P), ("hslot", P), ("tlist", P), ("tbase", I64),
                  ("tcount", I64), ("toff", P), ("tpos_a", P), ("tpos_b", P)]
 _BODY_FIELDS += [(k, P) for k in ("Xs", "L", "V0", "m0", "ac", "us", "rb", "v", "al",

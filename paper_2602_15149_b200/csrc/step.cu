@@ -53,8 +53,11 @@ using tl::mm3;
 // 256-thread launch bounds); tuned on B200 for the C4 workload: FP32 pass A
 // and pass B 4 (64 registers; 48 spills and measured slower); FP64 2 (128
 // registers: 64 spilled 2 KB in pass B, 136 in pass A left it at 3 CTAs/SM)
+#ifndef TL_MINB_A_GATHER
+#define TL_MINB_A_GATHER 3
+#endif
 #ifndef TL_MINB_A
-#define TL_MINB_A(R) (sizeof(R) == 4 ? 4 : 2)
+#define TL_MINB_A(R, TILED) (sizeof(R) == 4 ? ((TILED) ? 4 : TL_MINB_A_GATHER) : 2)
 #endif
 #ifndef TL_MINB_B
 #define TL_MINB_B(R) (sizeof(R) == 4 ? 4 : 2)
@@ -810,7 +813,7 @@ __device__ __forceinline__ void prefetch_own_b(const tl_body& b, int64_t p0) {
 // pass A
 // ---------------------------------------------------------------------------
 template <typename R, int DIM, int MODEL, bool FRAC, int KIND, int G, bool TILED>
-__global__ void __launch_bounds__(kThreads, TL_MINB_A(R)) k_pass_a(const tl_body b) {
+__global__ void __launch_bounds__(kThreads, TL_MINB_A(R, TILED)) k_pass_a(const tl_body b) {
     extern __shared__ __align__(16) unsigned char smem[];
     // a CTA of blockDim.x threads owns blockDim.x consecutive particles (TILED:
     // one shared tile of b.tile == blockDim.x particles); one particle per
@@ -1276,15 +1279,34 @@ __device__ __noinline__ EpiOut epi_slow(const tl_body* b, int64_t i, uint32_t ma
 // ---------------------------------------------------------------------------
 // pass B
 // ---------------------------------------------------------------------------
-template <typename R, int DIM, int MODE, bool FRAC, int KIND, int G, bool TILED>
-__global__ void __launch_bounds__(kThreads, TL_MINB_B(R)) k_pass_b(const __grid_constant__ tl_body b) {
+// SPLIT > 1 (tiled FP32 3D, high-k stencils): SPLIT threads per member, part
+// p summing the p-th share of the warp's slot groups; the shares are added in
+// part order through shared memory and part 0 runs the epilogue.  A radial
+// stencil's tile holds ~13 halo records per member, so shared memory allows
+// one CTA per SM: the split gives it SPLIT times the warps to hide the
+// shared-memory load latency of the pair loop.
+template <int SPLIT>
+constexpr int b_threads() { return SPLIT > 1 ? 1024 : kThreads; }
+
+template <typename R, int SPLIT>
+constexpr int b_minb() { return SPLIT > 1 ? 1 : TL_MINB_B(R); }
+
+template <typename R, int NREC>
+__host__ __device__ constexpr size_t split_off(int S, int slmax) {
+    return (tile_bytes<R, NREC>(S, slmax) + 15) & ~(size_t)15;
+}
+
+template <typename R, int DIM, int MODE, bool FRAC, int KIND, int G, bool TILED, int SPLIT = 1>
+__global__ void __launch_bounds__(b_threads<SPLIT>(), b_minb<R, SPLIT>())
+    k_pass_b(const __grid_constant__ tl_body b) {
     extern __shared__ __align__(16) unsigned char smem[];
     // a CTA of blockDim.x threads owns blockDim.x consecutive particles (TILED:
     // one shared tile of b.tile == blockDim.x particles); one particle per
     // thread -- larger tiles looped over by 256 threads measured slower
     // (shared memory per CTA cuts residency)
+    const int T = SPLIT > 1 ? b.tile : (int)blockDim.x;
     const int64_t tb = tile_of(b, TILED);
-    const int64_t p0 = tb * (int64_t)blockDim.x;
+    const int64_t p0 = tb * (int64_t)T;
     if (halted(b)) return;
     double v2 = 0.0, a2 = 0.0;
     long long bad_acc = LLONG_MAX;
@@ -1297,9 +1319,13 @@ __global__ void __launch_bounds__(kThreads, TL_MINB_B(R)) k_pass_b(const __grid_
         tl_ = tile_layout<R, 3>(smem, b.tile + b.hmax);
         stage_tile<R, 3>(b, tl_, tb, b.tpos_b, rbp, &bar);
     }
-    const int ms = (int)threadIdx.x;   // member slot
-    const int64_t i = p0 + ms;
-    if (i < b.n) {
+    const int ms = SPLIT > 1 ? (int)threadIdx.x % T : (int)threadIdx.x;   // member slot
+    const int part = SPLIT > 1 ? (int)threadIdx.x / T : 0;
+    const bool live = p0 + ms < b.n;
+    // SPLIT: every thread takes part in the share reduction; the dead ones of a
+    // partial last tile read the last particle's row and sum nothing
+    if (live || SPLIT > 1) {
+        const int64_t i = live ? p0 + ms : b.n - 1;
         const int64_t N = b.n_all;
         const int lane = (int)(i & 31);
         const int64_t w = i >> 5;
@@ -1317,10 +1343,17 @@ __global__ void __launch_bounds__(kThreads, TL_MINB_B(R)) k_pass_b(const __grid_
         if (TILED) {
             const V4<R> me = tl_.pos[ms];
             const uint32_t pos_sh = tl::smem_u32(tl_.pos), rec_sh = tl::smem_u32(tl_.rec);
-            const uint32_t sl_sh = tl::smem_u32(tl_.slots + (base - b.soff[p0 >> 5]) + lane * G);
+            uint32_t sl_sh = tl::smem_u32(tl_.slots + (base - b.soff[p0 >> 5]) + lane * G);
             const uint16_t* slg = b.slots + base + lane * G;
             const bool staged = b.slmax > 0;
-            const int lenr = b.wlen ? (int)b.wlen[w] : len;   // real longest row
+            int lenr = b.wlen ? (int)b.wlen[w] : len;   // real longest row
+            if (SPLIT > 1) {   // this part's share of the warp's slot groups
+                const int ng = (lenr + 3) >> 2;
+                const int k0 = 4 * (ng * part / SPLIT), k1 = min(lenr, 4 * (ng * (part + 1) / SPLIT));
+                sl_sh += 64u * (uint32_t)k0;
+                slg += 32 * k0;
+                lenr = live ? max(k1 - k0, 0) : 0;
+            }
 #define TL_LOOP_B(U, ST, V)                                                                        \
 loop_b<R, DIM, KIND, U, ST, V>(pos_sh, rec_sh, sl_sh, slg, lenr, me, vi0, vi1, vi2, inv_h,    \
                                eps_h2, B2, B1, s1, s2, s3)
@@ -1364,43 +1397,69 @@ if (visc) TL_LOOP_B(U, ST, true); else TL_LOOP_B(U, ST, false)
                                          vi2, visc, inv_h, eps_h2, B2, B1, s1, s2, s3);
             }
         }
-        {   // kernel constant (and m0 when uniform), once per particle
-            const R ck = kshape_const<R, KIND>(b) * (uni ? R(b.m0c) : R(1));
+        if constexpr (SPLIT > 1) {   // add the shares in part order
+            R* red = reinterpret_cast<R*>(smem + split_off<R, 3>(b.tile + b.hmax, b.slmax));
+            if (part > 0) {
+                R* o = red + (size_t)(part - 1) * 9 * T + ms;
 #pragma unroll
-            for (int q = 0; q < 3; ++q) {
-                s1[q] *= ck;
-                s2[q] *= ck;
-                s3[q] *= ck * inv_rho;
+                for (int q = 0; q < 3; ++q) {
+                    o[q * T] = s1[q];
+                    o[(3 + q) * T] = s2[q];
+                    o[(6 + q) * T] = s3[q];
+                }
+            }
+            __syncthreads();
+            if (part > 0) return;   // whole warps (T is a multiple of 32)
+#pragma unroll 1
+            for (int p = 1; p < SPLIT; ++p) {
+                const R* o = red + (size_t)(p - 1) * 9 * T + ms;
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    s1[q] += o[q * T];
+                    s2[q] += o[(3 + q) * T];
+                    s3[q] += o[(6 + q) * T];
+                }
             }
         }
-        // a_int = (PL_i s1 + s2)/rho0^2 - AL_i s3
-        const auto r0i = TILED ? tl_.rec[3 * ms] : tl::ld4(rbp + 12 * i);
-        const auto r1i = TILED ? tl_.rec[3 * ms + 1] : tl::ld4(rbp + 12 * i + 4);
-        const R PLi[9] = {r0i.x, r0i.y, r0i.z, r0i.w, r1i.x, r1i.y, r1i.z, r1i.w, r2i.x};
-        const R inv_rho2 = inv_rho * inv_rho;
-        double acc[3];
+        if (live) {   // the dead lanes of a split tile still join the warp reductions
+            {   // kernel constant (and m0 when uniform), once per particle
+                const R ck = kshape_const<R, KIND>(b) * (uni ? R(b.m0c) : R(1));
 #pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            R t = (PLi[3 * a] * s1[0] + PLi[3 * a + 1] * s1[1] + PLi[3 * a + 2] * s1[2] + s2[a]) * inv_rho2;
-            if (visc) {
-                const R* al = static_cast<const R*>(b.al);
-                t -= al[(3 * a) * N + i] * s3[0] + al[(3 * a + 1) * N + i] * s3[1] +
-                     al[(3 * a + 2) * N + i] * s3[2];
+                for (int q = 0; q < 3; ++q) {
+                    s1[q] *= ck;
+                    s2[q] *= ck;
+                    s3[q] *= ck * inv_rho;
+                }
             }
-            acc[a] = double(t);
+            // a_int = (PL_i s1 + s2)/rho0^2 - AL_i s3
+            const auto r0i = TILED ? tl_.rec[3 * ms] : tl::ld4(rbp + 12 * i);
+            const auto r1i = TILED ? tl_.rec[3 * ms + 1] : tl::ld4(rbp + 12 * i + 4);
+            const R PLi[9] = {r0i.x, r0i.y, r0i.z, r0i.w, r1i.x, r1i.y, r1i.z, r1i.w, r2i.x};
+            const R inv_rho2 = inv_rho * inv_rho;
+            double acc[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                R t = (PLi[3 * a] * s1[0] + PLi[3 * a + 1] * s1[1] + PLi[3 * a + 2] * s1[2] + s2[a]) * inv_rho2;
+                if (visc) {
+                    const R* al = static_cast<const R*>(b.al);
+                    t -= al[(3 * a) * N + i] * s3[0] + al[(3 * a + 1) * N + i] * s3[1] +
+                         al[(3 * a + 2) * N + i] * s3[2];
+                }
+                acc[a] = double(t);
+            }
+            // the rest of the particle's update: boundary conditions / restrictphi
+            // expressions only on the (rare) particles that carry them, out of
+            // line, so the common path holds no call frame
+            const uint32_t mask = b.bcmask ? b.bcmask[i] : 0u;
+            const bool slow = (b.nbc && (mask || b.bc_whole)) || (FRAC && b.restrict_prog >= 0);
+            const EpiOut o = slow ? epi_slow<R, DIM, MODE, FRAC>(&b, i, mask, acc[0], acc[1], acc[2],
+                                                                 vi0, vi1, vi2)
+                                  : epi_body<R, DIM, MODE, FRAC, false>(b, i, mask, acc[0], acc[1],
+                                                                        acc[2], vi0, vi1, vi2);
+            v2 = fmax(v2, o.v2);
+            a2 = fmax(a2, o.a2);
+            bad_acc = min(bad_acc, o.bad);
         }
-        // the rest of the particle's update: boundary conditions / restrictphi
-        // expressions only on the (rare) particles that carry them, out of
-        // line, so the common path holds no call frame
-        const uint32_t mask = b.bcmask ? b.bcmask[i] : 0u;
-        const bool slow = (b.nbc && (mask || b.bc_whole)) || (FRAC && b.restrict_prog >= 0);
-        const EpiOut o = slow ? epi_slow<R, DIM, MODE, FRAC>(&b, i, mask, acc[0], acc[1], acc[2],
-                                                             vi0, vi1, vi2)
-                              : epi_body<R, DIM, MODE, FRAC, false>(b, i, mask, acc[0], acc[1],
-                                                                    acc[2], vi0, vi1, vi2);
-        v2 = fmax(v2, o.v2);
-        a2 = fmax(a2, o.a2);
-        bad_acc = min(bad_acc, o.bad);
     }
     v2 = tl::warp_max(v2);
     a2 = tl::warp_max(a2);
@@ -1556,6 +1615,26 @@ int launch_a(cudaStream_t st, const tl_body& b) {
 template <typename R, int DIM, int MODE, bool FRAC, int KIND>
 int launch_b_one(cudaStream_t st, const tl_body& b) {
     constexpr int G = TL_GATHER_B;
+    if constexpr (sizeof(R) == 4 && DIM == 3) {
+        if (b.tile > 0 && b.bsplit == 4) {
+            constexpr int SP = 4;
+            if (b.tile * SP > 1024) {
+                tl_set_error("bsplit %d needs tile <= %d", SP, 1024 / SP);
+                return TL_ERR_ARG;
+            }
+            auto kern = k_pass_b<R, DIM, MODE, FRAC, KIND, G, true, SP>;
+            const size_t bytes = split_off<R, 3>(b.tile + b.hmax, b.slmax) +
+                                 (size_t)(SP - 1) * 9 * b.tile * sizeof(R);
+            int rc = smem_opt_in(kern, bytes);
+            if (rc) return rc;
+            kern<<<b.tlist ? (unsigned)b.tcount : tl_blocks(b.n, b.tile), b.tile * SP, bytes, st>>>(b);
+            return tl_check_launch("k_pass_b");
+        }
+    }
+    if (b.tile > 0 && b.bsplit > 1) {
+        tl_set_error("bsplit: tiled FP32 3D pass B only (bsplit 4)");
+        return TL_ERR_ARG;
+    }
     if (b.tile > 0) {
         auto kern = k_pass_b<R, DIM, MODE, FRAC, KIND, G, true>;
         const size_t bytes = tile_bytes<R, 3>(b.tile + b.hmax, b.slmax);

@@ -47,6 +47,12 @@ def _torch():
     return torch
 
 
+def _mean_row(dadj):
+    """Mean neighbours per particle of a device adjacency."""
+    n = int(dadj.indptr.shape[0]) - 1
+    return float(dadj.indptr[-1].item()) / max(n, 1)
+
+
 class DeviceBody:
     """Device buffers and the tl_body descriptor of one body."""
 
@@ -87,6 +93,11 @@ class DeviceBody:
         tile = DEFAULT_TILE[precision]
         if int(body.dim) == 2:
             tile = 128    # 2D stencils: thin 1-deep halos, measured best for pass A (C5)
+        elif precision == "fp32" and _mean_row(dadj) > 64.0:
+            # radial 3D stencils: pass A gathers from L2 and pass B runs one CTA
+            # per SM with split rows; the widest tile has the thinnest halo per
+            # member (pass B, C2: 1.38 -> 1.17 ms, C3: 5.78 -> 4.76 ms)
+            tile = 256
         tile = int(os.environ.get("TLSPH_TILE", str(tile)))
         if part is not None:
             part.complete(dadj)          # halo ids in exchange order (collective-free)
@@ -162,6 +173,17 @@ class DeviceBody:
         k_mean = float(lay.indptr[-1].item()) / max(n, 1)
         self.tile_a = bool(lay.tile) and (int(env_a) != 0 if env_a is not None
                                           else k_mean <= 64.0)
+        # radial 3D stencils, FP32: their tiled pass B runs one CTA per SM
+        # (shared memory), so 4 threads per member split each row to give that
+        # CTA 4x the warps (256-particle tiles, pass B: C2 1.48 -> 1.17 ms, C3
+        # 5.53 -> 4.76 ms).  TLSPH_BSPLIT=1/4 overrides.
+        env_s = os.environ.get("TLSPH_BSPLIT")
+        split_ok = (self.tile_b and precision == "fp32" and int(body.dim) == 3
+                    and 4 * int(lay.tile) <= 1024
+                    and ((lay.tile + lay.hmax) * 64 + 2 * lay.slmax + 16 + 3 * 36 * lay.tile
+                         <= TILE_SMEM_LIMIT))
+        self.bsplit = (4 if split_ok and (int(env_s) == 4 if env_s is not None
+                                          else k_mean > 64.0) else 1)
         # multi-GPU: interior tiles first (they overlap the halo exchange)
         self.tlist, self.n_interior = lay.split_tiles() if part is not None else (None, 0)
         self.counters = torch.zeros(N_COUNTERS, dtype=torch.int64, device=dev)
@@ -276,6 +298,7 @@ class DeviceBody:
         b.wlen = P(self.layout.wlen)
         lay = self.layout
         b.tile, b.hmax, b.slmax = int(lay.tile), int(lay.hmax), int(lay.slmax)
+        b.bsplit = int(getattr(self, "bsplit", 1))
         if lay.tile:
             b.hoff, b.halo, b.slots, b.hslot = (P(lay.hoff), P(lay.halo), P(lay.slots),
                                                 P(lay.hslot))

@@ -249,6 +249,25 @@ def test_device_step1_fp32(tag):
         assert e1[k] <= 1e-5, (k, e1[k])
 
 
+@pytest.mark.parametrize("tile", ["32", "160", "256"])
+@pytest.mark.parametrize("tag", ["taylor3d", "column3d", "kalthoff3d", "twisting3d"])
+def test_device_fp32_split_rows(tag, tile, monkeypatch):
+    """FP32 3D pass B with 4 threads per member (bsplit, the high-k path):
+    the row shares and their in-order sum give the step-1 fields within the
+    FP32 tolerance, including partial last tiles (tile 32)."""
+    monkeypatch.setenv("TLSPH_TILE", tile)
+    monkeypatch.setenv("TLSPH_BSPLIT", "4")
+    G = golden(f"run_{tag}")
+    cfg, sim = _sim(G, "fp32")
+    assert sim.dbodies[0].bsplit == 4
+    sim.initialize()
+    st = cfg.bodies[0].state
+    sim.step(G["dts"][0])
+    e1 = _errors(st, G, 1)
+    for k in ("F", "S", "a", "u", "v"):
+        assert e1[k] <= 1e-5, (k, e1[k])
+
+
 @pytest.mark.parametrize("tag", ["kalthoff2d", "beam2d"])
 def test_device_run_loop_adaptive(tag):
     """run() on the device clock reproduces the reference's adaptive dt
