@@ -166,13 +166,16 @@ class DeviceBody:
         env_b = os.environ.get("TLSPH_TILE_B")
         self.tile_b = bool(lay.tile) and (int(env_b) != 0 if env_b is not None
                                           else int(body.dim) == 3)
-        # pass A tiling: radial 3D stencils (k ~ 165) stage ~13 halo records
-        # per member and fit one CTA per SM; their pass A gathers faster from
-        # L2 (C2: 0.60 vs 0.68 ms, C3: 3.0 vs 3.55 ms).  TLSPH_TILE_A overrides.
+        # pass A tiling: radial 3D stencils (k ~ 165) on 160-particle tiles
+        # (FP64) stage ~13 halo records per member and gather faster from L2
+        # (measured in FP32: C2 0.60 vs 0.68 ms, C3 3.0 vs 3.55 ms); on the
+        # FP32 256-particle tiles the tiled pass A wins (C2 0.38 vs 0.58 ms,
+        # C3 2.55 vs 2.69 ms).  TLSPH_TILE_A overrides.
         env_a = os.environ.get("TLSPH_TILE_A")
         k_mean = float(lay.indptr[-1].item()) / max(n, 1)
+        wide = precision == "fp32" and int(body.dim) == 3
         self.tile_a = bool(lay.tile) and (int(env_a) != 0 if env_a is not None
-                                          else k_mean <= 64.0)
+                                          else (k_mean <= 64.0 or wide))
         # radial 3D stencils, FP32: their tiled pass B runs one CTA per SM
         # (shared memory), so 4 threads per member split each row to give that
         # CTA 4x the warps (256-particle tiles, pass B: C2 1.48 -> 1.17 ms, C3

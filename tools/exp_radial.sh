@@ -1,4 +1,5 @@
-python -m pytest tests -m gpu -q -x 2>&1 | tail -3
-for cfg in C2 C3 C5; do
-timeout 300 python bench.py --config $cfg --steps 30 --warmup 5 --e2e-steps 0 2>&1 | tail -1 | python -c "import sys,json; d=json.loads(sys.stdin.read()); print('$cfg', d['value'], d.get('passes'))"
+python -m pytest tests -m gpu -q -x 2>&1 | tail -2
+for cfg in C2 C3; do
+timeout 300 python bench.py --config $cfg --steps 50 --warmup 5 2>&1 | tail -1 > gpurun_out/bench_$cfg.json
+python -c "import json; d=json.load(open('gpurun_out/bench_$cfg.json')); print('$cfg', d['value'], d['e2e']['value'], d.get('passes'))"
 done
