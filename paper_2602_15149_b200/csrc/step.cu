@@ -550,14 +550,49 @@ __device__ __forceinline__ uint2 slot_group(uint32_t sl_sh, const uint16_t* sl_g
     return __ldg(reinterpret_cast<const uint2*>(sl_g + 32 * k));
 }
 
+// Visit this lane's len slots (raw slot values) group by group.  A warp's
+// slices are padded to a multiple of 4; `len` is the warp's real longest
+// row, so the last group runs only len % 4 pairs.  With the slot table in
+// global memory (!STAGED: the tile's table did not fit next to its halo) the
+// next group's load is issued before this group's pairs.
+template <bool STAGED, typename F>
+__device__ __forceinline__ void each_slot(uint32_t sl_sh, const uint16_t* sl_g, int len, F&& pair) {
+    const int full = len & ~3;
+    int k = 0;
+    uint2 v = make_uint2(0u, 0u);
+    if constexpr (STAGED) {
+        for (; k < full; k += 4) {
+            v = slot_group<true>(sl_sh, sl_g, k);
+            pair(v.x & 0xffffu);
+            pair(v.x >> 16);
+            pair(v.y & 0xffffu);
+            pair(v.y >> 16);
+        }
+        if (len & 3) v = slot_group<true>(sl_sh, sl_g, k);
+    } else {
+        if (len > 0) v = slot_group<false>(sl_sh, sl_g, 0);
+        for (; k < full; k += 4) {
+            const uint2 vn = k + 4 < len ? slot_group<false>(sl_sh, sl_g, k + 4) : v;
+            pair(v.x & 0xffffu);
+            pair(v.x >> 16);
+            pair(v.y & 0xffffu);
+            pair(v.y >> 16);
+            v = vn;
+        }
+    }
+    if (len & 3) {
+        pair(v.x & 0xffffu);
+        if ((len & 3) > 1) pair(v.x >> 16);
+        if ((len & 3) > 2) pair(v.y & 0xffffu);
+    }
+}
+
 // Neighbour loops over a staged tile.  Slots are slot * 16: the byte offset
 // of the neighbour's FP32 position record (FP64 records are twice as wide);
 // the gathered record sits at the same offset (pass A, one record) or
 // three times it (pass B, three records).
 // UNI (uniform V0 / m0) and STAGED (slot table in shared memory) are
 // compile-time so the loop body has no per-pair predicates or branches.
-// A warp's slices are padded to a multiple of 4 (slot groups); `len` is
-// the warp's real longest row, so the last group runs only len % 4 pairs.
 template <typename R, int DIM, bool FRAC, int KIND, bool UNI, bool STAGED>
 __device__ __forceinline__ void loop_a(uint32_t pos_sh, uint32_t rec_sh, uint32_t sl_sh,
                                        const uint16_t* sl_g, int len, const V4<R>& me,
@@ -569,21 +604,7 @@ __device__ __forceinline__ void loop_a(uint32_t pos_sh, uint32_t rec_sh, uint32_
         pair_a<R, DIM, FRAC, KIND>(me.x - pj.x, DIM == 3 ? me.y - pj.y : R(0), me.z - pj.z, uj, pj.w,
                                    UNI, ui, inv_h, D, M);
     };
-    const int full = len & ~3;
-    int k = 0;
-    for (; k < full; k += 4) {
-        const uint2 v = slot_group<STAGED>(sl_sh, sl_g, k);
-        pair(U * (v.x & 0xffffu));
-        pair(U * (v.x >> 16));
-        pair(U * (v.y & 0xffffu));
-        pair(U * (v.y >> 16));
-    }
-    if (len & 3) {
-        const uint2 v = slot_group<STAGED>(sl_sh, sl_g, k);
-        pair(U * (v.x & 0xffffu));
-        if ((len & 3) > 1) pair(U * (v.x >> 16));
-        if ((len & 3) > 2) pair(U * (v.y & 0xffffu));
-    }
+    each_slot<STAGED>(sl_sh, sl_g, len, [&](uint32_t sl) { pair(U * sl); });
 }
 
 template <typename R, int DIM, int KIND, bool UNI, bool STAGED, bool VISC>
@@ -598,21 +619,7 @@ __device__ __forceinline__ void loop_b(uint32_t pos_sh, uint32_t rec_sh, uint32_
                              lds4<R>(ra + sizeof(V4<R>)), lds4<R>(ra + 2 * sizeof(V4<R>)), pj.w, UNI,
                              vi0, vi1, vi2, VISC, inv_h, eps_h2, B2, B1, s1, s2, s3);
     };
-    const int full = len & ~3;
-    int k = 0;
-    for (; k < full; k += 4) {
-        const uint2 v = slot_group<STAGED>(sl_sh, sl_g, k);
-        pair(U * (v.x & 0xffffu));
-        pair(U * (v.x >> 16));
-        pair(U * (v.y & 0xffffu));
-        pair(U * (v.y >> 16));
-    }
-    if (len & 3) {
-        const uint2 v = slot_group<STAGED>(sl_sh, sl_g, k);
-        pair(U * (v.x & 0xffffu));
-        if ((len & 3) > 1) pair(U * (v.x >> 16));
-        if ((len & 3) > 2) pair(U * (v.y & 0xffffu));
-    }
+    each_slot<STAGED>(sl_sh, sl_g, len, [&](uint32_t sl) { pair(U * sl); });
 }
 
 // FP32 3D pass-A loop on packed FP32x2 arithmetic (Blackwell FFMA2 / FADD2 /
@@ -671,21 +678,7 @@ __device__ __forceinline__ void loop_a_f2(uint32_t pos_sh, uint32_t rec_sh, uint
         pair_a_f2<FRAC, KIND, UNI>(lds4<float>(pos_sh + o), lds4<float>(rec_sh + o), nme, nmz, nui,
                                    nuz, ui.w, inv_h, a);
     };
-    const int full = len & ~3;
-    int k = 0;
-    for (; k < full; k += 4) {
-        const uint2 v = slot_group<STAGED>(sl_sh, sl_g, k);
-        pair(v.x & 0xffffu);
-        pair(v.x >> 16);
-        pair(v.y & 0xffffu);
-        pair(v.y >> 16);
-    }
-    if (len & 3) {
-        const uint2 v = slot_group<STAGED>(sl_sh, sl_g, k);
-        pair(v.x & 0xffffu);
-        if ((len & 3) > 1) pair(v.x >> 16);
-        if ((len & 3) > 2) pair(v.y & 0xffffu);
-    }
+    each_slot<STAGED>(sl_sh, sl_g, len, pair);
     // back to row-major D (= -D') and the (xx yy zz xy xz yz) M of pair_a
     D[0] = -a.D01.x; D[1] = -a.D01.y; D[2] = -a.D25.x;
     D[3] = -a.D34.x; D[4] = -a.D34.y; D[5] = -a.D25.y;
