@@ -1,5 +1,4 @@
 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
-for cfg in C5 C1; do
-timeout 300 python bench.py --config $cfg --steps 50 --warmup 5 2>&1 | tail -1 > gpurun_out/bench_$cfg.json
-python -c "import json; d=json.load(open('gpurun_out/bench_$cfg.json')); print('$cfg', d['value'], (d.get('e2e') or {}).get('value'), d.get('passes'))"
+for s in 4 1; do
+TLSPH_BSPLIT=$s timeout 300 python bench.py --config C4 --steps 50 --warmup 5 --e2e-steps 0 2>&1 | tail -1 | python -c "import sys,json; d=json.loads(sys.stdin.read()); print('C4 split$s', d['value'], d.get('passes'))"
 done
