@@ -103,3 +103,14 @@ def test_multi_rank_device_bit_identical(tag, world, precision, tmp_path):
         mscale = max(np.abs(m_ref).max(), 1e-300)
         assert np.abs(d["mrow"] - m_ref).max() <= tol * mscale, (d["mrow"], m_ref)
     assert seen.all()
+
+
+def test_multi_rank_split_rows(tmp_path, monkeypatch):
+    """The 4-way row split of pass B (tl_body.bsplit) on slabs, whose tiled
+    passes launch interior and boundary tile lists separately."""
+    monkeypatch.setenv("TLSPH_BSPLIT", "4")   # inherited by the spawned ranks
+    from paper_2602_15149_b200.simulation import DeviceSimulation
+    sim = DeviceSimulation(run_case(golden("run_taylor3d")), precision="fp32")
+    assert sim.dbodies[0].bsplit == 4
+    del sim
+    test_multi_rank_device_bit_identical("taylor3d", 2, "fp32", tmp_path)
