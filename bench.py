@@ -203,6 +203,21 @@ def cpu_reference(config, steps, warmup, budget_s=25.0):
 
 # ---------------------------------------------------------------------------
 
+def spawn_ranks(n):
+    """`bench.py --gpus N` outside torchrun: launch the N ranks ourselves (one
+    process per GPU, the driver's own torchrun command line) and pass their
+    output through; rank 0 prints the JSON line."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -223,9 +238,13 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "ours" and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
 
     if args.impl == "reference":
         if rank != 0:
@@ -249,9 +268,17 @@ def main():
     from paper_2602_15149_b200 import cases
     from paper_2602_15149_b200.simulation import DeviceSimulation
 
-    torch.cuda.set_device(local % max(torch.cuda.device_count(), 1))
+    ndev = torch.cuda.device_count()
+    if world > 1 and args.dist_backend == "nccl" and world > ndev:
+        raise SystemExit(f"bench.py: {world} NCCL ranks need {world} GPUs, {ndev} visible")
+    torch.cuda.set_device(local % max(ndev, 1))
     if world > 1:
         if args.dist_backend == "nccl":
+            # communicator init lines (rank count, NVLink/NVLS transport) to
+            # stderr, so the JSON line on stdout stays the last line
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
             dist.init_process_group("nccl", init_method="env://",
                                     device_id=torch.device("cuda", local))
         else:

@@ -31,7 +31,7 @@ enum {
     TL_ERR_CASE = -4
 };
 
-#define TL_ABI_VERSION 9
+#define TL_ABI_VERSION 10
 
 int tl_abi_version(void);
 /* sizeof of the ABI structs, for binding checks: 0 tl_body, 1 tl_clock,
@@ -210,6 +210,20 @@ int tl_tile_pos(tl_stream_t st, int64_t n, int64_t n_all, int32_t T, int64_t nti
 int tl_tile_slots(tl_stream_t st, int64_t n, int32_t T, int32_t G, int32_t shift,
                   const int64_t* indptr, const int32_t* indices, const int64_t* hoff,
                   const int32_t* halo, const uint16_t* hslot, const int64_t* soff, uint16_t* slots);
+/* the same, plus keys (same layout): every pair's lattice offset class key,
+ * ((qx+7)*15 + qy+7)*15 + qz+7 for r0 = X_i - X_j = q dp (device FP64 planes X
+ * of stride n_all); 0xffff = self padding, 0xfffe = off the lattice.  The
+ * reference configuration is fixed (kernel_geom.py:1-6), so r0 of every pair
+ * is too: a lattice body's pairs take a handful of separations. */
+int tl_tile_slots_keyed(tl_stream_t st, int64_t n, int32_t T, int32_t G, int32_t shift,
+                        const int64_t* indptr, const int32_t* indices, const int64_t* hoff,
+                        const int32_t* halo, const uint16_t* hslot, const int64_t* soff,
+                        uint16_t* slots, const double* X, int64_t n_all, double dp,
+                        uint16_t* keys);
+/* rewrite m slot entries (slot << shift) as (cls_of_key[key] << 10) | slot
+ * (class 0 for the self padding) */
+int tl_class_slots(tl_stream_t st, int64_t m, int32_t shift, const uint16_t* keys,
+                   const int16_t* cls_of_key, uint16_t* slots);
 
 /* ---------------------------------------------------------------------------
  * Fused device-resident step (stepper.py:77-209, dynamics.py:28-217,
@@ -249,8 +263,15 @@ typedef struct {
     double cfl;
     int64_t step;       /* step_index */
     int64_t max_steps;  /* <0: unlimited */
-    int32_t halted;     /* 0 run, 1 finished, 2 output due, 3 max_steps, 4 dt collapsed */
+    int32_t halted;     /* 0 run, 1 finished, 2 output due, 3 max_steps, 4 dt collapsed,
+                           5 error raised inside the step, 6 non-finite state at a
+                           64-step commit (stepper.py:203-209) */
     int32_t out_step;   /* this step ends on an output boundary: mirror F, S, psi, a */
+    int32_t err;        /* errors of the step in flight: bit 0 stress (eigen / non-SPD:
+                           raised before momentum, constitutive.py:177-194, so pass B
+                           skips), bit 1 acceleration / expression / restrictphi; the
+                           step is not committed and the clock halts (5) */
+    int32_t nf_now;     /* this step left some u or v non-finite */
 } tl_clock;
 
 /* Per-body device view.  Layout (Real = float | double per `precision`):
@@ -285,6 +306,10 @@ typedef struct {
     int32_t slmax;          /* max slot-table entries of one tile (its warps' slices) */
     int32_t bsplit;         /* tiled FP32 3D pass B: 1, or 4 threads per member, each
                                summing a quarter of the row (high-k stencils) */
+    int32_t ncls;           /* bond classes (FP32, uniform lattice bodies): 0 = the pair
+                               geometry comes from staged positions; > 0 = slots hold
+                               (class << 10) | slot and bcls holds ncls entries */
+    int32_t ncls_pad;
     const int64_t* hoff;
     const int32_t* halo;
     const uint16_t* slots;
@@ -298,6 +323,12 @@ typedef struct {
     const int64_t* toff;
     const void* tpos_a;
     const void* tpos_b;
+    /* bond-class table, 8 floats per class: (W, kappa, U, 0) with W = w(r) r0,
+     * kappa = 1 / (w(r) (r^2 + 0.001 h^2)) (0 when w = 0), U = r0 / r^2, for the
+     * class's reference separation r0 = q dp (q an integer lattice offset;
+     * class 0 = the row's self padding, all zero).  The kernel shape w(r) as
+     * in the pair loops, the per-body constant applied once per particle. */
+    const float* bcls;
     /* geometry */
     const double* Xs;       /* FP64 planes x,y,z */
     const void* L;          /* 9 planes, correction matrix L_i */

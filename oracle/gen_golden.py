@@ -292,7 +292,15 @@ def gen_runs():
         ("twisting3d", lambda: L(C("twisting3d.xml"), dp_scale=4), 37, 10, (1, 10)),
         # two J2 bodies, penalty contact from step 1 (_touching)
         ("flyer2d", lambda: _touching(L(C("flyer2d.xml"), dp_scale=2)), None, 30, (1, 2, 30)),
+        # the paper's benchmark case: 3D SVK + phase field on the radial stencil,
+        # notch, restrictphi with compound `and` expressions (fourpoint3d.xml:49-59)
+        ("fourpoint3d", lambda: L(C("fourpoint3d.xml"), dp_scale=6), 38, 10, (1, 2, 10)),
+        # 3D SVK cantilever plate, artificial viscosity, cosh/sinh IC expression
+        ("plate3d", lambda: L(C("plate3d.xml"), dp_scale=6), 39, 10, (1, 2, 10)),
     ]
+    only = os.environ.get("GOLDEN_RUNS")
+    if only:
+        runs = [r for r in runs if r[0] in only.split(",")]
     for tag, make, seed, steps, checks in runs:
         cfg = make()
         if seed is not None:
@@ -387,6 +395,175 @@ def _with_algo(cfg, algo):
     return cfg
 
 
+LONG_STEPS = 2000
+
+
+def gen_long():
+    """beam2d (SVK, radial, IC expression) for 2,000 adaptive FP64 steps
+    through the reference's step loop (<= 1e-10 after
+    2,000 steps on a non-chaotic case).  End state only."""
+    cfg = caseio.load_case(os.path.join(CASES, "beam2d.xml"), dp_scale=2, mapfac=2)
+    out = dict(case_to_dict(cfg))
+    b = cfg.bodies[0]
+    out["adj0.indptr"] = b.adjacency.indptr
+    out["adj0.indices"] = b.adjacency.indices
+    sim = stepper.Simulation(cfg)
+    sim.initialize()
+    dts = []
+    for _ in range(LONG_STEPS):
+        dt = sim.pick_dt()
+        dts.append(dt)
+        sim.step(dt)
+    for k, v in _state(sim).items():
+        out[f"end.{k}"] = v
+    out["end.energies"] = _outputs(sim)["b0.energies"]
+    out["dts"] = np.array(dts)
+    save("long_beam2d", **out)
+
+
+def gen_branch():
+    """Dynamic crack branching (branch2d) with the reference's own benchmark
+    (bench.py:194-235 bench_branch; acceptance criterion 3 runs it at
+    scale 4, test_acceptance.py:149-159): initiation time near the notch
+    tip, the branched flag, FE monotone after initiation, SE decreasing, and
+    the final damage field."""
+    from solidsph import bench as rbench
+    cfg = rbench._load("branch2d", 4.0, None, None, None, None, False)
+    out = dict(case_to_dict(cfg))
+    b = cfg.bodies[0]
+    out["adj0.indptr"] = b.adjacency.indptr
+    out["adj0.indices"] = b.adjacency.indices
+    rep = rbench.bench_branch("branch2d", cfg, None, None)
+    rows = {m: v for m, v, _, _ in rep.rows}
+    print("branch2d:", rows)
+    ser = rep.extras["series"]
+    out["series.t"] = np.array(ser["t"])
+    out["series.se"] = np.array(ser["se"])
+    out["series.fe"] = np.array(ser["fe"])
+    for m in ("initiation_time_s", "branched", "fe_monotone", "se_decreases"):
+        out[f"metric.{m}"] = np.array([rows[m]])
+    out["final_s"] = rep.extras["final_s"]
+    out["end.t"] = np.array([ser["t"][-1]])
+    save("branch_branch2d", **out)
+
+
+# ---------------------------------------------------------------------------
+# error paths: the reference's exceptions raised inside the step
+# ---------------------------------------------------------------------------
+
+def _err_case(tag, make, seed, edits=(), steps=None, run=None, dt_override=None,
+              extra_exprs=(), extra_bcs=(), restrict=None, material=None, cp=None):
+    """Run one error scenario through the reference (numpy backend) and
+    record the case, the edits applied after initialize() and the exception.
+
+    edits: (field, particle, axis, value) applied to body.state after
+    initialize(); steps: number of step(dt) calls (dt from pick_dt); run:
+    (time_max, time_out) for Simulation.run; extra_exprs: (id, src, locals);
+    extra_bcs: BoundaryCondition kwargs; restrict: restrictphi expression id;
+    material: MaterialParams overrides; cp: (particle, 3x3) plastic metric."""
+    from solidsph import expr as rex2
+    from solidsph.core import BoundaryCondition
+    cfg = make()
+    if dt_override is not None:
+        cfg.dt_override = dt_override
+    if seed is not None:
+        _perturb(cfg, seed)
+    b = cfg.bodies[0]
+    for eid, src, loc in extra_exprs:
+        cfg.expressions[eid] = rex2.parse(src, loc)
+    for kw in extra_bcs:
+        b.bcs.append(BoundaryCondition(**kw))
+    if restrict is not None:
+        b.restrictphi_expr = restrict
+    for k, v in (material or {}).items():
+        setattr(b.material, k, v)
+    if cp is not None:
+        b.state.Cp[cp[0]] = np.asarray(cp[1])
+    out = {f"{tag}.{k}": v for k, v in case_to_dict(cfg).items()}
+    for k in ("u", "v", "s"):
+        out[f"{tag}.init.{k}"] = getattr(b.state, k).copy()
+    if cp is not None:
+        out[f"{tag}.init.Cp"] = b.state.Cp.copy()
+    out[f"{tag}.edits"] = np.array([(float(i), float(a), float(v)) for _, i, a, v in edits]
+                                   ).reshape(-1, 3)
+    out[f"{tag}.edit_fields"] = np.frombuffer(",".join(f for f, _, _, _ in edits).encode(),
+                                              dtype=np.uint8)
+    sim = stepper.Simulation(cfg)
+    exc = None
+    nsteps = 0
+    try:
+        sim.initialize()
+        for f, i, a, v in edits:
+            getattr(b.state, f)[int(i), int(a)] = v
+        if run is not None:
+            sim.run(time_max=run[0], time_out=run[1])
+        else:
+            for _ in range(steps):
+                sim.step(sim.pick_dt())
+                nsteps += 1
+    except Exception as e:  # the point: record what the reference raises
+        exc = e
+    assert exc is not None, f"{tag}: the reference raised nothing"
+    print(f"{tag}: {type(exc).__name__}: {exc} (after {nsteps} steps, t={sim.t!r})")
+    out[f"{tag}.driver"] = np.array([-1 if steps is None else steps,
+                                     -1.0 if run is None else run[0],
+                                     -1.0 if run is None else run[1]])
+    out[f"{tag}.exc"] = np.frombuffer(f"{type(exc).__name__}\n{exc}".encode(), dtype=np.uint8)
+    out[f"{tag}.steps_done"] = np.array([nsteps])
+    out[f"{tag}.t"] = np.array([sim.t])
+    return out
+
+
+def gen_errors():
+    L = caseio.load_case
+    C = lambda f: os.path.join(CASES, f)  # noqa: E731
+    beam = lambda: L(C("beam2d.xml"), dp_scale=2, mapfac=2)  # noqa: E731
+    kal = lambda: L(C("kalthoff2d.xml"), dp_scale=2, mapfac=1)  # noqa: E731
+    out = {}
+    # stepper.py:96-100 -- NaN velocity of one particle: its neighbours'
+    # accelerations go non-finite in the next force evaluation
+    out.update(_err_case("acc", beam, 41, edits=[("v", 1234, 0, float("nan"))], steps=3))
+    # stepper.py:203-209 -- a velocity BC drives one particle's v to inf at the
+    # end of step 64; the state check at the 64th commit raises
+    dt = 2.0e-6
+    out.update(_err_case(
+        "state64", beam, 42, steps=70, dt_override=dt,
+        extra_exprs=[(99, f"if(t>{63.5 * dt!r},cosh(1000),skip)", "")],
+        extra_bcs=[dict(kind="vel", expr=(99, None, None), target=np.array([777]))]))
+    # stepper.py:254-255 -- an overflowing |v|^2 (no viscosity, so the
+    # acceleration stays finite) makes the adaptive dt zero inside run()
+    out.update(_err_case("dtcollapse", beam, 43, edits=[("v", 321, 0, 1e200)],
+                         run=(1e-3, 1e-4), material=dict(beta1=0.0, beta2=0.0)))
+    # expr.py:513-515 -- a velocity BC expression dividing by zero
+    out.update(_err_case(
+        "div0", beam, 44, steps=2,
+        extra_exprs=[(98, "if(x0>0.05,1/(t-t),skip)", "")],
+        extra_bcs=[dict(kind="vel", expr=(None, None, 98))]))
+    # fracture.py:59-63 -- a time-dependent restrictphi leaving [0, 1]
+    out.update(_err_case(
+        "restrict", kal, 45, steps=5,
+        extra_exprs=[(97, "if(t>1.0e-12,1.5,skip)", "")], restrict=97))
+    # constitutive.py:191-194 -- a plastic metric whose radial return leaves
+    # the SPD cone (one negative eigen-direction): the first bad particle
+    T = lambda: L(C("taylor3d.xml"), dp_scale=4)  # noqa: E731
+    out.update(_err_case("nonspd", T, None, steps=2,
+                         cp=(517, np.diag([1e-4, 1e-4, 1e8]))))
+    # fast.py:254-256 -- SVK spectral split: Jacobi fails to converge on a
+    # matrix mixing NaN and finite entries (numba backend, plugin level)
+    from solidsph.backends import fast
+    rng = np.random.default_rng(46)
+    n = 64
+    F = np.broadcast_to(np.eye(3), (n, 3, 3)).copy() + rng.normal(scale=0.05, size=(n, 3, 3))
+    F[5, 0, 1] = np.nan
+    F[40, 2, 1] = np.nan
+    S, psi, psip = np.zeros((n, 3, 3)), np.zeros(n), np.zeros(n)
+    s = rng.uniform(0.2, 1.0, n)
+    nc = fast.svk_batch(F, 2.7733e6, 0.715e6, s, True, S, psi, psip)
+    print("noconv:", nc)
+    out.update({"noconv.F": F, "noconv.s": s, "noconv.n": np.array([nc])})
+    save("errors", **out)
+
+
 # ---------------------------------------------------------------------------
 EXPRS = [
     ("if(t>ramt,maxv,t/ramt*maxv)", "maxv=16.5; ramt=1.0e-6"),
@@ -450,6 +627,7 @@ def gen_targets():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["adjacency", "kernels", "runs", "expr", "targets", "crack"]
+    which = sys.argv[1:] or ["adjacency", "kernels", "runs", "expr", "targets", "crack",
+                             "long", "branch", "errors"]
     for w in which:
         globals()[f"gen_{w}"]()

@@ -13,7 +13,7 @@ import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("TLSPH_LIB", os.path.join(HERE, "libtlsph.so"))
-ABI_VERSION = 9
+ABI_VERSION = 10
 
 _lib = None
 
@@ -55,7 +55,7 @@ class tl_bc(C.Structure):
 class tl_clock(C.Structure):
     _fields_ = [("t", D), ("dt", D), ("next_out", D), ("t_max", D), ("eps", D),
                 ("dt_override", D), ("cfl", D), ("step", I64), ("max_steps", I64),
-                ("halted", I32), ("out_step", I32)]
+                ("halted", I32), ("out_step", I32), ("err", I32), ("nf_now", I32)]
 
 
 class tl_dtinfo(C.Structure):
@@ -74,9 +74,10 @@ _BODY_FIELDS += [(k, D) for k in ("h", "inv_h", "alpha", "rho0", "lam", "mu", "k
                                   "V0c", "m0c", "dp_body", "jac_tol", "inv_Gc", "inv_eps0",
                                   "inv_c0")]
 _BODY_FIELDS += [("f0", D * 3)]
-_BODY_FIELDS += [("soff", P), ("sidx", P), ("wlen", P), ("tile", I32), ("hmax", I32), ("slmax", I32), ("bsplit", I32), ("hoff", P),
+_BODY_FIELDS += [("soff", P), ("sidx", P), ("wlen", P), ("tile", I32), ("hmax", I32), ("slmax", I32), ("bsplit", I32),
+                 ("ncls", I32), ("ncls_pad", I32), ("hoff", P),
                  ("halo", P), ("slots", P), ("hslot", P), ("tlist", P), ("tbase", I64),
-                 ("tcount", I64), ("toff", P), ("tpos_a", P), ("tpos_b", P)]
+                 ("tcount", I64), ("toff", P), ("tpos_a", P), ("tpos_b", P), ("bcls", P)]
 _BODY_FIELDS += [(k, P) for k in ("Xs", "L", "V0", "m0", "ac", "us", "rb", "v", "al",
                                   "sdot", "sddot", "Hh", "Cpd", "epbar", "a", "F_out", "S_out",
                                   "psi_out", "psip_out", "perm", "bcmask", "bcs", "progs", "clock", "red",
@@ -123,6 +124,8 @@ _SIGS = {
     "tl_tile_hslots": (INT, [P, I64, I32, I32, I32, P, P, P, P]),
     "tl_tile_pos": (INT, [P, I64, I64, I32, I64, P, P, P, P, P, P, I32, P]),
     "tl_tile_slots": (INT, [P, I64, I32, I32, I32, P, P, P, P, P, P, P]),
+    "tl_tile_slots_keyed": (INT, [P, I64, I32, I32, I32, P, P, P, P, P, P, P, P, I64, D, P]),
+    "tl_class_slots": (INT, [P, I64, I32, P, P, P]),
     "tl_pass_a": (INT, [P, C.POINTER(tl_body)]),
     "tl_pass_b": (INT, [P, C.POINTER(tl_body), INT]),
     "tl_predict": (INT, [P, C.POINTER(tl_body)]),

@@ -70,6 +70,19 @@ __device__ __forceinline__ bool halted(const tl_body& b) {
     return b.clock != nullptr && *(volatile int32_t*)&b.clock->halted != 0;
 }
 
+// a stress error of this step (eigen non-convergence, non-SPD plastic
+// metric): the reference raises it inside update_stress, before momentum
+// and the kick (constitutive.py:177-194), so pass B does nothing
+__device__ __forceinline__ bool stress_failed(const tl_body& b) {
+    return b.clock != nullptr && (*(volatile int32_t*)&b.clock->err & 1);
+}
+
+// an error the reference raises inside the step: the clock does not commit
+// the step and halts at the next begin
+__device__ __forceinline__ void flag_step_error(tl_clock* c, int bit) {
+    if (c != nullptr) atomicOr(&c->err, bit);
+}
+
 // host-layout FP64 mirrors are written when the host asked for them on every
 // step (write_out) or the device clock flags this step as ending on an output
 // boundary, so run() never re-evaluates stress just to report it
@@ -686,6 +699,110 @@ __device__ __forceinline__ void loop_a_f2(uint32_t pos_sh, uint32_t rec_sh, uint
     M[0] = a.M01.x; M[1] = a.M01.y; M[2] = a.M2; M[3] = a.M3; M[4] = a.M4; M[5] = a.M5;
 }
 
+// ---------------------------------------------------------------------------
+// bond-class pair loops (b.ncls > 0, FP32): slot entry e = (class << 10) |
+// slot.  The pair geometry comes from the class table -- W = w(r) r0,
+// kappa = 1/(w (r^2 + eps h^2)), U = r0/r^2, computed once per body in FP64
+// from the lattice separation (kernel_geom.StepLayout.bond_classes) --
+// instead of a staged position record: no position load, no r, rsqrt or
+// kernel shape per pair.  A warp's lanes mostly share a class at a given k
+// (Morton bricks of one lattice), so the table loads are broadcasts.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t geo_slot(uint32_t e) { return e & 1023u; }
+__device__ __forceinline__ uint32_t geo_cls(uint32_t e) { return (e >> 10) * 32u; }
+
+// pass A, FP32 3D, packed FP32x2: D += (u_j - u_i) (x) W ; M += (s_i - s_j) W (x) U
+template <bool FRAC, bool STAGED>
+__device__ __forceinline__ void loop_a_geo_f2(uint32_t rec_sh, uint32_t cls_sh, uint32_t sl_sh,
+                                              const uint16_t* sl_g, int len, const float4& ui,
+                                              float* D, float* M) {
+    float2 D01 = make_float2(0.f, 0.f), D34 = D01, D67 = D01, D25 = D01, M01 = D01;
+    float D8 = 0.f, M2 = 0.f, M3 = 0.f, M4 = 0.f, M5 = 0.f;
+    const float2 nui = make_float2(-ui.x, -ui.y);
+    const float nuz = -ui.z;
+    each_slot<STAGED>(sl_sh, sl_g, len, [&](uint32_t e) {
+        const uint32_t c = cls_sh + geo_cls(e);
+        const float4 W = lds4<float>(c);
+        const float4 uj = lds4<float>(rec_sh + 16u * geo_slot(e));
+        const float2 wxy = make_float2(W.x, W.y);
+        const float2 du01 = __fadd2_rn(make_float2(uj.x, uj.y), nui);
+        const float du2 = uj.z + nuz;
+        D01 = __ffma2_rn(make_float2(du01.x, du01.x), wxy, D01);
+        D34 = __ffma2_rn(make_float2(du01.y, du01.y), wxy, D34);
+        D67 = __ffma2_rn(make_float2(du2, du2), wxy, D67);
+        D25 = __ffma2_rn(du01, make_float2(W.z, W.z), D25);
+        D8 = fmaf(du2, W.z, D8);
+        if (FRAC) {
+            const float4 U = lds4<float>(c + 16u);
+            const float ds = ui.w - uj.w;
+            const float2 cw = __fmul2_rn(make_float2(ds, ds), wxy);
+            const float cz = ds * W.z;
+            M01 = __ffma2_rn(cw, make_float2(U.x, U.y), M01);
+            M2 = fmaf(cz, U.z, M2);
+            M3 = fmaf(cw.x, U.y, M3);
+            M4 = fmaf(cw.x, U.z, M4);
+            M5 = fmaf(cw.y, U.z, M5);
+        }
+    });
+    D[0] = D01.x; D[1] = D01.y; D[2] = D25.x;
+    D[3] = D34.x; D[4] = D34.y; D[5] = D25.y;
+    D[6] = D67.x; D[7] = D67.y; D[8] = D8;
+    M[0] = M01.x; M[1] = M01.y; M[2] = M2; M[3] = M3; M[4] = M4; M[5] = M5;
+}
+
+// pass A, FP32 2D (x-z plane): the scalar form of the same terms
+template <bool FRAC, bool STAGED>
+__device__ __forceinline__ void loop_a_geo_2d(uint32_t rec_sh, uint32_t cls_sh, uint32_t sl_sh,
+                                              const uint16_t* sl_g, int len, const float4& ui,
+                                              float* D, float* M) {
+    each_slot<STAGED>(sl_sh, sl_g, len, [&](uint32_t e) {
+        const uint32_t c = cls_sh + geo_cls(e);
+        const float4 W = lds4<float>(c);
+        const float4 uj = lds4<float>(rec_sh + 16u * geo_slot(e));
+        const float du0 = uj.x - ui.x, du2 = uj.z - ui.z;
+        D[0] = fmaf(du0, W.x, D[0]); D[2] = fmaf(du0, W.z, D[2]);
+        D[6] = fmaf(du2, W.x, D[6]); D[8] = fmaf(du2, W.z, D[8]);
+        if (FRAC) {
+            const float4 U = lds4<float>(c + 16u);
+            const float ds = ui.w - uj.w;
+            const float cx = ds * W.x, cz = ds * W.z;
+            M[0] = fmaf(cx, U.x, M[0]); M[2] = fmaf(cz, U.z, M[2]); M[4] = fmaf(cx, U.z, M[4]);
+        }
+    });
+}
+
+// pass B: s1 += W ; s2 += PL_j W ; s3 += (B2 g^2 - B1 g) W with
+// g = (v_i - v_j).W kappa = (v_i - v_j).r0 / (r^2 + eps h^2)
+template <int DIM, bool STAGED, bool VISC>
+__device__ __forceinline__ void loop_b_geo(uint32_t rec_sh, uint32_t cls_sh, uint32_t sl_sh,
+                                           const uint16_t* sl_g, int len, float vi0, float vi1,
+                                           float vi2, float B2, float B1, float* s1, float* s2,
+                                           float* s3) {
+    each_slot<STAGED>(sl_sh, sl_g, len, [&](uint32_t e) {
+        const float4 W = lds4<float>(cls_sh + geo_cls(e));
+        const uint32_t ra = rec_sh + 48u * geo_slot(e);
+        const float4 q0 = lds4<float>(ra), q1 = lds4<float>(ra + 16u), q2 = lds4<float>(ra + 32u);
+        s1[0] += W.x; s1[2] += W.z;
+        if (DIM == 3) {
+            s1[1] += W.y;
+            s2[0] = fmaf(q0.z, W.z, fmaf(q0.y, W.y, fmaf(q0.x, W.x, s2[0])));
+            s2[1] = fmaf(q1.y, W.z, fmaf(q1.x, W.y, fmaf(q0.w, W.x, s2[1])));
+            s2[2] = fmaf(q2.x, W.z, fmaf(q1.w, W.y, fmaf(q1.z, W.x, s2[2])));
+        } else {
+            s2[0] = fmaf(q0.z, W.z, fmaf(q0.x, W.x, s2[0]));
+            s2[2] = fmaf(q2.x, W.z, fmaf(q1.z, W.x, s2[2]));
+        }
+        if (VISC) {
+            float dvw = (vi0 - q2.y) * W.x + (vi2 - q2.w) * W.z;
+            if (DIM == 3) dvw = fmaf(vi1 - q2.z, W.y, dvw);
+            const float g = dvw * W.w;
+            const float pw = (B2 * g - B1) * g;
+            s3[0] = fmaf(pw, W.x, s3[0]); s3[2] = fmaf(pw, W.z, s3[2]);
+            if (DIM == 3) s3[1] = fmaf(pw, W.y, s3[1]);
+        }
+    });
+}
+
 // Shared-memory tile of a CTA.  Two arrays indexed by slot, then the CTA's
 // block of the neighbour-slot table:
 //   pos[slot]             the staged position record (x, y, z, w) -- a copy of
@@ -697,24 +814,45 @@ __device__ __forceinline__ void loop_a_f2(uint32_t pos_sh, uint32_t rec_sh, uint
 // Members sit at slot p - p0, halo particles at their residue-aligned hslot
 // (tiles.cu k_hslots).  The capacity S = tile + hmax is the same for every
 // CTA of a launch.
+//
+// Bond-class mode (b.ncls > 0; FP32 lattice bodies with uniform V0, m0):
+// no position records at all.  The pair geometry is a per-class table entry
+// (tl_body.bcls) selected by the class field of the slot entry, staged after
+// the slot block:
+//   rec[slot * NREC + r] | slots | cls[2 * class + {0, 1}] = (W, kappa), (U, 0)
 template <typename R, int NREC>
 struct Tile {
-    V4<R>* pos;
+    V4<R>* pos;        // nullptr in bond-class mode
     V4<R>* rec;
     uint16_t* slots;   // the CTA's block of the slot table (its warps' slices)
+    float4* cls;       // bond-class table (bond-class mode)
 };
 
+__host__ __device__ constexpr size_t align16(size_t v) { return (v + 15) & ~(size_t)15; }
+
 template <typename R, int NREC>
-__host__ __device__ constexpr size_t tile_bytes(int S, int slmax) {
-    return (size_t)S * (NREC + 1) * sizeof(V4<R>) + (size_t)slmax * sizeof(uint16_t);
+__host__ __device__ constexpr size_t tile_bytes(int S, int slmax, int ncls = 0) {
+    return ncls > 0 ? (size_t)S * NREC * sizeof(V4<R>) + align16((size_t)slmax * sizeof(uint16_t)) +
+                          (size_t)ncls * 2 * sizeof(float4)
+                    : (size_t)S * (NREC + 1) * sizeof(V4<R>) + (size_t)slmax * sizeof(uint16_t);
 }
 
 template <typename R, int NREC>
-__device__ __forceinline__ Tile<R, NREC> tile_layout(unsigned char* smem, int S) {
+__device__ __forceinline__ Tile<R, NREC> tile_layout(unsigned char* smem, int S, int slmax = 0,
+                                                     int ncls = 0) {
     Tile<R, NREC> t;
+    if (ncls > 0) {
+        t.pos = nullptr;
+        t.rec = reinterpret_cast<V4<R>*>(smem);
+        t.slots = reinterpret_cast<uint16_t*>(t.rec + (size_t)S * NREC);
+        t.cls = reinterpret_cast<float4*>(reinterpret_cast<unsigned char*>(t.slots) +
+                                          align16((size_t)slmax * sizeof(uint16_t)));
+        return t;
+    }
     t.pos = reinterpret_cast<V4<R>*>(smem);
     t.rec = t.pos + S;
     t.slots = reinterpret_cast<uint16_t*>(t.rec + (size_t)S * NREC);
+    t.cls = nullptr;
     return t;
 }
 
@@ -732,17 +870,20 @@ __device__ __forceinline__ void stage_tile(const tl_body& b, const Tile<R, NREC>
     const int H = (int)(b.hoff[tile + 1] - hb);
     if (threadIdx.x == 0) {
         const int64_t nmem = min((int64_t)T, b.n - p0);
-        const int64_t r0 = b.toff[tile];
-        const uint32_t pos_bytes = (uint32_t)((b.toff[tile + 1] - r0) * sizeof(V4<R>));
+        const int64_t r0 = t.pos ? b.toff[tile] : 0;
+        const uint32_t pos_bytes =
+            t.pos ? (uint32_t)((b.toff[tile + 1] - r0) * sizeof(V4<R>)) : 0u;
         const uint32_t mem_bytes = (uint32_t)(nmem * NREC * sizeof(V4<R>));
         const int64_t w0 = p0 >> 5, w1 = min(w0 + T / 32, (b.n + 31) >> 5);
         const uint32_t sl_bytes =
             b.slmax > 0 ? (uint32_t)((b.soff[w1] - b.soff[w0]) * sizeof(uint16_t)) : 0u;
+        const uint32_t cls_bytes = t.cls ? (uint32_t)(b.ncls * 2 * sizeof(float4)) : 0u;
         tl::mbar_init(bar, 1);
-        tl::mbar_expect_tx(bar, pos_bytes + mem_bytes + sl_bytes);
-        tl::bulk_g2s(t.pos, static_cast<const V4<R>*>(tpos) + r0, pos_bytes, bar);
+        tl::mbar_expect_tx(bar, pos_bytes + mem_bytes + sl_bytes + cls_bytes);
+        if (pos_bytes) tl::bulk_g2s(t.pos, static_cast<const V4<R>*>(tpos) + r0, pos_bytes, bar);
         tl::bulk_g2s(t.rec, src + p0 * 4 * NREC, mem_bytes, bar);
         if (sl_bytes) tl::bulk_g2s(t.slots, b.slots + b.soff[w0], sl_bytes, bar);
+        if (cls_bytes) tl::bulk_g2s(t.cls, b.bcls, cls_bytes, bar);
     }
     constexpr int CH = (int)(sizeof(V4<R>) / 16);   // 16-byte chunks per record
     for (int s = threadIdx.x; s < H; s += blockDim.x) {
@@ -824,7 +965,7 @@ __global__ void __launch_bounds__(kThreads, TL_MINB_A(R, TILED)) k_pass_a(const 
     __shared__ uint64_t bar;
     if (TILED) {
         if (threadIdx.x == 32) prefetch_own_a<R, MODEL, FRAC>(b, p0);
-        tl_ = tile_layout<R, 1>(smem, b.tile + b.hmax);
+        tl_ = tile_layout<R, 1>(smem, b.tile + b.hmax, b.slmax, sizeof(R) == 4 ? b.ncls : 0);
         stage_tile<R, 1>(b, tl_, tb, b.tpos_a, us, &bar);
     }
     const int ms = (int)threadIdx.x;   // member slot
@@ -843,7 +984,25 @@ __global__ void __launch_bounds__(kThreads, TL_MINB_A(R, TILED)) k_pass_a(const 
 #pragma unroll
         for (int q = 0; q < 9; ++q) D[q] = R(0);
         R M[6] = {R(0), R(0), R(0), R(0), R(0), R(0)};   // xx yy zz xy xz yz
-        if (TILED) {
+        if (TILED && sizeof(R) == 4 && tl_.cls != nullptr) {
+          if constexpr (sizeof(R) == 4) {
+            // bond classes: geometry from the class table, no positions
+            const uint32_t rec_sh = tl::smem_u32(tl_.rec), cls_sh = tl::smem_u32(tl_.cls);
+            const uint32_t sl_sh = tl::smem_u32(tl_.slots + (base - b.soff[p0 >> 5]) + lane * G);
+            const uint16_t* slg = b.slots + base + lane * G;
+            const int lenr = b.wlen ? (int)b.wlen[w] : len;
+            const float4& uif = reinterpret_cast<const float4&>(ui);
+            float* Df = reinterpret_cast<float*>(D);
+            float* Mf = reinterpret_cast<float*>(M);
+            if constexpr (DIM == 3) {
+                if (b.slmax > 0) loop_a_geo_f2<FRAC, true>(rec_sh, cls_sh, sl_sh, slg, lenr, uif, Df, Mf);
+                else loop_a_geo_f2<FRAC, false>(rec_sh, cls_sh, sl_sh, slg, lenr, uif, Df, Mf);
+            } else {
+                if (b.slmax > 0) loop_a_geo_2d<FRAC, true>(rec_sh, cls_sh, sl_sh, slg, lenr, uif, Df, Mf);
+                else loop_a_geo_2d<FRAC, false>(rec_sh, cls_sh, sl_sh, slg, lenr, uif, Df, Mf);
+            }
+          }
+        } else if (TILED) {
             const V4<R> me = tl_.pos[ms];
             const uint32_t pos_sh = tl::smem_u32(tl_.pos), rec_sh = tl::smem_u32(tl_.rec);
             const uint32_t sl_sh = tl::smem_u32(tl_.slots + (base - b.soff[p0 >> 5]) + lane * G);
@@ -937,7 +1096,15 @@ __global__ void __launch_bounds__(kThreads, TL_MINB_A(R, TILED)) k_pass_a(const 
             for (int q = 0; q < 6; ++q) Cpd[q] = double(planeR<R>(b.Cpd, N, q, i));
             double epb = double(static_cast<const R*>(b.epbar)[i]);
             bad = j2_update(Fd, Cpd, epb, b.mu, b.kappa, b.sigma_y0, b.H_hard, Sd, psid, dwp, nonspd);
-            if (nonspd) atomicMin((long long*)&b.counters[2], (long long)(b.perm ? b.perm[i] : i));
+            if (nonspd) {
+                // the reference raises here (constitutive.py:191-194): no stress,
+                // no plastic update for this particle; pass B will not run
+#pragma unroll
+                for (int q = 0; q < 9; ++q) Sd[q] = 0.0;
+                psid = dwp = 0.0;
+                atomicMin((long long*)&b.counters[2], (long long)(b.perm ? b.perm[i] : i));
+                flag_step_error(b.clock, 1);
+            }
 #pragma unroll
             for (int q = 0; q < 6; ++q) static_cast<R*>(b.Cpd)[q * N + i] = R(Cpd[q]);
             static_cast<R*>(b.epbar)[i] = R(epb);
@@ -1015,7 +1182,10 @@ __global__ void __launch_bounds__(kThreads, TL_MINB_A(R, TILED)) k_pass_a(const 
         }
         if (bad || noconv) {
             if (bad) atomicAdd((unsigned long long*)&b.counters[0], (unsigned long long)bad);
-            if (noconv) atomicAdd((unsigned long long*)&b.counters[1], 1ull);
+            if (noconv) {
+                atomicAdd((unsigned long long*)&b.counters[1], 1ull);
+                flag_step_error(b.clock, 1);
+            }
         }
     }
     if (MODEL == 3) {
@@ -1053,16 +1223,20 @@ struct BcCtx {
     const tl_bc* bcs;
     const tl_prog* progs;
     int64_t* counters;
+    tl_clock* clock;
     double dp_body;
     int nbc, dim, restrict_prog;
 };
 
 __device__ __forceinline__ BcCtx bc_ctx(const tl_body& b) {
-    return BcCtx{b.bcs, b.progs, b.counters, b.dp_body, b.nbc, b.dim, b.restrict_prog};
+    return BcCtx{b.bcs, b.progs, b.counters, b.clock, b.dp_body, b.nbc, b.dim, b.restrict_prog};
 }
 
 __device__ __forceinline__ void note_err(const BcCtx& b, int err) {
-    if (err) atomicCAS((unsigned long long*)&b.counters[4], 0ull, (unsigned long long)err);
+    if (err) {
+        atomicCAS((unsigned long long*)&b.counters[4], 0ull, (unsigned long long)err);
+        flag_step_error(b.clock, 2);
+    }
 }
 
 __device__ __forceinline__ bool bc_applies(const tl_bc& c, uint32_t mask, double t) {
@@ -1136,7 +1310,10 @@ __device__ __noinline__ double restrict_floor(const BcCtx b, D3 X0, D3 u, double
     const double val = tl::expr_eval(b.progs[b.restrict_prog], V, &skip, &err);
     note_err(b, err);
     if (skip) return -1.0;
-    if (val < 0.0 || val > 1.0) atomicExch((unsigned long long*)&b.counters[5], 1ull);
+    if (val < 0.0 || val > 1.0) {
+        atomicExch((unsigned long long*)&b.counters[5], 1ull);
+        flag_step_error(b.clock, 2);
+    }
     return val;
 }
 
@@ -1209,6 +1386,7 @@ __device__ __forceinline__ EpiOut epi_body(const tl_body& b, int64_t i, uint32_t
     if (!(isfinite(acc[0]) && isfinite(acc[1]) && isfinite(acc[2]))) {
         o.bad = (long long)(b.perm ? b.perm[i] : i);
         if (b.clock) atomicMin((long long*)&b.counters[6], (long long)b.clock->step);
+        flag_step_error(b.clock, 2);
     }
     // velocity: v_i is the copy pass A put in the record
     D3 vel{double(vi0), double(vi1), double(vi2)};
@@ -1252,8 +1430,10 @@ __device__ __forceinline__ EpiOut epi_body(const tl_body& b, int64_t i, uint32_t
     }
     if (MODE != TL_B_INIT && b.clock &&
         !(isfinite(vel.x) && isfinite(vel.y) && isfinite(vel.z) && isfinite(double(us_new[0])) &&
-          isfinite(double(us_new[1])) && isfinite(double(us_new[2]))))
+          isfinite(double(us_new[1])) && isfinite(double(us_new[2])))) {
         atomicMin((long long*)&b.counters[7], (long long)b.clock->step + 1);
+        b.clock->nf_now = 1;
+    }
     const double vx = double(R(vel.x)), vy = double(R(vel.y)), vz = double(R(vel.z));
     const double ax = double(R(acc[0])), ay = double(R(acc[1])), az = double(R(acc[2]));
     o.v2 = sq3_rn(vx, vy, vz);
@@ -1300,7 +1480,7 @@ __global__ void __launch_bounds__(b_threads<SPLIT>(), b_minb<R, SPLIT>())
     const int T = SPLIT > 1 ? b.tile : (int)blockDim.x;
     const int64_t tb = tile_of(b, TILED);
     const int64_t p0 = tb * (int64_t)T;
-    if (halted(b)) return;
+    if (halted(b) || stress_failed(b)) return;
     double v2 = 0.0, a2 = 0.0;
     long long bad_acc = LLONG_MAX;
     const R* rbp = static_cast<const R*>(b.rb);
@@ -1309,7 +1489,8 @@ __global__ void __launch_bounds__(b_threads<SPLIT>(), b_minb<R, SPLIT>())
     __shared__ uint64_t bar;
     if (TILED) {
         if (threadIdx.x == 32) prefetch_own_b<R, FRAC>(b, p0);
-        tl_ = tile_layout<R, 3>(smem, b.tile + b.hmax);
+        tl_ = tile_layout<R, 3>(smem, b.tile + b.hmax, b.slmax,
+                                (sizeof(R) == 4 && SPLIT == 1) ? b.ncls : 0);
         stage_tile<R, 3>(b, tl_, tb, b.tpos_b, rbp, &bar);
     }
     const int ms = SPLIT > 1 ? (int)threadIdx.x % T : (int)threadIdx.x;   // member slot
@@ -1333,7 +1514,27 @@ __global__ void __launch_bounds__(b_threads<SPLIT>(), b_minb<R, SPLIT>())
         const R B1 = R(b.beta1 * b.c0 * b.h), B2 = R(b.beta2 * b.h * b.h);
         const R inv_rho = R(1.0 / b.rho0);
         R s1[3] = {R(0), R(0), R(0)}, s2[3] = {R(0), R(0), R(0)}, s3[3] = {R(0), R(0), R(0)};
-        if (TILED) {
+        if (TILED && sizeof(R) == 4 && SPLIT == 1 && tl_.cls != nullptr) {
+          if constexpr (sizeof(R) == 4 && SPLIT == 1) {
+            // bond classes: geometry from the class table, no positions
+            const uint32_t rec_sh = tl::smem_u32(tl_.rec), cls_sh = tl::smem_u32(tl_.cls);
+            const uint32_t sl_sh = tl::smem_u32(tl_.slots + (base - b.soff[p0 >> 5]) + lane * G);
+            const uint16_t* slg = b.slots + base + lane * G;
+            const int lenr = b.wlen ? (int)b.wlen[w] : len;
+            float* f1 = reinterpret_cast<float*>(s1);
+            float* f2 = reinterpret_cast<float*>(s2);
+            float* f3 = reinterpret_cast<float*>(s3);
+            const float v0 = float(vi0), v1 = float(vi1), v2f = float(vi2);
+            const float fB2 = float(B2), fB1 = float(B1);
+#define TL_LOOP_G(ST, V) loop_b_geo<DIM, ST, V>(rec_sh, cls_sh, sl_sh, slg, lenr, v0, v1, v2f, fB2, fB1, f1, f2, f3)
+            if (b.slmax > 0) {
+                if (visc) TL_LOOP_G(true, true); else TL_LOOP_G(true, false);
+            } else {
+                if (visc) TL_LOOP_G(false, true); else TL_LOOP_G(false, false);
+            }
+#undef TL_LOOP_G
+          }
+        } else if (TILED) {
             const V4<R> me = tl_.pos[ms];
             const uint32_t pos_sh = tl::smem_u32(tl_.pos), rec_sh = tl::smem_u32(tl_.rec);
             uint32_t sl_sh = tl::smem_u32(tl_.slots + (base - b.soff[p0 >> 5]) + lane * G);
@@ -1510,6 +1711,11 @@ struct DtInfos {
 
 __global__ void k_clock_begin(tl_clock* c, DtInfos info) {
     if (c->halted) return;
+    if (c->err) {          // the previous step raised: nothing more runs
+        c->halted = 5;
+        return;
+    }
+    c->nf_now = 0;
     if (!(c->t < c->t_max - c->eps)) {
         c->halted = 1;
         return;
@@ -1541,10 +1747,12 @@ __global__ void k_clock_begin(tl_clock* c, DtInfos info) {
 }
 
 __global__ void k_clock_commit(tl_clock* c) {
-    if (c->halted) return;
+    if (c->halted || c->err) return;   // a step that raised is not committed
     c->t += c->dt;
     c->step += 1;
-    if (c->t >= c->next_out - c->eps) c->halted = 2;
+    // stepper.py:203-209: the state check of every 64th commit
+    if (c->step % 64 == 0 && c->nf_now) c->halted = 6;
+    else if (c->t >= c->next_out - c->eps) c->halted = 2;
     else if (c->max_steps >= 0 && c->step >= c->max_steps) c->halted = 3;
 }
 
@@ -1579,9 +1787,13 @@ int smem_opt_in(K kernel, size_t bytes) {
 template <typename R, int DIM, int MODEL, bool FRAC, int KIND>
 int launch_a_one(cudaStream_t st, const tl_body& b) {
     constexpr int G = TL_GATHER_A;
+    if (b.tile > kThreads || (b.tile > 0 && b.tile % 32)) {
+        tl_set_error("tile %d: pass A needs a multiple of 32, at most %d", b.tile, kThreads);
+        return TL_ERR_ARG;
+    }
     if (b.tile > 0) {
         auto kern = k_pass_a<R, DIM, MODEL, FRAC, KIND, G, true>;
-        const size_t bytes = tile_bytes<R, 1>(b.tile + b.hmax, b.slmax);
+        const size_t bytes = tile_bytes<R, 1>(b.tile + b.hmax, b.slmax, sizeof(R) == 4 ? b.ncls : 0);
         int rc = smem_opt_in(kern, bytes);
         if (rc) return rc;
         kern<<<b.tlist ? (unsigned)b.tcount : tl_blocks(b.n, b.tile), b.tile, bytes, st>>>(b);
@@ -1615,6 +1827,10 @@ int launch_b_one(cudaStream_t st, const tl_body& b) {
                 tl_set_error("bsplit %d needs tile <= %d", SP, 1024 / SP);
                 return TL_ERR_ARG;
             }
+            if (b.ncls > 0) {
+                tl_set_error("bsplit 4 with bond classes (slot entries carry a class)");
+                return TL_ERR_ARG;
+            }
             auto kern = k_pass_b<R, DIM, MODE, FRAC, KIND, G, true, SP>;
             const size_t bytes = split_off<R, 3>(b.tile + b.hmax, b.slmax) +
                                  (size_t)(SP - 1) * 9 * b.tile * sizeof(R);
@@ -1628,9 +1844,13 @@ int launch_b_one(cudaStream_t st, const tl_body& b) {
         tl_set_error("bsplit: tiled FP32 3D pass B only (bsplit 4)");
         return TL_ERR_ARG;
     }
+    if (b.tile > kThreads || (b.tile > 0 && b.tile % 32)) {
+        tl_set_error("tile %d: pass B needs a multiple of 32, at most %d", b.tile, kThreads);
+        return TL_ERR_ARG;
+    }
     if (b.tile > 0) {
         auto kern = k_pass_b<R, DIM, MODE, FRAC, KIND, G, true>;
-        const size_t bytes = tile_bytes<R, 3>(b.tile + b.hmax, b.slmax);
+        const size_t bytes = tile_bytes<R, 3>(b.tile + b.hmax, b.slmax, sizeof(R) == 4 ? b.ncls : 0);
         int rc = smem_opt_in(kern, bytes);
         if (rc) return rc;
         kern<<<b.tlist ? (unsigned)b.tcount : tl_blocks(b.n, b.tile), b.tile, bytes, st>>>(b);

@@ -100,12 +100,37 @@ __global__ void k_halo_scatter(int64_t m, const uint64_t* __restrict__ keys,
     atomicAdd((unsigned long long*)&tile_count[keys[k] >> 32], 1ull);
 }
 
+// Lattice offset class of a pair (bond): the reference separation r0 =
+// X_i - X_j as an integer multiple q of the body's spacing dp, encoded as
+// key = ((qx+R)(2R+1) + qy+R)(2R+1) + qz+R.  TL_KEY_SELF marks the padding
+// entries (j == i), TL_KEY_OFF a pair off the lattice (|r0 - q dp| > 1e-6 dp
+// or |q| > R): such a body keeps the position path.
+#define TL_KEY_SELF 0xffff
+#define TL_KEY_OFF 0xfffe
+constexpr int kKeyR = 7;
+
+__device__ __forceinline__ uint16_t lattice_key(const double* __restrict__ X, int64_t n_all,
+                                                int64_t p, int64_t q, double dp, double inv_dp) {
+    int k = 0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double d = X[a * n_all + p] - X[a * n_all + q];
+        const double c = rint(d * inv_dp);
+        if (fabs(d - c * dp) > 1e-6 * dp || fabs(c) > kKeyR) return TL_KEY_OFF;
+        k = k * (2 * kKeyR + 1) + (int)c + kKeyR;
+    }
+    return (uint16_t)k;
+}
+
 // local slot of every pair, in the group-interleaved sliced layout:
-// slot(w, k, lane) at soff[w] + (k/G)*32*G + lane*G + k%G; padding = own slot
+// slot(w, k, lane) at soff[w] + (k/G)*32*G + lane*G + k%G; padding = own slot.
+// keys (optional): the pair's lattice offset class key in the same layout.
 __global__ void k_slots(int64_t n, int T, int G, int shift, const int64_t* __restrict__ indptr,
                         const int32_t* __restrict__ indices, const int64_t* __restrict__ hoff,
                         const int32_t* __restrict__ halo, const uint16_t* __restrict__ hslot,
-                        const int64_t* __restrict__ soff, uint16_t* __restrict__ slots) {
+                        const int64_t* __restrict__ soff, uint16_t* __restrict__ slots,
+                        const double* __restrict__ X, int64_t n_all, double dp,
+                        uint16_t* __restrict__ keys) {
     int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t nw = (n + 31) / 32;
     const int64_t w = p >> 5;
@@ -121,8 +146,10 @@ __global__ void k_slots(int64_t n, int T, int G, int shift, const int64_t* __res
     const int32_t* hs = halo + (p < n ? hoff[tile] : 0);
     const uint16_t* hsl = hslot + (p < n ? hoff[tile] : 0);
     const int64_t hn = p < n ? hoff[tile + 1] - hoff[tile] : 0;
+    const double inv_dp = keys ? 1.0 / dp : 0.0;
     for (int64_t k = 0; k < len; ++k) {
         uint16_t s = self;
+        uint16_t key = TL_KEY_SELF;
         if (k < rl) {
             const int64_t q = indices[rb + k];
             if (q >= t0 && q < t0 + T && q < n) {
@@ -135,9 +162,23 @@ __global__ void k_slots(int64_t n, int T, int G, int shift, const int64_t* __res
                 }
                 s = hsl[lo];
             }
+            if (keys) key = lattice_key(X, n_all, p, q, dp, inv_dp);
         }
-        slots[base + (k / G) * 32 * G + lane * G + (k % G)] = (uint16_t)(s << shift);
+        const int64_t e = base + (k / G) * 32 * G + lane * G + (k % G);
+        slots[e] = (uint16_t)(s << shift);
+        if (keys) keys[e] = key;
     }
+}
+
+// bond-class slot entries: (class << 10) | slot, from the plain slots
+// (slot << shift) and the per-key class table
+__global__ void k_class_slots(int64_t m, int shift, const uint16_t* __restrict__ keys,
+                              const int16_t* __restrict__ cls_of_key, uint16_t* __restrict__ slots) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= m) return;
+    const uint16_t key = keys[e];
+    const int c = key == TL_KEY_SELF ? 0 : cls_of_key[key];
+    slots[e] = (uint16_t)((c << 10) | (slots[e] >> shift));
 }
 
 // Shared-memory slot of every halo entry of every tile.  A quarter-warp's
@@ -371,13 +412,34 @@ extern "C" int tl_tile_slots(tl_stream_t st, int64_t n, int32_t T, int32_t G, in
                              const int64_t* indptr, const int32_t* indices, const int64_t* hoff,
                              const int32_t* halo, const uint16_t* hslot, const int64_t* soff,
                              uint16_t* slots) {
+    return tl_tile_slots_keyed(st, n, T, G, shift, indptr, indices, hoff, halo, hslot, soff, slots,
+                               nullptr, 0, 0.0, nullptr);
+}
+
+extern "C" int tl_tile_slots_keyed(tl_stream_t st, int64_t n, int32_t T, int32_t G, int32_t shift,
+                                   const int64_t* indptr, const int32_t* indices,
+                                   const int64_t* hoff, const int32_t* halo, const uint16_t* hslot,
+                                   const int64_t* soff, uint16_t* slots, const double* X,
+                                   int64_t n_all, double dp, uint16_t* keys) {
     if (n <= 0) return TL_OK;
     if (shift < 0 || shift > 8) {
         tl_set_error("tl_tile_slots: shift out of range");
         return TL_ERR_ARG;
     }
+    if (keys && (!X || !(dp > 0.0))) {
+        tl_set_error("tl_tile_slots_keyed: keys need positions and dp > 0");
+        return TL_ERR_ARG;
+    }
     const int64_t nt = ((n + 31) / 32) * 32;
-    k_slots<<<tl_blocks(nt, kThreads), kThreads, 0, (cudaStream_t)st>>>(n, T, G, shift, indptr, indices,
-                                                                      hoff, halo, hslot, soff, slots);
+    k_slots<<<tl_blocks(nt, kThreads), kThreads, 0, (cudaStream_t)st>>>(
+        n, T, G, shift, indptr, indices, hoff, halo, hslot, soff, slots, X, n_all, dp, keys);
     return tl_check_launch("k_slots");
+}
+
+extern "C" int tl_class_slots(tl_stream_t st, int64_t m, int32_t shift, const uint16_t* keys,
+                              const int16_t* cls_of_key, uint16_t* slots) {
+    if (m <= 0) return TL_OK;
+    k_class_slots<<<tl_blocks(m, kThreads), kThreads, 0, (cudaStream_t)st>>>(m, shift, keys,
+                                                                          cls_of_key, slots);
+    return tl_check_launch("k_class_slots");
 }

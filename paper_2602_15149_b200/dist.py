@@ -187,7 +187,7 @@ def allreduce(t, op="max", group=None):
     gloo.  MAX on the int64 bit patterns of non-negative doubles is the exact
     global max of the dt maxima."""
     import torch.distributed as dist
-    rop = {"max": dist.ReduceOp.MAX, "sum": dist.ReduceOp.SUM}[op]
+    rop = {"max": dist.ReduceOp.MAX, "min": dist.ReduceOp.MIN, "sum": dist.ReduceOp.SUM}[op]
     if dist.get_backend(group) == "gloo" and t.is_cuda:
         h = t.cpu()
         dist.all_reduce(h, op=rop, group=group)

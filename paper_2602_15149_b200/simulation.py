@@ -47,10 +47,17 @@ def _torch():
     return torch
 
 
-def _mean_row(dadj):
-    """Mean neighbours per particle of a device adjacency."""
+def _mean_row(dadj, rows=None):
+    """Mean neighbours per particle of a device adjacency, over ``rows``
+    (a rank's owned rows; default all).  A slab's halo-region rows have
+    truncated lists and must not steer the tile choice."""
     n = int(dadj.indptr.shape[0]) - 1
-    return float(dadj.indptr[-1].item()) / max(n, 1)
+    if rows is None:
+        return float(dadj.indptr[-1].item()) / max(n, 1)
+    torch = _torch()
+    r = torch.as_tensor(np.asarray(rows, dtype=np.int64), device=dadj.indptr.device)
+    cnt = (dadj.indptr[r + 1] - dadj.indptr[r]).sum()
+    return float(cnt.item()) / max(int(r.shape[0]), 1)
 
 
 class DeviceBody:
@@ -93,7 +100,8 @@ class DeviceBody:
         tile = DEFAULT_TILE[precision]
         if int(body.dim) == 2:
             tile = 128    # 2D stencils: thin 1-deep halos, measured best for pass A (C5)
-        elif precision == "fp32" and _mean_row(dadj) > 64.0:
+        elif precision == "fp32" and _mean_row(
+                dadj, part.owned_rows if part is not None else None) > 64.0:
             # radial 3D stencils: pass A gathers from L2 and pass B runs one CTA
             # per SM with split rows; the widest tile has the thinnest halo per
             # member (pass B, C2: 1.38 -> 1.17 ms, C3: 5.78 -> 4.76 ms)
@@ -346,6 +354,24 @@ class DeviceBody:
             cpd = np.stack([Cp[:, 0, 0] - 1.0, Cp[:, 1, 1] - 1.0, Cp[:, 2, 2] - 1.0,
                             Cp[:, 0, 1], Cp[:, 0, 2], Cp[:, 1, 2]])
             self.Cpd.copy_(torch.from_numpy(cpd).to(dev, R))
+        self.refresh_dt_maxima()
+
+    def refresh_dt_maxima(self):
+        """max |v|^2 and max |a|^2 of the owned rows into ``red`` (what pass B
+        leaves there), so pick_dt after a host edit sees the edited state like
+        the reference's (stepper.py:221-233): FP64 squares in numpy's einsum
+        order (x*x + z*z) + y*y of the mode's values; a NaN counts as 0 (pass B
+        reports it through the error counters).  Not collective: the slab path
+        all-reduces ``red`` in the next pass B."""
+        torch = _torch()
+        n = self.n
+        out = []
+        for pl in (self.v, self.a):
+            d = pl[:, :n].double()
+            sq = (d[0] * d[0] + d[2] * d[2]) + d[1] * d[1]
+            sq = torch.where(torch.isnan(sq), torch.zeros_like(sq), sq)
+            out.append(sq.max() if n else torch.zeros((), dtype=torch.float64, device=self.dev))
+        self.red.copy_(torch.stack(out).view(torch.int64))
 
     def pull_state(self, full=True):
         """Refresh body.state (host, original order) from the device."""
@@ -473,7 +499,10 @@ class DeviceSimulation:
     """Drop-in for solidsph.stepper.Simulation running on one B200."""
 
     def __init__(self, config, trace=None, precision="fp64", stream=None, mirrors=True,
-                 group=None):
+                 group=None, partition=None):
+        """partition: run the slab path (halo exchange, collectives) -- by
+        default whenever a process group of more than one rank is initialised;
+        True also with one rank (exercises the exchange plumbing)."""
         if precision not in ("fp32", "fp64"):
             raise ValueError("precision must be 'fp32' or 'fp64'")
         L = _lib.lib()  # fails loudly without the native library / GPU
@@ -495,9 +524,12 @@ class DeviceSimulation:
         import torch.distributed as tdist
         if tdist.is_available() and tdist.is_initialized():
             self.world = tdist.get_world_size(group)
-        if len(self.bodies) > 1 and self.world > 1:
+        self.partitioned = self.world > 1 if partition is None else bool(partition)
+        if self.partitioned and not (tdist.is_available() and tdist.is_initialized()):
+            raise ValueError("partition=True needs an initialised torch.distributed group")
+        if len(self.bodies) > 1 and self.partitioned:
             raise NotImplementedError("multi-body (contact) cases run on one GPU")
-        parts = [self._partition(b) if self.world > 1 else None for b in self.bodies]
+        parts = [self._partition(b) if self.partitioned else None for b in self.bodies]
         self.programs = ProgramTable()
         self.dbodies = [DeviceBody(b, config, precision, self.programs, mirrors, part)
                         for b, part in zip(self.bodies, parts)]
@@ -728,8 +760,12 @@ class DeviceSimulation:
             for db in self.dbodies:
                 self._pass_b(db, 2)
 
-    def _check_errors(self):
+    def _check_errors(self, clock=None):
         """Raise the reference's exceptions for events recorded on the device.
+
+        In-step errors first (stress, acceleration, expressions, restrictphi:
+        the reference raises them inside the step, before the commit), then
+        the non-finite state check of a 64-step commit (clock.halted == 6).
         Multi-GPU: every rank raises when any rank recorded an event."""
         if self.contact_counters is not None:
             cc = self.contact_counters.cpu().numpy()
@@ -737,17 +773,19 @@ class DeviceSimulation:
             if cc[1]:
                 raise SimulationError(f"contact: {int(cc[1])} candidate pairs over the per-particle "
                                       f"capacity (TL_CONTACT_CAP)")
-        if self.world > 1:
+        nf_halt = clock is not None and int(clock.halted) == 6
+        if self.partitioned:
             flag = _torch().zeros(1, dtype=_torch().int64, device="cuda")
             for db in self.dbodies:
                 c = db.counters
                 flag |= ((c[1] != 0) | (c[4] != 0) | (c[5] != 0) | (c[2] != INT64_MAX)
                          | (c[3] != INT64_MAX)).to(flag.dtype).reshape(1)
+            flag |= int(nf_halt)
             dist.allreduce(flag, "max", self.group)
             if int(flag.item()):
-                local = any(int(db.counters[k]) != v for db in self.dbodies
-                            for k, v in ((1, 0), (4, 0), (5, 0), (2, INT64_MAX),
-                                         (3, INT64_MAX)))
+                local = nf_halt or any(int(db.counters[k]) != v for db in self.dbodies
+                                       for k, v in ((1, 0), (4, 0), (5, 0), (2, INT64_MAX),
+                                                    (3, INT64_MAX)))
                 if not local:
                     raise SimulationError("numerical error reported by another rank")
         for db in self.dbodies:
@@ -774,12 +812,16 @@ class DeviceSimulation:
                 db._reset_counters()
                 raise SimulationError(f"non-finite acceleration at particle {int(c[3])} "
                                       f"(body {mk}, step {step})")
-            if c[7] != INT64_MAX:
-                first = int(c[7])
-                check_at = ((first + 63) // 64) * 64
-                if self.step_index >= check_at:
-                    db._reset_counters()
-                    raise SimulationError(f"non-finite state in body {mk} at step {check_at}")
+        if nf_halt:
+            self._raise_nonfinite_state(int(clock.step))
+
+    def _raise_nonfinite_state(self, step):
+        """stepper.py:203-209: the first body whose u or v is non-finite."""
+        for db in self.dbodies:
+            if int(db.counters[7].item()) != INT64_MAX:
+                db._reset_counters()
+                raise SimulationError(f"non-finite state in body {db.body.mk} at step {step}")
+        raise SimulationError(f"non-finite state at step {step} (another rank)")
 
     def sync_host(self, full=True):
         """Mark the host mirrors stale: the next read of a body.state field
@@ -788,7 +830,7 @@ class DeviceSimulation:
         for db in self.dbodies:
             db.dirty = True
             pw = db.pw_acc.clone()
-            if self.world > 1:
+            if self.partitioned:
                 dist.allreduce(pw, "sum", self.group)
             db.body.plastic_work = db.pw_base + float(pw.item())
 
@@ -826,11 +868,14 @@ class DeviceSimulation:
         self._check_errors()
 
     def step(self, dt):
-        """One Verlet or symplectic step of size dt (stepper.py:211-217)."""
+        """One Verlet or symplectic step of size dt (stepper.py:211-217).
+        An error the reference raises inside the step leaves t and
+        step_index uncommitted, as there."""
         if not self._initialized:
             self.initialize()
         verlet = int(self.config.step_algorithm) != 2
-        self._set_clock(t=self.t, dt=float(dt), out_step=int(self.mirrors))
+        self._set_clock(t=self.t, dt=float(dt), out_step=int(self.mirrors),
+                        step=self.step_index)
         if verlet:
             for ph in ("contact", "internal", "bc", "update", "commit"):
                 self._mark(ph)
@@ -838,10 +883,20 @@ class DeviceSimulation:
             for ph in ("predictor", "contact", "internal", "bc", "update", "commit"):
                 self._mark(ph)
         self._launch_step(verlet)
+        self.sync_host()
+        c = self._get_clock()
+        self._check_errors()
         self.t += dt
         self.step_index += 1
-        self.sync_host()
-        self._check_errors()
+        # stepper.py:203-209: every 64th commit checks the state
+        if self.step_index % 64 == 0:
+            nf = int(c.nf_now)
+            if self.partitioned:
+                f = _torch().tensor([nf], dtype=_torch().int64, device="cuda")
+                dist.allreduce(f, "max", self.group)
+                nf = int(f.item())
+            if nf:
+                self._raise_nonfinite_state(self.step_index)
 
     def pick_dt(self):
         """Adaptive dt from the device maxima, bit-identical to the
@@ -901,7 +956,7 @@ class DeviceSimulation:
         c = self._get_clock()
         self.t = float(c.t)
         self.step_index = int(c.step)
-        self._check_errors()
+        self._check_errors(c)
         if c.halted == 4:
             raise SimulationError(f"timestep collapsed to {c.dt!r}")
 
@@ -935,6 +990,8 @@ class DeviceSimulation:
                            "commit")
                 k += 1
             c = self._get_clock()
+            for db in self.dbodies:
+                db.dirty = True           # host mirrors refresh on read (also after a raise)
             steps_done = int(c.step) - self.step_index
             if self.trace is not None:
                 seq = ("contact", "internal", "bc", "update", "commit") if verlet else \
@@ -942,7 +999,7 @@ class DeviceSimulation:
                 self.trace.extend(seq * steps_done)
             self.t = float(c.t)
             self.step_index = int(c.step)
-            self._check_errors()
+            self._check_errors(c)
             if c.halted == 4:
                 raise SimulationError(f"timestep collapsed to {c.dt!r}")
             if c.halted == 2:

@@ -50,7 +50,8 @@ def _worker(rank, world, port, tag, precision, out_dir):
     idx = np.arange(0, st.X.shape[0], 5)
     mrow = np.array(output.measure_row(cfg.bodies[0], idx, sim.t)[1:7])  # collective
     np.savez(os.path.join(out_dir, f"r{rank}.npz"), gid=g, u=st.u[g], v=st.v[g], s=st.s[g],
-             S=st.S[g], n_halo=db.n_all - db.n, dt=dt_next, energies=energies, mrow=mrow)
+             S=st.S[g], n_halo=db.n_all - db.n, dt=dt_next, energies=energies, mrow=mrow,
+             bsplit=db.bsplit, tile=db.layout.tile)
     dist.barrier()
     dist.destroy_process_group()
 
@@ -114,3 +115,54 @@ def test_multi_rank_split_rows(tmp_path, monkeypatch):
     assert sim.dbodies[0].bsplit == 4
     del sim
     test_multi_rank_device_bit_identical("taylor3d", 2, "fp32", tmp_path)
+    for r in range(2):   # every slab ran the split kernel, not a bsplit=1 fallback
+        d = np.load(tmp_path / f"r{r}.npz")
+        assert int(d["bsplit"]) == 4, (r, int(d["bsplit"]), int(d["tile"]))
+
+
+def _nccl_worker(rank, port, out_dir):
+    import sys
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    from paper_2602_15149_b200 import dist as D
+    from paper_2602_15149_b200.simulation import DeviceSimulation
+    # the collectives of the step on NCCL: MAX on FP64 bit patterns, MIN, SUM
+    t = torch.tensor([3, -7, 11], dtype=torch.int64, device="cuda")
+    red = [D.allreduce(t.clone(), op).cpu().numpy() for op in ("max", "min", "sum")]
+    G = golden("run_kalthoff3d")
+    cfg = run_case(G)
+    sim = DeviceSimulation(cfg, precision="fp64", partition=True)
+    assert sim.partitioned and sim.dbodies[0].exchange is not None
+    sim.initialize()
+    for k in range(NSTEPS):
+        sim.step(G["dts"][k])
+    st = cfg.bodies[0].state
+    np.savez(os.path.join(out_dir, "nccl.npz"), u=st.u, v=st.v, s=st.s, S=st.S,
+             red=np.stack(red), backend=dist.get_backend())
+    dist.destroy_process_group()
+
+
+def test_nccl_world1_slab_path(tmp_path):
+    """The NCCL branch of the slab path on a one-rank NCCL group: the halo
+    plan's all_to_all, the (empty) exchanges and the all-reduces run through
+    NCCL, and the state is bit-identical to the unpartitioned run."""
+    mp.spawn(_nccl_worker, args=(_port(), str(tmp_path)), nprocs=1, join=True)
+    d = np.load(tmp_path / "nccl.npz")
+    assert str(d["backend"]) == "nccl"
+    assert d["red"].tolist() == [[3, -7, 11]] * 3
+    from paper_2602_15149_b200.simulation import DeviceSimulation
+    G = golden("run_kalthoff3d")
+    cfg = run_case(G)
+    sim = DeviceSimulation(cfg, precision="fp64")
+    sim.initialize()
+    for k in range(NSTEPS):
+        sim.step(G["dts"][k])
+    st = cfg.bodies[0].state
+    for k in ("u", "v", "s", "S"):
+        assert np.array_equal(d[k], getattr(st, k)), k

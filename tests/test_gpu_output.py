@@ -155,3 +155,64 @@ def test_fp32_drift_after_n_steps(tag):
         assert errs[k] <= tol, (k, errs[k])
     if "s_abs" in errs:
         assert errs["s_abs"] <= 1e-4
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_branch2d_crack_branching_matches_reference(precision):
+    """Dynamic crack branching (branch2d at the reference's acceptance scale 4,
+    test_acceptance.py:149-159) with the reference's own benchmark semantics
+    (bench.py:194-235): initiation time of damage at the notch tip, the
+    branched flag (damage above and below the notch plane downstream), FE
+    monotone after initiation and SE decreasing -- on the device run through
+    run() with the device output reductions, against the reference's run."""
+    from paper_2602_15149_b200 import output
+    from paper_2602_15149_b200.simulation import DeviceSimulation
+    G = golden("branch_branch2d")
+    cfg = run_case(G)
+    body = cfg.bodies[0]
+    st = body.state
+    sim = DeviceSimulation(cfg, precision=precision)
+    st = body.state            # the device-backed state (DeviceState) from here on
+    quad = np.asarray(body.notches[0].points)
+    i = int(np.argmax(quad[:, 0]))
+    tip = np.array([quad[i, 0], 0.0, quad[i, 2]])
+    near_tip = np.flatnonzero(np.sqrt((st.X[:, 0] - tip[0]) ** 2 + (st.X[:, 2] - tip[2]) ** 2)
+                              <= 2.0 * body.dp_body)
+    ser = {"t": [], "se": [], "fe": [], "t_init": None}
+
+    def sampler(s):
+        se, ke, fe, pe = output.compute_energies(body, s.be)
+        ser["t"].append(s.t)
+        ser["se"].append(se)
+        ser["fe"].append(fe)
+        if ser["t_init"] is None and np.any(st.s[near_tip] < 0.5):
+            ser["t_init"] = s.t
+
+    sim.run(on_output=sampler)
+    ref_t = G["series.t"]
+    assert len(ser["t"]) == len(ref_t)
+    assert np.allclose(ser["t"], ref_t, rtol=1e-12, atol=0)
+    t_init = ser["t_init"]
+    ref_init = float(G["metric.initiation_time_s"][0])
+    assert t_init is not None
+    dt_out = float(ref_t[1] - ref_t[0])
+    assert abs(t_init - ref_init) <= 1.01 * dt_out, (t_init, ref_init)
+    z_n, eps0 = tip[2], body.material.eps0
+    damaged = st.s < 0.5
+    downstream = damaged & (st.X[:, 0] > tip[0] + 4.0 * body.dp_body)
+    branched = bool(np.any(downstream & (st.X[:, 2] > z_n + 3.0 * eps0))
+                    and np.any(downstream & (st.X[:, 2] < z_n - 3.0 * eps0)))
+    assert float(branched) == float(G["metric.branched"][0]) == 1.0
+    fe, se = np.array(ser["fe"]), np.array(ser["se"])
+    i0 = int(np.searchsorted(ser["t"], t_init))
+    fe_post = fe[i0:]
+    assert bool(np.all(np.diff(fe_post) >= -1e-3 * max(fe_post.max(), 1e-300)))
+    assert bool(se[-1] < se[i0:].max())
+    # the damaged sets themselves: Jaccard index against the reference's
+    ref_dmg = G["final_s"] < 0.5
+    jac = np.count_nonzero(damaged & ref_dmg) / max(np.count_nonzero(damaged | ref_dmg), 1)
+    print(precision, f"t_init {t_init:.3g} (ref {ref_init:.3g}), damaged "
+          f"{np.count_nonzero(damaged)} (ref {np.count_nonzero(ref_dmg)}), Jaccard {jac:.3f}, "
+          f"FE end {fe[-1]:.4g} (ref {G['series.fe'][-1]:.4g})")
+    assert jac >= 0.8, jac
+    assert abs(fe[-1] - G["series.fe"][-1]) <= 0.05 * abs(G["series.fe"][-1])
