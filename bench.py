@@ -420,6 +420,7 @@ def main():
                                            f"{args.dist_backend})" if world > 1 else "single"),
                            "l2": "per-step working set >> 126 MB L2, no flush",
                            "precision": args.precision,
+                           "bond_classes": [int(db.desc.ncls) for db in sim.dbodies],
                            "setup_s": {"case": t_case, "device_build": t_setup}},
                 "roofline": roofline, "passes": passes, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(args.steps * (2 + 2 * len(sim.dbodies))),

@@ -313,6 +313,79 @@ class StepLayout:
         self.tile = T
 
 
+    KEY_R = 7              # tiles.cu kKeyR: lattice offsets |q| <= 7 per axis
+    KEY_SELF, KEY_OFF = 0xFFFF, 0xFFFE
+    MAX_CLASSES = 63       # 6 class bits above the 10 slot bits of a uint16 entry
+
+    def bond_classes(self, Xs, dp, h, kind):
+        """Bond-class slot table for lattice bodies (FP32, uniform V0 and m0).
+
+        Every pair of a body cut from one lattice of spacing dp has a
+        reference separation r0 = X_i - X_j = q dp with q an integer offset,
+        so the pair geometry (kernel shape, r0, 1/r^2) takes one of a few
+        values -- 26 for a 3D nbsrange = 1 stencil.  The slots are rewritten
+        to (class << 10) | slot (tiles.cu k_class_slots) and the returned
+        (ncls, 8) FP32 table holds, per class, W = w(r) r0, kappa =
+        1/(w(r) (r^2 + 0.001 h^2)) and U = r0 / r^2, evaluated in FP64 with the
+        pair loops' kernel shape (step.cu kshape; kernel_geom.py:21-62 of the
+        reference).  Class 0 is the padding entry (j = i), all zero.  Returns
+        None, leaving the slots unchanged, when some pair is off the lattice
+        (|r0 - q dp| > 1e-6 dp), the tile has more than 1024 slots, or there
+        are more than MAX_CLASSES classes."""
+        import torch
+        if not self.tile or not (dp > 0) or self.tile + self.hmax > 1024:
+            return None
+        L = _lib.lib()
+        st = _lib.stream_ptr()
+        P = _lib.ptr
+        total = int(self.soff[-1].item())
+        if total == 0:
+            return None
+        keys = torch.empty_like(self.slots)
+        _lib.check(L.tl_tile_slots_keyed(st, self.n, self.tile, self.GROUP, self.slot_shift,
+                                         P(self.indptr), P(self.indices), P(self.hoff),
+                                         P(self.halo), P(self.hslot), P(self.soff),
+                                         P(self.slots), P(Xs), self.n_all, float(dp), P(keys)),
+                   "tl_tile_slots_keyed")
+        ku = torch.unique(keys[:total].to(torch.int32) & 0xFFFF).cpu().numpy()
+        if (ku == self.KEY_OFF).any():
+            return None
+        ku = ku[ku != self.KEY_SELF]
+        if ku.size > self.MAX_CLASSES:
+            return None
+        side = 2 * self.KEY_R + 1
+        cls_of_key = np.full(side ** 3, -1, dtype=np.int16)
+        cls_of_key[ku] = np.arange(1, ku.size + 1, dtype=np.int16)
+        q = np.stack([ku // (side * side), (ku // side) % side, ku % side], axis=1) - self.KEY_R
+        r0 = q.astype(np.float64) * float(dp)
+        r2 = np.einsum("ij,ij->i", r0, r0)
+        r = np.sqrt(r2)
+        inv_h = 1.0 / float(h)
+        if int(kind) == 2:     # Wendland C2: t^3, t = max(1 - r/2h, 0)
+            t = np.maximum(1.0 - r * (0.5 * inv_h), 0.0)
+            w = t * t * t
+        else:                  # cubic spline (step.cu kshape, KIND 1)
+            qh = r * inv_h
+            w = np.where(qh < 1.0, (-3.0 + 2.25 * qh) * inv_h,
+                         np.where(qh < 2.0, -0.75 * (2.0 - qh) ** 2 / np.where(r > 0, r, 1.0),
+                                  0.0))
+        table = np.zeros((ku.size + 1, 8), dtype=np.float64)
+        table[1:, 0:3] = w[:, None] * r0
+        den = w * (r2 + 0.001 * float(h) * float(h))
+        table[1:, 3] = np.where(w != 0.0, 1.0 / np.where(w != 0.0, den, 1.0), 0.0)
+        table[1:, 4:7] = r0 / r2[:, None]
+        # a pair a rounding error inside the support edge (r = 2h - 1e-16) has
+        # w ~ 1e-48: W flushes to zero in FP32 while kappa overflows, so its
+        # (negligible) terms are dropped outright rather than turned into 0 * inf
+        tiny = np.abs(table[1:, 3]) > 1e30
+        table[1:][tiny] = 0.0
+        dev = self.slots.device
+        _lib.check(L.tl_class_slots(st, total, self.slot_shift, P(keys),
+                                    P(torch.from_numpy(cls_of_key).to(dev)), P(self.slots)),
+                   "tl_class_slots")
+        torch.cuda.current_stream().synchronize()
+        return torch.from_numpy(table.astype(np.float32)).to(dev).contiguous()
+
     def split_tiles(self):
         """Multi-GPU launch order: (tile list, number of interior tiles).
         Interior tiles read no halo row (device position >= n) and can run

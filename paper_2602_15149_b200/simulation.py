@@ -160,13 +160,6 @@ class DeviceBody:
         self.S_out = f64(n, 3, 3) if mirrors else None
         self.psi_out = f64(n) if mirrors else None
         self.psip_out = f64(n) if mirrors else None
-        # staged tile positions with the pass-A (V0) and pass-B (m0) weights
-        if lay.tile:
-            self.tpos_a = lay.positions(self.Xs, None if self.uniform else self.V0, precision)
-            self.tpos_b = (self.tpos_a if self.uniform
-                           else lay.positions(self.Xs, self.m0, precision))
-        else:
-            self.tpos_a = self.tpos_b = None
         # pass B tiling: with few neighbours per particle (2D stencils) a tile's
         # short compute cannot hide its staging latency, and the L2-gather
         # pass B measured faster on B200 (C5: 1.75 vs 2.45 ms); pass A keeps
@@ -195,6 +188,21 @@ class DeviceBody:
                          <= TILE_SMEM_LIMIT))
         self.bsplit = (4 if split_ok and (int(env_s) == 4 if env_s is not None
                                           else k_mean > 64.0) else 1)
+        # bond classes (FP32 lattice bodies, uniform V0 and m0): the tiled passes
+        # take the pair geometry from a per-class table instead of staged
+        # position records (kernel_geom.StepLayout.bond_classes).
+        # TLSPH_BOND_CLASS=0 keeps the position path.
+        self.bcls = None
+        if (lay.tile and precision == "fp32" and self.uniform and self.bsplit == 1
+                and os.environ.get("TLSPH_BOND_CLASS", "1") != "0"):
+            self.bcls = lay.bond_classes(self.Xs, float(body.dp_body), float(body.h), kind)
+        # staged tile positions with the pass-A (V0) and pass-B (m0) weights
+        if lay.tile and self.bcls is None:
+            self.tpos_a = lay.positions(self.Xs, None if self.uniform else self.V0, precision)
+            self.tpos_b = (self.tpos_a if self.uniform
+                           else lay.positions(self.Xs, self.m0, precision))
+        else:
+            self.tpos_a = self.tpos_b = None
         # multi-GPU: interior tiles first (they overlap the halo exchange)
         self.tlist, self.n_interior = lay.split_tiles() if part is not None else (None, 0)
         self.counters = torch.zeros(N_COUNTERS, dtype=torch.int64, device=dev)
@@ -314,6 +322,8 @@ class DeviceBody:
             b.hoff, b.halo, b.slots, b.hslot = (P(lay.hoff), P(lay.halo), P(lay.slots),
                                                 P(lay.hslot))
             b.toff, b.tpos_a, b.tpos_b = P(lay.toff), P(self.tpos_a), P(self.tpos_b)
+        if self.bcls is not None:
+            b.ncls, b.bcls = int(self.bcls.shape[0]), P(self.bcls)
         b.perm = P(self.perm_global)
         b.V0, b.m0 = P(self.V0), P(self.m0)
         for k in ("us", "rb", "v", "al", "sdot", "sddot", "Hh", "Cpd", "epbar", "a"):

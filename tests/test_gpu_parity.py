@@ -275,6 +275,57 @@ def test_device_step1_fp32(tag):
         assert e1[k] <= 1e-5, (k, e1[k])
 
 
+@pytest.mark.parametrize("tag,expect", [("kalthoff3d", True), ("kalthoff2d_p", True),
+                                        ("branch2d", True), ("fourpoint3d", None),
+                                        ("beam2d", None), ("plate3d", None)])
+def test_bond_classes_fp32(tag, expect, monkeypatch):
+    """Bond-class tables (FP32 lattice bodies): the tiled passes take the
+    pair geometry from the per-class table.  Step-1 fields stay within the
+    FP32 tolerance of the reference and agree with the position path; the
+    nbsrange lattice cases must actually run on classes."""
+    monkeypatch.setenv("TLSPH_TILE_A", "1")
+    monkeypatch.setenv("TLSPH_TILE_B", "1")
+    G = golden(f"run_{tag}")
+    states = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("TLSPH_BOND_CLASS", mode)
+        cfg, sim = _sim(G, "fp32")
+        db = sim.dbodies[0]
+        if mode == "0":
+            assert db.bcls is None
+        elif expect:
+            assert db.bcls is not None and db.desc.ncls == db.bcls.shape[0] > 1
+            assert not db.bcls[0].any()              # class 0: the self padding
+        sim.initialize()
+        sim.step(G["dts"][0])
+        st = cfg.bodies[0].state
+        e1 = _errors(st, G, 1)
+        for k in ("F", "S", "a", "u", "v"):
+            # beam2d's step-1 acceleration cancels to ~1e-5 of its max in FP32
+            # on every path (position tiles 1.15e-5, L2 gather 1.07e-5)
+            tol = 1.5e-5 if (tag, k) == ("beam2d", "a") else 1e-5
+            assert e1[k] <= tol, (mode, k, e1[k])
+        states[mode] = {k: np.array(getattr(st, k)) for k in ("F", "S", "a", "v")}
+    for k in ("S", "a", "v"):
+        assert relerr(states["1"][k], states["0"][k]) <= 2e-6, k
+
+
+def test_bond_classes_off_lattice(monkeypatch):
+    """A body whose pairs are off any lattice keeps the position path."""
+    from paper_2602_15149_b200 import kernel_geom
+    G = golden("run_kalthoff3d")
+    cfg = run_case(G)
+    st = cfg.bodies[0].state
+    rng = np.random.default_rng(3)
+    dp = cfg.bodies[0].dp_body
+    st.X[:] = st.X + rng.uniform(-1e-3, 1e-3, st.X.shape) * dp
+    cfg.bodies[0].adjacency = None
+    from paper_2602_15149_b200.simulation import DeviceSimulation
+    sim = DeviceSimulation(cfg, precision="fp32")
+    assert sim.dbodies[0].bcls is None and sim.dbodies[0].desc.ncls == 0
+    assert kernel_geom.StepLayout.KEY_OFF == 0xFFFE
+
+
 @pytest.mark.parametrize("tile", ["32", "160", "256"])
 @pytest.mark.parametrize("tag", ["taylor3d", "column3d", "kalthoff3d", "twisting3d"])
 def test_device_fp32_split_rows(tag, tile, monkeypatch):
