@@ -323,12 +323,12 @@ typedef struct {
     const int64_t* toff;
     const void* tpos_a;
     const void* tpos_b;
-    /* bond-class table, 8 floats per class: (W, kappa, U, 0) with W = w(r) r0,
+    /* bond-class table, 8 Reals per class: (W, kappa, U, 0) with W = w(r) r0,
      * kappa = 1 / (w(r) (r^2 + 0.001 h^2)) (0 when w = 0), U = r0 / r^2, for the
      * class's reference separation r0 = q dp (q an integer lattice offset;
      * class 0 = the row's self padding, all zero).  The kernel shape w(r) as
      * in the pair loops, the per-body constant applied once per particle. */
-    const float* bcls;
+    const void* bcls;       /* float (FP32 bodies) or double (FP64) */
     /* geometry */
     const double* Xs;       /* FP64 planes x,y,z */
     const void* L;          /* 9 planes, correction matrix L_i */
@@ -398,6 +398,14 @@ int tl_clock_commit(tl_stream_t st, tl_clock* clock);
 int tl_reset_red(tl_stream_t st, unsigned long long* red);
 /* deterministic sum of nparts partials into *acc (plastic work) */
 int tl_reduce_partials(tl_stream_t st, const double* partials, int64_t nparts, double* acc);
+
+/* Test hook: the fused pass A's FP64 SVK + spectral split (fast.py:224-284
+ * semantics, fracture on) on caller-given H = F - I (n x 9, row-major):
+ * S (n x 9), psi, psi+ (n); closed[i] = 1 where the closed-form split ran,
+ * 0 where it fell back to cyclic Jacobi (near-degenerate spectrum at the
+ * sign boundary). */
+int tl_svk_split_check(tl_stream_t st, int64_t n, const double* H, double lam, double mu,
+                       const double* s, double* S, double* psi, double* psip, int32_t* closed);
 
 /* CTAs of an untiled tl_pass_a (256 particles each); a tiled launch has
  * ceil(n / tile).  pw_partial needs one double per CTA. */

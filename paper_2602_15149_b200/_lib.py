@@ -134,6 +134,7 @@ _SIGS = {
     "tl_reset_red": (INT, [P, P]),
     "tl_reduce_partials": (INT, [P, P, I64, P]),
     "tl_pass_blocks": (I64, [I64]),
+    "tl_svk_split_check": (INT, [P, I64, P, D, D, P, P, P, P, P]),
     "tl_energy_blocks": (I64, [I64]),
     "tl_energies": (INT, [P, C.POINTER(tl_body), P]),
     "tl_measure": (INT, [P, C.POINTER(tl_body), P, I64, P]),

@@ -58,8 +58,13 @@ def build(force=False, verbose=False, defines=(), out=None):
     objdir = os.path.join(HERE, "_obj" + tag)
     os.makedirs(objdir, exist_ok=True)
     objs = [os.path.join(objdir, s.replace(".cu", ".o")) for s in SOURCES]
+    # without force, recompile only the objects older than their source or a header
+    hdr = max(os.path.getmtime(f) for f in _deps() if not f.endswith(".cu"))
+    todo = [(src, obj) for src, obj in zip(SOURCES, objs)
+            if force or not os.path.exists(obj)
+            or os.path.getmtime(obj) < max(hdr, os.path.getmtime(os.path.join(CSRC, src)))]
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
-        logs = list(ex.map(lambda a: _compile(a[0], a[1], defines), zip(SOURCES, objs)))
+        logs = list(ex.map(lambda a: _compile(a[0], a[1], defines), todo))
     if verbose:
         for log in logs:
             print(log, file=sys.stderr)

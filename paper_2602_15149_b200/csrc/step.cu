@@ -213,6 +213,62 @@ __device__ __forceinline__ void svk_split_f32(const float* H, float lam, float m
     psip = pp;
 }
 
+// FP64 positive part E+ by the same closed form (trigonometric eigenvalues +
+// the Sylvester projector of the sign-isolated eigenvalue), on full 3x3
+// storage.  Its only ill-conditioned input is the isolated eigenvalue l_k
+// when a same-sign partner lies within g of it: the trigonometric formula
+// then carries an error ~ 2 eps p^2 / g (p = the deviatoric scale).  When
+// g < TL_SPLIT_GAP * p that error could exceed ~1e-13 of |E|, and the split
+// returns false: the caller runs the reference's cyclic Jacobi instead.
+#define TL_SPLIT_GAP 1e-3
+__device__ __forceinline__ bool positive_part64(const double* E, double* Ep) {
+    const double q = (E[0] + E[4] + E[8]) * (1.0 / 3.0);
+    const double o1 = E[1], o2 = E[2], o5 = E[5];
+    const double d0 = E[0] - q, d1 = E[4] - q, d2 = E[8] - q;
+    const double p2 = d0 * d0 + d1 * d1 + d2 * d2 + 2.0 * (o1 * o1 + o2 * o2 + o5 * o5);
+    if (p2 <= 0.0) {   // E = q I
+#pragma unroll
+        for (int k = 0; k < 9; ++k) Ep[k] = q > 0.0 ? E[k] : 0.0;
+        return true;
+    }
+    const double p = sqrt(p2 * (1.0 / 6.0));
+    const double ip = 1.0 / p;
+    const double b0 = d0 * ip, b4 = d1 * ip, b8 = d2 * ip;
+    const double b1 = o1 * ip, b2 = o2 * ip, b5 = o5 * ip;
+    const double detB = b0 * (b4 * b8 - b5 * b5) - b1 * (b1 * b8 - b5 * b2) + b2 * (b1 * b5 - b4 * b2);
+    const double r = fmin(fmax(0.5 * detB, -1.0), 1.0);
+    const double phi = acos(r) * (1.0 / 3.0);
+    double sp, cp;
+    sincos(phi, &sp, &cp);
+    const double l1 = q + 2.0 * p * cp;
+    const double l3 = q - p * (cp + 1.7320508075688772 * sp);
+    const double l2 = 3.0 * q - l1 - l3;
+    if (l3 >= 0.0) {
+#pragma unroll
+        for (int k = 0; k < 9; ++k) Ep[k] = E[k];
+        return true;
+    }
+    if (l1 <= 0.0) {
+#pragma unroll
+        for (int k = 0; k < 9; ++k) Ep[k] = 0.0;
+        return true;
+    }
+    const bool top = l2 <= 0.0;          // l1 alone positive: E+ = l1 P1
+    const double lk = top ? l1 : l3, la = top ? l2 : l1, lb = top ? l3 : l2;
+    if (fmin(fabs(lk - la), fabs(lk - lb)) < TL_SPLIT_GAP * p) return false;
+    const double c = lk / ((lk - la) * (lk - lb));
+    const double sab = la + lb, pab = la * lb;
+#pragma unroll
+    for (int rr = 0; rr < 3; ++rr)
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc) {
+            const double e2 = E[3 * rr] * E[cc] + E[3 * rr + 1] * E[3 + cc] + E[3 * rr + 2] * E[6 + cc];
+            const double pk = c * (e2 - sab * E[3 * rr + cc] + (rr == cc ? pab : 0.0));
+            Ep[3 * rr + cc] = top ? pk : E[3 * rr + cc] - pk;
+        }
+    return true;
+}
+
 // SVK with optional spectral split (reference.py:94-116, fast.py:224-284)
 template <typename R>
 __device__ __forceinline__ int svk_update(const R* H, R lam, R mu, R s, bool fracture, R jtol,
@@ -243,10 +299,33 @@ __device__ __forceinline__ int svk_update(const R* H, R lam, R mu, R s, bool fra
                       reinterpret_cast<float&>(psip));
         return 0;
     }
+    const R s2 = s * s;
+    if constexpr (sizeof(R) == 8) {
+        double Ep[9];
+        if (positive_part64(E, Ep)) {
+            double fp = 0.0, fm = 0.0;
+#pragma unroll
+            for (int k = 0; k < 9; ++k) {
+                const double a = Ep[k], m = E[k] - Ep[k];
+                fp += a * a;
+                fm += m * m;
+                double sp = 2.0 * mu * a, sm = 2.0 * mu * m;
+                if (k % 4 == 0) {
+                    sp += lam * trp;
+                    sm += lam * trm;
+                }
+                S[k] = s2 * sp + sm;
+            }
+            const double pp = 0.5 * lam * trp * trp + mu * fp;
+            const double pm = 0.5 * lam * trm * trm + mu * fm;
+            psi = s2 * pp + pm;
+            psip = pp;
+            return 0;
+        }
+    }
     R w[3], Q[9];
     const int sw = tl::eig3_jacobi(E, w, Q, jtol);
     R pp = R(0.5) * lam * trp * trp, pm = R(0.5) * lam * trm * trm;
-    const R s2 = s * s;
     R lp[3], lm[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -513,17 +592,19 @@ __device__ __forceinline__ void pair_b(R dx, R dy, R dz, const V4<R>& q0, const 
     const R wx = w * dx, wz = w * dz;
     const R wy = DIM == 3 ? w * dy : R(0);
     s1[0] += wx; s1[2] += wz;
+    // record layout (RecB): q0 = (PL00 PL10 PL01 PL11), q1 = (PL02 PL12 PL20 PL21),
+    // q2 = (v0 v1 v2 PL22)
     if (DIM == 3) {
         s1[1] += wy;
-        s2[0] = fma(q0.z, wz, fma(q0.y, wy, fma(q0.x, wx, s2[0])));
-        s2[1] = fma(q1.y, wz, fma(q1.x, wy, fma(q0.w, wx, s2[1])));
-        s2[2] = fma(q2.x, wz, fma(q1.w, wy, fma(q1.z, wx, s2[2])));
+        s2[0] = fma(q1.x, wz, fma(q0.z, wy, fma(q0.x, wx, s2[0])));
+        s2[1] = fma(q1.y, wz, fma(q0.w, wy, fma(q0.y, wx, s2[1])));
+        s2[2] = fma(q2.w, wz, fma(q1.w, wy, fma(q1.z, wx, s2[2])));
     } else {
-        s2[0] = fma(q0.z, wz, fma(q0.x, wx, s2[0]));
-        s2[2] = fma(q2.x, wz, fma(q1.z, wx, s2[2]));
+        s2[0] = fma(q1.x, wz, fma(q0.x, wx, s2[0]));
+        s2[2] = fma(q2.w, wz, fma(q1.z, wx, s2[2]));
     }
     if (visc) {
-        const R dvr = (vi0 - q2.y) * dx + (DIM == 3 ? (vi1 - q2.z) * dy : R(0)) + (vi2 - q2.w) * dz;
+        const R dvr = (vi0 - q2.x) * dx + (DIM == 3 ? (vi1 - q2.y) * dy : R(0)) + (vi2 - q2.z) * dz;
         const R g = fdiv(dvr, r2 + eps_h2);
         const R pw = (B2 * g - B1) * g;
         s3[0] += pw * wx; s3[2] += pw * wz;
@@ -710,6 +791,7 @@ __device__ __forceinline__ void loop_a_f2(uint32_t pos_sh, uint32_t rec_sh, uint
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t geo_slot(uint32_t e) { return e & 1023u; }
 __device__ __forceinline__ uint32_t geo_cls(uint32_t e) { return (e >> 10) * 32u; }
+__device__ __forceinline__ uint32_t geo_cls64(uint32_t e) { return (e >> 10) * 64u; }
 
 // pass A, FP32 3D, packed FP32x2: D += (u_j - u_i) (x) W ; M += (s_i - s_j) W (x) U
 template <bool FRAC, bool STAGED>
@@ -772,33 +854,119 @@ __device__ __forceinline__ void loop_a_geo_2d(uint32_t rec_sh, uint32_t cls_sh, 
 }
 
 // pass B: s1 += W ; s2 += PL_j W ; s3 += (B2 g^2 - B1 g) W with
-// g = (v_i - v_j).W kappa = (v_i - v_j).r0 / (r^2 + eps h^2)
+// g = (v_i - v_j).W kappa = (v_i - v_j).r0 / (r^2 + eps h^2).  3D runs on
+// packed FP32x2: the RecB layout pairs rows 0 and 1 of PL_j column by column,
+// so (s2_0, s2_1) takes three FFMA2 with a broadcast W component, and
+// (s1_0, s1_1), (s3_0, s3_1) and (v_i - v_j)_{0,1} are register pairs too.
 template <int DIM, bool STAGED, bool VISC>
 __device__ __forceinline__ void loop_b_geo(uint32_t rec_sh, uint32_t cls_sh, uint32_t sl_sh,
                                            const uint16_t* sl_g, int len, float vi0, float vi1,
                                            float vi2, float B2, float B1, float* s1, float* s2,
                                            float* s3) {
+    if constexpr (DIM == 3) {
+        float2 s1a = make_float2(0.f, 0.f), s2a = s1a, s3a = s1a;
+        float s1b = 0.f, s2b = 0.f, s3b = 0.f;
+        const float2 vi01 = make_float2(vi0, vi1);
+        const float2 neg1 = make_float2(-1.f, -1.f);
+        each_slot<STAGED>(sl_sh, sl_g, len, [&](uint32_t e) {
+            const float4 W = lds4<float>(cls_sh + geo_cls(e));
+            const uint32_t ra = rec_sh + 48u * geo_slot(e);
+            const float4 q0 = lds4<float>(ra), q1 = lds4<float>(ra + 16u), q2 = lds4<float>(ra + 32u);
+            const float2 wxy = make_float2(W.x, W.y);
+            s1a = __fadd2_rn(s1a, wxy);
+            s1b += W.z;
+            s2a = __ffma2_rn(make_float2(q0.x, q0.y), make_float2(W.x, W.x), s2a);
+            s2a = __ffma2_rn(make_float2(q0.z, q0.w), make_float2(W.y, W.y), s2a);
+            s2a = __ffma2_rn(make_float2(q1.x, q1.y), make_float2(W.z, W.z), s2a);
+            s2b = fmaf(q2.w, W.z, fmaf(q1.w, W.y, fmaf(q1.z, W.x, s2b)));
+            if (VISC) {
+                const float2 dv = __ffma2_rn(make_float2(q2.x, q2.y), neg1, vi01);
+                const float2 pr = __fmul2_rn(dv, wxy);
+                const float dvw = fmaf(vi2 - q2.z, W.z, pr.x + pr.y);
+                const float g = dvw * W.w;
+                const float pw = (B2 * g - B1) * g;
+                s3a = __ffma2_rn(make_float2(pw, pw), wxy, s3a);
+                s3b = fmaf(pw, W.z, s3b);
+            }
+        });
+        s1[0] = s1a.x; s1[1] = s1a.y; s1[2] = s1b;
+        s2[0] = s2a.x; s2[1] = s2a.y; s2[2] = s2b;
+        s3[0] = s3a.x; s3[1] = s3a.y; s3[2] = s3b;
+    } else {
+        each_slot<STAGED>(sl_sh, sl_g, len, [&](uint32_t e) {
+            const float4 W = lds4<float>(cls_sh + geo_cls(e));
+            const uint32_t ra = rec_sh + 48u * geo_slot(e);
+            const float4 q0 = lds4<float>(ra), q1 = lds4<float>(ra + 16u), q2 = lds4<float>(ra + 32u);
+            s1[0] += W.x; s1[2] += W.z;
+            s2[0] = fmaf(q1.x, W.z, fmaf(q0.x, W.x, s2[0]));
+            s2[2] = fmaf(q2.w, W.z, fmaf(q1.z, W.x, s2[2]));
+            if (VISC) {
+                const float dvw = (vi0 - q2.x) * W.x + (vi2 - q2.z) * W.z;
+                const float g = dvw * W.w;
+                const float pw = (B2 * g - B1) * g;
+                s3[0] = fmaf(pw, W.x, s3[0]); s3[2] = fmaf(pw, W.z, s3[2]);
+            }
+        });
+    }
+}
+
+// FP64 bond-class loops (scalar): the same pair terms as pair_a / pair_b with
+// the class table's W, kappa, U in place of the per-pair geometry
+template <int DIM, bool FRAC, bool STAGED>
+__device__ __forceinline__ void loop_a_geo64(uint32_t rec_sh, uint32_t cls_sh, uint32_t sl_sh,
+                                             const uint16_t* sl_g, int len, const double4& ui,
+                                             double* D, double* M) {
     each_slot<STAGED>(sl_sh, sl_g, len, [&](uint32_t e) {
-        const float4 W = lds4<float>(cls_sh + geo_cls(e));
-        const uint32_t ra = rec_sh + 48u * geo_slot(e);
-        const float4 q0 = lds4<float>(ra), q1 = lds4<float>(ra + 16u), q2 = lds4<float>(ra + 32u);
+        const uint32_t c = cls_sh + geo_cls64(e);
+        const double4 W = lds4<double>(c);
+        const double4 uj = lds4<double>(rec_sh + 32u * geo_slot(e));
+        const double du0 = uj.x - ui.x, du2 = uj.z - ui.z;
+        D[0] = fma(du0, W.x, D[0]); D[2] = fma(du0, W.z, D[2]);
+        D[6] = fma(du2, W.x, D[6]); D[8] = fma(du2, W.z, D[8]);
+        if (DIM == 3) {
+            const double du1 = uj.y - ui.y;
+            D[1] = fma(du0, W.y, D[1]); D[7] = fma(du2, W.y, D[7]);
+            D[3] = fma(du1, W.x, D[3]); D[4] = fma(du1, W.y, D[4]); D[5] = fma(du1, W.z, D[5]);
+        }
+        if (FRAC) {
+            const double4 U = lds4<double>(c + 32u);
+            const double ds = ui.w - uj.w;
+            const double cx = ds * W.x, cz = ds * W.z;
+            M[0] = fma(cx, U.x, M[0]); M[2] = fma(cz, U.z, M[2]); M[4] = fma(cx, U.z, M[4]);
+            if (DIM == 3) {
+                const double cy = ds * W.y;
+                M[1] = fma(cy, U.y, M[1]); M[3] = fma(cx, U.y, M[3]); M[5] = fma(cy, U.z, M[5]);
+            }
+        }
+    });
+}
+
+template <int DIM, bool STAGED, bool VISC>
+__device__ __forceinline__ void loop_b_geo64(uint32_t rec_sh, uint32_t cls_sh, uint32_t sl_sh,
+                                             const uint16_t* sl_g, int len, double vi0, double vi1,
+                                             double vi2, double B2, double B1, double* s1,
+                                             double* s2, double* s3) {
+    each_slot<STAGED>(sl_sh, sl_g, len, [&](uint32_t e) {
+        const double4 W = lds4<double>(cls_sh + geo_cls64(e));
+        const uint32_t ra = rec_sh + 96u * geo_slot(e);
+        const double4 q0 = lds4<double>(ra), q1 = lds4<double>(ra + 32u), q2 = lds4<double>(ra + 64u);
         s1[0] += W.x; s1[2] += W.z;
         if (DIM == 3) {
             s1[1] += W.y;
-            s2[0] = fmaf(q0.z, W.z, fmaf(q0.y, W.y, fmaf(q0.x, W.x, s2[0])));
-            s2[1] = fmaf(q1.y, W.z, fmaf(q1.x, W.y, fmaf(q0.w, W.x, s2[1])));
-            s2[2] = fmaf(q2.x, W.z, fmaf(q1.w, W.y, fmaf(q1.z, W.x, s2[2])));
+            s2[0] = fma(q1.x, W.z, fma(q0.z, W.y, fma(q0.x, W.x, s2[0])));
+            s2[1] = fma(q1.y, W.z, fma(q0.w, W.y, fma(q0.y, W.x, s2[1])));
+            s2[2] = fma(q2.w, W.z, fma(q1.w, W.y, fma(q1.z, W.x, s2[2])));
         } else {
-            s2[0] = fmaf(q0.z, W.z, fmaf(q0.x, W.x, s2[0]));
-            s2[2] = fmaf(q2.x, W.z, fmaf(q1.z, W.x, s2[2]));
+            s2[0] = fma(q1.x, W.z, fma(q0.x, W.x, s2[0]));
+            s2[2] = fma(q2.w, W.z, fma(q1.z, W.x, s2[2]));
         }
         if (VISC) {
-            float dvw = (vi0 - q2.y) * W.x + (vi2 - q2.w) * W.z;
-            if (DIM == 3) dvw = fmaf(vi1 - q2.z, W.y, dvw);
-            const float g = dvw * W.w;
-            const float pw = (B2 * g - B1) * g;
-            s3[0] = fmaf(pw, W.x, s3[0]); s3[2] = fmaf(pw, W.z, s3[2]);
-            if (DIM == 3) s3[1] = fmaf(pw, W.y, s3[1]);
+            const double dvw = (vi0 - q2.x) * W.x + (DIM == 3 ? (vi1 - q2.y) * W.y : 0.0) +
+                               (vi2 - q2.z) * W.z;
+            const double g = dvw * W.w;
+            const double pw = (B2 * g - B1) * g;
+            s3[0] = fma(pw, W.x, s3[0]); s3[2] = fma(pw, W.z, s3[2]);
+            if (DIM == 3) s3[1] = fma(pw, W.y, s3[1]);
         }
     });
 }
@@ -825,7 +993,7 @@ struct Tile {
     V4<R>* pos;        // nullptr in bond-class mode
     V4<R>* rec;
     uint16_t* slots;   // the CTA's block of the slot table (its warps' slices)
-    float4* cls;       // bond-class table (bond-class mode)
+    V4<R>* cls;        // bond-class table (bond-class mode)
 };
 
 __host__ __device__ constexpr size_t align16(size_t v) { return (v + 15) & ~(size_t)15; }
@@ -833,7 +1001,7 @@ __host__ __device__ constexpr size_t align16(size_t v) { return (v + 15) & ~(siz
 template <typename R, int NREC>
 __host__ __device__ constexpr size_t tile_bytes(int S, int slmax, int ncls = 0) {
     return ncls > 0 ? (size_t)S * NREC * sizeof(V4<R>) + align16((size_t)slmax * sizeof(uint16_t)) +
-                          (size_t)ncls * 2 * sizeof(float4)
+                          (size_t)ncls * 2 * sizeof(V4<R>)
                     : (size_t)S * (NREC + 1) * sizeof(V4<R>) + (size_t)slmax * sizeof(uint16_t);
 }
 
@@ -845,7 +1013,7 @@ __device__ __forceinline__ Tile<R, NREC> tile_layout(unsigned char* smem, int S,
         t.pos = nullptr;
         t.rec = reinterpret_cast<V4<R>*>(smem);
         t.slots = reinterpret_cast<uint16_t*>(t.rec + (size_t)S * NREC);
-        t.cls = reinterpret_cast<float4*>(reinterpret_cast<unsigned char*>(t.slots) +
+        t.cls = reinterpret_cast<V4<R>*>(reinterpret_cast<unsigned char*>(t.slots) +
                                           align16((size_t)slmax * sizeof(uint16_t)));
         return t;
     }
@@ -877,13 +1045,13 @@ __device__ __forceinline__ void stage_tile(const tl_body& b, const Tile<R, NREC>
         const int64_t w0 = p0 >> 5, w1 = min(w0 + T / 32, (b.n + 31) >> 5);
         const uint32_t sl_bytes =
             b.slmax > 0 ? (uint32_t)((b.soff[w1] - b.soff[w0]) * sizeof(uint16_t)) : 0u;
-        const uint32_t cls_bytes = t.cls ? (uint32_t)(b.ncls * 2 * sizeof(float4)) : 0u;
+        const uint32_t cls_bytes = t.cls ? (uint32_t)(b.ncls * 2 * sizeof(V4<R>)) : 0u;
         tl::mbar_init(bar, 1);
         tl::mbar_expect_tx(bar, pos_bytes + mem_bytes + sl_bytes + cls_bytes);
         if (pos_bytes) tl::bulk_g2s(t.pos, static_cast<const V4<R>*>(tpos) + r0, pos_bytes, bar);
         tl::bulk_g2s(t.rec, src + p0 * 4 * NREC, mem_bytes, bar);
         if (sl_bytes) tl::bulk_g2s(t.slots, b.slots + b.soff[w0], sl_bytes, bar);
-        if (cls_bytes) tl::bulk_g2s(t.cls, b.bcls, cls_bytes, bar);
+        if (cls_bytes) tl::bulk_g2s(t.cls, static_cast<const V4<R>*>(b.bcls), cls_bytes, bar);
     }
     constexpr int CH = (int)(sizeof(V4<R>) / 16);   // 16-byte chunks per record
     for (int s = threadIdx.x; s < H; s += blockDim.x) {
@@ -965,7 +1133,7 @@ __global__ void __launch_bounds__(kThreads, TL_MINB_A(R, TILED)) k_pass_a(const 
     __shared__ uint64_t bar;
     if (TILED) {
         if (threadIdx.x == 32) prefetch_own_a<R, MODEL, FRAC>(b, p0);
-        tl_ = tile_layout<R, 1>(smem, b.tile + b.hmax, b.slmax, sizeof(R) == 4 ? b.ncls : 0);
+        tl_ = tile_layout<R, 1>(smem, b.tile + b.hmax, b.slmax, b.ncls);
         stage_tile<R, 1>(b, tl_, tb, b.tpos_a, us, &bar);
     }
     const int ms = (int)threadIdx.x;   // member slot
@@ -984,13 +1152,19 @@ __global__ void __launch_bounds__(kThreads, TL_MINB_A(R, TILED)) k_pass_a(const 
 #pragma unroll
         for (int q = 0; q < 9; ++q) D[q] = R(0);
         R M[6] = {R(0), R(0), R(0), R(0), R(0), R(0)};   // xx yy zz xy xz yz
-        if (TILED && sizeof(R) == 4 && tl_.cls != nullptr) {
-          if constexpr (sizeof(R) == 4) {
-            // bond classes: geometry from the class table, no positions
-            const uint32_t rec_sh = tl::smem_u32(tl_.rec), cls_sh = tl::smem_u32(tl_.cls);
-            const uint32_t sl_sh = tl::smem_u32(tl_.slots + (base - b.soff[p0 >> 5]) + lane * G);
-            const uint16_t* slg = b.slots + base + lane * G;
-            const int lenr = b.wlen ? (int)b.wlen[w] : len;
+        if (TILED && tl_.cls != nullptr) {
+          // bond classes: geometry from the class table, no positions
+          const uint32_t rec_sh = tl::smem_u32(tl_.rec), cls_sh = tl::smem_u32(tl_.cls);
+          const uint32_t sl_sh = tl::smem_u32(tl_.slots + (base - b.soff[p0 >> 5]) + lane * G);
+          const uint16_t* slg = b.slots + base + lane * G;
+          const int lenr = b.wlen ? (int)b.wlen[w] : len;
+          if constexpr (sizeof(R) == 8) {
+            const double4& uid = reinterpret_cast<const double4&>(ui);
+            double* Dd = reinterpret_cast<double*>(D);
+            double* Md = reinterpret_cast<double*>(M);
+            if (b.slmax > 0) loop_a_geo64<DIM, FRAC, true>(rec_sh, cls_sh, sl_sh, slg, lenr, uid, Dd, Md);
+            else loop_a_geo64<DIM, FRAC, false>(rec_sh, cls_sh, sl_sh, slg, lenr, uid, Dd, Md);
+          } else {
             const float4& uif = reinterpret_cast<const float4&>(ui);
             float* Df = reinterpret_cast<float*>(D);
             float* Mf = reinterpret_cast<float*>(M);
@@ -1168,9 +1342,11 @@ __global__ void __launch_bounds__(kThreads, TL_MINB_A(R, TILED)) k_pass_a(const 
         // pass-B gather record: PL (9) + v (3)
         const R* vv = static_cast<const R*>(b.v);
         R* rb = static_cast<R*>(b.rb) + 12 * i;
-        tl::st4(rb, PL[0], PL[1], PL[2], PL[3]);
-        tl::st4(rb + 4, PL[4], PL[5], PL[6], PL[7]);
-        tl::st4(rb + 8, PL[8], vv[i], vv[N + i], vv[2 * N + i]);
+        // RecB layout: rows 0 and 1 of PL interleaved by column (packed FP32x2
+        // sums in pass B), then row 2, v, PL22
+        tl::st4(rb, PL[0], PL[3], PL[1], PL[4]);
+        tl::st4(rb + 4, PL[2], PL[5], PL[6], PL[7]);
+        tl::st4(rb + 8, vv[i], vv[N + i], vv[2 * N + i], PL[8]);
         if (mirror_out(b)) {
 #pragma unroll
             for (int q = 0; q < 9; ++q) {
@@ -1489,8 +1665,7 @@ __global__ void __launch_bounds__(b_threads<SPLIT>(), b_minb<R, SPLIT>())
     __shared__ uint64_t bar;
     if (TILED) {
         if (threadIdx.x == 32) prefetch_own_b<R, FRAC>(b, p0);
-        tl_ = tile_layout<R, 3>(smem, b.tile + b.hmax, b.slmax,
-                                (sizeof(R) == 4 && SPLIT == 1) ? b.ncls : 0);
+        tl_ = tile_layout<R, 3>(smem, b.tile + b.hmax, b.slmax, SPLIT == 1 ? b.ncls : 0);
         stage_tile<R, 3>(b, tl_, tb, b.tpos_b, rbp, &bar);
     }
     const int ms = SPLIT > 1 ? (int)threadIdx.x % T : (int)threadIdx.x;   // member slot
@@ -1507,20 +1682,32 @@ __global__ void __launch_bounds__(b_threads<SPLIT>(), b_minb<R, SPLIT>())
         const int len = (int)((b.soff[w + 1] - base) >> 5);
         // own record: v_i now, P L_i after the neighbour loop (fewer live registers)
         const auto r2i = TILED ? tl_.rec[3 * ms + 2] : tl::ld4(rbp + 12 * i + 8);
-        const R vi0 = r2i.y, vi1 = r2i.z, vi2 = r2i.w;
+        const R vi0 = r2i.x, vi1 = r2i.y, vi2 = r2i.z;
         const R inv_h = R(b.inv_h);
         const bool visc = b.visc != 0;
         const R eps_h2 = R(0.001 * b.h * b.h);
         const R B1 = R(b.beta1 * b.c0 * b.h), B2 = R(b.beta2 * b.h * b.h);
         const R inv_rho = R(1.0 / b.rho0);
         R s1[3] = {R(0), R(0), R(0)}, s2[3] = {R(0), R(0), R(0)}, s3[3] = {R(0), R(0), R(0)};
-        if (TILED && sizeof(R) == 4 && SPLIT == 1 && tl_.cls != nullptr) {
-          if constexpr (sizeof(R) == 4 && SPLIT == 1) {
-            // bond classes: geometry from the class table, no positions
-            const uint32_t rec_sh = tl::smem_u32(tl_.rec), cls_sh = tl::smem_u32(tl_.cls);
-            const uint32_t sl_sh = tl::smem_u32(tl_.slots + (base - b.soff[p0 >> 5]) + lane * G);
-            const uint16_t* slg = b.slots + base + lane * G;
-            const int lenr = b.wlen ? (int)b.wlen[w] : len;
+        if (TILED && SPLIT == 1 && tl_.cls != nullptr) {
+          // bond classes: geometry from the class table, no positions
+          const uint32_t rec_sh = tl::smem_u32(tl_.rec), cls_sh = tl::smem_u32(tl_.cls);
+          const uint32_t sl_sh = tl::smem_u32(tl_.slots + (base - b.soff[p0 >> 5]) + lane * G);
+          const uint16_t* slg = b.slots + base + lane * G;
+          const int lenr = b.wlen ? (int)b.wlen[w] : len;
+          if constexpr (sizeof(R) == 8) {
+            double* d1 = reinterpret_cast<double*>(s1);
+            double* d2 = reinterpret_cast<double*>(s2);
+            double* d3 = reinterpret_cast<double*>(s3);
+            const double B2d = double(B2), B1d = double(B1);
+#define TL_LOOP_G64(ST, V) loop_b_geo64<DIM, ST, V>(rec_sh, cls_sh, sl_sh, slg, lenr, double(vi0), double(vi1), double(vi2), B2d, B1d, d1, d2, d3)
+            if (b.slmax > 0) {
+                if (visc) TL_LOOP_G64(true, true); else TL_LOOP_G64(true, false);
+            } else {
+                if (visc) TL_LOOP_G64(false, true); else TL_LOOP_G64(false, false);
+            }
+#undef TL_LOOP_G64
+          } else if constexpr (SPLIT == 1) {
             float* f1 = reinterpret_cast<float*>(s1);
             float* f2 = reinterpret_cast<float*>(s2);
             float* f3 = reinterpret_cast<float*>(s3);
@@ -1628,7 +1815,7 @@ if (visc) TL_LOOP_B(U, ST, true); else TL_LOOP_B(U, ST, false)
             // a_int = (PL_i s1 + s2)/rho0^2 - AL_i s3
             const auto r0i = TILED ? tl_.rec[3 * ms] : tl::ld4(rbp + 12 * i);
             const auto r1i = TILED ? tl_.rec[3 * ms + 1] : tl::ld4(rbp + 12 * i + 4);
-            const R PLi[9] = {r0i.x, r0i.y, r0i.z, r0i.w, r1i.x, r1i.y, r1i.z, r1i.w, r2i.x};
+            const R PLi[9] = {r0i.x, r0i.z, r1i.x, r0i.y, r0i.w, r1i.y, r1i.z, r1i.w, r2i.w};
             const R inv_rho2 = inv_rho * inv_rho;
             double acc[3];
 #pragma unroll
@@ -1793,7 +1980,7 @@ int launch_a_one(cudaStream_t st, const tl_body& b) {
     }
     if (b.tile > 0) {
         auto kern = k_pass_a<R, DIM, MODEL, FRAC, KIND, G, true>;
-        const size_t bytes = tile_bytes<R, 1>(b.tile + b.hmax, b.slmax, sizeof(R) == 4 ? b.ncls : 0);
+        const size_t bytes = tile_bytes<R, 1>(b.tile + b.hmax, b.slmax, b.ncls);
         int rc = smem_opt_in(kern, bytes);
         if (rc) return rc;
         kern<<<b.tlist ? (unsigned)b.tcount : tl_blocks(b.n, b.tile), b.tile, bytes, st>>>(b);
@@ -1850,7 +2037,7 @@ int launch_b_one(cudaStream_t st, const tl_body& b) {
     }
     if (b.tile > 0) {
         auto kern = k_pass_b<R, DIM, MODE, FRAC, KIND, G, true>;
-        const size_t bytes = tile_bytes<R, 3>(b.tile + b.hmax, b.slmax, sizeof(R) == 4 ? b.ncls : 0);
+        const size_t bytes = tile_bytes<R, 3>(b.tile + b.hmax, b.slmax, b.ncls);
         int rc = smem_opt_in(kern, bytes);
         if (rc) return rc;
         kern<<<b.tlist ? (unsigned)b.tcount : tl_blocks(b.n, b.tile), b.tile, bytes, st>>>(b);
@@ -1893,6 +2080,30 @@ int check_body(const tl_body* b) {
         return TL_ERR_ARG;
     }
     return TL_OK;
+}
+
+// FP64 SVK split of the fused pass A on caller-given strains (test hook):
+// the closed form where it applies, the cyclic Jacobi elsewhere
+__global__ void k_svk_split_check(int64_t n, const double* H, double lam, double mu, const double* s,
+                                  double* S, double* psi, double* psip, int32_t* closed) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double h[9], Sv[9], ps, pp;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) h[k] = H[9 * i + k];
+    svk_update<double>(h, lam, mu, s[i], true, 1e-30, Sv, ps, pp);
+#pragma unroll
+    for (int k = 0; k < 9; ++k) S[9 * i + k] = Sv[k];
+    psi[i] = ps;
+    psip[i] = pp;
+    double E[9], Ep[9];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+            E[3 * r + c] = 0.5 * (h[3 * r + c] + h[3 * c + r] +
+                                  (h[r] * h[c] + h[3 + r] * h[3 + c] + h[6 + r] * h[6 + c]));
+    closed[i] = positive_part64(E, Ep) ? 1 : 0;
 }
 
 }  // namespace
@@ -1951,4 +2162,13 @@ extern "C" int tl_reduce_partials(tl_stream_t st, const double* partials, int64_
     if (nparts <= 0) return TL_OK;
     k_reduce_partials<<<1, 1024, 0, (cudaStream_t)st>>>(partials, nparts, acc);
     return tl_check_launch("k_reduce_partials");
+}
+
+extern "C" int tl_svk_split_check(tl_stream_t st, int64_t n, const double* H, double lam, double mu,
+                                  const double* s, double* S, double* psi, double* psip,
+                                  int32_t* closed) {
+    if (n <= 0) return TL_OK;
+    k_svk_split_check<<<tl_blocks(n, kThreads), kThreads, 0, (cudaStream_t)st>>>(n, H, lam, mu, s, S,
+                                                                                psi, psip, closed);
+    return tl_check_launch("k_svk_split_check");
 }

@@ -317,15 +317,15 @@ class StepLayout:
     KEY_SELF, KEY_OFF = 0xFFFF, 0xFFFE
     MAX_CLASSES = 63       # 6 class bits above the 10 slot bits of a uint16 entry
 
-    def bond_classes(self, Xs, dp, h, kind):
-        """Bond-class slot table for lattice bodies (FP32, uniform V0 and m0).
+    def bond_classes(self, Xs, dp, h, kind, precision="fp32"):
+        """Bond-class slot table for lattice bodies (uniform V0 and m0).
 
         Every pair of a body cut from one lattice of spacing dp has a
         reference separation r0 = X_i - X_j = q dp with q an integer offset,
         so the pair geometry (kernel shape, r0, 1/r^2) takes one of a few
         values -- 26 for a 3D nbsrange = 1 stencil.  The slots are rewritten
         to (class << 10) | slot (tiles.cu k_class_slots) and the returned
-        (ncls, 8) FP32 table holds, per class, W = w(r) r0, kappa =
+        (ncls, 8) table (FP32 or FP64, the body's precision) holds, per class, W = w(r) r0, kappa =
         1/(w(r) (r^2 + 0.001 h^2)) and U = r0 / r^2, evaluated in FP64 with the
         pair loops' kernel shape (step.cu kshape; kernel_geom.py:21-62 of the
         reference).  Class 0 is the padding entry (j = i), all zero.  Returns
@@ -377,14 +377,15 @@ class StepLayout:
         # a pair a rounding error inside the support edge (r = 2h - 1e-16) has
         # w ~ 1e-48: W flushes to zero in FP32 while kappa overflows, so its
         # (negligible) terms are dropped outright rather than turned into 0 * inf
-        tiny = np.abs(table[1:, 3]) > 1e30
+        tiny = np.abs(table[1:, 3]) > (1e30 if precision == "fp32" else 1e300)
         table[1:][tiny] = 0.0
         dev = self.slots.device
         _lib.check(L.tl_class_slots(st, total, self.slot_shift, P(keys),
                                     P(torch.from_numpy(cls_of_key).to(dev)), P(self.slots)),
                    "tl_class_slots")
         torch.cuda.current_stream().synchronize()
-        return torch.from_numpy(table.astype(np.float32)).to(dev).contiguous()
+        dt = np.float32 if precision == "fp32" else np.float64
+        return torch.from_numpy(table.astype(dt)).to(dev).contiguous()
 
     def split_tiles(self):
         """Multi-GPU launch order: (tile list, number of interior tiles).

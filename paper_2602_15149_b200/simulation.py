@@ -188,14 +188,15 @@ class DeviceBody:
                          <= TILE_SMEM_LIMIT))
         self.bsplit = (4 if split_ok and (int(env_s) == 4 if env_s is not None
                                           else k_mean > 64.0) else 1)
-        # bond classes (FP32 lattice bodies, uniform V0 and m0): the tiled passes
+        # bond classes (lattice bodies, uniform V0 and m0): the tiled passes
         # take the pair geometry from a per-class table instead of staged
         # position records (kernel_geom.StepLayout.bond_classes).
         # TLSPH_BOND_CLASS=0 keeps the position path.
         self.bcls = None
-        if (lay.tile and precision == "fp32" and self.uniform and self.bsplit == 1
+        if (lay.tile and self.uniform and self.bsplit == 1
                 and os.environ.get("TLSPH_BOND_CLASS", "1") != "0"):
-            self.bcls = lay.bond_classes(self.Xs, float(body.dp_body), float(body.h), kind)
+            self.bcls = lay.bond_classes(self.Xs, float(body.dp_body), float(body.h), kind,
+                                         precision)
         # staged tile positions with the pass-A (V0) and pass-B (m0) weights
         if lay.tile and self.bcls is None:
             self.tpos_a = lay.positions(self.Xs, None if self.uniform else self.V0, precision)
