@@ -161,13 +161,29 @@ WORKLOAD_NAMES = {
     "C5": "C5: 2D crack-branching plate (branch2d), SVK+PF AT2, nbsrange=1, adaptive dt"}
 
 
-def cpu_reference(config, steps, warmup, budget_s=25.0):
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# Port vs the reference's own numba backend, measured in the build container
+# (the reference cannot travel to the GPU box): tools/cpu_calibrate.py
+CALIB = os.path.join(ROOT, "profiles", "cpu_calibration.json")
+
+
+def cpu_reference(config, steps, warmup, budget_s=25.0, threads=None):
     """Time the oracle (C/OpenMP restatement of the reference's numba
     kernels + numpy stepper) on a bounded sample of the workload."""
     from oracle import oracle as O
     from paper_2602_15149_b200 import cases
     O.build()
-    threads = os.cpu_count() or 1
+    threads = threads or os.cpu_count() or 1
     O.set_threads(threads)
     smp = CPU_SAMPLE[config]
     cfg = cases.make_case(smp["spec"], dp_scale=smp["dp_scale"], mapfac=smp["mapfac"],
@@ -198,7 +214,22 @@ def cpu_reference(config, steps, warmup, budget_s=25.0):
                        f"N={n}, k={k:.1f}, {done} timed Verlet steps after {max(warmup, 1)} "
                        f"warm-up, FP64, oracle/liboracle.so OpenMP x{threads} "
                        f"(adjacency setup {setup:.1f}s untimed)"),
-            "steps": done, "seconds": el, "n": n}
+            "steps": done, "seconds": el, "n": n, "cpu_model": cpu_model()}
+
+
+def cpu_baseline_full(config):
+    """All host threads (the reported baseline), a 1-thread figure on a
+    shorter budget, the CPU model, and the port-vs-numba calibration."""
+    ref = cpu_reference(config, 10, 1)
+    one = cpu_reference(config, 3, 1, budget_s=8.0, threads=1)
+    out = {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model")}
+    out["value_1thread"] = one["value"]
+    try:
+        with open(CALIB) as f:
+            out["calibration"] = json.load(f)
+    except Exception:
+        out["calibration"] = None
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -228,8 +259,10 @@ def main():
     ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4", "C5"],
                     help="BASELINE.json configs: C4 is the headline; the others are extra "
                          "measurements (no CPU baseline sample)")
-    ap.add_argument("--e2e-steps", type=int, default=128)
+    ap.add_argument("--e2e-steps", type=int, default=200)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-fp64", action="store_true",
+                    help="skip the FP64 (parity mode) sub-measurement of an FP32 run")
     ap.add_argument("--dp-scale", type=float, default=1.0,
                     help="multiply the config's particle spacing (profiling at reduced size)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
@@ -266,7 +299,6 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_2602_15149_b200 import cases
-    from paper_2602_15149_b200.simulation import DeviceSimulation
 
     ndev = torch.cuda.device_count()
     if world > 1 and args.dist_backend == "nccl" and world > ndev:
@@ -284,15 +316,82 @@ def main():
         else:
             dist.init_process_group("gloo", init_method="env://")
 
-    t0 = time.perf_counter()
     base_scale = cases.WORKLOADS[args.config][1].get("dp_scale", 1.0)
-    cfg = cases.make_case(args.config, lean=True, build_adjacency=False,
-                          lenient_targets=args.config == "C5",
-                          dp_scale=base_scale * args.dp_scale)
-    perturb(cfg, seed=0)      # one global state; ranks own slabs of it
-    t_case = time.perf_counter() - t0
+
+    def make_cfg():
+        t0 = time.perf_counter()
+        cfg = cases.make_case(args.config, lean=True, build_adjacency=False,
+                              lenient_targets=args.config == "C5",
+                              dp_scale=base_scale * args.dp_scale)
+        perturb(cfg, seed=0)      # one global state; ranks own slabs of it
+        return cfg, time.perf_counter() - t0
+
+    cfg, t_case = make_cfg()
+    res = measure(args, cfg, args.precision, world, local, clocks_on=True)
+    sim = res.pop("sim")
+    n, n_total = res["n"], res["n_total"]
+    value = res["value"]
+
+    # end to end through the public API: the host state goes up, run() steps
+    # with the case's output cadence (energies + measure rows through the
+    # device reductions output.install routes the reference's OutputManager
+    # to), and the final state comes back to the host
+    e2e = e2e_run(sim, args.e2e_steps, n_total) if args.e2e_steps > 0 else None
+    del sim
+    torch.cuda.empty_cache()
+
+    # the reference's own precision beside the headline (FP64 parity mode)
+    fp64 = None
+    if args.precision == "fp32" and not args.no_fp64:
+        cfg64, _ = make_cfg()
+        r64 = measure(args, cfg64, "fp64", world, local, clocks_on=False)
+        del r64["sim"]
+        fp64 = {k: r64[k] for k in ("value", "ms_per_step", "roofline", "passes")}
+        fp64["unit"] = "particle-steps/s"
+        del cfg64
+        torch.cuda.empty_cache()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config in CPU_SAMPLE:
+        try:
+            cpu = cpu_baseline_full(args.config)
+        except Exception as exc:  # the baseline must not kill the GPU line
+            cpu = {"value": None, "error": repr(exc)}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "particle-steps/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": res["ms_per_step"], "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None,
+                "dtype": "f32" if args.precision == "fp32" else "f64",
+                "data": "synthetic (seeded perturbed lattice state, SURVEY.md 8(d))",
+                "config": {"workload": WORKLOAD_NAMES[args.config],
+                           "particles_per_gpu": n, "particles": int(n_total),
+                           "pairs_per_particle": res["k_mean"],
+                           "parallelism": (f"slab{world} (halo exchange over "
+                                           f"{args.dist_backend})" if world > 1 else "single"),
+                           "l2": "per-step working set >> 126 MB L2, no flush",
+                           "precision": args.precision,
+                           "bond_classes": res["bond_classes"],
+                           "cuda_graphs": res["graphs"],
+                           "setup_s": {"case": t_case, "device_build": res["t_setup"]}},
+                "roofline": res["roofline"], "passes": res["passes"], "fp64": fp64,
+                "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": res["launches"],
+                "clocks": res["clocks"]}
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def measure(args, cfg, precision, world, local, clocks_on):
+    """Device throughput of `args.steps` timed steps (inputs resident in HBM),
+    max over ranks, plus per-pass kernel times for the roofline."""
+    import torch
+    import torch.distributed as dist
+    from paper_2602_15149_b200.simulation import DeviceSimulation
     t0 = time.perf_counter()
-    sim = DeviceSimulation(cfg, precision=args.precision, mirrors=False)
+    sim = DeviceSimulation(cfg, precision=precision, mirrors=True)
     torch.cuda.synchronize()
     t_setup = time.perf_counter() - t0
     n = sum(db.n for db in sim.dbodies)
@@ -301,28 +400,35 @@ def main():
     sim.initialize()
     sim.advance(args.warmup)
     sim.finish_advance()
+    if sim.use_graphs and args.steps >= 64:
+        sim.advance(64)               # capture the 64-step graph outside the timed region
+        sim.finish_advance()
     torch.cuda.synchronize()
-
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     pass_ev = []
-    with ClockSampler(local) as clocks:
+    sampler = ClockSampler(local) if clocks_on else None
+    if sampler:
+        sampler.__enter__()
+    try:
         torch.cuda.nvtx.range_push("timed")      # ncu --nvtx --nvtx-include timed/
         ev0.record(sim.stream)
         sim.advance(args.steps)
         ev1.record(sim.stream)
         torch.cuda.synchronize()
         torch.cuda.nvtx.range_pop()
+    finally:
+        if sampler:
+            sampler.__exit__(None, None, None)
     if world > 1:
         dist.barrier()
     ms = ev0.elapsed_time(ev1)
     sim.finish_advance()
     # per-pass kernel times for the roofline: a further short run with events
-    # around each pass (which launches the passes back to back, without the
-    # single-GPU pass overlap of the timed steps)
+    # around each pass (eager launches)
     sim.advance(min(args.steps, 20), pass_events=pass_ev)
     torch.cuda.synchronize()
     sim.finish_advance()
@@ -338,11 +444,10 @@ def main():
         n_total = float(nt.item())
     else:
         n_total = float(n)
-    ms_step = ms / args.steps
     value = n_total * args.steps / (ms / 1e3)
 
     # roofline of the dominant kernel (per-launch algorithmic bytes / event time)
-    w = 4 if args.precision == "fp32" else 8
+    w = 4 if precision == "fp32" else 8
     b0 = cfg.bodies[0]
     ba, bb = pass_bytes(w, k_mean, dim=int(b0.dim), fracture=bool(b0.fracture),
                         j2=int(b0.material.model) == 3)
@@ -354,7 +459,7 @@ def main():
     try:
         with open(TRAFFIC) as f:
             tr = json.load(f)
-        traffic = tr.get(f"{args.config}.{args.precision}.{dom[0]}")
+        traffic = tr.get(f"{args.config}.{precision}.{dom[0]}")
     except Exception:
         pass
     roofline = {"bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": peak,
@@ -365,69 +470,80 @@ def main():
     passes = {"pass_a_ms": ma, "pass_b_ms": mb, "bytes_a": ba, "bytes_b": bb,
               "frac_a": ba * n / (ma / 1e3) / 1e9 / peak,
               "frac_b": bb * n / (mb / 1e3) / 1e9 / peak}
+    # kernels per timed step: clock begin + commit, and per body pass A, the
+    # dt-maxima reset, pass B (+ the plastic-work reduction for J2 bodies)
+    per_step = 2 + sum(3 + (int(db.body.material.model) == 3) for db in sim.dbodies)
+    return {"sim": sim, "n": n, "n_total": n_total, "k_mean": k_mean, "value": value,
+            "ms_per_step": ms / args.steps, "roofline": roofline, "passes": passes,
+            "t_setup": t_setup, "bond_classes": [int(db.desc.ncls) for db in sim.dbodies],
+            "graphs": bool(sim.use_graphs), "launches": int(args.steps * per_step),
+            "clocks": sampler.summary() if sampler else None}
 
-    # end to end through the public API (stepper.Simulation's): run() -- the
-    # throughput entry point, device-clock batches of 64 steps with one host
-    # round trip per batch -- and pick_dt() + step() with a round trip per step
-    e2e = None
-    if args.e2e_steps > 0:
-        import math as _m
-        nb = len(sim.dbodies)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        sim.run(time_max=1e30, time_out=1e30, max_steps=sim.step_index + args.e2e_steps)
-        torch.cuda.synchronize()
-        el = time.perf_counter() - t0
-        batches = _m.ceil(args.e2e_steps / 64)
-        e2e = {"value": n_total * args.e2e_steps / el, "unit": "particle-steps/s",
-               # per batch: clock struct in; clock, error counters, plastic work out
-               "h2d_bytes_per_step": 80 * batches / args.e2e_steps,
-               "d2h_bytes_per_step": (80 + 72 * nb) * batches / args.e2e_steps,
-               "steps": args.e2e_steps,
-               "api": "DeviceSimulation.run(max_steps=...) (the reference's Simulation.run); "
-                      "host state arrays refresh lazily on access (DeviceState)"}
-        k = min(args.e2e_steps, 32)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for _ in range(k):
-            sim.step(sim.pick_dt())
-        torch.cuda.synchronize()
-        el = time.perf_counter() - t0
-        e2e["per_step_api"] = {"value": n_total * k / el, "steps": k,
-                               "api": "pick_dt() + step(dt), one host round trip per step",
-                               "h2d_bytes_per_step": 80,
-                               "d2h_bytes_per_step": 16 * nb + 64 * nb + 8 * nb}
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config in CPU_SAMPLE:
-        try:
-            ref = cpu_reference(args.config, 10, 1)
-            cpu = {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")}
-        except Exception as exc:  # the baseline must not kill the GPU line
-            cpu = {"value": None, "error": repr(exc)}
+def _state_bytes(sim, pull):
+    """Bytes one push_state (pull=False) or full pull_state (True) moves."""
+    tot = 0
+    for db in sim.dbodies:
+        names = ["us", "v", "sdot", "sddot", "Hh", "epbar"] + (["a"] if not pull else [])
+        if int(db.body.material.model) == 3:
+            names.append("Cpd")
+        rows = db.n if pull else db.n_all
+        for k in names:
+            t = getattr(db, k)
+            tot += t.element_size() * t.numel() * rows // max(db.n_all, 1)
+        if pull and db.mirrors:
+            tot += 8 * db.n * (3 + 9 + 9 + 1 + 1)     # a, F, S, psi_e, psi_plus (FP64)
+    return tot
 
-    if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": "particle-steps/s",
-                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": ms_step, "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None,
-                "dtype": "f32" if args.precision == "fp32" else "f64",
-                "data": "synthetic (seeded perturbed lattice state, SURVEY.md 8(d))",
-                "config": {"workload": WORKLOAD_NAMES[args.config],
-                           "particles_per_gpu": n, "particles": int(n_total),
-                           "pairs_per_particle": k_mean,
-                           "parallelism": (f"slab{world} (halo exchange over "
-                                           f"{args.dist_backend})" if world > 1 else "single"),
-                           "l2": "per-step working set >> 126 MB L2, no flush",
-                           "precision": args.precision,
-                           "bond_classes": [int(db.desc.ncls) for db in sim.dbodies],
-                           "setup_s": {"case": t_case, "device_build": t_setup}},
-                "roofline": roofline, "passes": passes, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": int(args.steps * (2 + 2 * len(sim.dbodies))),
-                "clocks": clocks.summary()}
-        print(json.dumps(line))
-    if world > 1:
-        dist.destroy_process_group()
+
+def e2e_run(sim, steps, n_total):
+    """run() through the public API with host buffers: push the host state,
+    step with outputs at the case's TimeOut (energies + measure rows, the
+    reference OutputManager's CSV rows, through paper_2602_15149_b200.output),
+    then pull the final state into body.state."""
+    import torch
+    from paper_2602_15149_b200 import output
+    rows = []
+
+    def on_output(s):
+        for body in s.bodies:
+            rows.append(output.compute_energies(body))
+            for idx in getattr(body, "measure_sets", []) or []:
+                rows.append(output.measure_row(body, idx, s.t))
+
+    for db in sim.dbodies:           # the reference's full ParticleArrays (lean cases skip F, S)
+        st = db.host
+        nb = st.X.shape[0]
+        for k, shape in (("F", (nb, 3, 3)), ("S", (nb, 3, 3))):
+            if getattr(st, k) is None:
+                setattr(st, k, np.zeros(shape))
+    sim.pull_host()                  # the host state a user of the API holds
+    sim.pin_host_state()             # page-locked once, as a user's repeated runs would
+    torch.cuda.synchronize()
+    t_out = float(sim.config.time_out)
+    # a fresh run from t = 0 (the reference's run() puts its first output
+    # boundary at time_out, so it restarts the clock like a new Simulation)
+    sim.t, sim.step_index = 0.0, 0
+    start = sim.step_index
+    t0 = time.perf_counter()
+    sim.push_state()                                           # host -> device
+    sim.run(time_max=float(sim.config.time_max), time_out=t_out, on_output=on_output,
+            max_steps=start + steps)
+    sim.pull_host()                                            # device -> host
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t0
+    done = sim.step_index - start
+    h2d = _state_bytes(sim, pull=False)
+    d2h = _state_bytes(sim, pull=True)
+    n_out = len(rows)
+    return {"value": n_total * done / el, "unit": "particle-steps/s", "steps": done,
+            "h2d_bytes_per_step": h2d / max(done, 1),
+            "d2h_bytes_per_step": (d2h + 8 * 64 * n_out) / max(done, 1),
+            "outputs": n_out, "time_out": t_out,
+            "api": "push_state(); DeviceSimulation.run(time_out=case TimeOut, on_output=energies "
+                   "+ measure rows via output.install's device reductions, max_steps); "
+                   "pull_host() -- the reference's Simulation.run + OutputManager CSV rows "
+                   "(VTK writer out of scope)"}
 
 
 if __name__ == "__main__":

@@ -344,28 +344,106 @@ class DeviceBody:
         c[7] = INT64_MAX
 
     # -- host mirrors ------------------------------------------------------------
+    def _gid_dev(self):
+        """Device copy of gid (device row -> host row), and for a whole-body
+        device its inverse over the owned rows."""
+        if getattr(self, "_gidd", None) is None:
+            torch = _torch()
+            self._gidd = torch.from_numpy(np.asarray(self.gid, dtype=np.int64)).to(self.dev)
+            nh = int(self.host.X.shape[0])
+            if self.n == nh:
+                inv = torch.empty(nh, dtype=torch.int64, device=self.dev)
+                inv[self._gidd[:self.n]] = torch.arange(self.n, dtype=torch.int64,
+                                                        device=self.dev)
+                self._invd = inv
+            else:
+                self._invd = None
+        return self._gidd, self._invd
+
     def push_state(self):
         """Upload body.state (host, FP64, original order) into the device
-        layout and order."""
+        layout and order: each host array goes up as is (one contiguous copy,
+        DMA when the host state is pinned, see pin_host) and is permuted on
+        the device."""
         torch = _torch()
         st = self.host
-        R, dev, pm = self.R, self.dev, self.gid       # all n_all device rows
-        us = np.empty((self.n_all, 4))
-        us[:, :3] = st.u[pm]
-        us[:, 3] = st.s[pm]
-        self.us.copy_(torch.from_numpy(us).to(dev, R))
-        self.v.copy_(torch.from_numpy(np.ascontiguousarray(st.v[pm].T)).to(dev, R))
-        self.a.copy_(torch.from_numpy(np.ascontiguousarray(st.a[pm].T)).to(dev, R))
+        R, dev = self.R, self.dev
+        g, _ = self._gid_dev()
+
+        def up(arr):
+            t = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64)).to(dev)
+            return t.index_select(0, g)
+
+        self.us[:, :3].copy_(up(st.u))
+        self.us[:, 3].copy_(up(st.s))
+        self.v.copy_(up(st.v).t())
+        self.a.copy_(up(st.a).t())
         for name, arr in (("sdot", st.sdot), ("sddot", st.sddot), ("Hh", st.Hhist),
                           ("epbar", st.epbar)):
-            host = np.asarray(arr, dtype=np.float64)[pm]
-            getattr(self, name).copy_(torch.from_numpy(host).to(dev, R))
+            getattr(self, name).copy_(up(arr))
         if self.body.material.model == Model.J2 and st.Cp is not None:
-            Cp = np.asarray(st.Cp, dtype=np.float64)[pm]
-            cpd = np.stack([Cp[:, 0, 0] - 1.0, Cp[:, 1, 1] - 1.0, Cp[:, 2, 2] - 1.0,
-                            Cp[:, 0, 1], Cp[:, 0, 2], Cp[:, 1, 2]])
-            self.Cpd.copy_(torch.from_numpy(cpd).to(dev, R))
+            Cp = up(np.asarray(st.Cp, dtype=np.float64).reshape(-1, 9))
+            cpd = torch.stack([Cp[:, 0] - 1.0, Cp[:, 4] - 1.0, Cp[:, 8] - 1.0,
+                               Cp[:, 1], Cp[:, 2], Cp[:, 5]])
+            self.Cpd.copy_(cpd)
         self.refresh_dt_maxima()
+
+    def pin_host(self):
+        """Page-lock the host state arrays (cudaHostRegister) so push_state /
+        pull_state move them by DMA.  Idempotent."""
+        if getattr(self, "_pinned", False):
+            return
+        torch = _torch()
+        st = self.host
+        for k in ("u", "v", "a", "s", "sdot", "sddot", "Hhist", "epbar", "F", "S", "psi_e",
+                  "psi_plus", "Cp"):
+            arr = getattr(st, k, None)
+            if isinstance(arr, np.ndarray) and arr.flags.c_contiguous and arr.nbytes:
+                # a failure (e.g. pages shared with an already registered
+                # array) leaves that array on the pageable path
+                torch._C._cudart.cudaHostRegister(arr.ctypes.data, arr.nbytes, 0)
+        self._pinned = True
+
+    def pull_state(self, full=True):
+        """Refresh body.state (host, original order) from the device.  A
+        whole-body device permutes on the device and copies each field
+        straight into the host array; a slab fills its owned rows."""
+        torch = _torch()
+        st = self.host
+        n = self.n
+        self.dirty = False
+        _, inv = self._gid_dev()
+        pm = self.gid[:n]                              # owned device rows only
+
+        def put(dst, val):
+            """val: device (n_rows, ...) in device order, rows >= n ignored.
+            A host field the case did not allocate (lean layouts) is skipped."""
+            if dst is None:
+                return
+            val = val[:n].double()
+            if inv is not None and dst.flags.c_contiguous and dst.dtype == np.float64:
+                torch.from_numpy(dst).copy_(val.index_select(0, inv).reshape(dst.shape))
+            else:
+                dst[pm] = val.cpu().numpy().reshape((n,) + dst.shape[1:])
+
+        put(st.u, self.us[:, :3])
+        put(st.s, self.us[:, 3])
+        put(st.v, self.v.t())
+        put(st.sdot, self.sdot)
+        put(st.sddot, self.sddot)
+        put(st.Hhist, self.Hh)
+        put(st.epbar, self.epbar)
+        if full and self.mirrors:
+            put(st.a, self.a.t())
+            put(st.F, self.F_out)
+            put(st.S, self.S_out)
+            put(st.psi_e, self.psi_out)
+            put(st.psi_plus, self.psip_out)
+        if self.body.material.model == Model.J2 and st.Cp is not None:
+            c = self.Cpd.double()[:, :n]
+            Cp = torch.stack([1.0 + c[0], c[3], c[4], c[3], 1.0 + c[1], c[5],
+                              c[4], c[5], 1.0 + c[2]], dim=1).reshape(n, 3, 3)
+            put(st.Cp, Cp)
 
     def refresh_dt_maxima(self):
         """max |v|^2 and max |a|^2 of the owned rows into ``red`` (what pass B
@@ -383,39 +461,6 @@ class DeviceBody:
             sq = torch.where(torch.isnan(sq), torch.zeros_like(sq), sq)
             out.append(sq.max() if n else torch.zeros((), dtype=torch.float64, device=self.dev))
         self.red.copy_(torch.stack(out).view(torch.int64))
-
-    def pull_state(self, full=True):
-        """Refresh body.state (host, original order) from the device."""
-        st = self.host
-        n = self.n
-        pm = self.gid[:n]                              # owned device rows only
-        self.dirty = False
-
-        def put(dst, val):
-            dst[pm] = val[:n]
-
-        us = self.us.double().cpu().numpy()
-        put(st.u, us[:, :3])
-        put(st.s, us[:, 3])
-        put(st.v, self.v.double().cpu().numpy().T)
-        put(st.sdot, self.sdot.double().cpu().numpy())
-        put(st.sddot, self.sddot.double().cpu().numpy())
-        put(st.Hhist, self.Hh.double().cpu().numpy())
-        put(st.epbar, self.epbar.double().cpu().numpy())
-        if full and self.mirrors:
-            put(st.a, self.a.double().cpu().numpy().T)
-            put(st.F, self.F_out.cpu().numpy())
-            put(st.S, self.S_out.cpu().numpy())
-            put(st.psi_e, self.psi_out.cpu().numpy())
-            put(st.psi_plus, self.psip_out.cpu().numpy())
-        if self.body.material.model == Model.J2 and st.Cp is not None:
-            c = self.Cpd.double().cpu().numpy()[:, :n]
-            Cp = np.empty((n, 3, 3))
-            Cp[:, 0, 0], Cp[:, 1, 1], Cp[:, 2, 2] = 1.0 + c[0], 1.0 + c[1], 1.0 + c[2]
-            Cp[:, 0, 1] = Cp[:, 1, 0] = c[3]
-            Cp[:, 0, 2] = Cp[:, 2, 0] = c[4]
-            Cp[:, 1, 2] = Cp[:, 2, 1] = c[5]
-            put(st.Cp, Cp)
 
     def dtinfo(self):
         return _lib.tl_dtinfo(h=float(self.body.h), c0=float(self.body.material.c0),
@@ -568,6 +613,13 @@ class DeviceSimulation:
         self._lib = L
         self._dt_arr = (_lib.tl_dtinfo * len(self.dbodies))(*[db.dtinfo() for db in self.dbodies])
         self.workspaces = [None for _ in self.bodies]
+        # CUDA graphs of fixed-length device-clock step batches (run / advance).
+        # The descriptors are passed by value, so a graph stays valid while
+        # they do; multi-GPU slabs keep eager launches (host-side exchange
+        # scheduling).  TLSPH_GRAPHS=0 disables.
+        self._graphs = {}
+        self.use_graphs = (not self.partitioned and
+                           os.environ.get("TLSPH_GRAPHS", "1") != "0")
 
     # -- penalty contact (dynamics.py:81-135) --------------------------------
     CONTACT_CELLS = 1 << 20      # cell-grid capacity of one body pair
@@ -850,6 +902,11 @@ class DeviceSimulation:
         for db in self.dbodies:
             db.pull_state()
 
+    def pin_host_state(self):
+        """Page-lock every body's host state arrays (DMA for push/pull)."""
+        for db in self.dbodies:
+            db.pin_host()
+
     def push_state(self):
         """Upload host edits of body.state to the device."""
         for db in self.dbodies:
@@ -925,6 +982,39 @@ class DeviceSimulation:
             dt = min(dt, cand)
         return dt
 
+    def _clock_steps(self, nsteps, verlet):
+        """Launch nsteps device-clock steps (clock begin, passes, commit)."""
+        for _ in range(nsteps):
+            _lib.check(self._lib.tl_clock_begin(self._st(), _lib.ptr(self.clock_dev),
+                                                 len(self.dbodies), self._dt_arr), "clock")
+            self._launch_step(verlet)
+            _lib.check(self._lib.tl_clock_commit(self._st(), _lib.ptr(self.clock_dev)), "commit")
+
+    def _launch_batch(self, nsteps, verlet):
+        """nsteps device-clock steps, as one replay of a captured CUDA graph
+        when graphs are on (captured on first use for each (nsteps, mode))."""
+        if not self.use_graphs:
+            self._clock_steps(nsteps, verlet)
+            return
+        torch = _torch()
+        key = (int(nsteps), bool(verlet))
+        g = self._graphs.get(key)
+        if g is None:
+            g = torch.cuda.CUDAGraph()
+            cap = torch.cuda.Stream()
+            cap.wait_stream(self.stream)
+            saved = self.stream
+            self.stream = cap
+            try:
+                with torch.cuda.graph(g, stream=cap, capture_error_mode="thread_local"):
+                    self._clock_steps(nsteps, verlet)
+            finally:
+                self.stream = saved
+            self.stream.wait_stream(cap)
+            self._graphs[key] = g
+        with torch.cuda.stream(self.stream):
+            g.replay()
+
     def advance(self, nsteps, pass_events=None):
         """Launch exactly ``nsteps`` device-clock steps (adaptive dt, or the
         override) with no host synchronisation; the throughput entry point.
@@ -936,13 +1026,16 @@ class DeviceSimulation:
         verlet = int(cfg.step_algorithm) != 2
         dto = -1.0 if cfg.dt_override is None else float(cfg.dt_override)
         self._set_clock(t=self.t, next_out=math.inf, t_max=math.inf, eps=0.0, dt_override=dto)
-        torch = _torch()
-        for _ in range(nsteps):
-            _lib.check(self._lib.tl_clock_begin(self._st(), _lib.ptr(self.clock_dev),
-                                                 len(self.dbodies), self._dt_arr), "clock")
-            if pass_events is None:
-                self._launch_step(verlet)
-            else:
+        if pass_events is None:
+            full, rest = divmod(nsteps, 64)
+            for _ in range(full):
+                self._launch_batch(64, verlet)
+            self._clock_steps(rest, verlet)
+        else:
+            torch = _torch()
+            for _ in range(nsteps):
+                _lib.check(self._lib.tl_clock_begin(self._st(), _lib.ptr(self.clock_dev),
+                                                     len(self.dbodies), self._dt_arr), "clock")
                 ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
                 if not verlet:
                     for db in self.dbodies:
@@ -957,7 +1050,8 @@ class DeviceSimulation:
                     self._pass_b(db, 1 if verlet else 2)
                 ev[3].record(self.stream)
                 pass_events.append(ev)
-            _lib.check(self._lib.tl_clock_commit(self._st(), _lib.ptr(self.clock_dev)), "commit")
+                _lib.check(self._lib.tl_clock_commit(self._st(), _lib.ptr(self.clock_dev)),
+                           "commit")
         self.step_index += nsteps
         for db in self.dbodies:
             db.dirty = True
@@ -988,18 +1082,10 @@ class DeviceSimulation:
         eps = 1e-12 * max(t_max, 1.0)
         verlet = int(cfg.step_algorithm) != 2
         dto = -1.0 if cfg.dt_override is None else float(cfg.dt_override)
-        dtinfo = self._dt_arr
         while self.t < t_max - eps:
             self._set_clock(t=self.t, next_out=next_out, t_max=t_max, eps=eps, dt_override=dto,
                             max_steps=-1 if max_steps is None else int(max_steps))
-            k = 0
-            while k < batch:
-                _lib.check(self._lib.tl_clock_begin(self._st(), _lib.ptr(self.clock_dev),
-                                                     len(self.dbodies), dtinfo), "clock")
-                self._launch_step(verlet)
-                _lib.check(self._lib.tl_clock_commit(self._st(), _lib.ptr(self.clock_dev)),
-                           "commit")
-                k += 1
+            self._launch_batch(batch, verlet)
             c = self._get_clock()
             for db in self.dbodies:
                 db.dirty = True           # host mirrors refresh on read (also after a raise)

@@ -601,3 +601,27 @@ def test_fp64_spectral_split_closed_form():
     for k, fb in enumerate(expect_fallback):
         if fb is not None:
             assert closed[k] == (0 if fb else 1), (k, fb)
+
+
+@pytest.mark.parametrize("tag", ["kalthoff2d_sym", "taylor3d", "kalthoff3d"])
+def test_graph_batches_match_eager(tag, monkeypatch):
+    """run() and advance() replay captured CUDA graphs of 64-step batches;
+    the state is bit-identical to eager launches (same kernels, same order),
+    including a batch that halts at max_steps part way."""
+    G = golden(f"run_{tag}")
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("TLSPH_GRAPHS", mode)
+        cfg, sim = _sim(G, "fp64")
+        assert sim.use_graphs == (mode == "1")
+        sim.run(time_max=1e30, time_out=1e30, max_steps=70)       # 64 + a partial batch
+        sim.advance(64)
+        sim.finish_advance()
+        assert sim.step_index == 134
+        if mode == "1":
+            assert (64, True) in sim._graphs or (64, False) in sim._graphs
+        st = cfg.bodies[0].state
+        out[mode] = (sim.t, np.array(st.u), np.array(st.v), np.array(st.S))
+    assert out["1"][0] == out["0"][0]
+    for a, b in zip(out["1"][1:], out["0"][1:]):
+        assert np.array_equal(a, b)
