@@ -151,14 +151,17 @@ def perturb(cfg, seed=0):
 # CPU reference arm / baseline (oracle port; test infrastructure)
 # ---------------------------------------------------------------------------
 
-CPU_SAMPLE = {"C4": dict(spec="kalthoff3d", dp_scale=0.918 * 4, mapfac=5)}
+CPU_SAMPLE = {"C4": dict(spec="kalthoff3d", dp_scale=0.918 * 4, mapfac=5),
+              "P1": dict(spec="fourpoint3d", dp_scale=1.26 * 2, mapfac=None)}
 WORKLOAD_NAMES = {
     "C1": "C1: 2D elastic cantilever plate (beam2d), SVK, radial, Verlet, adaptive dt",
     "C2": "C2: 3D elastic column (column3d), Neo-Hookean, radial (k~160), adaptive dt",
     "C3": "C3: 3D Taylor bar impact (taylor3d), J2 finite-strain plasticity, radial, adaptive dt",
     "C4": "C4: 3D Kalthoff-Winkler phase-field fracture, SVK+spectral split, nbsrange=1, "
           "Verlet, adaptive dt",
-    "C5": "C5: 2D crack-branching plate (branch2d), SVK+PF AT2, nbsrange=1, adaptive dt"}
+    "C5": "C5: 2D crack-branching plate (branch2d), SVK+PF AT2, nbsrange=1, adaptive dt",
+    "P1": "P1 (paper anchor, PAPER.md:1605-1611): four-point bending beam (fourpoint3d), "
+          "3D SVK+PF, radial (k~170), notch, restrictphi, 1M particles, adaptive dt"}
 
 
 def cpu_model():
@@ -256,7 +259,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
-    ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4", "C5"],
+    ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4", "C5", "P1"],
                     help="BASELINE.json configs: C4 is the headline; the others are extra "
                          "measurements (no CPU baseline sample)")
     ap.add_argument("--e2e-steps", type=int, default=200)
@@ -346,7 +349,8 @@ def main():
         cfg64, _ = make_cfg()
         r64 = measure(args, cfg64, "fp64", world, local, clocks_on=False)
         del r64["sim"]
-        fp64 = {k: r64[k] for k in ("value", "ms_per_step", "roofline", "passes")}
+        fp64 = {k: r64[k] for k in ("value", "ms_per_step", "roofline", "passes",
+                                    "device_bytes_per_particle")}
         fp64["unit"] = "particle-steps/s"
         del cfg64
         torch.cuda.empty_cache()
@@ -373,6 +377,7 @@ def main():
                            "l2": "per-step working set >> 126 MB L2, no flush",
                            "precision": args.precision,
                            "bond_classes": res["bond_classes"],
+                           "device_bytes_per_particle": res["device_bytes_per_particle"],
                            "cuda_graphs": res["graphs"],
                            "setup_s": {"case": t_case, "device_build": res["t_setup"]}},
                 "roofline": res["roofline"], "passes": res["passes"], "fp64": fp64,
@@ -391,7 +396,8 @@ def measure(args, cfg, precision, world, local, clocks_on):
     import torch.distributed as dist
     from paper_2602_15149_b200.simulation import DeviceSimulation
     t0 = time.perf_counter()
-    sim = DeviceSimulation(cfg, precision=precision, mirrors=True)
+    # host-layout FP64 mirrors (F, S, psi) only when the e2e outputs need them
+    sim = DeviceSimulation(cfg, precision=precision, mirrors=args.e2e_steps > 0)
     torch.cuda.synchronize()
     t_setup = time.perf_counter() - t0
     n = sum(db.n for db in sim.dbodies)
@@ -473,7 +479,9 @@ def measure(args, cfg, precision, world, local, clocks_on):
     # kernels per timed step: clock begin + commit, and per body pass A, the
     # dt-maxima reset, pass B (+ the plastic-work reduction for J2 bodies)
     per_step = 2 + sum(3 + (int(db.body.material.model) == 3) for db in sim.dbodies)
+    mem = torch.cuda.max_memory_allocated()
     return {"sim": sim, "n": n, "n_total": n_total, "k_mean": k_mean, "value": value,
+            "device_bytes_per_particle": mem / max(n, 1),
             "ms_per_step": ms / args.steps, "roofline": roofline, "passes": passes,
             "t_setup": t_setup, "bond_classes": [int(db.desc.ncls) for db in sim.dbodies],
             "graphs": bool(sim.use_graphs), "launches": int(args.steps * per_step),

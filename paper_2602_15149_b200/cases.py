@@ -206,6 +206,32 @@ def _branch_spec():
                                [50.030625e-3, 25e-3, 0.02], [-2e-3, 25e-3, 0.02]]])])
 
 
+def _fourpoint_spec():
+    # fourpoint3d.xml:1-86: the paper's benchmark body (80 x 10 x 20 mm beam,
+    # 3D SVK + phase field on the radial stencil, notch, restrictphi and a
+    # velocity BC built from compound `and` expressions)
+    rp = ("if(z0<0.00090 and x0>=0.002525 and x0<=0.005475, 0.9999, "
+          "if(z0<0.00090 and x0>=0.074525 and x0<=0.077475, 0.9999, "
+          "if(z0>0.01910 and x0>=0.018450 and x0<=0.021400, 0.9999, "
+          "if(z0>0.01910 and x0>=0.058600 and x0<=0.061550, 0.9999,skip))))")
+    zb = ("if(z0<0.00010 and x0>=0.003825 and x0<=0.004225, Velmax, "
+          "if(z0<0.00010 and x0>=0.075625 and x0<=0.076175, Velmax, "
+          "if(z0>0.01990 and x0>=0.01970 and x0<=0.020100, -Velmax, "
+          "if(z0>0.01990 and x0>=0.059900 and x0<=0.060250, -Velmax, skip))))")
+    xc0 = 40.0e-3
+    return dict(
+        dp=0.2e-3, dim=3, y_plane=0.0, coefh=1.0, cfl=0.1, kernel=2, algo=1,
+        time_max=250.0e-6, time_out=2.0e-6,
+        shapes=[dict(mk=1, kind="box", point=[0.0, 0.0, 0.0], size=[80.0e-3, 10.0e-3, 20.0e-3])],
+        expressions={1: (rp, ""), 2: (zb, "Velmax=10.0")},
+        bodies=[dict(mk=1, cards=dict(density=50.0, youngmod=12.44e9, poissratio=0.3,
+                                      fracture=True, Gc=11.8e3, pflenscale=0.25e-3),
+                     restrictphi=1,
+                     bcs=[dict(kind="vel", expr=(None, None, 2))],
+                     notches=[[[0.04, 0.0, -1.0e-3], [0.04, 0.0, 0.0056],
+                               [xc0, 10.0e-3, 0.0056], [xc0, 10.0e-3, -1.0e-3]]])])
+
+
 SPECS = {
     "kalthoff2d": lambda: _kalthoff_spec(2),
     "kalthoff3d": lambda: _kalthoff_spec(3),
@@ -213,6 +239,7 @@ SPECS = {
     "column3d": _column_spec,
     "taylor3d": _taylor_spec,
     "branch2d": _branch_spec,
+    "fourpoint3d": _fourpoint_spec,
 }
 
 # BASELINE.json configs -> (spec, overrides); sizes per SURVEY.md 8(d)
@@ -224,6 +251,9 @@ WORKLOADS = {
     # C5: the shipped branch2d force-BC boxes are thinner than dp at this scale
     # (the reference's loader rejects it); built with lenient_targets=True
     "C5": ("branch2d", dict(dp_scale=0.0893, mapfac=2)),             # N = 128,135,336
+    # paper anchor (not a BASELINE config): the paper's own benchmark case at
+    # the 1M particles of its GPU-vs-CPU comparison
+    "P1": ("fourpoint3d", dict(dp_scale=1.26)),                       # N = 1,001,720
 }
 
 
@@ -308,7 +338,8 @@ def make_case(name, dp_scale=1.0, mapfac=None, eps0=None, cfl=None, dt_override=
         h = spec["coefh"] * dp_body * math.sqrt(dim)   # kernel_geom.py:21-27
         body = Body(mk=bspec["mk"], state=st, material=mat, dp_body=dp_body, h=h, dim=dim,
                     fracture=frac, notches=[Quad(points=q) for q in bspec["notches"]],
-                    nbsrange=cards.get("nbsrange"), f0=np.zeros(3))
+                    nbsrange=cards.get("nbsrange"), f0=np.zeros(3),
+                    restrictphi_expr=bspec.get("restrictphi"))
         for b in bspec["bcs"]:
             bc = BoundaryCondition(kind=b["kind"], ftype=b.get("ftype", 0), mkid=b.get("mkid"),
                                    const=tuple(b.get("const", (None, None, None))),

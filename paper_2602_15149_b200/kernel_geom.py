@@ -347,7 +347,13 @@ class StepLayout:
                                          P(self.halo), P(self.hslot), P(self.soff),
                                          P(self.slots), P(Xs), self.n_all, float(dp), P(keys)),
                    "tl_tile_slots_keyed")
-        ku = torch.unique(keys[:total].to(torch.int32) & 0xFFFF).cpu().numpy()
+        seen = torch.zeros(1 << 16, dtype=torch.bool, device=keys.device)
+        chunk = 1 << 26                     # bounded temporaries at 10^9 pairs (C5)
+        for c0 in range(0, total, chunk):
+            k = keys[c0:min(c0 + chunk, total)].to(torch.int32) & 0xFFFF
+            seen[k.long()] = True
+            del k
+        ku = torch.nonzero(seen).flatten().cpu().numpy()
         if (ku == self.KEY_OFF).any():
             return None
         ku = ku[ku != self.KEY_SELF]
@@ -384,6 +390,7 @@ class StepLayout:
                                     P(torch.from_numpy(cls_of_key).to(dev)), P(self.slots)),
                    "tl_class_slots")
         torch.cuda.current_stream().synchronize()
+        del keys
         dt = np.float32 if precision == "fp32" else np.float64
         return torch.from_numpy(table.astype(dt)).to(dev).contiguous()
 
