@@ -31,7 +31,7 @@ enum {
     TL_ERR_CASE = -4
 };
 
-#define TL_ABI_VERSION 10
+#define TL_ABI_VERSION 11
 
 int tl_abi_version(void);
 /* sizeof of the ABI structs, for binding checks: 0 tl_body, 1 tl_clock,
@@ -338,7 +338,8 @@ typedef struct {
     const double* ac;
     /* state */
     void* us;               /* records of 4: ux uy uz s        (pass-A gather) */
-    void* rb;               /* records of 12: (P L_i) row-major, vx vy vz (pass-B gather) */
+    void* rb;               /* records of 12 (pass-B gather): PL00 PL10 PL01 PL11 | PL02 PL12
+                               PL20 PL21 | vx vy vz PL22 (rows 0, 1 interleaved by column) */
     void* v;                /* 3 planes */
     void* al;               /* 9 planes: det(F) F^-1 L_i (viscosity) */
     void* sdot;             /* plane */
@@ -366,7 +367,39 @@ typedef struct {
                                   [5] restrictphi out of [0,1], [6] step of [3],
                                   [7] first step with non-finite u or v */
     double* pw_partial;        /* plastic-work block partials (J2) */
+    /* lattice-brick mode (3D lattice bodies with wide stencils; brick[0] = 0:
+     * off).  The CTA of brick t owns the lattice cells [o, o + brick) and
+     * stages the gather records of the (brick + 2 reach) box of cells around
+     * them, addressed by cell: no neighbour or slot tables.  Particle i's
+     * bonds are the set bits of bmask (class c = bit c, classes in the
+     * reference's CSR summation order); class c's partner sits at i's box
+     * cell + bdelta[c], and bbcls holds its geometry as the bond-class table
+     * above.  Grid = nbrick[0] * nbrick[1] * nbrick[2] CTAs of brick[0] *
+     * brick[1] * brick[2] threads, brick index z fastest. */
+    int32_t brick[3];          /* cells per brick and axis */
+    int32_t nbrick[3];         /* bricks per axis */
+    int32_t cells[3];          /* lattice cells per axis of the body's box */
+    int32_t reach;             /* max |q| per axis over the classes */
+    int32_t nbcls;             /* bond classes of the brick table */
+    int32_t nmask;             /* bond-mask words per particle */
+    const int32_t* cellmap;    /* cell (x slowest, z fastest) -> device position, -1 empty */
+    const uint32_t* bmask;     /* nmask planes of n_all words */
+    const int32_t* bdelta;     /* per class: box-cell offset of the partner */
+    const void* bbcls;         /* per class 2 Real4: (W, kappa), (U, 0) */
+    /* HOST copies of bdelta / bbcls: the launch passes the class table to the
+     * brick kernels as a kernel parameter (constant bank: the loop index is
+     * warp-uniform, so every class load is a broadcast); at most
+     * TL_BRICK_MAX_CLASSES classes */
+    const int32_t* bdelta_host;
+    const void* bbcls_host;
+    /* bcmask bit flagging the particles where the restrictphi expression is
+     * not skip (its skip pattern depends on x0, y0, z0 only); -1 = evaluate
+     * it on every particle */
+    int32_t restrict_bit;
+    int32_t pad_rb;
 } tl_body;
+
+#define TL_BRICK_MAX_CLASSES 256
 
 /* pass A: F (gated), stress model, history, Laplacian, s-ddot, P L_i and
  * Avis L_i.  Replaces deformation_gradient + update_stress +

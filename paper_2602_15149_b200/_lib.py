@@ -13,7 +13,7 @@ import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("TLSPH_LIB", os.path.join(HERE, "libtlsph.so"))
-ABI_VERSION = 10
+ABI_VERSION = 11
 
 _lib = None
 
@@ -82,6 +82,10 @@ _BODY_FIELDS += [(k, P) for k in ("Xs", "L", "V0", "m0", "ac", "us", "rb", "v", 
                                   "sdot", "sddot", "Hh", "Cpd", "epbar", "a", "F_out", "S_out",
                                   "psi_out", "psip_out", "perm", "bcmask", "bcs", "progs", "clock", "red",
                                   "counters", "pw_partial")]
+_BODY_FIELDS += [("brick", I32 * 3), ("nbrick", I32 * 3), ("cells", I32 * 3), ("reach", I32),
+                 ("nbcls", I32), ("nmask", I32), ("cellmap", P), ("bmask", P), ("bdelta", P),
+                 ("bbcls", P), ("bdelta_host", P), ("bbcls_host", P), ("restrict_bit", I32),
+                 ("pad_rb", I32)]
 
 
 class tl_body(C.Structure):

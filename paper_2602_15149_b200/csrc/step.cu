@@ -1114,6 +1114,151 @@ __device__ __forceinline__ void prefetch_own_b(const tl_body& b, int64_t p0) {
 // ---------------------------------------------------------------------------
 // pass A
 // ---------------------------------------------------------------------------
+// Pass A after the neighbour sums, shared by the tiled, L2-gather and brick
+// kernels: D = sum (u_j - u_i) (x) w r0 and M = sum (s_i - s_j) w r0 r0^T / r^2
+// (without the kernel constant) in, then F, the constitutive update, the phase
+// field, P L_i, the viscosity tensor and the pass-B record of particle i.
+// Returns this particle's plastic work increment dwp V0 (J2).
+template <typename R, int DIM, int MODEL, bool FRAC, int KIND>
+__device__ __forceinline__ double a_finish(const tl_body& b, int64_t i, R* D, R* M, R si,
+                                          bool gated) {
+    const int64_t N = b.n_all;
+    const bool uni = b.uniform != 0;
+    double pw = 0.0;
+    {   // kernel constant (and V0 when uniform), once per particle
+        const R ck = kshape_const<R, KIND>(b) * (uni ? R(b.V0c) : R(1));
+#pragma unroll
+        for (int q = 0; q < 9; ++q) D[q] *= ck;
+#pragma unroll
+        for (int q = 0; q < 6; ++q) M[q] *= R(2) * ck;
+    }
+    // L_i (9 planes)
+    R Li[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) Li[q] = planeR<R>(b.L, N, q, i);
+    // H = F - I = D L^T
+    R Hm[9];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+            Hm[3 * r + c] = D[3 * r] * Li[3 * c] + D[3 * r + 1] * Li[3 * c + 1] + D[3 * r + 2] * Li[3 * c + 2];
+    if (gated) {
+#pragma unroll
+        for (int q = 0; q < 9; ++q) Hm[q] = R(0);
+    }
+    // constitutive update
+    R S[9], psi = R(0), psip = R(0);
+    int bad = 0, noconv = 0;
+    if (MODEL == 1) {
+        noconv = svk_update<R>(Hm, R(b.lam), R(b.mu), si, FRAC, R(b.jac_tol), S, psi, psip);
+    } else if (MODEL == 2) {
+        bad = nh_update<R>(Hm, R(b.kappa), R(b.mu), si, FRAC, S, psi, psip);
+    } else {
+        double Fd[9], Cpd[6], Sd[9], psid, dwp;
+        bool nonspd;
+#pragma unroll
+        for (int q = 0; q < 9; ++q) Fd[q] = double(Hm[q]) + ((q % 4 == 0) ? 1.0 : 0.0);
+#pragma unroll
+        for (int q = 0; q < 6; ++q) Cpd[q] = double(planeR<R>(b.Cpd, N, q, i));
+        double epb = double(static_cast<const R*>(b.epbar)[i]);
+        bad = j2_update(Fd, Cpd, epb, b.mu, b.kappa, b.sigma_y0, b.H_hard, Sd, psid, dwp, nonspd);
+        if (nonspd) {
+            // the reference raises here (constitutive.py:191-194): no stress,
+            // no plastic update for this particle; pass B will not run
+#pragma unroll
+            for (int q = 0; q < 9; ++q) Sd[q] = 0.0;
+            psid = dwp = 0.0;
+            atomicMin((long long*)&b.counters[2], (long long)(b.perm ? b.perm[i] : i));
+            flag_step_error(b.clock, 1);
+        }
+#pragma unroll
+        for (int q = 0; q < 6; ++q) static_cast<R*>(b.Cpd)[q * N + i] = R(Cpd[q]);
+        static_cast<R*>(b.epbar)[i] = R(epb);
+#pragma unroll
+        for (int q = 0; q < 9; ++q) S[q] = R(Sd[q]);
+        psi = R(psid);
+        psip = R(0);
+        pw = dwp * (b.uniform ? b.V0c : b.V0[i]);
+    }
+    // phase field: history, Laplacian, s-ddot (fracture.py:12-43)
+    if (FRAC) {
+        R* Hh = static_cast<R*>(b.Hh);
+        const R Hn = fmax(psip, Hh[i]);
+        Hh[i] = Hn;
+        const R lap = Li[0] * M[0] + Li[4] * M[1] + Li[8] * M[2] + (Li[1] + Li[3]) * M[3] +
+                      (Li[2] + Li[6]) * M[4] + (Li[5] + Li[7]) * M[5];
+        // fracture.py:25-32 with the divisions as host-side reciprocals
+        const R eps0 = R(b.eps0), c0 = R(b.c0), ieps = R(b.inv_eps0);
+        const R ratio = Hn * R(b.inv_Gc);
+        const R damp = R(2) * sqrt(R(4) * eps0 * ratio + R(1)) * R(b.inv_c0);
+        const R sd = static_cast<const R*>(b.sdot)[i];
+        static_cast<R*>(b.sddot)[i] =
+            (R(0.5) * c0 * c0 * ieps) *
+            (R(2) * eps0 * lap + R(0.5) * (R(1) - si) * ieps - damp * sd - R(2) * si * ratio);
+    }
+    // P = F S = S + H S ; PL = P L_i
+    R P[9], PL[9];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+            P[3 * r + c] = S[3 * r + c] + (Hm[3 * r] * S[c] + Hm[3 * r + 1] * S[3 + c] + Hm[3 * r + 2] * S[6 + c]);
+    mm3(P, Li, PL);
+    // viscosity tensor: det(F) F^-1 = adj(F), zero when det F <= J_MIN
+    R* al = static_cast<R*>(b.al);
+    if (b.visc) {
+        R Fm[9], A[9];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) Fm[q] = Hm[q] + ((q % 4 == 0) ? R(1) : R(0));
+        const R J = R(1) + jm1_of(Hm);
+        if (J > R(TL_J_MIN)) {
+            R adj[9];
+            adj[0] = Fm[4] * Fm[8] - Fm[5] * Fm[7];
+            adj[1] = Fm[2] * Fm[7] - Fm[1] * Fm[8];
+            adj[2] = Fm[1] * Fm[5] - Fm[2] * Fm[4];
+            adj[3] = Fm[5] * Fm[6] - Fm[3] * Fm[8];
+            adj[4] = Fm[0] * Fm[8] - Fm[2] * Fm[6];
+            adj[5] = Fm[2] * Fm[3] - Fm[0] * Fm[5];
+            adj[6] = Fm[3] * Fm[7] - Fm[4] * Fm[6];
+            adj[7] = Fm[1] * Fm[6] - Fm[0] * Fm[7];
+            adj[8] = Fm[0] * Fm[4] - Fm[1] * Fm[3];
+            mm3(adj, Li, A);
+        } else {
+#pragma unroll
+            for (int q = 0; q < 9; ++q) A[q] = R(0);
+            bad += 1;
+        }
+#pragma unroll
+        for (int q = 0; q < 9; ++q) al[q * N + i] = A[q];
+    }
+    // pass-B gather record: PL (9) + v (3)
+    const R* vv = static_cast<const R*>(b.v);
+    R* rb = static_cast<R*>(b.rb) + 12 * i;
+    // RecB layout: rows 0 and 1 of PL interleaved by column (packed FP32x2
+    // sums in pass B), then row 2, v, PL22
+    tl::st4(rb, PL[0], PL[3], PL[1], PL[4]);
+    tl::st4(rb + 4, PL[2], PL[5], PL[6], PL[7]);
+    tl::st4(rb + 8, vv[i], vv[N + i], vv[2 * N + i], PL[8]);
+    if (mirror_out(b)) {
+#pragma unroll
+        for (int q = 0; q < 9; ++q) {
+            b.F_out[9 * i + q] = double(Hm[q]) + ((q % 4 == 0) ? 1.0 : 0.0);
+            b.S_out[9 * i + q] = double(S[q]);
+        }
+        b.psi_out[i] = double(psi);
+        b.psip_out[i] = double(psip);
+    }
+    if (bad || noconv) {
+        if (bad) atomicAdd((unsigned long long*)&b.counters[0], (unsigned long long)bad);
+        if (noconv) {
+            atomicAdd((unsigned long long*)&b.counters[1], 1ull);
+            flag_step_error(b.clock, 1);
+        }
+    }
+    return pw;
+}
+
 template <typename R, int DIM, int MODEL, bool FRAC, int KIND, int G, bool TILED>
 __global__ void __launch_bounds__(kThreads, TL_MINB_A(R, TILED)) k_pass_a(const tl_body b) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -1232,137 +1377,7 @@ __global__ void __launch_bounds__(kThreads, TL_MINB_A(R, TILED)) k_pass_a(const 
                                                D, M);
             }
         }
-        {   // kernel constant (and V0 when uniform), once per particle
-            const R ck = kshape_const<R, KIND>(b) * (uni ? R(b.V0c) : R(1));
-#pragma unroll
-            for (int q = 0; q < 9; ++q) D[q] *= ck;
-#pragma unroll
-            for (int q = 0; q < 6; ++q) M[q] *= R(2) * ck;
-        }
-        // L_i (9 planes)
-        R Li[9];
-#pragma unroll
-        for (int q = 0; q < 9; ++q) Li[q] = planeR<R>(b.L, N, q, i);
-        // H = F - I = D L^T
-        R Hm[9];
-#pragma unroll
-        for (int r = 0; r < 3; ++r)
-#pragma unroll
-            for (int c = 0; c < 3; ++c)
-                Hm[3 * r + c] = D[3 * r] * Li[3 * c] + D[3 * r + 1] * Li[3 * c + 1] + D[3 * r + 2] * Li[3 * c + 2];
-        if (gated) {
-#pragma unroll
-            for (int q = 0; q < 9; ++q) Hm[q] = R(0);
-        }
-        // constitutive update
-        R S[9], psi = R(0), psip = R(0);
-        int bad = 0, noconv = 0;
-        if (MODEL == 1) {
-            noconv = svk_update<R>(Hm, R(b.lam), R(b.mu), si, FRAC, R(b.jac_tol), S, psi, psip);
-        } else if (MODEL == 2) {
-            bad = nh_update<R>(Hm, R(b.kappa), R(b.mu), si, FRAC, S, psi, psip);
-        } else {
-            double Fd[9], Cpd[6], Sd[9], psid, dwp;
-            bool nonspd;
-#pragma unroll
-            for (int q = 0; q < 9; ++q) Fd[q] = double(Hm[q]) + ((q % 4 == 0) ? 1.0 : 0.0);
-#pragma unroll
-            for (int q = 0; q < 6; ++q) Cpd[q] = double(planeR<R>(b.Cpd, N, q, i));
-            double epb = double(static_cast<const R*>(b.epbar)[i]);
-            bad = j2_update(Fd, Cpd, epb, b.mu, b.kappa, b.sigma_y0, b.H_hard, Sd, psid, dwp, nonspd);
-            if (nonspd) {
-                // the reference raises here (constitutive.py:191-194): no stress,
-                // no plastic update for this particle; pass B will not run
-#pragma unroll
-                for (int q = 0; q < 9; ++q) Sd[q] = 0.0;
-                psid = dwp = 0.0;
-                atomicMin((long long*)&b.counters[2], (long long)(b.perm ? b.perm[i] : i));
-                flag_step_error(b.clock, 1);
-            }
-#pragma unroll
-            for (int q = 0; q < 6; ++q) static_cast<R*>(b.Cpd)[q * N + i] = R(Cpd[q]);
-            static_cast<R*>(b.epbar)[i] = R(epb);
-#pragma unroll
-            for (int q = 0; q < 9; ++q) S[q] = R(Sd[q]);
-            psi = R(psid);
-            psip = R(0);
-            pw = dwp * (b.uniform ? b.V0c : b.V0[i]);
-        }
-        // phase field: history, Laplacian, s-ddot (fracture.py:12-43)
-        if (FRAC) {
-            R* Hh = static_cast<R*>(b.Hh);
-            const R Hn = fmax(psip, Hh[i]);
-            Hh[i] = Hn;
-            const R lap = Li[0] * M[0] + Li[4] * M[1] + Li[8] * M[2] + (Li[1] + Li[3]) * M[3] +
-                          (Li[2] + Li[6]) * M[4] + (Li[5] + Li[7]) * M[5];
-            // fracture.py:25-32 with the divisions as host-side reciprocals
-            const R eps0 = R(b.eps0), c0 = R(b.c0), ieps = R(b.inv_eps0);
-            const R ratio = Hn * R(b.inv_Gc);
-            const R damp = R(2) * sqrt(R(4) * eps0 * ratio + R(1)) * R(b.inv_c0);
-            const R sd = static_cast<const R*>(b.sdot)[i];
-            static_cast<R*>(b.sddot)[i] =
-                (R(0.5) * c0 * c0 * ieps) *
-                (R(2) * eps0 * lap + R(0.5) * (R(1) - si) * ieps - damp * sd - R(2) * si * ratio);
-        }
-        // P = F S = S + H S ; PL = P L_i
-        R P[9], PL[9];
-#pragma unroll
-        for (int r = 0; r < 3; ++r)
-#pragma unroll
-            for (int c = 0; c < 3; ++c)
-                P[3 * r + c] = S[3 * r + c] + (Hm[3 * r] * S[c] + Hm[3 * r + 1] * S[3 + c] + Hm[3 * r + 2] * S[6 + c]);
-        mm3(P, Li, PL);
-        // viscosity tensor: det(F) F^-1 = adj(F), zero when det F <= J_MIN
-        R* al = static_cast<R*>(b.al);
-        if (b.visc) {
-            R Fm[9], A[9];
-#pragma unroll
-            for (int q = 0; q < 9; ++q) Fm[q] = Hm[q] + ((q % 4 == 0) ? R(1) : R(0));
-            const R J = R(1) + jm1_of(Hm);
-            if (J > R(TL_J_MIN)) {
-                R adj[9];
-                adj[0] = Fm[4] * Fm[8] - Fm[5] * Fm[7];
-                adj[1] = Fm[2] * Fm[7] - Fm[1] * Fm[8];
-                adj[2] = Fm[1] * Fm[5] - Fm[2] * Fm[4];
-                adj[3] = Fm[5] * Fm[6] - Fm[3] * Fm[8];
-                adj[4] = Fm[0] * Fm[8] - Fm[2] * Fm[6];
-                adj[5] = Fm[2] * Fm[3] - Fm[0] * Fm[5];
-                adj[6] = Fm[3] * Fm[7] - Fm[4] * Fm[6];
-                adj[7] = Fm[1] * Fm[6] - Fm[0] * Fm[7];
-                adj[8] = Fm[0] * Fm[4] - Fm[1] * Fm[3];
-                mm3(adj, Li, A);
-            } else {
-#pragma unroll
-                for (int q = 0; q < 9; ++q) A[q] = R(0);
-                bad += 1;
-            }
-#pragma unroll
-            for (int q = 0; q < 9; ++q) al[q * N + i] = A[q];
-        }
-        // pass-B gather record: PL (9) + v (3)
-        const R* vv = static_cast<const R*>(b.v);
-        R* rb = static_cast<R*>(b.rb) + 12 * i;
-        // RecB layout: rows 0 and 1 of PL interleaved by column (packed FP32x2
-        // sums in pass B), then row 2, v, PL22
-        tl::st4(rb, PL[0], PL[3], PL[1], PL[4]);
-        tl::st4(rb + 4, PL[2], PL[5], PL[6], PL[7]);
-        tl::st4(rb + 8, vv[i], vv[N + i], vv[2 * N + i], PL[8]);
-        if (mirror_out(b)) {
-#pragma unroll
-            for (int q = 0; q < 9; ++q) {
-                b.F_out[9 * i + q] = double(Hm[q]) + ((q % 4 == 0) ? 1.0 : 0.0);
-                b.S_out[9 * i + q] = double(S[q]);
-            }
-            b.psi_out[i] = double(psi);
-            b.psip_out[i] = double(psip);
-        }
-        if (bad || noconv) {
-            if (bad) atomicAdd((unsigned long long*)&b.counters[0], (unsigned long long)bad);
-            if (noconv) {
-                atomicAdd((unsigned long long*)&b.counters[1], 1ull);
-                flag_step_error(b.clock, 1);
-            }
-        }
+        pw = a_finish<R, DIM, MODEL, FRAC, KIND>(b, i, D, M, si, gated);
     }
     if (MODEL == 3) {
         // deterministic block partial of sum(dwp * V0)
@@ -1495,14 +1510,22 @@ __device__ __noinline__ double restrict_floor(const BcCtx b, D3 X0, D3 u, double
 
 // sdot += dtr*sddot; s += dts*sdot; clamp [0,1]; restrictphi floor
 // (stepper.py:125-130, fracture.py:66-83)
+// restrictphi applies to this particle: the expression is set and either
+// its skip pattern is not static or the particle carries the restrict bit
+// (the host found the expression non-skip there, simulation.py _setup_bcs)
+__device__ __forceinline__ bool restrict_applies(const tl_body& b, uint32_t mask) {
+    return b.restrict_prog >= 0 && (b.restrict_bit < 0 || ((mask >> b.restrict_bit) & 1u));
+}
+
 template <typename R, bool RESTRICT = true>
 __device__ __forceinline__ void advance_phase(const tl_body& b, R& s, R& sd, R sdd, double dts,
-                                              double dtr, D3 X0, D3 u, double t, double dt) {
+                                              double dtr, D3 X0, D3 u, double t, double dt,
+                                              uint32_t mask) {
     sd = tl::axpy_rn(sd, R(dtr), sdd);
     s = tl::axpy_rn(s, R(dts), sd);
     if (s < R(0)) { s = R(0); sd = R(0); }
     if (s > R(1)) { s = R(1); sd = R(0); }
-    if (RESTRICT && b.restrict_prog >= 0) {
+    if (RESTRICT && restrict_applies(b, mask)) {
         const double fl = restrict_floor(bc_ctx(b), X0, u, t, dt);
         if (fl >= 0.0 && double(s) < fl) {
             s = R(fl);
@@ -1550,7 +1573,7 @@ __device__ __forceinline__ EpiOut epi_body(const tl_body& b, int64_t i, uint32_t
     const double tf = MODE == TL_B_INIT ? 0.0 : (MODE == TL_B_SYMPL ? t0 + 0.5 * dt : t0);
     const double dtf = MODE == TL_B_INIT ? 0.0 : dt;
     // reference positions only feed boundary-condition / restrictphi expressions
-    const bool need_x = has_bc || (BC && FRAC && b.restrict_prog >= 0);
+    const bool need_x = has_bc || (BC && FRAC && restrict_applies(b, mask));
     const D3 X0 = need_x ? D3{b.Xs[i], b.Xs[N + i], b.Xs[2 * N + i]} : D3{0.0, 0.0, 0.0};
     const D3 u0{double(ui.x), double(ui.y), double(ui.z)};
     if (has_bc) {
@@ -1590,7 +1613,7 @@ __device__ __forceinline__ EpiOut epi_body(const tl_body& b, int64_t i, uint32_t
             const R sdd = static_cast<const R*>(b.sddot)[i];
             advance_phase<R, BC>(b, s, sd, sdd, kick, kick, X0,
                              D3{double(us_new[0]), double(us_new[1]), double(us_new[2])},
-                             t_new, dt);
+                             t_new, dt, mask);
             us_new[3] = s;
             sdp[i] = sd;
         }
@@ -1634,6 +1657,51 @@ __device__ __noinline__ EpiOut epi_slow(const tl_body* b, int64_t i, uint32_t ma
 // stencil's tile holds ~13 halo records per member, so shared memory allows
 // one CTA per SM: the split gives it SPLIT times the warps to hide the
 // shared-memory load latency of the pair loop.
+// Pass B after the neighbour sums s1 = sum w r0, s2 = sum w PL_j r0, s3 =
+// sum pi w r0 (without the kernel constant), shared by the tiled, L2-gather
+// and brick kernels: the internal acceleration, then the particle's update
+// (epi_body; the rare particles with BCs / restrictphi out of line).
+template <typename R, int DIM, int MODE, bool FRAC, int KIND>
+__device__ __forceinline__ EpiOut b_finish(const tl_body& b, int64_t i, R* s1, R* s2, R* s3,
+                                           const R* PLi, R vi0, R vi1, R vi2) {
+    const int64_t N = b.n_all;
+    const bool uni = b.uniform != 0;
+    const bool visc = b.visc != 0;
+    const R inv_rho = R(1.0 / b.rho0);
+    {   // kernel constant (and m0 when uniform), once per particle
+        const R ck = kshape_const<R, KIND>(b) * (uni ? R(b.m0c) : R(1));
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            s1[q] *= ck;
+            s2[q] *= ck;
+            s3[q] *= ck * inv_rho;
+        }
+    }
+    // a_int = (PL_i s1 + s2)/rho0^2 - AL_i s3
+    const R inv_rho2 = inv_rho * inv_rho;
+    double acc[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        R t = (PLi[3 * a] * s1[0] + PLi[3 * a + 1] * s1[1] + PLi[3 * a + 2] * s1[2] + s2[a]) * inv_rho2;
+        if (visc) {
+            const R* al = static_cast<const R*>(b.al);
+            t -= al[(3 * a) * N + i] * s3[0] + al[(3 * a + 1) * N + i] * s3[1] +
+                 al[(3 * a + 2) * N + i] * s3[2];
+        }
+        acc[a] = double(t);
+    }
+    // the rest of the particle's update: boundary conditions / restrictphi
+    // expressions only on the (rare) particles that carry them, out of
+    // line, so the common path holds no call frame
+    const uint32_t mask = b.bcmask ? b.bcmask[i] : 0u;
+    const bool slow = (b.nbc && (mask || b.bc_whole)) || (FRAC && restrict_applies(b, mask));
+    const EpiOut o = slow ? epi_slow<R, DIM, MODE, FRAC>(&b, i, mask, acc[0], acc[1], acc[2],
+                                                         vi0, vi1, vi2)
+                          : epi_body<R, DIM, MODE, FRAC, false>(b, i, mask, acc[0], acc[1],
+                                                                acc[2], vi0, vi1, vi2);
+    return o;
+}
+
 template <int SPLIT>
 constexpr int b_threads() { return SPLIT > 1 ? 1024 : kThreads; }
 
@@ -1803,44 +1871,284 @@ if (visc) TL_LOOP_B(U, ST, true); else TL_LOOP_B(U, ST, false)
             }
         }
         if (live) {   // the dead lanes of a split tile still join the warp reductions
-            {   // kernel constant (and m0 when uniform), once per particle
-                const R ck = kshape_const<R, KIND>(b) * (uni ? R(b.m0c) : R(1));
-#pragma unroll
-                for (int q = 0; q < 3; ++q) {
-                    s1[q] *= ck;
-                    s2[q] *= ck;
-                    s3[q] *= ck * inv_rho;
-                }
-            }
-            // a_int = (PL_i s1 + s2)/rho0^2 - AL_i s3
             const auto r0i = TILED ? tl_.rec[3 * ms] : tl::ld4(rbp + 12 * i);
             const auto r1i = TILED ? tl_.rec[3 * ms + 1] : tl::ld4(rbp + 12 * i + 4);
             const R PLi[9] = {r0i.x, r0i.z, r1i.x, r0i.y, r0i.w, r1i.y, r1i.z, r1i.w, r2i.w};
-            const R inv_rho2 = inv_rho * inv_rho;
-            double acc[3];
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                R t = (PLi[3 * a] * s1[0] + PLi[3 * a + 1] * s1[1] + PLi[3 * a + 2] * s1[2] + s2[a]) * inv_rho2;
-                if (visc) {
-                    const R* al = static_cast<const R*>(b.al);
-                    t -= al[(3 * a) * N + i] * s3[0] + al[(3 * a + 1) * N + i] * s3[1] +
-                         al[(3 * a + 2) * N + i] * s3[2];
-                }
-                acc[a] = double(t);
-            }
-            // the rest of the particle's update: boundary conditions / restrictphi
-            // expressions only on the (rare) particles that carry them, out of
-            // line, so the common path holds no call frame
-            const uint32_t mask = b.bcmask ? b.bcmask[i] : 0u;
-            const bool slow = (b.nbc && (mask || b.bc_whole)) || (FRAC && b.restrict_prog >= 0);
-            const EpiOut o = slow ? epi_slow<R, DIM, MODE, FRAC>(&b, i, mask, acc[0], acc[1], acc[2],
-                                                                 vi0, vi1, vi2)
-                                  : epi_body<R, DIM, MODE, FRAC, false>(b, i, mask, acc[0], acc[1],
-                                                                        acc[2], vi0, vi1, vi2);
+            const EpiOut o = b_finish<R, DIM, MODE, FRAC, KIND>(b, i, s1, s2, s3, PLi, vi0, vi1, vi2);
             v2 = fmax(v2, o.v2);
             a2 = fmax(a2, o.a2);
             bad_acc = min(bad_acc, o.bad);
         }
+    }
+    v2 = tl::warp_max(v2);
+    a2 = tl::warp_max(a2);
+    bad_acc = tl::warp_min_ll(bad_acc);
+    if ((threadIdx.x & 31) == 0) {
+        tl::atomic_max_nonneg(&b.red[0], v2);
+        tl::atomic_max_nonneg(&b.red[1], a2);
+        if (bad_acc != LLONG_MAX) atomicMin((long long*)&b.counters[3], bad_acc);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// lattice-brick kernels (tl_body.brick): 3D lattice bodies with wide stencils
+// ---------------------------------------------------------------------------
+// A radial 3D stencil (k ~ 170) carries ~170 slot entries per particle in the
+// tiled kernels -- more bytes than the particle's own state -- and a halo of
+// ~13 records per member.  A body cut from one lattice needs neither: the
+// CTA of a brick of lattice cells stages the records of the box of cells
+// around it *by cell*, so a bond of class c (lattice offset q_c) is a fixed
+// box offset from the member's cell, the same for every member.  Per
+// particle only the bond mask (one bit per class, the reference CSR's
+// membership: notches and body edges) is read; per pair a broadcast class
+// load and the partner's records from shared memory.  Classes run in the
+// reference's CSR order, so sums keep its summation order.
+struct BrickGeo {
+    int SX, SY, SZ, S;     // staged box (cells)
+    int ox, oy, oz;        // box origin (global cell)
+    int tx, ty, tz;        // this thread's member cell within the brick
+};
+
+__device__ __forceinline__ BrickGeo brick_geo(const tl_body& b, int64_t t) {
+    BrickGeo g;
+    const int Rr = b.reach;
+    g.SX = b.brick[0] + 2 * Rr;
+    g.SY = b.brick[1] + 2 * Rr;
+    g.SZ = b.brick[2] + 2 * Rr;
+    g.S = g.SX * g.SY * g.SZ;
+    const int bz = (int)(t % b.nbrick[2]);
+    const int by = (int)((t / b.nbrick[2]) % b.nbrick[1]);
+    const int bx = (int)(t / ((int64_t)b.nbrick[2] * b.nbrick[1]));
+    g.ox = bx * b.brick[0] - Rr;
+    g.oy = by * b.brick[1] - Rr;
+    g.oz = bz * b.brick[2] - Rr;
+    const int tid = (int)threadIdx.x;
+    g.tz = tid % b.brick[2];
+    g.ty = (tid / b.brick[2]) % b.brick[1];
+    g.tx = tid / (b.brick[2] * b.brick[1]);
+    return g;
+}
+
+__device__ __forceinline__ int64_t cell_particle(const tl_body& b, int gx, int gy, int gz) {
+    if (gx < 0 || gy < 0 || gz < 0 || gx >= b.cells[0] || gy >= b.cells[1] || gz >= b.cells[2])
+        return -1;
+    return b.cellmap[((int64_t)gx * b.cells[1] + gy) * b.cells[2] + gz];
+}
+
+// The class table rides in the kernel parameters (constant bank): the class
+// loop is warp-uniform, so each class's W / U / box offset is one broadcast
+// constant load with no shared-memory round trip ahead of the record loads.
+template <typename R>
+struct BrickTab {
+    V4<R> W[TL_BRICK_MAX_CLASSES];   // (W, kappa)
+    V4<R> U[TL_BRICK_MAX_CLASSES];   // (U, 0)
+    int d[TL_BRICK_MAX_CLASSES];     // box-cell offset of the partner
+};
+
+// stage the NREC records of every occupied box cell (LDGSTS gathers; empty
+// cells are never read)
+template <typename R, int NREC>
+__device__ __forceinline__ void stage_brick(const tl_body& b, const BrickGeo& g, const R* src,
+                                            V4<R>* rec) {
+    const int nt = (int)blockDim.x;
+    constexpr int CH = (int)(sizeof(V4<R>) / 16) * NREC;   // 16-byte chunks per cell
+    for (int sc = threadIdx.x; sc < g.S; sc += nt) {
+        const int sz = sc % g.SZ, sy = (sc / g.SZ) % g.SY, sx = sc / (g.SZ * g.SY);
+        const int64_t q = cell_particle(b, g.ox + sx, g.oy + sy, g.oz + sz);
+        if (q >= 0) {
+            const char* gp = reinterpret_cast<const char*>(src + q * 4 * NREC);
+            char* sp = reinterpret_cast<char*>(rec + (int64_t)sc * NREC);
+#pragma unroll
+            for (int c = 0; c < CH; ++c) tl::cp_async16(sp + 16 * c, gp + 16 * c);
+        }
+    }
+    tl::cp_async_wait_all();
+    __syncthreads();
+}
+
+// visit particle i's bonds in class order: a warp-uniform loop over the
+// classes, predicated on the particle's mask bit (interior particles have
+// every bit set; edges and notches clear some)
+template <typename F>
+__device__ __forceinline__ void each_bond(const tl_body& b, int64_t i, bool live, F&& pair) {
+    const int64_t N = b.n_all;
+    const int nc = b.nbcls;
+    for (int w = 0; w < b.nmask; ++w) {
+        const uint32_t m = live ? b.bmask[w * N + i] : 0u;
+        const int cend = min(32, nc - 32 * w);
+#pragma unroll 4
+        for (int j = 0; j < cend; ++j)
+            if ((m >> j) & 1u) pair(32 * w + j);
+    }
+}
+
+template <typename R, int MODEL, bool FRAC, int KIND>
+__global__ void __launch_bounds__(1024, 1)
+    k_brick_a(const __grid_constant__ tl_body b, const __grid_constant__ BrickTab<R> tab) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ double s_pw[32];
+    if (halted(b)) return;
+    const int64_t t = blockIdx.x;
+    const BrickGeo g = brick_geo(b, t);
+    V4<R>* rec = reinterpret_cast<V4<R>*>(smem);
+    stage_brick<R, 1>(b, g, static_cast<const R*>(b.us), rec);
+    const int64_t i = cell_particle(b, g.ox + b.reach + g.tx, g.oy + b.reach + g.ty,
+                                    g.oz + b.reach + g.tz);
+    const bool live = i >= 0 && i < b.n;
+    const int me = ((g.tx + b.reach) * g.SY + g.ty + b.reach) * g.SZ + g.tz + b.reach;
+    const V4<R> ui = rec[me];
+    const R si = ui.w;
+    R D[9], M[6];
+    if constexpr (sizeof(R) == 4) {
+        // packed FP32x2 as loop_a_geo_f2
+        float2 D01 = make_float2(0.f, 0.f), D34 = D01, D67 = D01, D25 = D01, M01 = D01;
+        float D8 = 0.f, M2 = 0.f, M3 = 0.f, M4 = 0.f, M5 = 0.f;
+        const float2 nui = make_float2(-float(ui.x), -float(ui.y));
+        const float nuz = -float(ui.z), uis = float(ui.w);
+        const float4* rf = reinterpret_cast<const float4*>(rec);
+        each_bond(b, i, live, [&](int c) {
+            const float4 W = reinterpret_cast<const float4&>(tab.W[c]);
+            const float4 uj = rf[me + tab.d[c]];
+            const float2 wxy = make_float2(W.x, W.y);
+            const float2 du01 = __fadd2_rn(make_float2(uj.x, uj.y), nui);
+            const float du2 = uj.z + nuz;
+            D01 = __ffma2_rn(make_float2(du01.x, du01.x), wxy, D01);
+            D34 = __ffma2_rn(make_float2(du01.y, du01.y), wxy, D34);
+            D67 = __ffma2_rn(make_float2(du2, du2), wxy, D67);
+            D25 = __ffma2_rn(du01, make_float2(W.z, W.z), D25);
+            D8 = fmaf(du2, W.z, D8);
+            if (FRAC) {
+                const float4 U = reinterpret_cast<const float4&>(tab.U[c]);
+                const float ds = uis - uj.w;
+                const float2 cw = __fmul2_rn(make_float2(ds, ds), wxy);
+                const float cz = ds * W.z;
+                M01 = __ffma2_rn(cw, make_float2(U.x, U.y), M01);
+                M2 = fmaf(cz, U.z, M2);
+                M3 = fmaf(cw.x, U.y, M3);
+                M4 = fmaf(cw.x, U.z, M4);
+                M5 = fmaf(cw.y, U.z, M5);
+            }
+        });
+        D[0] = R(D01.x); D[1] = R(D01.y); D[2] = R(D25.x);
+        D[3] = R(D34.x); D[4] = R(D34.y); D[5] = R(D25.y);
+        D[6] = R(D67.x); D[7] = R(D67.y); D[8] = R(D8);
+        M[0] = R(M01.x); M[1] = R(M01.y); M[2] = R(M2); M[3] = R(M3); M[4] = R(M4); M[5] = R(M5);
+    } else {
+#pragma unroll
+        for (int q = 0; q < 9; ++q) D[q] = R(0);
+#pragma unroll
+        for (int q = 0; q < 6; ++q) M[q] = R(0);
+        each_bond(b, i, live, [&](int c) {
+            const V4<R> W = tab.W[c];
+            const V4<R> uj = rec[me + tab.d[c]];
+            const R du0 = uj.x - ui.x, du1 = uj.y - ui.y, du2 = uj.z - ui.z;
+            D[0] = fma(du0, W.x, D[0]); D[1] = fma(du0, W.y, D[1]); D[2] = fma(du0, W.z, D[2]);
+            D[3] = fma(du1, W.x, D[3]); D[4] = fma(du1, W.y, D[4]); D[5] = fma(du1, W.z, D[5]);
+            D[6] = fma(du2, W.x, D[6]); D[7] = fma(du2, W.y, D[7]); D[8] = fma(du2, W.z, D[8]);
+            if (FRAC) {
+                const V4<R> U = tab.U[c];
+                const R ds = si - uj.w;
+                const R cx = ds * W.x, cy = ds * W.y, cz = ds * W.z;
+                M[0] = fma(cx, U.x, M[0]); M[1] = fma(cy, U.y, M[1]); M[2] = fma(cz, U.z, M[2]);
+                M[3] = fma(cx, U.y, M[3]); M[4] = fma(cx, U.z, M[4]); M[5] = fma(cy, U.z, M[5]);
+            }
+        });
+    }
+    double pw = 0.0;
+    if (live) pw = a_finish<R, 3, MODEL, FRAC, KIND>(b, i, D, M, si, FRAC && si <= R(b.s_l));
+    if (MODEL == 3) {   // deterministic CTA partial of sum(dwp * V0)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) pw += __shfl_xor_sync(0xffffffffu, pw, o);
+        if ((threadIdx.x & 31) == 0) s_pw[threadIdx.x >> 5] = pw;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double acc = 0.0;
+            for (int k = 0; k < (int)((blockDim.x + 31) >> 5); ++k) acc += s_pw[k];
+            b.pw_partial[t] = acc;
+        }
+    }
+}
+
+template <typename R, int MODE, bool FRAC, int KIND>
+__global__ void __launch_bounds__(1024, 1)
+    k_brick_b(const __grid_constant__ tl_body b, const __grid_constant__ BrickTab<R> tab) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    if (halted(b) || stress_failed(b)) return;
+    const int64_t t = blockIdx.x;
+    const BrickGeo g = brick_geo(b, t);
+    V4<R>* rec = reinterpret_cast<V4<R>*>(smem);
+    stage_brick<R, 3>(b, g, static_cast<const R*>(b.rb), rec);
+    const int64_t i = cell_particle(b, g.ox + b.reach + g.tx, g.oy + b.reach + g.ty,
+                                    g.oz + b.reach + g.tz);
+    const bool live = i >= 0 && i < b.n;
+    const int me = ((g.tx + b.reach) * g.SY + g.ty + b.reach) * g.SZ + g.tz + b.reach;
+    const V4<R> r2i = rec[3 * me + 2];
+    const R vi0 = r2i.x, vi1 = r2i.y, vi2 = r2i.z;
+    const bool visc = b.visc != 0;
+    const R B1 = R(b.beta1 * b.c0 * b.h), B2 = R(b.beta2 * b.h * b.h);
+    R s1[3], s2[3], s3[3];
+    if constexpr (sizeof(R) == 4) {
+        float2 s1a = make_float2(0.f, 0.f), s2a = s1a, s3a = s1a;
+        float s1b = 0.f, s2b = 0.f, s3b = 0.f;
+        const float2 vi01 = make_float2(float(vi0), float(vi1));
+        const float2 neg1 = make_float2(-1.f, -1.f);
+        const float fvi2 = float(vi2), fB1 = float(B1), fB2 = float(B2);
+        const float4* rf = reinterpret_cast<const float4*>(rec);
+        auto pair = [&](int c, auto V_) {
+            constexpr bool V = decltype(V_)::value;
+            const float4 W = reinterpret_cast<const float4&>(tab.W[c]);
+            const int o = 3 * (me + tab.d[c]);
+            const float4 q0 = rf[o], q1 = rf[o + 1], q2 = rf[o + 2];
+            const float2 wxy = make_float2(W.x, W.y);
+            s1a = __fadd2_rn(s1a, wxy);
+            s1b += W.z;
+            s2a = __ffma2_rn(make_float2(q0.x, q0.y), make_float2(W.x, W.x), s2a);
+            s2a = __ffma2_rn(make_float2(q0.z, q0.w), make_float2(W.y, W.y), s2a);
+            s2a = __ffma2_rn(make_float2(q1.x, q1.y), make_float2(W.z, W.z), s2a);
+            s2b = fmaf(q2.w, W.z, fmaf(q1.w, W.y, fmaf(q1.z, W.x, s2b)));
+            if (V) {
+                const float2 dv = __ffma2_rn(make_float2(q2.x, q2.y), neg1, vi01);
+                const float2 pr = __fmul2_rn(dv, wxy);
+                const float dvw = fmaf(fvi2 - q2.z, W.z, pr.x + pr.y);
+                const float gg = dvw * W.w;
+                const float pw = (fB2 * gg - fB1) * gg;
+                s3a = __ffma2_rn(make_float2(pw, pw), wxy, s3a);
+                s3b = fmaf(pw, W.z, s3b);
+            }
+        };
+        if (visc) each_bond(b, i, live, [&](int c) { pair(c, std::true_type{}); });
+        else each_bond(b, i, live, [&](int c) { pair(c, std::false_type{}); });
+        s1[0] = R(s1a.x); s1[1] = R(s1a.y); s1[2] = R(s1b);
+        s2[0] = R(s2a.x); s2[1] = R(s2a.y); s2[2] = R(s2b);
+        s3[0] = R(s3a.x); s3[1] = R(s3a.y); s3[2] = R(s3b);
+    } else {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) s1[q] = s2[q] = s3[q] = R(0);
+        each_bond(b, i, live, [&](int c) {
+            const V4<R> W = tab.W[c];
+            const int o = 3 * (me + tab.d[c]);
+            const V4<R> q0 = rec[o], q1 = rec[o + 1], q2 = rec[o + 2];
+            s1[0] += W.x; s1[1] += W.y; s1[2] += W.z;
+            s2[0] = fma(q1.x, W.z, fma(q0.z, W.y, fma(q0.x, W.x, s2[0])));
+            s2[1] = fma(q1.y, W.z, fma(q0.w, W.y, fma(q0.y, W.x, s2[1])));
+            s2[2] = fma(q2.w, W.z, fma(q1.w, W.y, fma(q1.z, W.x, s2[2])));
+            if (visc) {
+                const R dvw = (vi0 - q2.x) * W.x + (vi1 - q2.y) * W.y + (vi2 - q2.z) * W.z;
+                const R gg = dvw * W.w;
+                const R pw = (B2 * gg - B1) * gg;
+                s3[0] = fma(pw, W.x, s3[0]); s3[1] = fma(pw, W.y, s3[1]); s3[2] = fma(pw, W.z, s3[2]);
+            }
+        });
+    }
+    double v2 = 0.0, a2 = 0.0;
+    long long bad_acc = LLONG_MAX;
+    if (live) {
+        const V4<R> r0i = rec[3 * me], r1i = rec[3 * me + 1];
+        const R PLi[9] = {r0i.x, r0i.z, r1i.x, r0i.y, r0i.w, r1i.y, r1i.z, r1i.w, r2i.w};
+        const EpiOut o = b_finish<R, 3, MODE, FRAC, KIND>(b, i, s1, s2, s3, PLi, vi0, vi1, vi2);
+        v2 = o.v2;
+        a2 = o.a2;
+        bad_acc = o.bad;
     }
     v2 = tl::warp_max(v2);
     a2 = tl::warp_max(a2);
@@ -1879,7 +2187,7 @@ __global__ void __launch_bounds__(kThreads) k_predict(const tl_body b) {
         R* sdp = static_cast<R*>(b.sdot);
         R sd = sdp[i], s = ui.w;
         advance_phase<R>(b, s, sd, static_cast<const R*>(b.sddot)[i], half, half, X0,
-                         D3{double(un[0]), double(un[1]), double(un[2])}, th, dt);
+                         D3{double(un[0]), double(un[1]), double(un[2])}, th, dt, mask);
         un[3] = s;
         sdp[i] = sd;
     }
@@ -1971,9 +2279,44 @@ int smem_opt_in(K kernel, size_t bytes) {
     return TL_OK;
 }
 
+template <typename R, typename K>
+int launch_brick(K kern, cudaStream_t st, const tl_body& b, int nrec) {
+    const int T = b.brick[0] * b.brick[1] * b.brick[2];
+    if (T <= 0 || T > 1024 || b.nbcls <= 0 || b.nbcls > TL_BRICK_MAX_CLASSES || b.nmask <= 0 ||
+        b.nmask * 32 < b.nbcls || !b.bdelta_host || !b.bbcls_host) {
+        tl_set_error("tl_body: invalid brick descriptor");
+        return TL_ERR_ARG;
+    }
+    BrickTab<R> tab;
+    const V4<R>* hc = static_cast<const V4<R>*>(b.bbcls_host);
+    for (int c = 0; c < TL_BRICK_MAX_CLASSES; ++c) {
+        if (c < b.nbcls) {
+            tab.W[c] = hc[2 * c];
+            tab.U[c] = hc[2 * c + 1];
+            tab.d[c] = b.bdelta_host[c];
+        } else {
+            tab.W[c] = tab.U[c] = V4<R>{};
+            tab.d[c] = 0;
+        }
+    }
+    const int S = (b.brick[0] + 2 * b.reach) * (b.brick[1] + 2 * b.reach) * (b.brick[2] + 2 * b.reach);
+    const size_t bytes = (size_t)S * nrec * sizeof(V4<R>);
+    int rc = smem_opt_in(kern, bytes);
+    if (rc) return rc;
+    const int64_t nb = (int64_t)b.nbrick[0] * b.nbrick[1] * b.nbrick[2];
+    kern<<<(unsigned)nb, T, bytes, st>>>(b, tab);
+    return TL_OK;
+}
+
 template <typename R, int DIM, int MODEL, bool FRAC, int KIND>
 int launch_a_one(cudaStream_t st, const tl_body& b) {
     constexpr int G = TL_GATHER_A;
+    if constexpr (DIM == 3) {
+        if (b.brick[0] > 0) {
+            int rc = launch_brick<R>(k_brick_a<R, MODEL, FRAC, KIND>, st, b, 1);
+            return rc ? rc : tl_check_launch("k_brick_a");
+        }
+    }
     if (b.tile > kThreads || (b.tile > 0 && b.tile % 32)) {
         tl_set_error("tile %d: pass A needs a multiple of 32, at most %d", b.tile, kThreads);
         return TL_ERR_ARG;
@@ -2007,6 +2350,12 @@ int launch_a(cudaStream_t st, const tl_body& b) {
 template <typename R, int DIM, int MODE, bool FRAC, int KIND>
 int launch_b_one(cudaStream_t st, const tl_body& b) {
     constexpr int G = TL_GATHER_B;
+    if constexpr (DIM == 3) {
+        if (b.brick[0] > 0) {
+            int rc = launch_brick<R>(k_brick_b<R, MODE, FRAC, KIND>, st, b, 3);
+            return rc ? rc : tl_check_launch("k_brick_b");
+        }
+    }
     if constexpr (sizeof(R) == 4 && DIM == 3) {
         if (b.tile > 0 && b.bsplit == 4) {
             constexpr int SP = 4;

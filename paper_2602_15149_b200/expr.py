@@ -476,3 +476,137 @@ def pretty(ast_or_node):
     if tag == "if":
         return f"if({pretty(node[1])}, {pretty(node[2])}, {pretty(node[3])})"
     raise ExprError(f"unknown node {tag!r}")
+
+
+# -- static skip patterns ---------------------------------------------------
+# A whole-body boundary condition or a restrictphi expression is evaluated on
+# every particle every step, but it usually selects a few particles by their
+# reference coordinates (``if(x0<=0.0, 0.0, skip)``).  When every ``if`` on
+# the way to a ``skip`` tests x0, y0, z0 and constants only, the particles
+# where the expression is not skip are fixed: the device evaluates it on
+# those alone (simulation.py DeviceBody._setup_bcs) with the same result.
+
+STATIC_VARS = frozenset(("x0", "y0", "z0"))
+
+
+class _NotStatic(Exception):
+    pass
+
+
+def _has_skip(node):
+    tag = node[0]
+    if tag == "skip":
+        return True
+    if tag == "if":
+        return _has_skip(node[2]) or _has_skip(node[3])
+    return False          # skip is only legal in if branches (_skip_legal)
+
+
+def skip_static(ast):
+    """True when whether ``ast`` evaluates to skip depends on x0, y0, z0
+    (and constants) only."""
+    def ok(node):
+        if not _has_skip(node) or node[0] == "skip":
+            return True
+        return (frozenset(_walk_vars(node[1])) <= STATIC_VARS and ok(node[2]) and ok(node[3]))
+    root = ast.root if isinstance(ast, ExprAst) else ast
+    return ok(root)
+
+
+_VFUN = {"sin": np.sin, "cos": np.cos, "tan": np.tan, "sinh": np.sinh, "cosh": np.cosh,
+         "tanh": np.tanh, "abs": np.abs}
+_VCMP = {"<": np.less, ">": np.greater, "<=": np.less_equal, ">=": np.greater_equal,
+         "==": np.equal, "!=": np.not_equal}
+
+
+def _veval(node, env):
+    """Vectorised value of a skip-free static subexpression; any domain
+    error makes the pattern non-static (the device then evaluates it
+    everywhere and reports the error as the reference would)."""
+    tag = node[0]
+    if tag == "num":
+        return np.float64(node[1])
+    if tag == "var":
+        return env[node[1]]
+    if tag == "un":
+        return -_veval(node[2], env)
+    if tag == "if":
+        c = _veval(node[1], env)
+        return np.where(c != 0.0, _veval(node[2], env), _veval(node[3], env))
+    if tag == "call":
+        args = [_veval(a, env) for a in node[2]]
+        name = node[1]
+        with np.errstate(all="ignore"):
+            if name in _VFUN:
+                r = _VFUN[name](args[0])
+            elif name == "sqrt":
+                if np.any(args[0] < 0.0):
+                    raise _NotStatic
+                r = np.sqrt(args[0])
+            elif name in ("log", "ln"):
+                if np.any(args[0] <= 0.0):
+                    raise _NotStatic
+                r = np.log10(args[0]) if name == "log" else np.log(args[0])
+            elif name == "pow":
+                r = np.power(args[0], args[1])
+            elif name == "cot":
+                r = np.cos(args[0]) / np.sin(args[0])
+            elif name == "coth":
+                r = np.cosh(args[0]) / np.sinh(args[0])
+            else:
+                raise _NotStatic
+        if not np.all(np.isfinite(r)):
+            raise _NotStatic
+        return r
+    op = node[1]
+    a, b = _veval(node[2], env), _veval(node[3], env)
+    if op in _VCMP:
+        return _VCMP[op](a, b).astype(np.float64)
+    if op == "and":
+        return ((a != 0.0) & (b != 0.0)).astype(np.float64)
+    if op == "or":
+        return ((a != 0.0) | (b != 0.0)).astype(np.float64)
+    with np.errstate(all="ignore"):
+        if op == "+":
+            r = a + b
+        elif op == "-":
+            r = a - b
+        elif op == "*":
+            r = a * b
+        elif op == "/":
+            if np.any(b == 0.0):
+                raise _NotStatic
+            r = a / b
+        elif op == "^":
+            r = np.power(a, b)
+        else:
+            raise _NotStatic
+    if not np.all(np.isfinite(r)):
+        raise _NotStatic
+    return r
+
+
+def nonskip_mask(ast, X0):
+    """Boolean (n,) mask of the particles (reference positions X0, (n, 3))
+    where ``ast`` is not skip, or None when its skip pattern is not static."""
+    if not skip_static(ast):
+        return None
+    X0 = np.asarray(X0, dtype=np.float64)
+    env = {"x0": X0[:, 0], "y0": X0[:, 1], "z0": X0[:, 2]}
+    n = X0.shape[0]
+
+    def walk(node, sel):
+        # sel: particles reaching this node; returns the non-skip subset
+        if node[0] == "skip":
+            return np.zeros(n, dtype=bool)
+        if not _has_skip(node):
+            return sel
+        c = _veval(node[1], env)
+        c = np.broadcast_to(c, (n,)) != 0.0
+        return walk(node[2], sel & c) | walk(node[3], sel & ~c)
+
+    root = ast.root if isinstance(ast, ExprAst) else ast
+    try:
+        return walk(root, np.ones(n, dtype=bool))
+    except _NotStatic:
+        return None

@@ -174,6 +174,36 @@ class DeviceAdjacency:
         return out
 
 
+def class_geometry(q, dp, h, kind, precision):
+    """(m, 8) table of bond classes with lattice offsets q (r0 = q dp = X_i -
+    X_j): W = w(r) r0, kappa = 1/(w(r) (r^2 + 0.001 h^2)) (0 when w = 0),
+    U = r0 / r^2, 0 -- evaluated in FP64 with the pair loops' kernel shape
+    (step.cu kshape; the reference's kernel_geom.py:21-62 without the
+    per-body constant)."""
+    r0 = np.asarray(q, dtype=np.float64).reshape(-1, 3) * float(dp)
+    r2 = np.einsum("ij,ij->i", r0, r0)
+    r = np.sqrt(r2)
+    inv_h = 1.0 / float(h)
+    if int(kind) == 2:     # Wendland C2: t^3, t = max(1 - r/2h, 0)
+        t = np.maximum(1.0 - r * (0.5 * inv_h), 0.0)
+        w = t * t * t
+    else:                  # cubic spline (step.cu kshape, KIND 1)
+        qh = r * inv_h
+        w = np.where(qh < 1.0, (-3.0 + 2.25 * qh) * inv_h,
+                     np.where(qh < 2.0, -0.75 * (2.0 - qh) ** 2 / np.where(r > 0, r, 1.0), 0.0))
+    table = np.zeros((r0.shape[0], 8), dtype=np.float64)
+    table[:, 0:3] = w[:, None] * r0
+    den = w * (r2 + 0.001 * float(h) * float(h))
+    table[:, 3] = np.where(w != 0.0, 1.0 / np.where(w != 0.0, den, 1.0), 0.0)
+    table[:, 4:7] = r0 / r2[:, None]
+    # a pair a rounding error inside the support edge (r = 2h - 1e-16) has
+    # w ~ 1e-48: W flushes to zero in FP32 while kappa overflows, so its
+    # (negligible) terms are dropped outright rather than turned into 0 * inf
+    tiny = np.abs(table[:, 3]) > (1e30 if precision == "fp32" else 1e300)
+    table[tiny] = 0.0
+    return table
+
+
 class StepLayout:
     """Device particle order and neighbour tiles for the step kernels.
 
@@ -188,11 +218,13 @@ class StepLayout:
     GROUP = 4   # TL_SELL_GROUP
     RESIDUE = int(os.environ.get("TLSPH_HALO_RESIDUE", "8"))   # 8 = bank-aligned halo slots
 
-    def __init__(self, dadj, tile=256, rows=None, halo=None, precision="fp64"):
+    def __init__(self, dadj, tile=256, rows=None, halo=None, precision="fp64", order=None):
         """rows: adjacency rows this device owns (default all); halo: adjacency
         ids of the off-rank particles those rows reference, in exchange order
         (multi-GPU, see dist.py).  Device positions: owned [0, n) in Morton
-        order, then the halo block [n, n_all) in the given order."""
+        order (or ``order``: device position -> index into rows, e.g. the
+        brick-major order of BrickLayout), then the halo block [n, n_all) in
+        the given order."""
         import torch
         L = _lib.lib()
         st = _lib.stream_ptr()
@@ -213,11 +245,14 @@ class StepLayout:
         vol = float(np.prod(ext[active])) if active.any() else 1.0
         cell = (vol / n) ** (1.0 / max(int(active.sum()), 1)) if active.any() else 1.0
         cell = max(cell, 1e-300)
-        pown = torch.empty(n, dtype=torch.int32, device=dev)
-        ipown = torch.empty(n, dtype=torch.int32, device=dev)
-        lo_arr = (_lib.D * 3)(*lo)
-        _lib.check(L.tl_reorder(st, n, _lib.ptr(Xh), lo_arr, float(cell), _lib.ptr(pown),
-                                _lib.ptr(ipown)), "tl_reorder")
+        if order is not None:
+            pown = torch.as_tensor(order, device=dev).to(torch.int32)
+        else:
+            pown = torch.empty(n, dtype=torch.int32, device=dev)
+            ipown = torch.empty(n, dtype=torch.int32, device=dev)
+            lo_arr = (_lib.D * 3)(*lo)
+            _lib.check(L.tl_reorder(st, n, _lib.ptr(Xh), lo_arr, float(cell), _lib.ptr(pown),
+                                    _lib.ptr(ipown)), "tl_reorder")
         prow = rows.index_select(0, pown.long()).to(torch.int32)     # device pos -> adj row
         # adjacency id -> device position (owned, then halo); -1 = never referenced
         iperm = torch.full((dadj.n,), -1, dtype=torch.int32, device=dev)
@@ -363,28 +398,8 @@ class StepLayout:
         cls_of_key = np.full(side ** 3, -1, dtype=np.int16)
         cls_of_key[ku] = np.arange(1, ku.size + 1, dtype=np.int16)
         q = np.stack([ku // (side * side), (ku // side) % side, ku % side], axis=1) - self.KEY_R
-        r0 = q.astype(np.float64) * float(dp)
-        r2 = np.einsum("ij,ij->i", r0, r0)
-        r = np.sqrt(r2)
-        inv_h = 1.0 / float(h)
-        if int(kind) == 2:     # Wendland C2: t^3, t = max(1 - r/2h, 0)
-            t = np.maximum(1.0 - r * (0.5 * inv_h), 0.0)
-            w = t * t * t
-        else:                  # cubic spline (step.cu kshape, KIND 1)
-            qh = r * inv_h
-            w = np.where(qh < 1.0, (-3.0 + 2.25 * qh) * inv_h,
-                         np.where(qh < 2.0, -0.75 * (2.0 - qh) ** 2 / np.where(r > 0, r, 1.0),
-                                  0.0))
         table = np.zeros((ku.size + 1, 8), dtype=np.float64)
-        table[1:, 0:3] = w[:, None] * r0
-        den = w * (r2 + 0.001 * float(h) * float(h))
-        table[1:, 3] = np.where(w != 0.0, 1.0 / np.where(w != 0.0, den, 1.0), 0.0)
-        table[1:, 4:7] = r0 / r2[:, None]
-        # a pair a rounding error inside the support edge (r = 2h - 1e-16) has
-        # w ~ 1e-48: W flushes to zero in FP32 while kappa overflows, so its
-        # (negligible) terms are dropped outright rather than turned into 0 * inf
-        tiny = np.abs(table[1:, 3]) > (1e30 if precision == "fp32" else 1e300)
-        table[1:][tiny] = 0.0
+        table[1:] = class_geometry(q, dp, h, kind, precision)
         dev = self.slots.device
         _lib.check(L.tl_class_slots(st, total, self.slot_shift, P(keys),
                                     P(torch.from_numpy(cls_of_key).to(dev)), P(self.slots)),
@@ -428,6 +443,170 @@ class StepLayout:
             _lib.ptr(weight) if weight is not None else None, 4 if precision == "fp32" else 8,
             _lib.ptr(out)), "tl_tile_pos")
         return out
+
+
+class BrickLayout:
+    """Lattice-brick mode of the step kernels (tl_body.brick; step.cu
+    k_brick_a / k_brick_b) for 3D bodies cut from one lattice with wide
+    (radial, k ~ 170) stencils.
+
+    Every particle sits on a lattice cell c = round((X - X_min) / dp); a
+    bond i -> j has class q = c_i - c_j (r0 = q dp).  The device order is
+    brick-major (bricks of B cells, z fastest), a CTA per brick stages the
+    records of the (B + 2 reach) box of cells around it by cell, and each
+    particle's bonds are one mask bit per class -- exactly its CSR row, with
+    the classes numbered in the reference's CSR summation order (the order of
+    a complete row).  ``plan`` returns None when the body is not a single
+    lattice (a position off the lattice by > 1e-6 dp, two particles in one
+    cell, |q| > 7) or has more than MAX_CLASSES classes."""
+
+    MAX_CLASSES = 256     # TL_BRICK_MAX_CLASSES
+    KEY_R = 7
+    SMEM = 226 * 1024
+    CANDIDATES = [(16, 8, 8), (8, 16, 8), (8, 8, 16), (8, 8, 8), (16, 8, 4), (16, 4, 8),
+                  (8, 16, 4), (4, 16, 8), (8, 4, 16), (4, 8, 16), (8, 8, 4), (8, 4, 8),
+                  (4, 8, 8), (4, 4, 8), (4, 8, 4), (8, 4, 4), (4, 4, 4)]
+
+    @classmethod
+    def plan(cls, dadj, dp, h, kind, precision):
+        import torch
+        X = dadj.X
+        dev = X.device
+        n = int(X.shape[0])
+        if n == 0 or not (dp > 0):
+            return None
+        lo = X.min(dim=0).values
+        cf = torch.round((X - lo) / dp)
+        if float((X - (lo + cf * dp)).abs().max().item()) > 1e-6 * dp:
+            return None
+        c = cf.to(torch.int64)
+        cells = (c.max(dim=0).values + 1).cpu().numpy().astype(np.int64)
+        if int(np.prod(cells)) > (1 << 31) - 1:
+            return None
+        lin = (c[:, 0] * int(cells[1]) + c[:, 1]) * int(cells[2]) + c[:, 2]
+        if int(torch.unique(lin).shape[0]) != n:
+            return None                                   # two particles in one cell
+        # classes (lattice offsets) of every bond, in chunks
+        side = 2 * cls.KEY_R + 1
+        seen = torch.zeros(side ** 3, dtype=torch.bool, device=dev)
+        counts = dadj.indptr[1:] - dadj.indptr[:-1]
+        nnz = int(dadj.indptr[-1].item())
+        chunk = 1 << 25
+        rows_all = torch.repeat_interleave(torch.arange(n, device=dev), counts)
+        for a in range(0, nnz, chunk):
+            rr = rows_all[a:a + chunk]
+            jj = dadj.indices[a:a + chunk].long()
+            q = c[rr] - c[jj]
+            if int(q.abs().max().item()) > cls.KEY_R:
+                return None
+            key = ((q[:, 0] + cls.KEY_R) * side + q[:, 1] + cls.KEY_R) * side + q[:, 2] + cls.KEY_R
+            seen[key] = True
+        ku = torch.nonzero(seen).flatten().cpu().numpy()
+        if ku.size == 0 or ku.size > cls.MAX_CLASSES:
+            return None
+        # class order: the CSR order of a longest (complete) row
+        rmax = int(torch.argmax(counts).item())
+        a0, a1 = int(dadj.indptr[rmax].item()), int(dadj.indptr[rmax + 1].item())
+        q = (c[rmax][None, :] - c[dadj.indices[a0:a1].long()]).cpu().numpy()
+        first = ((q[:, 0] + cls.KEY_R) * side + q[:, 1] + cls.KEY_R) * side + q[:, 2] + cls.KEY_R
+        rest = np.setdiff1d(ku, first)
+        keys = np.concatenate([first, rest]).astype(np.int64)
+        qk = np.stack([keys // (side * side), (keys // side) % side, keys % side], 1) - cls.KEY_R
+        reach = int(np.abs(qk).max())
+        k_mean = nnz / n
+        rsz = 16 if precision == "fp32" else 32
+        best = None
+        for B in cls.CANDIDATES:
+            T = B[0] * B[1] * B[2]
+            S = (B[0] + 2 * reach) * (B[1] + 2 * reach) * (B[2] + 2 * reach)
+            if S * 3 * rsz + keys.size * (2 * rsz + 4) > cls.SMEM:
+                continue
+            nbv = [int(-(-int(cells[k]) // B[k])) for k in range(3)]
+            bid = ((c[:, 0] // B[0]) * nbv[1] + c[:, 1] // B[1]) * nbv[2] + c[:, 2] // B[2]
+            nbr = int(torch.unique(bid).shape[0])
+            cost = nbr * (T * k_mean + 8.0 * S)
+            if best is None or cost < best[0]:
+                best = (cost, B, nbv)
+        if best is None:
+            return None
+        _, B, nbv = best
+        bid = ((c[:, 0] // B[0]) * nbv[1] + c[:, 1] // B[1]) * nbv[2] + c[:, 2] // B[2]
+        loc = ((c[:, 0] % B[0]) * B[1] + c[:, 1] % B[1]) * B[2] + c[:, 2] % B[2]
+        order = torch.argsort(bid * (B[0] * B[1] * B[2]) + loc)
+        self = cls()
+        self.order = order                 # device position -> adjacency row
+        self.c = c
+        self.cells = cells
+        self.brick = B
+        self.nbrick = nbv
+        self.reach = reach
+        self.keys = keys
+        self.q = qk
+        self.table = class_geometry(qk, dp, h, kind, precision)
+        self.precision = precision
+        return self
+
+    def finish(self, lay):
+        """Device structures for the layout's device order: cell map, bond
+        masks, box offsets, class table."""
+        import torch
+        dev = lay.indptr.device
+        n, n_all = lay.n, lay.n_all
+        cd = self.c.index_select(0, lay.perm[:n].long())     # device order cells
+        C1, C2 = int(self.cells[1]), int(self.cells[2])
+        lin = (cd[:, 0] * C1 + cd[:, 1]) * C2 + cd[:, 2]
+        self.cellmap = torch.full((int(np.prod(self.cells)),), -1, dtype=torch.int32, device=dev)
+        self.cellmap[lin] = torch.arange(n, dtype=torch.int32, device=dev)
+        side = 2 * self.KEY_R + 1
+        cls_of_key = torch.full((side ** 3,), -1, dtype=torch.int64, device=dev)
+        cls_of_key[torch.from_numpy(self.keys).to(dev)] = torch.arange(
+            self.keys.size, dtype=torch.int64, device=dev)
+        nmask = (self.keys.size + 31) // 32
+        acc = torch.zeros((nmask, n_all), dtype=torch.int64, device=dev)
+        counts = lay.indptr[1:] - lay.indptr[:-1]
+        nnz = int(lay.indptr[-1].item())
+        rows_all = torch.repeat_interleave(torch.arange(n, device=dev), counts)
+        chunk = 1 << 25
+        for a in range(0, nnz, chunk):
+            rr = rows_all[a:a + chunk]
+            jj = lay.indices[a:a + chunk].long()
+            q = cd[rr] - cd[jj]
+            key = ((q[:, 0] + self.KEY_R) * side + q[:, 1] + self.KEY_R) * side + q[:, 2] + self.KEY_R
+            k = cls_of_key[key]
+            # one distinct bit per (row, class): a sum is an OR
+            acc.view(-1).index_add_(0, (k // 32) * n_all + rr, torch.bitwise_left_shift(
+                torch.ones_like(k), k % 32))
+        acc = torch.where(acc >= (1 << 31), acc - (1 << 32), acc)
+        self.bmask = acc.to(torch.int32).contiguous()
+        self.nmask = nmask
+        SY = self.brick[1] + 2 * self.reach
+        SZ = self.brick[2] + 2 * self.reach
+        delta = -((self.q[:, 0] * SY + self.q[:, 1]) * SZ + self.q[:, 2])
+        self.bdelta = torch.from_numpy(delta.astype(np.int32)).to(dev)
+        dt = torch.float32 if self.precision == "fp32" else torch.float64
+        self.bbcls = torch.from_numpy(self.table).to(dev, dt).contiguous()
+        self.nbricks = int(np.prod(self.nbrick))
+        del self.c
+        return self
+
+    def fill(self, d):
+        """Set the brick fields of a tl_body descriptor."""
+        for k in range(3):
+            d.brick[k] = int(self.brick[k])
+            d.nbrick[k] = int(self.nbrick[k])
+            d.cells[k] = int(self.cells[k])
+        d.reach = int(self.reach)
+        d.nbcls = int(self.keys.size)
+        d.nmask = int(self.nmask)
+        d.cellmap = _lib.ptr(self.cellmap)
+        d.bmask = _lib.ptr(self.bmask)
+        d.bdelta = _lib.ptr(self.bdelta)
+        d.bbcls = _lib.ptr(self.bbcls)
+        # host copies for the launch's kernel-parameter class table
+        self._delta_host = np.ascontiguousarray(self.bdelta.cpu().numpy())
+        self._cls_host = np.ascontiguousarray(self.bbcls.cpu().numpy())
+        d.bdelta_host = self._delta_host.ctypes.data
+        d.bbcls_host = self._cls_host.ctypes.data
 
 
 class LazyAdjacency(Adjacency):

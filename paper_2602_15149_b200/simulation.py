@@ -107,10 +107,26 @@ class DeviceBody:
             # member (pass B, C2: 1.38 -> 1.17 ms, C3: 5.78 -> 4.76 ms)
             tile = 256
         tile = int(os.environ.get("TLSPH_TILE", str(tile)))
+        # lattice-brick mode (kernel_geom.BrickLayout): single-device 3D lattice
+        # bodies with wide stencils (> 64 neighbours per particle), uniform V0
+        # and m0.  TLSPH_BRICK=0 disables it, =force ignores the stencil width.
+        V0h = np.asarray(st.V0, dtype=np.float64)
+        m0h = np.asarray(st.m0, dtype=np.float64)
+        uniform = bool(np.all(V0h == V0h[0]) and np.all(m0h == m0h[0]))
+        self.brick = None
+        env_k = os.environ.get("TLSPH_BRICK", "1")
+        if (part is None and int(body.dim) == 3 and uniform and env_k != "0"
+                and (env_k == "force" or _mean_row(dadj) > 64.0)):
+            self.brick = kernel_geom.BrickLayout.plan(dadj, float(body.dp_body), float(body.h),
+                                                      kind, precision)
         if part is not None:
             part.complete(dadj)          # halo ids in exchange order (collective-free)
             lay = kernel_geom.StepLayout(dadj, tile=tile, rows=part.owned_rows,
                                          halo=part.halo_rows, precision=precision)
+        elif self.brick is not None:
+            lay = kernel_geom.StepLayout(dadj, tile=0, precision=precision,
+                                         order=self.brick.order)
+            self.brick.finish(lay)
         else:
             lay = kernel_geom.StepLayout(dadj, tile=tile, precision=precision)
         rec = 64 if precision == "fp32" else 128          # pass-B bytes per staged particle
@@ -213,6 +229,8 @@ class DeviceBody:
         self.nblocks = int(_lib.lib().tl_pass_blocks(n))
         if lay.tile:
             self.nblocks = max(self.nblocks, (n + lay.tile - 1) // lay.tile)
+        if self.brick is not None:
+            self.nblocks = max(self.nblocks, self.brick.nbricks)
         self.pw_partial = torch.zeros(max(self.nblocks, 1), dtype=torch.float64, device=dev)
         self.pw_acc = torch.zeros(1, dtype=torch.float64, device=dev)
         self.pw_base = float(getattr(body, "plastic_work", 0.0))
@@ -232,15 +250,30 @@ class DeviceBody:
         arr = (_lib.tl_bc * max(len(bcs), 1))()
         bit = 0
         self.bc_whole = 0
+        X0 = np.asarray(self.host.X, dtype=np.float64)
+        # static skip patterns (expr.nonskip_mask) become targeted bits while
+        # bits remain for the explicit targets and restrictphi;
+        # TLSPH_STATIC_SKIP=0 keeps every whole-body expression whole
+        n_explicit = sum(1 for bc in bcs if bc.target is not None)
+        static_ok = os.environ.get("TLSPH_STATIC_SKIP", "1") != "0"
         for k, bc in enumerate(bcs):
             d = arr[k]
             d.kind = 0 if bc.kind == "vel" else 1
             d.ftype = int(getattr(bc, "ftype", 0) or 0)
             if d.kind == 1 and d.ftype not in (1, 2, 3):
                 raise CaseError(f"unknown force BC type {bc.ftype}")
-            if bc.target is None:
+            tgt_static = None
+            if bc.target is None and static_ok and bit + n_explicit < 31:
+                tgt_static = self._static_targets(bc, config, X0)
+            if bc.target is None and tgt_static is None:
                 d.bit = -1
                 self.bc_whole = 1
+            elif tgt_static is not None:
+                # whole-body BC whose skip pattern is fixed by x0, y0, z0: a
+                # targeted BC on the particles where it is not skip
+                d.bit = bit
+                mask[tgt_static] |= np.uint32(1 << bit)
+                bit += 1
             else:
                 if bit >= 32:
                     raise CaseError(f"body {body.mk}: more than 32 targeted boundary conditions")
@@ -269,16 +302,47 @@ class DeviceBody:
         self.bcs_dev = torch.empty(nbytes, dtype=torch.uint8, device=self.dev)
         host = torch.frombuffer(bytearray(C.string_at(C.addressof(arr), nbytes)), dtype=torch.uint8)
         self.bcs_dev.copy_(host)
-        self.bcmask = torch.from_numpy(mask[self.gid].view(np.int32)).to(self.dev)
         rp = getattr(body, "restrictphi_expr", None)
+        self.restrict_bit = -1
         if rp is not None:
             ast = config.expressions.get(rp)
             if ast is None:
                 raise CaseError(f"restrictphi references unknown expression id {rp} "
                                 f"(body {body.mk})")
             self.restrict_prog = programs.index_of(rp, ast)
+            nz = ex.nonskip_mask(ast, X0) if (static_ok and bit < 32) else None
+            if nz is not None:     # evaluate it only where it is not skip
+                self.restrict_bit = bit
+                mask[np.flatnonzero(nz)] |= np.uint32(1 << bit)
+                bit += 1
         else:
             self.restrict_prog = -1
+        self.bcmask = torch.from_numpy(mask[self.gid].view(np.int32)).to(self.dev)
+
+    @staticmethod
+    def _static_targets(bc, config, X0):
+        """Particles a whole-body BC can act on when every expression axis
+        has a static skip pattern (expr.nonskip_mask) and no axis is a
+        constant; None otherwise (or when that is every particle)."""
+        sel = np.zeros(X0.shape[0], dtype=bool)
+        any_expr = False
+        for ax in range(3):
+            c, e = bc.const[ax], bc.expr[ax]
+            if c is not None:
+                return None
+            if e is None:
+                continue
+            ast = config.expressions.get(e)
+            if ast is None:
+                return None            # _setup_bcs raises the reference's error
+            nz = ex.nonskip_mask(ast, X0)
+            if nz is None:
+                return None
+            sel |= nz
+            any_expr = True
+        if not any_expr or sel.all():
+            return None
+        return np.flatnonzero(sel)
 
     def _descriptor(self, mat, body, kind, precision):
         b = _lib.tl_body()
@@ -296,6 +360,7 @@ class DeviceBody:
         b.nbc = self.nbc
         b.mk = int(body.mk)
         b.restrict_prog = self.restrict_prog
+        b.restrict_bit = self.restrict_bit
         b.bc_whole = self.bc_whole
         h = float(body.h)
         b.h, b.inv_h = h, 1.0 / h
@@ -325,6 +390,8 @@ class DeviceBody:
             b.toff, b.tpos_a, b.tpos_b = P(lay.toff), P(self.tpos_a), P(self.tpos_b)
         if self.bcls is not None:
             b.ncls, b.bcls = int(self.bcls.shape[0]), P(self.bcls)
+        if self.brick is not None:
+            self.brick.fill(b)
         b.perm = P(self.perm_global)
         b.V0, b.m0 = P(self.V0), P(self.m0)
         for k in ("us", "rb", "v", "al", "sdot", "sddot", "Hh", "Cpd", "epbar", "a"):

@@ -197,3 +197,22 @@ def test_fourpoint3d_spec_matches_reference_case():
         assert g.expressions[k].source.strip() == c.expressions[k].source.strip()
         assert g.expressions[k].locals == c.expressions[k].locals
     assert np.array_equal(np.asarray(bg.notches[0].points), np.asarray(bc.notches[0].points))
+
+
+def test_static_skip_patterns_of_shipped_expressions():
+    """expr.skip_static / nonskip_mask on the shipped cases' expressions."""
+    from paper_2602_15149_b200 import cases, expr as ex
+    X = np.array([[-1e-3, 0, 0], [0.0, 0, 0], [0.05, 0, 0], [0.1, 0, 0.0]])
+    col = cases.make_case("column3d", dp_scale=8, build_adjacency=False)
+    assert ex.nonskip_mask(col.expressions[2], X).tolist() == [True, True, False, False]
+    assert ex.nonskip_mask(col.expressions[1], X).tolist() == [False, False, False, True]
+    tay = cases.make_case("taylor3d", dp_scale=8, build_adjacency=False)
+    assert not ex.skip_static(tay.expressions[1])       # tests the current z
+    assert ex.nonskip_mask(tay.expressions[1], X) is None
+    fp = cases.make_case("fourpoint3d", dp_scale=8, build_adjacency=False)
+    Xb = fp.bodies[0].state.X
+    m = ex.nonskip_mask(fp.expressions[1], Xb)
+    ref = np.array([ex.eval_expr(fp.expressions[1], ex.EvalContext(x0=p[0], y0=p[1], z0=p[2]))
+                    is not ex.SKIP for p in Xb])
+    assert np.array_equal(m, ref) and 0 < m.sum() < m.size
+    assert ex.nonskip_mask(ex.parse("if(x0/(x0-x0)>0,1,skip)"), X) is None   # domain error

@@ -60,11 +60,17 @@ def _worker(rank, world, port, tag, precision, out_dir):
                                                  ("kalthoff2d_p", 3, "fp64"),
                                                  ("taylor3d", 2, "fp64"),
                                                  ("taylor3d", 2, "fp32")])
-def test_multi_rank_device_bit_identical(tag, world, precision, tmp_path):
+def test_multi_rank_device_bit_identical(tag, world, precision, tmp_path, monkeypatch):
     from paper_2602_15149_b200.simulation import DeviceSimulation
     mp.spawn(_worker, args=(world, _port(), tag, precision, str(tmp_path)), nprocs=world,
              join=True)
     G = golden(f"run_{tag}")
+    if precision == "fp64":
+        # slabs run the tiled kernels: the 1-GPU reference of the bit-identity
+        # check runs them too (the brick kernels' sums round differently; the
+        # brick path is held to the slabs at 1e-12 below)
+        _brick_vs_slabs(tag, world, tmp_path, G)
+        monkeypatch.setenv("TLSPH_BRICK", "0")
     cfg = run_case(G)
     sim = DeviceSimulation(cfg, precision=precision)
     sim.initialize()
@@ -106,15 +112,35 @@ def test_multi_rank_device_bit_identical(tag, world, precision, tmp_path):
     assert seen.all()
 
 
+def _brick_vs_slabs(tag, world, tmp_path, G):
+    """The default 1-GPU kernels (lattice bricks where they apply) against
+    the slab runs, FP64, within 1e-12 of each field's scale."""
+    from paper_2602_15149_b200.simulation import DeviceSimulation
+    cfg = run_case(G)
+    sim = DeviceSimulation(cfg, precision="fp64")
+    sim.initialize()
+    for k in range(NSTEPS):
+        sim.step(G["dts"][k])
+    st = cfg.bodies[0].state
+    for r in range(world):
+        d = np.load(tmp_path / f"r{r}.npz")
+        g = d["gid"]
+        for k in ("u", "v", "s", "S"):
+            ref = getattr(st, k)
+            err = np.abs(d[k] - ref[g]).max() / max(np.abs(ref).max(), 1e-300)
+            assert err <= 1e-12, (r, k, err)
+
+
 def test_multi_rank_split_rows(tmp_path, monkeypatch):
     """The 4-way row split of pass B (tl_body.bsplit) on slabs, whose tiled
     passes launch interior and boundary tile lists separately."""
     monkeypatch.setenv("TLSPH_BSPLIT", "4")   # inherited by the spawned ranks
+    monkeypatch.setenv("TLSPH_BRICK", "0")    # the 1-GPU reference on tiles too
     from paper_2602_15149_b200.simulation import DeviceSimulation
     sim = DeviceSimulation(run_case(golden("run_taylor3d")), precision="fp32")
     assert sim.dbodies[0].bsplit == 4
     del sim
-    test_multi_rank_device_bit_identical("taylor3d", 2, "fp32", tmp_path)
+    test_multi_rank_device_bit_identical("taylor3d", 2, "fp32", tmp_path, monkeypatch)
     for r in range(2):   # every slab ran the split kernel, not a bsplit=1 fallback
         d = np.load(tmp_path / f"r{r}.npz")
         assert int(d["bsplit"]) == 4, (r, int(d["bsplit"]), int(d["tile"]))

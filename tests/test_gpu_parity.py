@@ -191,6 +191,7 @@ def test_layout_variants_agree(tag, tile, monkeypatch):
     """Shared-memory tiles (various sizes) and the L2-gather path give the
     same FP64 state: sums run in the same order either way."""
     monkeypatch.setenv("TLSPH_TILE", tile)
+    monkeypatch.setenv("TLSPH_BRICK", "0")     # the tile kernels (slabs, non-lattice bodies)
     monkeypatch.setenv("TLSPH_TILE_A", "1")    # both passes tiled whatever the stencil
     monkeypatch.setenv("TLSPH_TILE_B", "1")
     G = golden(f"run_{tag}")
@@ -335,6 +336,7 @@ def test_device_fp32_split_rows(tag, tile, monkeypatch):
     the row shares and their in-order sum give the step-1 fields within the
     FP32 tolerance, including partial last tiles (tile 32)."""
     monkeypatch.setenv("TLSPH_TILE", tile)
+    monkeypatch.setenv("TLSPH_BRICK", "0")     # the tile kernels (slabs, non-lattice bodies)
     monkeypatch.setenv("TLSPH_BSPLIT", "4")
     G = golden(f"run_{tag}")
     cfg, sim = _sim(G, "fp32")
@@ -624,4 +626,94 @@ def test_graph_batches_match_eager(tag, monkeypatch):
         out[mode] = (sim.t, np.array(st.u), np.array(st.v), np.array(st.S))
     assert out["1"][0] == out["0"][0]
     for a, b in zip(out["1"][1:], out["0"][1:]):
+        assert np.array_equal(a, b)
+
+
+BRICK_TAGS = ["column3d", "taylor3d", "fourpoint3d", "twisting3d", "plate3d", "kalthoff3d"]
+
+
+@pytest.mark.parametrize("tag", BRICK_TAGS)
+def test_brick_mode_fp64_step1_1e12(tag, monkeypatch):
+    """Lattice-brick kernels (k_brick_a / k_brick_b, forced on): FP64 step-1
+    fields on the perturbed state within 1e-12 of the reference, as the
+    tiled kernels."""
+    monkeypatch.setenv("TLSPH_BRICK", "force")
+    G = golden(f"run_{tag}")
+    cfg, sim = _sim(G, "fp64")
+    db = sim.dbodies[0]
+    assert db.brick is not None and db.desc.brick[0] > 0, "brick mode not taken"
+    assert int(db.desc.nbcls) == int(db.brick.keys.size)
+    sim.initialize()
+    st = cfg.bodies[0].state
+    e0 = _errors(st, G, 0)
+    sim.step(G["dts"][0])
+    e1 = _errors(st, G, 1)
+    for k in ("F", "S", "a"):
+        assert e0[k] <= TOL_STEP1_64, ("init", k, e0[k])
+        assert e1[k] <= TOL_STEP1_64, ("step1", k, e1[k])
+    for k in ("u", "v", "s"):
+        if k in e1:
+            assert e1[k] <= TOL_STEP1_64, ("step1", k, e1[k])
+
+
+@pytest.mark.parametrize("tag", BRICK_TAGS)
+def test_brick_mode_runs_match_reference(tag, monkeypatch):
+    """Brick kernels over the golden runs: FP64 at the run tolerances at every
+    checkpoint, FP32 at step 1 within 1e-5."""
+    monkeypatch.setenv("TLSPH_BRICK", "force")
+    G = golden(f"run_{tag}")
+    cfg, sim = _sim(G, "fp64")
+    assert sim.dbodies[0].brick is not None
+    sim.initialize()
+    checks = set(int(c) for c in G["checkpoints"])
+    for step in range(1, len(G["dts"]) + 1):
+        sim.step(G["dts"][step - 1])
+        if step in checks:
+            for k, err in _errors(cfg.bodies[0].state, G, step).items():
+                assert err <= TOL64[k], (step, k, err)
+    cfg, sim = _sim(G, "fp32")
+    assert sim.dbodies[0].brick is not None
+    sim.initialize()
+    sim.step(G["dts"][0])
+    e1 = _errors(cfg.bodies[0].state, G, 1)
+    for k in ("F", "S", "a", "u", "v"):
+        assert e1[k] <= 1e-5, (k, e1[k])
+
+
+def test_brick_mode_plastic_work_and_graphs(monkeypatch):
+    """J2 plastic work summed over brick CTAs, and brick launches inside the
+    captured step graphs, agree with the tiled path."""
+    G = golden("run_taylor3d")
+    out = {}
+    for mode in ("force", "0"):
+        monkeypatch.setenv("TLSPH_BRICK", mode)
+        cfg, sim = _sim(G, "fp64")
+        sim.run(time_max=1e30, time_out=1e30, max_steps=70)
+        out[mode] = (cfg.bodies[0].plastic_work, np.array(cfg.bodies[0].state.u))
+    assert out["force"][0] == pytest.approx(out["0"][0], rel=1e-10)
+    assert relerr(out["force"][1], out["0"][1]) <= 1e-10
+
+
+@pytest.mark.parametrize("tag", ["column3d", "fourpoint3d", "beam2d", "kalthoff2d"])
+def test_static_skip_bcs_bit_identical(tag, monkeypatch):
+    """Whole-body BC / restrictphi expressions whose skip pattern depends on
+    x0, y0, z0 only run on their non-skip particles alone: the FP64 state is
+    bit-identical to evaluating them on every particle."""
+    G = golden(f"run_{tag}")
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("TLSPH_STATIC_SKIP", mode)
+        cfg, sim = _sim(G, "fp64")
+        db = sim.dbodies[0]
+        if mode == "0":
+            assert db.restrict_bit == -1
+        sim.initialize()
+        for step in range(1, min(len(G["dts"]), 10) + 1):
+            sim.step(G["dts"][step - 1])
+        st = cfg.bodies[0].state
+        out[mode] = [np.array(getattr(st, k)) for k in ("u", "v", "a", "s")]
+        out[mode + "w"] = db.bc_whole
+    if tag in ("column3d", "fourpoint3d"):
+        assert out["1w"] == 0 and out["0w"] == 1      # the conversion happened
+    for a, b in zip(out["1"], out["0"]):
         assert np.array_equal(a, b)

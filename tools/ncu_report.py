@@ -6,6 +6,9 @@ import json
 import subprocess
 import sys
 
+sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.abspath(__file__)))
+import ncu_io  # noqa: E402
+
 KEYS = ['gpu__time_duration.sum', 'smsp__inst_executed.sum',
         'smsp__issue_active.avg.pct_of_peak_sustained_active',
         'sm__warps_active.avg.per_cycle_active', 'smsp__warps_eligible.avg.per_cycle_active',
@@ -20,8 +23,7 @@ KEYS = ['gpu__time_duration.sum', 'smsp__inst_executed.sum',
 
 
 def main():
-    out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv"],
-                         capture_output=True, text=True).stdout
+    out = ncu_io.raw(sys.argv[1])
     rows = list(csv.reader(io.StringIO(out)))
     h = rows[0]
     summary = {}

@@ -7,6 +7,9 @@ import os
 import subprocess
 import sys
 
+sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.abspath(__file__)))
+import ncu_io  # noqa: E402
+
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 import sass_lines as S  # noqa: E402
 
@@ -15,8 +18,7 @@ def main():
     rep, kre, obj, mangled = sys.argv[1:5]
     which = sys.argv[5] if len(sys.argv) > 5 else "long_sb"
     top = int(sys.argv[6]) if len(sys.argv) > 6 else 15
-    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass",
-                          "-k", f"regex:{kre}"], capture_output=True, text=True).stdout
+    out = ncu_io.source(rep, kre)
     rows = list(csv.reader(io.StringIO(out)))
     hdr = rows[1]
     ia = hdr.index("Address")
