@@ -1973,6 +1973,20 @@ template <typename F>
 __device__ __forceinline__ void each_bond(const tl_body& b, int64_t i, bool live, F&& pair) {
     const int64_t N = b.n_all;
     const int nc = b.nbcls;
+    // a warp whose particles all have every bond (the interior of the body)
+    // runs the classes unconditionally: no bit tests or branches, and the
+    // unrolled iterations' loads overlap
+    bool full = live;
+    for (int w = 0; w < b.nmask && full; ++w) {
+        const int nb = min(32, nc - 32 * w);
+        const uint32_t want = nb == 32 ? 0xffffffffu : ((1u << nb) - 1u);
+        full = b.bmask[w * N + i] == want;
+    }
+    if (__all_sync(0xffffffffu, full)) {
+#pragma unroll 4
+        for (int c = 0; c < nc; ++c) pair(c);
+        return;
+    }
     for (int w = 0; w < b.nmask; ++w) {
         const uint32_t m = live ? b.bmask[w * N + i] : 0u;
         const int cend = min(32, nc - 32 * w);
