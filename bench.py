@@ -132,16 +132,43 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def _mix64(x):
+    """splitmix64 finaliser on uint64 arrays (wrapping arithmetic)."""
+    x = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return x ^ (x >> np.uint64(31))
+
+
+def _uniform(gid, stream, seed):
+    """Counter-based U(0, 1) per global particle id: every rank draws the
+    same numbers for the same particle, whatever part of the body it holds."""
+    with np.errstate(over="ignore"):
+        x = _mix64(gid.astype(np.uint64) * np.uint64(64) + np.uint64(stream)
+                   + np.uint64(seed) * np.uint64(0x9E3779B97F4A7C15))
+    return ((x >> np.uint64(11)).astype(np.float64) + 0.5) * (1.0 / 9007199254740992.0)
+
+
+def _normal(gid, stream, seed):
+    u1, u2 = _uniform(gid, 2 * stream, seed), _uniform(gid, 2 * stream + 1, seed)
+    return np.sqrt(-2.0 * np.log(u1)) * np.cos(2.0 * np.pi * u2)
+
+
 def perturb(cfg, seed=0):
-    """SURVEY.md 8(d) synthetic block state (mirrors backend_bench.py:29-34)."""
-    rng = np.random.default_rng(seed)
+    """SURVEY.md 8(d) synthetic block state (mirrors backend_bench.py:29-34):
+    u ~ N(0, (2e-5 dp/1e-3)^2), v ~ N(0, 1), s ~ U(0.3, 1), drawn per global
+    particle id so a slab-local rank (cases.make_case(slab=...)) holds the
+    same state as the whole-body build."""
     for b in cfg.bodies:
         st = b.state
         n = st.X.shape[0]
-        st.u[:] = rng.normal(scale=2e-5 * b.dp_body / 1e-3, size=(n, 3))
-        st.v[:] = rng.normal(scale=1.0, size=(n, 3))
+        slab = getattr(b, "slab", None)
+        gid = slab.gid if slab is not None else np.arange(n, dtype=np.int64)
+        scale = 2e-5 * b.dp_body / 1e-3
+        for c in range(3):
+            st.u[:, c] = scale * _normal(gid, c, seed)
+            st.v[:, c] = _normal(gid, 3 + c, seed)
         if b.fracture:
-            st.s[:] = rng.uniform(0.3, 1.0, n)
+            st.s[:] = 0.3 + 0.7 * _uniform(gid, 20, seed)
         if b.dim == 2:
             st.u[:, 1] = 0.0
             st.v[:, 1] = 0.0
@@ -323,9 +350,11 @@ def main():
 
     def make_cfg():
         t0 = time.perf_counter()
+        # N > 1: each rank builds only its slab of the lattice on the host
         cfg = cases.make_case(args.config, lean=True, build_adjacency=False,
                               lenient_targets=args.config == "C5",
-                              dp_scale=base_scale * args.dp_scale)
+                              dp_scale=base_scale * args.dp_scale,
+                              slab=(rank, world) if world > 1 else None)
         perturb(cfg, seed=0)      # one global state; ranks own slabs of it
         return cfg, time.perf_counter() - t0
 

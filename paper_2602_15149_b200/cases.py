@@ -282,11 +282,49 @@ def _near_boxes(X, boxes, dp):
     return np.flatnonzero(dist < dist.min() + dp).astype(np.int64)
 
 
+def _slab_lattice(shape, dp, dim, y_plane, slab, reach):
+    """The planes of a box lattice one rank holds: its slab of whole x-planes
+    (dist.LatticeSlab.plane_bounds) plus ``reach`` on each side, with the
+    full lattice's x-major global ids; None when the box's longest axis is
+    not x (slabs of x-planes are then not the dist.slab_owner cut)."""
+    from .dist import LatticeSlab
+    origin = np.asarray(shape["point"], dtype=np.float64)
+    size = np.asarray(shape["size"], dtype=np.float64)
+    axes = []
+    for ax in range(3):
+        if dim == 2 and ax == 1:
+            axes.append(np.array([y_plane]))
+            continue
+        c = _centers(origin[ax], size[ax], dp, False)
+        if c.size == 0:
+            raise CaseError(f"box produced zero particles (extent {size[ax]!r} at dp {dp!r})")
+        axes.append(c)
+    ext = [a[-1] - a[0] for a in axes]
+    if int(np.argmax(ext)) != 0:
+        return None
+    rank, nranks = slab
+    nx = axes[0].size
+    bounds = LatticeSlab.plane_bounds(nx, nranks)
+    rp = int(math.floor(reach * (1.0 + 1e-6) / dp)) + 1
+    lo = max(int(bounds[rank]) - rp, 0)
+    hi = min(int(bounds[rank + 1]) + rp, nx)
+    g = np.meshgrid(axes[0][lo:hi], axes[1], axes[2], indexing="ij")
+    X = np.column_stack([a.ravel() for a in g])
+    ps = axes[1].size * axes[2].size
+    return X, LatticeSlab(rank=rank, nranks=nranks, bounds=bounds, plane_size=ps, lo=lo, hi=hi,
+                          n_global=nx * ps)
+
+
 def make_case(name, dp_scale=1.0, mapfac=None, eps0=None, cfl=None, dt_override=None,
               time_max=None, time_out=None, build_adjacency=True, precision="fp64",
-              lean=False, lenient_targets=False):
+              lean=False, lenient_targets=False, slab=None):
     """Assemble a CaseConfig the way caseio.build_case does (caseio.py:481-598)
-    for one of ``SPECS`` or a ``WORKLOADS`` key ("C1".."C5")."""
+    for one of ``SPECS`` or a ``WORKLOADS`` key ("C1".."C5").
+
+    slab = (rank, nranks): build only this rank's slab of x-planes plus the
+    interaction reach on the host (single-box bodies; each body gets
+    ``body.slab``, a dist.LatticeSlab, and DeviceSimulation partitions it
+    without the rest of the body).  Other bodies are built whole."""
     if name in WORKLOADS:
         spec_name, kw = WORKLOADS[name]
         kw = dict(kw)
@@ -297,7 +335,7 @@ def make_case(name, dp_scale=1.0, mapfac=None, eps0=None, cfl=None, dt_override=
         return make_case(spec_name, eps0=eps0, cfl=cfl, dt_override=dt_override,
                          time_max=time_max, time_out=time_out,
                          build_adjacency=build_adjacency, precision=precision, lean=lean,
-                         lenient_targets=lenient_targets, **kw)
+                         lenient_targets=lenient_targets, slab=slab, **kw)
     spec = SPECS[name]()
     dp = spec["dp"] * dp_scale
     dim = spec["dim"]
@@ -322,8 +360,17 @@ def make_case(name, dp_scale=1.0, mapfac=None, eps0=None, cfl=None, dt_override=
         frac = bool(cards.get("fracture", False)) and mat.model != Model.J2
         mat.validate(frac, where=f"mk={bspec['mk']}")
         dp_body = dp / int(round(cards.get("mapfac", 1)))
-        X = _shapes_lattice([s for s in spec["shapes"] if s["mk"] == bspec["mk"]], dp_body,
-                            dim, spec["y_plane"])
+        h = spec["coefh"] * dp_body * math.sqrt(dim)   # kernel_geom.py:21-27
+        own_shapes = [s for s in spec["shapes"] if s["mk"] == bspec["mk"]]
+        body_slab = None
+        if slab is not None and len(own_shapes) == 1 and own_shapes[0]["kind"] == "box":
+            nbs = cards.get("nbsrange")
+            reach = nbs * dp_body * (1.0 + 1e-9) if nbs is not None else 2.0 * h
+            got = _slab_lattice(own_shapes[0], dp_body, dim, spec["y_plane"], slab, reach)
+            if got is not None:
+                X, body_slab = got
+        if body_slab is None:
+            X = _shapes_lattice(own_shapes, dp_body, dim, spec["y_plane"])
         V0 = np.full(X.shape[0], dp_body ** 2 if dim == 2 else dp_body ** 3)
         if lean:
             # large synthetic runs: no host (n,3,3) tensors; the device owns
@@ -335,11 +382,12 @@ def make_case(name, dp_scale=1.0, mapfac=None, eps0=None, cfl=None, dt_override=
                                 epbar=np.zeros(n), psi_e=np.zeros(n), psi_plus=np.zeros(n))
         else:
             st = ParticleArrays.from_reference(X, V0, mat.rho0)
-        h = spec["coefh"] * dp_body * math.sqrt(dim)   # kernel_geom.py:21-27
         body = Body(mk=bspec["mk"], state=st, material=mat, dp_body=dp_body, h=h, dim=dim,
                     fracture=frac, notches=[Quad(points=q) for q in bspec["notches"]],
                     nbsrange=cards.get("nbsrange"), f0=np.zeros(3),
                     restrictphi_expr=bspec.get("restrictphi"))
+        if body_slab is not None:
+            body.slab = body_slab
         for b in bspec["bcs"]:
             bc = BoundaryCondition(kind=b["kind"], ftype=b.get("ftype", 0), mkid=b.get("mkid"),
                                    const=tuple(b.get("const", (None, None, None))),
@@ -353,7 +401,8 @@ def make_case(name, dp_scale=1.0, mapfac=None, eps0=None, cfl=None, dt_override=
                     # particle layer nearest to the box itself
                     boxes = [sh for sh in spec["shapes"] if sh["mk"] == bc.mkid]
                     bc.target = _near_boxes(X, boxes, 0.5 * dp_body)
-                if bc.target.size == 0:
+                if bc.target.size == 0 and body_slab is None:
+                    # (a slab may hold none of the targets; they lie on other ranks)
                     raise CaseError(f"empty target set for mkid {bc.mkid}")
             body.bcs.append(bc)
         if build_adjacency:

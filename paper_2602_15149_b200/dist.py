@@ -197,14 +197,68 @@ def allreduce(t, op="max", group=None):
     return t
 
 
+class PlaneOwner:
+    """owner[g] for the global ids g of an x-major box lattice cut into slabs
+    of whole planes: plane = g // plane_size, owner = the slab holding it."""
+
+    def __init__(self, bounds, plane_size):
+        self.bounds = np.asarray(bounds, dtype=np.int64)
+        self.plane_size = int(plane_size)
+
+    def __getitem__(self, g):
+        plane = np.asarray(g, dtype=np.int64) // self.plane_size
+        return (np.searchsorted(self.bounds, plane, side="right") - 1).astype(np.int32)
+
+
+@dataclass
+class LatticeSlab:
+    """A rank's part of a box-lattice body built without the rest of it
+    (cases.make_case(slab=...)): the planes [lo, hi) it holds on the host --
+    its own slab [bounds[rank], bounds[rank + 1]) plus the interaction reach --
+    and their global ids (x-major: g = plane * plane_size + in-plane index)."""
+    rank: int
+    nranks: int
+    bounds: np.ndarray
+    plane_size: int
+    lo: int
+    hi: int
+    n_global: int
+
+    @property
+    def gid(self):
+        return np.arange(self.lo * self.plane_size, self.hi * self.plane_size, dtype=np.int64)
+
+    @staticmethod
+    def plane_bounds(nplanes, nranks):
+        return np.array([(nplanes * r) // nranks for r in range(nranks + 1)], dtype=np.int64)
+
+
 class BodyPartition:
     """One rank's share of one body: its slab, the halo region it reads,
-    and (after ``complete``) the halo block in exchange order."""
+    and (after ``complete``) the halo block in exchange order.
+
+    ``sub``: global ids of the region (ascending); ``host_rows``: their rows
+    in the host state arrays (the global ids when the host holds the whole
+    body, 0..len(sub) for a slab-local build)."""
 
     def __init__(self, X, owner, rank, axis, reach):
+        self._init(subset_for_rank(X, owner, rank, axis, reach), owner, rank, None)
+
+    @classmethod
+    def from_slab(cls, slab):
+        """Partition of a slab-local body: owners by whole planes, the host
+        arrays hold exactly the slab plus its reach."""
+        self = cls.__new__(cls)
+        owner = PlaneOwner(slab.bounds, slab.plane_size)
+        sub = slab.gid
+        self._init(sub, owner, slab.rank, np.arange(sub.shape[0], dtype=np.int64))
+        return self
+
+    def _init(self, sub, owner, rank, host_rows):
         self.rank = rank
         self.owner = owner
-        self.sub = subset_for_rank(X, owner, rank, axis, reach)       # global ids
+        self.sub = sub                                                # global ids
+        self.host_rows = sub if host_rows is None else host_rows
         self.owned_mask = owner[self.sub] == rank
         self.owned_rows = np.flatnonzero(self.owned_mask)             # subset rows
         self.owned_gid = self.sub[self.owned_rows]
@@ -223,5 +277,4 @@ class BodyPartition:
         gid = self.sub[cols]
         off = self.owner[gid] != self.rank
         self.needed_gid = halo_order(gid[off], self.owner)
-        pos = {g: k for k, g in enumerate(self.sub.tolist())}
-        self.halo_rows = np.array([pos[g] for g in self.needed_gid.tolist()], dtype=np.int64)
+        self.halo_rows = np.searchsorted(self.sub, self.needed_gid).astype(np.int64)   # sub ascending

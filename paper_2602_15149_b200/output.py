@@ -79,9 +79,9 @@ def _positions(db, idx):
     """Device positions of the owned particles among global ids ``idx``."""
     import torch
     if getattr(db, "_pos_of", None) is None:
-        gid = np.asarray(db.gid[:db.n], dtype=np.int64)
+        rows = np.asarray(db.hrow[:db.n], dtype=np.int64)      # host rows of the owned particles
         pos_of = np.full(int(db.host.X.shape[0]), -1, dtype=np.int64)
-        pos_of[gid] = np.arange(db.n)
+        pos_of[rows] = np.arange(db.n)
         db._pos_of = pos_of
     pos = db._pos_of[np.asarray(idx, dtype=np.int64)]
     pos = pos[pos >= 0]

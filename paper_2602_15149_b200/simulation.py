@@ -80,7 +80,7 @@ class DeviceBody:
         kind = int(config.kernel)
         corr = getattr(body, "kernel_correction", True)
         if part is not None:
-            sub = part.sub
+            sub = part.host_rows
             dadj = kernel_geom.build_device_adjacency(
                 st.X[sub], st.V0[sub], body.h, body.dim, kind, nbsrange=body.nbsrange,
                 dp_body=body.dp_body, notches=body.notches, correction=corr,
@@ -143,6 +143,9 @@ class DeviceBody:
         adj_ids = lay.perm.cpu().numpy().astype(np.int64)
         # device position -> caller (global) particle index
         self.gid = part.sub[adj_ids] if part is not None else adj_ids
+        # device position -> row of the host state arrays (== gid unless the
+        # host holds only this rank's slab, cases.make_case(slab=...))
+        self.hrow = part.host_rows[adj_ids] if part is not None else adj_ids
         self.perm_h = self.gid
         if part is not None:
             self.perm_global = torch.from_numpy(self.gid.astype(np.int32)).to(dev)
@@ -157,8 +160,8 @@ class DeviceBody:
         V0 = np.asarray(st.V0, dtype=np.float64)
         m0 = np.asarray(st.m0, dtype=np.float64)
         self.uniform = bool(np.all(V0 == V0[0]) and np.all(m0 == m0[0]))
-        self.V0 = torch.from_numpy(V0[self.gid]).to(dev)
-        self.m0 = torch.from_numpy(m0[self.gid]).to(dev)
+        self.V0 = torch.from_numpy(V0[self.hrow]).to(dev)
+        self.m0 = torch.from_numpy(m0[self.hrow]).to(dev)
         N = n_all
         self.us = z(N, 4)
         self.rb = z(N, 12)
@@ -317,7 +320,7 @@ class DeviceBody:
                 bit += 1
         else:
             self.restrict_prog = -1
-        self.bcmask = torch.from_numpy(mask[self.gid].view(np.int32)).to(self.dev)
+        self.bcmask = torch.from_numpy(mask[self.hrow].view(np.int32)).to(self.dev)
 
     @staticmethod
     def _static_targets(bc, config, X0):
@@ -416,7 +419,7 @@ class DeviceBody:
         device its inverse over the owned rows."""
         if getattr(self, "_gidd", None) is None:
             torch = _torch()
-            self._gidd = torch.from_numpy(np.asarray(self.gid, dtype=np.int64)).to(self.dev)
+            self._gidd = torch.from_numpy(np.asarray(self.hrow, dtype=np.int64)).to(self.dev)
             nh = int(self.host.X.shape[0])
             if self.n == nh:
                 inv = torch.empty(nh, dtype=torch.int64, device=self.dev)
@@ -480,7 +483,7 @@ class DeviceBody:
         n = self.n
         self.dirty = False
         _, inv = self._gid_dev()
-        pm = self.gid[:n]                              # owned device rows only
+        pm = self.hrow[:n]                             # owned device rows only
 
         def put(dst, val):
             """val: device (n_rows, ...) in device order, rows >= n ignored.
@@ -752,6 +755,12 @@ class DeviceSimulation:
         """This rank's slab of ``body`` (dist.py): equal-count slabs along the
         longest axis; the halo region extends one interaction reach."""
         import torch.distributed as tdist
+        slab = getattr(body, "slab", None)
+        if slab is not None:
+            if slab.nranks != self.world or slab.rank != tdist.get_rank(self.group):
+                raise ValueError(f"body {body.mk} was built for slab {slab.rank} of "
+                                 f"{slab.nranks}, not this rank of {self.world}")
+            return dist.BodyPartition.from_slab(slab)
         X = body.state.X
         owner, axis = dist.slab_owner(X, self.world)
         reach = (body.nbsrange * body.dp_body * (1.0 + 1e-9) if body.nbsrange is not None

