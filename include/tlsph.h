@@ -397,6 +397,11 @@ typedef struct {
      * it on every particle */
     int32_t restrict_bit;
     int32_t pad_rb;
+    /* opt-in hourglass control (tl_hourglass; no reference counterpart, so no
+     * CPU check): pass A writes F into Fh (9 planes) when non-NULL; hg_coef =
+     * alpha E / (2 rho0) */
+    double hg_coef;
+    void* Fh;
 } tl_body;
 
 #define TL_BRICK_MAX_CLASSES 256
@@ -431,6 +436,17 @@ int tl_clock_commit(tl_stream_t st, tl_clock* clock);
 int tl_reset_red(tl_stream_t st, unsigned long long* red);
 /* deterministic sum of nparts partials into *acc (plastic work) */
 int tl_reduce_partials(tl_stream_t st, const double* partials, int64_t nparts, double* acc);
+
+/* Opt-in hourglass control (north star item 6; the reference has none, so
+ * it has no CPU check and is off unless requested): the Ganzenmueller (2015)
+ * pair force of total-Lagrangian SPH,
+ *   f_ij = -(alpha/2) V0_i V0_j W(|X_ij|) E / |X_ij|^2 (d_ij + d_ji) x_ij / |x_ij|,
+ *   d_ij = (F_i X_ij - x_ij) . x_ij / |x_ij|,   d_ji with F_j,
+ * with X_ij = X_j - X_i and x_ij = x_j - x_i.  It vanishes for an affine
+ * deformation and is antisymmetric (momentum conserving).  Adds a_i =
+ * sum_j f_ij / m_i into the acceleration planes b->ac (FP64), which pass B
+ * adds with the contact term.  Needs the F planes pass A wrote (b->Fh). */
+int tl_hourglass(tl_stream_t st, const tl_body* b);
 
 /* Test hook: the fused pass A's FP64 SVK + spectral split (fast.py:224-284
  * semantics, fracture on) on caller-given H = F - I (n x 9, row-major):

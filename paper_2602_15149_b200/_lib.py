@@ -85,7 +85,7 @@ _BODY_FIELDS += [(k, P) for k in ("Xs", "L", "V0", "m0", "ac", "us", "rb", "v", 
 _BODY_FIELDS += [("brick", I32 * 3), ("nbrick", I32 * 3), ("cells", I32 * 3), ("reach", I32),
                  ("nbcls", I32), ("nmask", I32), ("cellmap", P), ("bmask", P), ("bdelta", P),
                  ("bbcls", P), ("bdelta_host", P), ("bbcls_host", P), ("restrict_bit", I32),
-                 ("pad_rb", I32)]
+                 ("pad_rb", I32), ("hg_coef", D), ("Fh", P)]
 
 
 class tl_body(C.Structure):
@@ -139,6 +139,7 @@ _SIGS = {
     "tl_reduce_partials": (INT, [P, P, I64, P]),
     "tl_pass_blocks": (I64, [I64]),
     "tl_svk_split_check": (INT, [P, I64, P, D, D, P, P, P, P, P]),
+    "tl_hourglass": (INT, [P, C.POINTER(tl_body)]),
     "tl_energy_blocks": (I64, [I64]),
     "tl_energies": (INT, [P, C.POINTER(tl_body), P]),
     "tl_measure": (INT, [P, C.POINTER(tl_body), P, I64, P]),

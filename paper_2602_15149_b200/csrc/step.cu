@@ -1197,6 +1197,11 @@ __device__ __forceinline__ double a_finish(const tl_body& b, int64_t i, R* D, R*
             (R(0.5) * c0 * c0 * ieps) *
             (R(2) * eps0 * lap + R(0.5) * (R(1) - si) * ieps - damp * sd - R(2) * si * ratio);
     }
+    if (b.Fh) {   // F for the opt-in hourglass control (tl_hourglass)
+        R* Fh = static_cast<R*>(b.Fh);
+#pragma unroll
+        for (int q = 0; q < 9; ++q) Fh[q * N + i] = Hm[q] + ((q % 4 == 0) ? R(1) : R(0));
+    }
     // P = F S = S + H S ; PL = P L_i
     R P[9], PL[9];
 #pragma unroll
@@ -2174,6 +2179,77 @@ __global__ void __launch_bounds__(1024, 1)
     }
 }
 
+// ---------------------------------------------------------------------------
+// opt-in hourglass control (tl_hourglass; include/tlsph.h)
+// ---------------------------------------------------------------------------
+template <typename R, int DIM, int KIND>
+__global__ void __launch_bounds__(kThreads) k_hourglass(const tl_body b) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (halted(b) || i >= b.n) return;
+    const int64_t N = b.n_all;
+    const R* Fh = static_cast<const R*>(b.Fh);
+    const R* us = static_cast<const R*>(b.us);
+    double Fi[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) Fi[q] = double(Fh[q * N + i]);
+    const double Xi[3] = {b.Xs[i], b.Xs[N + i], b.Xs[2 * N + i]};
+    const auto ui = tl::ld4(us + 4 * i);
+    const double xi[3] = {Xi[0] + double(ui.x), Xi[1] + double(ui.y), Xi[2] + double(ui.z)};
+    const int lane = (int)(i & 31);
+    const int64_t w = i >> 5;
+    const int64_t base = b.soff[w];
+    const int len = (int)((b.soff[w + 1] - base) >> 5);
+    const int32_t* sidx = b.sidx + base + lane;
+    double acc[3] = {0.0, 0.0, 0.0};
+    for (int k = 0; k < len; ++k) {
+        const int64_t j = sidx[32 * k];
+        if (j == i) continue;                 // row padding
+        double Xij[3], xij[3], Fj[9];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) Xij[a] = b.Xs[a * N + j] - Xi[a];
+        const auto uj = tl::ld4(us + 4 * j);
+        xij[0] = Xij[0] + double(uj.x) - double(ui.x);
+        xij[1] = Xij[1] + double(uj.y) - double(ui.y);
+        xij[2] = Xij[2] + double(uj.z) - double(ui.z);
+        if (DIM == 2) { Xij[1] = 0.0; xij[1] = 0.0; }
+#pragma unroll
+        for (int q = 0; q < 9; ++q) Fj[q] = double(Fh[q * N + j]);
+        const double R2 = Xij[0] * Xij[0] + Xij[1] * Xij[1] + Xij[2] * Xij[2];
+        const double r = sqrt(xij[0] * xij[0] + xij[1] * xij[1] + xij[2] * xij[2]);
+        if (!(r > 0.0) || !(R2 > 0.0)) continue;
+        const double Rn = sqrt(R2);
+        // kernel value W(|X_ij|) (kernel_geom.py:30-62)
+        const double q = Rn * b.inv_h;
+        double Wv;
+        if (KIND == 2) {
+            const double t = fmax(1.0 - 0.5 * q, 0.0);
+            Wv = b.alpha * t * t * t * t * (2.0 * q + 1.0);
+        } else {
+            const double tm = 2.0 - q;
+            Wv = b.alpha * (q < 1.0 ? 1.0 - 1.5 * q * q + 0.75 * q * q * q
+                                    : (q < 2.0 ? 0.25 * tm * tm * tm : 0.0));
+        }
+        double di = 0.0, dj = 0.0;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const double pi_ = Fi[3 * a] * Xij[0] + Fi[3 * a + 1] * Xij[1] + Fi[3 * a + 2] * Xij[2];
+            const double pj_ = Fj[3 * a] * Xij[0] + Fj[3 * a + 1] * Xij[1] + Fj[3 * a + 2] * Xij[2];
+            di += (pi_ - xij[a]) * xij[a];
+            dj += (pj_ - xij[a]) * xij[a];
+        }
+        const double Vj = b.uniform ? b.V0c : b.V0[j];
+        // a_i += -(alpha E / (2 rho0)) V_j W / |X|^2 (d_ij + d_ji) x_ij / |x_ij|, with
+        // d = (F X_ij - x_ij) . x_ij / |x_ij|
+        const double c = -b.hg_coef * Vj * Wv / R2 * (di + dj) / (r * r);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) acc[a] += c * xij[a];
+    }
+    double* ac = const_cast<double*>(b.ac);
+    ac[i] += acc[0];
+    ac[N + i] += DIM == 2 ? 0.0 : acc[1];
+    ac[2 * N + i] += acc[2];
+}
+
 // symplectic predictor (stepper.py:168-175)
 template <typename R, int DIM, bool FRAC>
 __global__ void __launch_bounds__(kThreads) k_predict(const tl_body b) {
@@ -2534,4 +2610,33 @@ extern "C" int tl_svk_split_check(tl_stream_t st, int64_t n, const double* H, do
     k_svk_split_check<<<tl_blocks(n, kThreads), kThreads, 0, (cudaStream_t)st>>>(n, H, lam, mu, s, S,
                                                                                 psi, psip, closed);
     return tl_check_launch("k_svk_split_check");
+}
+
+extern "C" int tl_hourglass(tl_stream_t st_, const tl_body* b) {
+    int rc = check_body(b);
+    if (rc) return rc;
+    if (!b->Fh || !b->ac) {
+        tl_set_error("tl_hourglass: needs the F planes (Fh) and the acceleration planes (ac)");
+        return TL_ERR_ARG;
+    }
+    cudaStream_t st = (cudaStream_t)st_;
+    const unsigned g = tl_blocks(b->n, kThreads);
+    if (b->precision == 4) {
+        if (b->dim == 3) {
+            if (b->kind == 2) k_hourglass<float, 3, 2><<<g, kThreads, 0, st>>>(*b);
+            else k_hourglass<float, 3, 1><<<g, kThreads, 0, st>>>(*b);
+        } else {
+            if (b->kind == 2) k_hourglass<float, 2, 2><<<g, kThreads, 0, st>>>(*b);
+            else k_hourglass<float, 2, 1><<<g, kThreads, 0, st>>>(*b);
+        }
+    } else {
+        if (b->dim == 3) {
+            if (b->kind == 2) k_hourglass<double, 3, 2><<<g, kThreads, 0, st>>>(*b);
+            else k_hourglass<double, 3, 1><<<g, kThreads, 0, st>>>(*b);
+        } else {
+            if (b->kind == 2) k_hourglass<double, 2, 2><<<g, kThreads, 0, st>>>(*b);
+            else k_hourglass<double, 2, 1><<<g, kThreads, 0, st>>>(*b);
+        }
+    }
+    return tl_check_launch("k_hourglass");
 }

@@ -625,10 +625,15 @@ class DeviceSimulation:
     """Drop-in for solidsph.stepper.Simulation running on one B200."""
 
     def __init__(self, config, trace=None, precision="fp64", stream=None, mirrors=True,
-                 group=None, partition=None):
+                 group=None, partition=None, hourglass=0.0):
         """partition: run the slab path (halo exchange, collectives) -- by
         default whenever a process group of more than one rank is initialised;
-        True also with one rank (exercises the exchange plumbing)."""
+        True also with one rank (exercises the exchange plumbing).
+
+        hourglass: alpha of the opt-in hourglass control (tl_hourglass,
+        Ganzenmueller 2015; one GPU).  The reference has no such term, so there
+        is nothing to check it against; 0 (the default) leaves the step the
+        reference's."""
         if precision not in ("fp32", "fp64"):
             raise ValueError("precision must be 'fp32' or 'fp64'")
         L = _lib.lib()  # fails loudly without the native library / GPU
@@ -655,6 +660,12 @@ class DeviceSimulation:
             raise ValueError("partition=True needs an initialised torch.distributed group")
         if len(self.bodies) > 1 and self.partitioned:
             raise NotImplementedError("multi-body (contact) cases run on one GPU")
+        self.hourglass = float(hourglass)
+        if self.hourglass < 0.0:
+            raise ValueError("hourglass alpha must be >= 0")
+        if self.hourglass and self.partitioned:
+            raise NotImplementedError("hourglass control runs on one GPU (it reads F of "
+                                      "halo partners, which the slab exchange does not carry)")
         parts = [self._partition(b) if self.partitioned else None for b in self.bodies]
         self.programs = ProgramTable()
         self.dbodies = [DeviceBody(b, config, precision, self.programs, mirrors, part)
@@ -673,6 +684,17 @@ class DeviceSimulation:
         for b, db in zip(self.bodies, self.dbodies):
             b.state = DeviceState(db.host, db)
         self._setup_contact(torch)
+        if self.hourglass:
+            from .core import youngs_from_lame
+            for db in self.dbodies:
+                db.Fh = torch.zeros((9, db.n_all), dtype=db.R, device=db.dev)
+                if getattr(db, "ac", None) is None:
+                    db.ac = torch.zeros((3, db.n_all), dtype=torch.float64, device=db.dev)
+                mat = db.body.material
+                E = youngs_from_lame(mat.lam, mat.mu)[0]
+                db.desc.Fh = _lib.ptr(db.Fh)
+                db.desc.ac = _lib.ptr(db.ac)
+                db.desc.hg_coef = self.hourglass * E / (2.0 * mat.rho0)
         prog_table = self.programs.upload()
         self.clock_dev = torch.zeros(C.sizeof(_lib.tl_clock), dtype=torch.uint8,
                                      device="cuda")
@@ -750,6 +772,17 @@ class DeviceSimulation:
                 self._st(), C.byref(A.contact_side), C.byref(B.contact_side), dim, dpc, k_n, c_n,
                 kfric, self.CONTACT_CELLS, _lib.ptr(work), int(work.numel()), _lib.ptr(A.ac),
                 _lib.ptr(B.ac), _lib.ptr(self.contact_counters)), "tl_contact_pair")
+
+    def _between_passes(self):
+        """Between pass A and pass B: penalty contact, then the opt-in
+        hourglass control, both into the acceleration planes pass B adds."""
+        self._contact()
+        if not self.hourglass:
+            return
+        for db in self.dbodies:
+            if not self.contact_pairs:
+                db.ac.zero_()
+            _lib.check(self._lib.tl_hourglass(self._st(), C.byref(db.desc)), "tl_hourglass")
 
     def _partition(self, body):
         """This rank's slab of ``body`` (dist.py): equal-count slabs along the
@@ -887,7 +920,7 @@ class DeviceSimulation:
         if mode_verlet:
             for db in self.dbodies:
                 self._pass_a(db)
-            self._contact()
+            self._between_passes()
             for db in self.dbodies:
                 self._pass_b(db, 1)
         else:
@@ -895,7 +928,7 @@ class DeviceSimulation:
                 _lib.check(self._lib.tl_predict(self._st(), C.byref(db.desc)), "tl_predict")
             for db in self.dbodies:
                 self._pass_a(db)
-            self._contact()
+            self._between_passes()
             for db in self.dbodies:
                 self._pass_b(db, 2)
 
@@ -1000,7 +1033,7 @@ class DeviceSimulation:
         self._mark("internal")
         for db in self.dbodies:
             self._pass_a(db)
-        self._contact()
+        self._between_passes()
         for db in self.dbodies:
             self._pass_b(db, 0)
         for db in self.dbodies:
@@ -1119,7 +1152,7 @@ class DeviceSimulation:
                 ev[0].record(self.stream)
                 for db in self.dbodies:
                     self._pass_a(db)
-                self._contact()
+                self._between_passes()
                 ev[1].record(self.stream)
                 ev[2].record(self.stream)
                 for db in self.dbodies:

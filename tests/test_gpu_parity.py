@@ -719,3 +719,48 @@ def test_static_skip_bcs_bit_identical(tag, monkeypatch):
         assert out["1w"] == 0 and out["0w"] == 1      # the conversion happened
     for a, b in zip(out["1"], out["0"]):
         assert np.array_equal(a, b)
+
+
+def _accel(G, hourglass, u=None, v0=False):
+    from paper_2602_15149_b200.simulation import DeviceSimulation
+    cfg = run_case(G)
+    st = cfg.bodies[0].state
+    if u is not None:
+        st.u[:] = u
+    if v0:
+        st.v[:] = 0.0
+    sim = DeviceSimulation(cfg, precision="fp64", hourglass=hourglass)
+    sim.initialize()
+    return cfg, np.array(cfg.bodies[0].state.a)
+
+
+@pytest.mark.parametrize("tag", ["kalthoff3d", "column3d", "kalthoff2d_p"])
+def test_hourglass_control_properties(tag):
+    """The opt-in hourglass control (no reference counterpart, so no oracle):
+    off by default; zero for an affine deformation (the corrected gradient
+    reproduces it, so F X_ij = x_ij for every bond); antisymmetric pair
+    forces (total momentum unchanged); and restoring: on a perturbed state
+    the added acceleration opposes the non-affine displacement."""
+    G = golden(f"run_{tag}")
+    cfg0 = run_case(G)
+    X = cfg0.bodies[0].state.X
+    dim = cfg0.bodies[0].dim
+    F0 = np.array([[1.001, 2e-4, -1e-4], [3e-4, 0.999, 2e-4], [-2e-4, 1e-4, 1.0005]])
+    if dim == 2:
+        F0[1, :] = [0.0, 1.0, 0.0]
+        F0[:, 1] = [0.0, 1.0, 0.0]
+    ua = X @ (F0 - np.eye(3)).T
+    _, a_off = _accel(G, 0.0, ua, v0=True)
+    _, a_on = _accel(G, 50.0, ua, v0=True)
+    # affine: the hourglass term is at rounding level against the elastic one
+    assert np.abs(a_on - a_off).max() <= 1e-9 * np.abs(a_off).max()
+    # perturbed state: the golden's seeded u on top of the affine field
+    up = ua + np.asarray(G["init.b0.u"])
+    cfg_off, a_off = _accel(G, 0.0, up)
+    cfg_on, a_on = _accel(G, 50.0, up)
+    da = a_on - a_off
+    m0 = np.asarray(cfg_on.bodies[0].state.m0)
+    assert np.abs(da).max() > 1e-6 * np.abs(a_off).max()          # it acts
+    mom = (m0[:, None] * da).sum(axis=0)
+    assert np.abs(mom).max() <= 1e-10 * (m0[:, None] * np.abs(da)).sum()
+    assert (da * np.asarray(G["init.b0.u"])).sum() < 0.0            # restoring
