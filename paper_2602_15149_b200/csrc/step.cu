@@ -60,7 +60,10 @@ using tl::mm3;
 #define TL_MINB_A(R, TILED) (sizeof(R) == 4 ? ((TILED) ? 4 : TL_MINB_A_GATHER) : 2)
 #endif
 #ifndef TL_MINB_B
-#define TL_MINB_B(R) (sizeof(R) == 4 ? 4 : 2)
+#ifndef TL_MINB_B_F32
+#define TL_MINB_B_F32 4
+#endif
+#define TL_MINB_B(R) (sizeof(R) == 4 ? TL_MINB_B_F32 : 2)
 #endif
 static_assert(TL_SELL_GROUP % TL_GATHER_A == 0 && TL_SELL_GROUP % TL_GATHER_B == 0, "gather group");
 static_assert(TL_SELL_GROUP == 4, "tiled neighbour loops read 4 slots per group");
@@ -1707,8 +1710,11 @@ __device__ __forceinline__ EpiOut b_finish(const tl_body& b, int64_t i, R* s1, R
     return o;
 }
 
+#ifndef TL_B_THREADS
+#define TL_B_THREADS kThreads
+#endif
 template <int SPLIT>
-constexpr int b_threads() { return SPLIT > 1 ? 1024 : kThreads; }
+constexpr int b_threads() { return SPLIT > 1 ? 1024 : TL_B_THREADS; }
 
 template <typename R, int SPLIT>
 constexpr int b_minb() { return SPLIT > 1 ? 1 : TL_MINB_B(R); }
