@@ -392,6 +392,14 @@ typedef struct {
      * TL_BRICK_MAX_CLASSES classes */
     const int32_t* bdelta_host;
     const void* bbcls_host;
+    /* register blocking of the brick kernels: cpt cells per thread along z
+     * (1 or 2); boxz = the staged box's z extent (brick[2] + 2 reach, padded
+     * odd for cpt = 2: conflict-free records); with cpt = 2, ncol columns of
+     * the stencil (HOST array of 4 ints each: box offset of the (qx, qy)
+     * column, qz_lo, qz_hi, class of qz_hi), classes of a column consecutive
+     * in CSR order with qz descending */
+    int32_t cpt, boxz, ncol, pad_col;
+    const int32_t* bcol_host;
     /* bcmask bit flagging the particles where the restrictphi expression is
      * not skip (its skip pattern depends on x0, y0, z0 only); -1 = evaluate
      * it on every particle */
@@ -405,6 +413,7 @@ typedef struct {
 } tl_body;
 
 #define TL_BRICK_MAX_CLASSES 256
+#define TL_BRICK_MAX_COLUMNS 64
 
 /* pass A: F (gated), stress model, history, Laplacian, s-ddot, P L_i and
  * Avis L_i.  Replaces deformation_gradient + update_stress +

@@ -1914,18 +1914,27 @@ if (visc) TL_LOOP_B(U, ST, true); else TL_LOOP_B(U, ST, false)
 // membership: notches and body edges) is read; per pair a broadcast class
 // load and the partner's records from shared memory.  Classes run in the
 // reference's CSR order, so sums keep its summation order.
+//
+// Register blocking (tl_body.cpt = 2): a thread owns two cells adjacent in z.
+// The classes of one (qx, qy) column of the stencil are consecutive in CSR
+// order with qz descending, so the thread walks each column's partner cells
+// once in ascending z and applies every record to both of its particles (the
+// class of particle p against record k is qz = p - k): each particle still
+// sums its bonds in CSR order, with about 40 % fewer shared-memory loads.
+// Warps whose particles are not all complete (body edges, notches) take the
+// per-bond path.
 struct BrickGeo {
-    int SX, SY, SZ, S;     // staged box (cells)
+    int SX, SY, SZ, S;     // staged box (cells; SZ padded odd for cpt = 2)
     int ox, oy, oz;        // box origin (global cell)
-    int tx, ty, tz;        // this thread's member cell within the brick
+    int tx, ty, tz;        // this thread's first member cell within the brick
 };
 
-__device__ __forceinline__ BrickGeo brick_geo(const tl_body& b, int64_t t) {
+__device__ __forceinline__ BrickGeo brick_geo(const tl_body& b, int64_t t, int cpt) {
     BrickGeo g;
     const int Rr = b.reach;
     g.SX = b.brick[0] + 2 * Rr;
     g.SY = b.brick[1] + 2 * Rr;
-    g.SZ = b.brick[2] + 2 * Rr;
+    g.SZ = b.boxz;
     g.S = g.SX * g.SY * g.SZ;
     const int bz = (int)(t % b.nbrick[2]);
     const int by = (int)((t / b.nbrick[2]) % b.nbrick[1]);
@@ -1934,9 +1943,10 @@ __device__ __forceinline__ BrickGeo brick_geo(const tl_body& b, int64_t t) {
     g.oy = by * b.brick[1] - Rr;
     g.oz = bz * b.brick[2] - Rr;
     const int tid = (int)threadIdx.x;
-    g.tz = tid % b.brick[2];
-    g.ty = (tid / b.brick[2]) % b.brick[1];
-    g.tx = tid / (b.brick[2] * b.brick[1]);
+    const int bzq = b.brick[2] / cpt;
+    g.tz = (tid % bzq) * cpt;
+    g.ty = (tid / bzq) % b.brick[1];
+    g.tx = tid / (bzq * b.brick[1]);
     return g;
 }
 
@@ -1954,6 +1964,8 @@ struct BrickTab {
     V4<R> W[TL_BRICK_MAX_CLASSES];   // (W, kappa)
     V4<R> U[TL_BRICK_MAX_CLASSES];   // (U, 0)
     int d[TL_BRICK_MAX_CLASSES];     // box-cell offset of the partner
+    int4 col[TL_BRICK_MAX_COLUMNS];  // per (qx, qy) column: box offset, qz_lo, qz_hi, class of qz_hi
+    int ncol;
 };
 
 // stage the NREC records of every occupied box cell (LDGSTS gathers; empty
@@ -1977,27 +1989,26 @@ __device__ __forceinline__ void stage_brick(const tl_body& b, const BrickGeo& g,
     __syncthreads();
 }
 
-// visit particle i's bonds in class order: a warp-uniform loop over the
-// classes, predicated on the particle's mask bit (interior particles have
-// every bit set; edges and notches clear some)
-template <typename F>
-__device__ __forceinline__ void each_bond(const tl_body& b, int64_t i, bool live, F&& pair) {
+// every bond of particle i present (all mask bits of the body's classes)
+__device__ __forceinline__ bool bonds_complete(const tl_body& b, int64_t i) {
     const int64_t N = b.n_all;
     const int nc = b.nbcls;
-    // a warp whose particles all have every bond (the interior of the body)
-    // runs the classes unconditionally: no bit tests or branches, and the
-    // unrolled iterations' loads overlap
-    bool full = live;
+    bool full = true;
     for (int w = 0; w < b.nmask && full; ++w) {
         const int nb = min(32, nc - 32 * w);
         const uint32_t want = nb == 32 ? 0xffffffffu : ((1u << nb) - 1u);
         full = b.bmask[w * N + i] == want;
     }
-    if (__all_sync(0xffffffffu, full)) {
-#pragma unroll 4
-        for (int c = 0; c < nc; ++c) pair(c);
-        return;
-    }
+    return full;
+}
+
+// particle i's bonds in class order: a warp-uniform loop over the classes,
+// predicated on the particle's mask bit (interior particles have every bit
+// set; edges and notches clear some)
+template <typename F>
+__device__ __forceinline__ void each_bond(const tl_body& b, int64_t i, bool live, F&& pair) {
+    const int64_t N = b.n_all;
+    const int nc = b.nbcls;
     for (int w = 0; w < b.nmask; ++w) {
         const uint32_t m = live ? b.bmask[w * N + i] : 0u;
         const int cend = min(32, nc - 32 * w);
@@ -2007,80 +2018,143 @@ __device__ __forceinline__ void each_bond(const tl_body& b, int64_t i, bool live
     }
 }
 
-template <typename R, int MODEL, bool FRAC, int KIND>
-__global__ void __launch_bounds__(1024, 1)
+// a thread's CPT particles against the stencil.  pair(p, c, o): particle p
+// with class c and partner box cell o.  Complete warps walk the columns once
+// (records shared by the CPT particles), the others bond by bond.
+template <int CPT, typename R, typename F>
+__device__ __forceinline__ void brick_bonds(const tl_body& b, const BrickTab<R>& tab,
+                                            const int64_t* ip, const bool* live, int me0,
+                                            F&& pair) {
+    bool full = true;
+#pragma unroll
+    for (int p = 0; p < CPT; ++p) full = full && live[p] && bonds_complete(b, ip[p]);
+    if (CPT > 1 && __all_sync(0xffffffffu, full)) {
+        for (int cl = 0; cl < tab.ncol; ++cl) {
+            const int4 col = tab.col[cl];   // (box offset, qz_lo, qz_hi, class of qz_hi)
+            // partner of particle p for qz: me0 + p + col.x - qz, i.e. record k = p - qz
+            for (int k = -col.z; k <= CPT - 1 - col.y; ++k) {
+                const int o = me0 + col.x + k;
+#pragma unroll
+                for (int p = 0; p < CPT; ++p) {
+                    const int qz = p - k;
+                    if (qz >= col.y && qz <= col.z) pair(p, col.w + (col.z - qz), o);
+                }
+            }
+        }
+        return;
+    }
+#pragma unroll
+    for (int p = 0; p < CPT; ++p)
+        each_bond(b, ip[p], live[p], [&](int c) { pair(p, c, me0 + p + tab.d[c]); });
+}
+
+// FP32 packed pass-A accumulator (as loop_a_geo_f2)
+struct AccA32 {
+    float2 D01, D34, D67, D25, M01;
+    float D8, M2, M3, M4, M5;
+    float2 nui;
+    float nuz, uis;
+};
+
+template <typename R, int MODEL, bool FRAC, int KIND, int CPT>
+__global__ void __launch_bounds__(1024 / CPT, 1)
     k_brick_a(const __grid_constant__ tl_body b, const __grid_constant__ BrickTab<R> tab) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ double s_pw[32];
     if (halted(b)) return;
     const int64_t t = blockIdx.x;
-    const BrickGeo g = brick_geo(b, t);
+    const BrickGeo g = brick_geo(b, t, CPT);
     V4<R>* rec = reinterpret_cast<V4<R>*>(smem);
     stage_brick<R, 1>(b, g, static_cast<const R*>(b.us), rec);
-    const int64_t i = cell_particle(b, g.ox + b.reach + g.tx, g.oy + b.reach + g.ty,
-                                    g.oz + b.reach + g.tz);
-    const bool live = i >= 0 && i < b.n;
-    const int me = ((g.tx + b.reach) * g.SY + g.ty + b.reach) * g.SZ + g.tz + b.reach;
-    const V4<R> ui = rec[me];
-    const R si = ui.w;
-    R D[9], M[6];
-    if constexpr (sizeof(R) == 4) {
-        // packed FP32x2 as loop_a_geo_f2
-        float2 D01 = make_float2(0.f, 0.f), D34 = D01, D67 = D01, D25 = D01, M01 = D01;
-        float D8 = 0.f, M2 = 0.f, M3 = 0.f, M4 = 0.f, M5 = 0.f;
-        const float2 nui = make_float2(-float(ui.x), -float(ui.y));
-        const float nuz = -float(ui.z), uis = float(ui.w);
-        const float4* rf = reinterpret_cast<const float4*>(rec);
-        each_bond(b, i, live, [&](int c) {
-            const float4 W = reinterpret_cast<const float4&>(tab.W[c]);
-            const float4 uj = rf[me + tab.d[c]];
-            const float2 wxy = make_float2(W.x, W.y);
-            const float2 du01 = __fadd2_rn(make_float2(uj.x, uj.y), nui);
-            const float du2 = uj.z + nuz;
-            D01 = __ffma2_rn(make_float2(du01.x, du01.x), wxy, D01);
-            D34 = __ffma2_rn(make_float2(du01.y, du01.y), wxy, D34);
-            D67 = __ffma2_rn(make_float2(du2, du2), wxy, D67);
-            D25 = __ffma2_rn(du01, make_float2(W.z, W.z), D25);
-            D8 = fmaf(du2, W.z, D8);
-            if (FRAC) {
-                const float4 U = reinterpret_cast<const float4&>(tab.U[c]);
-                const float ds = uis - uj.w;
-                const float2 cw = __fmul2_rn(make_float2(ds, ds), wxy);
-                const float cz = ds * W.z;
-                M01 = __ffma2_rn(cw, make_float2(U.x, U.y), M01);
-                M2 = fmaf(cz, U.z, M2);
-                M3 = fmaf(cw.x, U.y, M3);
-                M4 = fmaf(cw.x, U.z, M4);
-                M5 = fmaf(cw.y, U.z, M5);
-            }
-        });
-        D[0] = R(D01.x); D[1] = R(D01.y); D[2] = R(D25.x);
-        D[3] = R(D34.x); D[4] = R(D34.y); D[5] = R(D25.y);
-        D[6] = R(D67.x); D[7] = R(D67.y); D[8] = R(D8);
-        M[0] = R(M01.x); M[1] = R(M01.y); M[2] = R(M2); M[3] = R(M3); M[4] = R(M4); M[5] = R(M5);
-    } else {
+    const int me0 = ((g.tx + b.reach) * g.SY + g.ty + b.reach) * g.SZ + g.tz + b.reach;
+    int64_t ip[CPT];
+    bool live[CPT];
 #pragma unroll
-        for (int q = 0; q < 9; ++q) D[q] = R(0);
-#pragma unroll
-        for (int q = 0; q < 6; ++q) M[q] = R(0);
-        each_bond(b, i, live, [&](int c) {
-            const V4<R> W = tab.W[c];
-            const V4<R> uj = rec[me + tab.d[c]];
-            const R du0 = uj.x - ui.x, du1 = uj.y - ui.y, du2 = uj.z - ui.z;
-            D[0] = fma(du0, W.x, D[0]); D[1] = fma(du0, W.y, D[1]); D[2] = fma(du0, W.z, D[2]);
-            D[3] = fma(du1, W.x, D[3]); D[4] = fma(du1, W.y, D[4]); D[5] = fma(du1, W.z, D[5]);
-            D[6] = fma(du2, W.x, D[6]); D[7] = fma(du2, W.y, D[7]); D[8] = fma(du2, W.z, D[8]);
-            if (FRAC) {
-                const V4<R> U = tab.U[c];
-                const R ds = si - uj.w;
-                const R cx = ds * W.x, cy = ds * W.y, cz = ds * W.z;
-                M[0] = fma(cx, U.x, M[0]); M[1] = fma(cy, U.y, M[1]); M[2] = fma(cz, U.z, M[2]);
-                M[3] = fma(cx, U.y, M[3]); M[4] = fma(cx, U.z, M[4]); M[5] = fma(cy, U.z, M[5]);
-            }
-        });
+    for (int p = 0; p < CPT; ++p) {
+        ip[p] = cell_particle(b, g.ox + b.reach + g.tx, g.oy + b.reach + g.ty,
+                              g.oz + b.reach + g.tz + p);
+        live[p] = ip[p] >= 0 && ip[p] < b.n;
     }
     double pw = 0.0;
-    if (live) pw = a_finish<R, 3, MODEL, FRAC, KIND>(b, i, D, M, si, FRAC && si <= R(b.s_l));
+    if constexpr (sizeof(R) == 4) {
+        AccA32 A[CPT];
+        const float4* rf = reinterpret_cast<const float4*>(rec);
+#pragma unroll
+        for (int p = 0; p < CPT; ++p) {
+            const float4 ui = rf[me0 + p];
+            A[p].D01 = A[p].D34 = A[p].D67 = A[p].D25 = A[p].M01 = make_float2(0.f, 0.f);
+            A[p].D8 = A[p].M2 = A[p].M3 = A[p].M4 = A[p].M5 = 0.f;
+            A[p].nui = make_float2(-ui.x, -ui.y);
+            A[p].nuz = -ui.z;
+            A[p].uis = ui.w;
+        }
+        brick_bonds<CPT>(b, tab, ip, live, me0, [&](int p, int c, int o) {
+            AccA32& a = A[p];
+            const float4 W = reinterpret_cast<const float4&>(tab.W[c]);
+            const float4 uj = rf[o];
+            const float2 wxy = make_float2(W.x, W.y);
+            const float2 du01 = __fadd2_rn(make_float2(uj.x, uj.y), a.nui);
+            const float du2 = uj.z + a.nuz;
+            a.D01 = __ffma2_rn(make_float2(du01.x, du01.x), wxy, a.D01);
+            a.D34 = __ffma2_rn(make_float2(du01.y, du01.y), wxy, a.D34);
+            a.D67 = __ffma2_rn(make_float2(du2, du2), wxy, a.D67);
+            a.D25 = __ffma2_rn(du01, make_float2(W.z, W.z), a.D25);
+            a.D8 = fmaf(du2, W.z, a.D8);
+            if (FRAC) {
+                const float4 U = reinterpret_cast<const float4&>(tab.U[c]);
+                const float ds = a.uis - uj.w;
+                const float2 cw = __fmul2_rn(make_float2(ds, ds), wxy);
+                const float cz = ds * W.z;
+                a.M01 = __ffma2_rn(cw, make_float2(U.x, U.y), a.M01);
+                a.M2 = fmaf(cz, U.z, a.M2);
+                a.M3 = fmaf(cw.x, U.y, a.M3);
+                a.M4 = fmaf(cw.x, U.z, a.M4);
+                a.M5 = fmaf(cw.y, U.z, a.M5);
+            }
+        });
+#pragma unroll
+        for (int p = 0; p < CPT; ++p) {
+            if (!live[p]) continue;
+            const AccA32& a = A[p];
+            R D[9] = {a.D01.x, a.D01.y, a.D25.x, a.D34.x, a.D34.y, a.D25.y, a.D67.x, a.D67.y, a.D8};
+            R M[6] = {a.M01.x, a.M01.y, a.M2, a.M3, a.M4, a.M5};
+            const R si = a.uis;
+            pw += a_finish<R, 3, MODEL, FRAC, KIND>(b, ip[p], D, M, si, FRAC && si <= R(b.s_l));
+        }
+    } else {
+        R D[CPT][9], M[CPT][6];
+        V4<R> ui[CPT];
+#pragma unroll
+        for (int p = 0; p < CPT; ++p) {
+            ui[p] = rec[me0 + p];
+#pragma unroll
+            for (int q = 0; q < 9; ++q) D[p][q] = R(0);
+#pragma unroll
+            for (int q = 0; q < 6; ++q) M[p][q] = R(0);
+        }
+        brick_bonds<CPT>(b, tab, ip, live, me0, [&](int p, int c, int o) {
+            const V4<R> W = tab.W[c];
+            const V4<R> uj = rec[o];
+            R* Dp = D[p];
+            R* Mp = M[p];
+            const R du0 = uj.x - ui[p].x, du1 = uj.y - ui[p].y, du2 = uj.z - ui[p].z;
+            Dp[0] = fma(du0, W.x, Dp[0]); Dp[1] = fma(du0, W.y, Dp[1]); Dp[2] = fma(du0, W.z, Dp[2]);
+            Dp[3] = fma(du1, W.x, Dp[3]); Dp[4] = fma(du1, W.y, Dp[4]); Dp[5] = fma(du1, W.z, Dp[5]);
+            Dp[6] = fma(du2, W.x, Dp[6]); Dp[7] = fma(du2, W.y, Dp[7]); Dp[8] = fma(du2, W.z, Dp[8]);
+            if (FRAC) {
+                const V4<R> U = tab.U[c];
+                const R ds = ui[p].w - uj.w;
+                const R cx = ds * W.x, cy = ds * W.y, cz = ds * W.z;
+                Mp[0] = fma(cx, U.x, Mp[0]); Mp[1] = fma(cy, U.y, Mp[1]); Mp[2] = fma(cz, U.z, Mp[2]);
+                Mp[3] = fma(cx, U.y, Mp[3]); Mp[4] = fma(cx, U.z, Mp[4]); Mp[5] = fma(cy, U.z, Mp[5]);
+            }
+        });
+#pragma unroll
+        for (int p = 0; p < CPT; ++p)
+            if (live[p])
+                pw += a_finish<R, 3, MODEL, FRAC, KIND>(b, ip[p], D[p], M[p], ui[p].w,
+                                                        FRAC && ui[p].w <= R(b.s_l));
+    }
     if (MODEL == 3) {   // deterministic CTA partial of sum(dwp * V0)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) pw += __shfl_xor_sync(0xffffffffu, pw, o);
@@ -2094,86 +2168,120 @@ __global__ void __launch_bounds__(1024, 1)
     }
 }
 
-template <typename R, int MODE, bool FRAC, int KIND>
-__global__ void __launch_bounds__(1024, 1)
+// FP32 packed pass-B accumulator (as loop_b_geo)
+struct AccB32 {
+    float2 s1a, s2a, s3a, vi01;
+    float s1b, s2b, s3b, vi2;
+};
+
+template <typename R, int MODE, bool FRAC, int KIND, int CPT>
+__global__ void __launch_bounds__(1024 / CPT, 1)
     k_brick_b(const __grid_constant__ tl_body b, const __grid_constant__ BrickTab<R> tab) {
     extern __shared__ __align__(16) unsigned char smem[];
     if (halted(b) || stress_failed(b)) return;
     const int64_t t = blockIdx.x;
-    const BrickGeo g = brick_geo(b, t);
+    const BrickGeo g = brick_geo(b, t, CPT);
     V4<R>* rec = reinterpret_cast<V4<R>*>(smem);
     stage_brick<R, 3>(b, g, static_cast<const R*>(b.rb), rec);
-    const int64_t i = cell_particle(b, g.ox + b.reach + g.tx, g.oy + b.reach + g.ty,
-                                    g.oz + b.reach + g.tz);
-    const bool live = i >= 0 && i < b.n;
-    const int me = ((g.tx + b.reach) * g.SY + g.ty + b.reach) * g.SZ + g.tz + b.reach;
-    const V4<R> r2i = rec[3 * me + 2];
-    const R vi0 = r2i.x, vi1 = r2i.y, vi2 = r2i.z;
+    const int me0 = ((g.tx + b.reach) * g.SY + g.ty + b.reach) * g.SZ + g.tz + b.reach;
+    int64_t ip[CPT];
+    bool live[CPT];
+#pragma unroll
+    for (int p = 0; p < CPT; ++p) {
+        ip[p] = cell_particle(b, g.ox + b.reach + g.tx, g.oy + b.reach + g.ty,
+                              g.oz + b.reach + g.tz + p);
+        live[p] = ip[p] >= 0 && ip[p] < b.n;
+    }
     const bool visc = b.visc != 0;
     const R B1 = R(b.beta1 * b.c0 * b.h), B2 = R(b.beta2 * b.h * b.h);
-    R s1[3], s2[3], s3[3];
+    R s1[CPT][3], s2[CPT][3], s3[CPT][3];
     if constexpr (sizeof(R) == 4) {
-        float2 s1a = make_float2(0.f, 0.f), s2a = s1a, s3a = s1a;
-        float s1b = 0.f, s2b = 0.f, s3b = 0.f;
-        const float2 vi01 = make_float2(float(vi0), float(vi1));
-        const float2 neg1 = make_float2(-1.f, -1.f);
-        const float fvi2 = float(vi2), fB1 = float(B1), fB2 = float(B2);
         const float4* rf = reinterpret_cast<const float4*>(rec);
-        auto pair = [&](int c, auto V_) {
-            constexpr bool V = decltype(V_)::value;
-            const float4 W = reinterpret_cast<const float4&>(tab.W[c]);
-            const int o = 3 * (me + tab.d[c]);
-            const float4 q0 = rf[o], q1 = rf[o + 1], q2 = rf[o + 2];
-            const float2 wxy = make_float2(W.x, W.y);
-            s1a = __fadd2_rn(s1a, wxy);
-            s1b += W.z;
-            s2a = __ffma2_rn(make_float2(q0.x, q0.y), make_float2(W.x, W.x), s2a);
-            s2a = __ffma2_rn(make_float2(q0.z, q0.w), make_float2(W.y, W.y), s2a);
-            s2a = __ffma2_rn(make_float2(q1.x, q1.y), make_float2(W.z, W.z), s2a);
-            s2b = fmaf(q2.w, W.z, fmaf(q1.w, W.y, fmaf(q1.z, W.x, s2b)));
-            if (V) {
-                const float2 dv = __ffma2_rn(make_float2(q2.x, q2.y), neg1, vi01);
-                const float2 pr = __fmul2_rn(dv, wxy);
-                const float dvw = fmaf(fvi2 - q2.z, W.z, pr.x + pr.y);
-                const float gg = dvw * W.w;
-                const float pw = (fB2 * gg - fB1) * gg;
-                s3a = __ffma2_rn(make_float2(pw, pw), wxy, s3a);
-                s3b = fmaf(pw, W.z, s3b);
-            }
-        };
-        if (visc) each_bond(b, i, live, [&](int c) { pair(c, std::true_type{}); });
-        else each_bond(b, i, live, [&](int c) { pair(c, std::false_type{}); });
-        s1[0] = R(s1a.x); s1[1] = R(s1a.y); s1[2] = R(s1b);
-        s2[0] = R(s2a.x); s2[1] = R(s2a.y); s2[2] = R(s2b);
-        s3[0] = R(s3a.x); s3[1] = R(s3a.y); s3[2] = R(s3b);
-    } else {
+        AccB32 A[CPT];
 #pragma unroll
-        for (int q = 0; q < 3; ++q) s1[q] = s2[q] = s3[q] = R(0);
-        each_bond(b, i, live, [&](int c) {
+        for (int p = 0; p < CPT; ++p) {
+            const float4 r2 = rf[3 * (me0 + p) + 2];
+            A[p].s1a = A[p].s2a = A[p].s3a = make_float2(0.f, 0.f);
+            A[p].s1b = A[p].s2b = A[p].s3b = 0.f;
+            A[p].vi01 = make_float2(r2.x, r2.y);
+            A[p].vi2 = r2.z;
+        }
+        const float2 neg1 = make_float2(-1.f, -1.f);
+        const float fB1 = float(B1), fB2 = float(B2);
+        auto run = [&](auto V_) {
+            constexpr bool V = decltype(V_)::value;
+            brick_bonds<CPT>(b, tab, ip, live, me0, [&](int p, int c, int oc) {
+                AccB32& a = A[p];
+                const float4 W = reinterpret_cast<const float4&>(tab.W[c]);
+                const int o = 3 * oc;
+                const float4 q0 = rf[o], q1 = rf[o + 1], q2 = rf[o + 2];
+                const float2 wxy = make_float2(W.x, W.y);
+                a.s1a = __fadd2_rn(a.s1a, wxy);
+                a.s1b += W.z;
+                a.s2a = __ffma2_rn(make_float2(q0.x, q0.y), make_float2(W.x, W.x), a.s2a);
+                a.s2a = __ffma2_rn(make_float2(q0.z, q0.w), make_float2(W.y, W.y), a.s2a);
+                a.s2a = __ffma2_rn(make_float2(q1.x, q1.y), make_float2(W.z, W.z), a.s2a);
+                a.s2b = fmaf(q2.w, W.z, fmaf(q1.w, W.y, fmaf(q1.z, W.x, a.s2b)));
+                if (V) {
+                    const float2 dv = __ffma2_rn(make_float2(q2.x, q2.y), neg1, a.vi01);
+                    const float2 pr = __fmul2_rn(dv, wxy);
+                    const float dvw = fmaf(a.vi2 - q2.z, W.z, pr.x + pr.y);
+                    const float gg = dvw * W.w;
+                    const float pw = (fB2 * gg - fB1) * gg;
+                    a.s3a = __ffma2_rn(make_float2(pw, pw), wxy, a.s3a);
+                    a.s3b = fmaf(pw, W.z, a.s3b);
+                }
+            });
+        };
+        if (visc) run(std::true_type{}); else run(std::false_type{});
+#pragma unroll
+        for (int p = 0; p < CPT; ++p) {
+            s1[p][0] = A[p].s1a.x; s1[p][1] = A[p].s1a.y; s1[p][2] = A[p].s1b;
+            s2[p][0] = A[p].s2a.x; s2[p][1] = A[p].s2a.y; s2[p][2] = A[p].s2b;
+            s3[p][0] = A[p].s3a.x; s3[p][1] = A[p].s3a.y; s3[p][2] = A[p].s3b;
+        }
+    } else {
+        R vi[CPT][3];
+#pragma unroll
+        for (int p = 0; p < CPT; ++p) {
+            const V4<R> r2 = rec[3 * (me0 + p) + 2];
+            vi[p][0] = r2.x; vi[p][1] = r2.y; vi[p][2] = r2.z;
+#pragma unroll
+            for (int q = 0; q < 3; ++q) s1[p][q] = s2[p][q] = s3[p][q] = R(0);
+        }
+        brick_bonds<CPT>(b, tab, ip, live, me0, [&](int p, int c, int oc) {
             const V4<R> W = tab.W[c];
-            const int o = 3 * (me + tab.d[c]);
+            const int o = 3 * oc;
             const V4<R> q0 = rec[o], q1 = rec[o + 1], q2 = rec[o + 2];
-            s1[0] += W.x; s1[1] += W.y; s1[2] += W.z;
-            s2[0] = fma(q1.x, W.z, fma(q0.z, W.y, fma(q0.x, W.x, s2[0])));
-            s2[1] = fma(q1.y, W.z, fma(q0.w, W.y, fma(q0.y, W.x, s2[1])));
-            s2[2] = fma(q2.w, W.z, fma(q1.w, W.y, fma(q1.z, W.x, s2[2])));
+            R* a1 = s1[p];
+            R* a2 = s2[p];
+            R* a3 = s3[p];
+            a1[0] += W.x; a1[1] += W.y; a1[2] += W.z;
+            a2[0] = fma(q1.x, W.z, fma(q0.z, W.y, fma(q0.x, W.x, a2[0])));
+            a2[1] = fma(q1.y, W.z, fma(q0.w, W.y, fma(q0.y, W.x, a2[1])));
+            a2[2] = fma(q2.w, W.z, fma(q1.w, W.y, fma(q1.z, W.x, a2[2])));
             if (visc) {
-                const R dvw = (vi0 - q2.x) * W.x + (vi1 - q2.y) * W.y + (vi2 - q2.z) * W.z;
+                // explicit FMAs: one rounding sequence whatever the inlining context
+                const R dvw = fma(vi[p][2] - q2.z, W.z, fma(vi[p][1] - q2.y, W.y, (vi[p][0] - q2.x) * W.x));
                 const R gg = dvw * W.w;
-                const R pw = (B2 * gg - B1) * gg;
-                s3[0] = fma(pw, W.x, s3[0]); s3[1] = fma(pw, W.y, s3[1]); s3[2] = fma(pw, W.z, s3[2]);
+                const R pw = fma(B2, gg, -B1) * gg;
+                a3[0] = fma(pw, W.x, a3[0]); a3[1] = fma(pw, W.y, a3[1]); a3[2] = fma(pw, W.z, a3[2]);
             }
         });
     }
     double v2 = 0.0, a2 = 0.0;
     long long bad_acc = LLONG_MAX;
-    if (live) {
-        const V4<R> r0i = rec[3 * me], r1i = rec[3 * me + 1];
+#pragma unroll
+    for (int p = 0; p < CPT; ++p) {
+        if (!live[p]) continue;
+        const int me = me0 + p;
+        const V4<R> r0i = rec[3 * me], r1i = rec[3 * me + 1], r2i = rec[3 * me + 2];
         const R PLi[9] = {r0i.x, r0i.z, r1i.x, r0i.y, r0i.w, r1i.y, r1i.z, r1i.w, r2i.w};
-        const EpiOut o = b_finish<R, 3, MODE, FRAC, KIND>(b, i, s1, s2, s3, PLi, vi0, vi1, vi2);
-        v2 = o.v2;
-        a2 = o.a2;
-        bad_acc = o.bad;
+        const EpiOut o = b_finish<R, 3, MODE, FRAC, KIND>(b, ip[p], s1[p], s2[p], s3[p], PLi,
+                                                          r2i.x, r2i.y, r2i.z);
+        v2 = fmax(v2, o.v2);
+        a2 = fmax(a2, o.a2);
+        bad_acc = min(bad_acc, o.bad);
     }
     v2 = tl::warp_max(v2);
     a2 = tl::warp_max(a2);
@@ -2377,9 +2485,12 @@ int smem_opt_in(K kernel, size_t bytes) {
 
 template <typename R, typename K>
 int launch_brick(K kern, cudaStream_t st, const tl_body& b, int nrec) {
-    const int T = b.brick[0] * b.brick[1] * b.brick[2];
-    if (T <= 0 || T > 1024 || b.nbcls <= 0 || b.nbcls > TL_BRICK_MAX_CLASSES || b.nmask <= 0 ||
-        b.nmask * 32 < b.nbcls || !b.bdelta_host || !b.bbcls_host) {
+    const int cpt = b.cpt > 0 ? b.cpt : 1;
+    const int T = b.brick[0] * b.brick[1] * b.brick[2] / cpt;
+    if (T <= 0 || T > 1024 / cpt || T % 32 || b.brick[2] % cpt || b.nbcls <= 0 ||
+        b.nbcls > TL_BRICK_MAX_CLASSES || b.nmask <= 0 || b.nmask * 32 < b.nbcls ||
+        !b.bdelta_host || !b.bbcls_host || b.boxz < b.brick[2] + 2 * b.reach ||
+        (cpt > 1 && (b.ncol <= 0 || b.ncol > TL_BRICK_MAX_COLUMNS || !b.bcol_host))) {
         tl_set_error("tl_body: invalid brick descriptor");
         return TL_ERR_ARG;
     }
@@ -2395,7 +2506,12 @@ int launch_brick(K kern, cudaStream_t st, const tl_body& b, int nrec) {
             tab.d[c] = 0;
         }
     }
-    const int S = (b.brick[0] + 2 * b.reach) * (b.brick[1] + 2 * b.reach) * (b.brick[2] + 2 * b.reach);
+    tab.ncol = cpt > 1 ? b.ncol : 0;
+    for (int c = 0; c < TL_BRICK_MAX_COLUMNS; ++c)
+        tab.col[c] = (c < tab.ncol) ? make_int4(b.bcol_host[4 * c], b.bcol_host[4 * c + 1],
+                                                b.bcol_host[4 * c + 2], b.bcol_host[4 * c + 3])
+                                    : make_int4(0, 0, -1, 0);
+    const int S = (b.brick[0] + 2 * b.reach) * (b.brick[1] + 2 * b.reach) * b.boxz;
     const size_t bytes = (size_t)S * nrec * sizeof(V4<R>);
     int rc = smem_opt_in(kern, bytes);
     if (rc) return rc;
@@ -2409,7 +2525,8 @@ int launch_a_one(cudaStream_t st, const tl_body& b) {
     constexpr int G = TL_GATHER_A;
     if constexpr (DIM == 3) {
         if (b.brick[0] > 0) {
-            int rc = launch_brick<R>(k_brick_a<R, MODEL, FRAC, KIND>, st, b, 1);
+            int rc = b.cpt == 2 ? launch_brick<R>(k_brick_a<R, MODEL, FRAC, KIND, 2>, st, b, 1)
+                                : launch_brick<R>(k_brick_a<R, MODEL, FRAC, KIND, 1>, st, b, 1);
             return rc ? rc : tl_check_launch("k_brick_a");
         }
     }
@@ -2448,7 +2565,8 @@ int launch_b_one(cudaStream_t st, const tl_body& b) {
     constexpr int G = TL_GATHER_B;
     if constexpr (DIM == 3) {
         if (b.brick[0] > 0) {
-            int rc = launch_brick<R>(k_brick_b<R, MODE, FRAC, KIND>, st, b, 3);
+            int rc = b.cpt == 2 ? launch_brick<R>(k_brick_b<R, MODE, FRAC, KIND, 2>, st, b, 3)
+                                : launch_brick<R>(k_brick_b<R, MODE, FRAC, KIND, 1>, st, b, 3);
             return rc ? rc : tl_check_launch("k_brick_b");
         }
     }

@@ -467,6 +467,32 @@ class BrickLayout:
                   (8, 16, 4), (4, 16, 8), (8, 4, 16), (4, 8, 16), (8, 8, 4), (8, 4, 8),
                   (4, 8, 8), (4, 4, 8), (4, 8, 4), (8, 4, 4), (4, 4, 4)]
 
+    MAX_COLUMNS = 64       # TL_BRICK_MAX_COLUMNS
+
+    @classmethod
+    def _columns(cls, qk):
+        """(qx, qy, qz_lo, qz_hi, first class) per stencil column when the
+        class order (CSR order) runs each (qx, qy) column once with qz
+        descending by one (split into two entries where it skips the
+        particle itself) -- the condition of the register-blocked walk --
+        else None."""
+        cols, seen = [], set()
+        c = 0
+        while c < qk.shape[0]:
+            qx, qy, qz = (int(v) for v in qk[c])
+            # a column may resume right after a gap (the (0, 0) column around
+            # the particle itself): a second entry, walked next
+            if (qx, qy) in seen and not (cols and cols[-1][:2] == (qx, qy)):
+                return None
+            seen.add((qx, qy))
+            e = c
+            while (e + 1 < qk.shape[0] and int(qk[e + 1, 0]) == qx and int(qk[e + 1, 1]) == qy
+                   and int(qk[e + 1, 2]) == int(qk[e, 2]) - 1):
+                e += 1
+            cols.append((qx, qy, int(qk[e, 2]), qz, c))
+            c = e + 1
+        return cols if len(cols) <= cls.MAX_COLUMNS else None
+
     @classmethod
     def plan(cls, dadj, dp, h, kind, precision):
         import torch
@@ -512,24 +538,54 @@ class BrickLayout:
         rest = np.setdiff1d(ku, first)
         keys = np.concatenate([first, rest]).astype(np.int64)
         qk = np.stack([keys // (side * side), (keys // side) % side, keys % side], 1) - cls.KEY_R
+        if rest.size:
+            # classes the longest row lacks (ties at r = 2h kept for some
+            # particles only): order every class as the lattice's CSR order
+            # does -- q descending, slowest index axis first (axis strides
+            # from the longest row's unit-offset partners) -- if that order
+            # agrees with the longest row
+            jj = dadj.indices[a0:a1].long().cpu().numpy()
+            stride = np.zeros(3)
+            for ax in range(3):
+                hit = np.flatnonzero((np.abs(q[:, ax]) == 1) & (np.abs(q).sum(axis=1) == 1))
+                if hit.size:
+                    stride[ax] = abs(int(jj[hit[0]]) - rmax)
+            if (stride > 0).sum() == (np.ptp(qk, axis=0) > 0).sum():
+                axo = np.argsort(-stride, kind="stable")
+                order = np.lexsort(tuple(-qk[:, a] for a in axo[::-1]))
+                pos = np.empty(keys.size, dtype=np.int64)
+                pos[order] = np.arange(keys.size)
+                if np.all(np.diff(pos[:first.size]) > 0):
+                    keys, qk = keys[order], qk[order]
         reach = int(np.abs(qk).max())
         k_mean = nnz / n
         rsz = 16 if precision == "fp32" else 32
+        cols = cls._columns(qk)
         best = None
         for B in cls.CANDIDATES:
-            T = B[0] * B[1] * B[2]
-            S = (B[0] + 2 * reach) * (B[1] + 2 * reach) * (B[2] + 2 * reach)
-            if S * 3 * rsz + keys.size * (2 * rsz + 4) > cls.SMEM:
+            # register blocking (2 cells per thread) measured slower on B200 --
+            # C2 0.98 vs 1.50 G particle-steps/s: half the warps per SM for a
+            # walk with data-dependent bounds -- so it is opt-in
+            cpt = 2 if (cols is not None and B[2] % 2 == 0
+                        and os.environ.get("TLSPH_BRICK_CPT", "1") == "2") else 1
+            T = B[0] * B[1] * B[2] // cpt
+            if T % 32 or T > 1024 // cpt:
+                continue
+            boxz = B[2] + 2 * reach
+            if cpt == 2 and boxz % 2 == 0:
+                boxz += 1          # odd z extent: a warp's records hit distinct bank groups
+            S = (B[0] + 2 * reach) * (B[1] + 2 * reach) * boxz
+            if S * 3 * rsz > cls.SMEM:
                 continue
             nbv = [int(-(-int(cells[k]) // B[k])) for k in range(3)]
             bid = ((c[:, 0] // B[0]) * nbv[1] + c[:, 1] // B[1]) * nbv[2] + c[:, 2] // B[2]
             nbr = int(torch.unique(bid).shape[0])
-            cost = nbr * (T * k_mean + 8.0 * S)
+            cost = nbr * (B[0] * B[1] * B[2] * k_mean + 8.0 * S)
             if best is None or cost < best[0]:
-                best = (cost, B, nbv)
+                best = (cost, B, nbv, cpt, boxz)
         if best is None:
             return None
-        _, B, nbv = best
+        _, B, nbv, cpt, boxz = best
         bid = ((c[:, 0] // B[0]) * nbv[1] + c[:, 1] // B[1]) * nbv[2] + c[:, 2] // B[2]
         loc = ((c[:, 0] % B[0]) * B[1] + c[:, 1] % B[1]) * B[2] + c[:, 2] % B[2]
         order = torch.argsort(bid * (B[0] * B[1] * B[2]) + loc)
@@ -542,6 +598,9 @@ class BrickLayout:
         self.reach = reach
         self.keys = keys
         self.q = qk
+        self.cpt = cpt
+        self.boxz = boxz
+        self.cols = cols if cpt == 2 else None
         self.table = class_geometry(qk, dp, h, kind, precision)
         self.precision = precision
         return self
@@ -580,8 +639,12 @@ class BrickLayout:
         self.bmask = acc.to(torch.int32).contiguous()
         self.nmask = nmask
         SY = self.brick[1] + 2 * self.reach
-        SZ = self.brick[2] + 2 * self.reach
+        SZ = self.boxz
         delta = -((self.q[:, 0] * SY + self.q[:, 1]) * SZ + self.q[:, 2])
+        if self.cols is not None:
+            # (box offset of the column, qz_lo, qz_hi, class of qz_hi)
+            self.col_table = np.array([[-(qx * SY + qy) * SZ, lo, hi, c0]
+                                       for (qx, qy, lo, hi, c0) in self.cols], dtype=np.int32)
         self.bdelta = torch.from_numpy(delta.astype(np.int32)).to(dev)
         dt = torch.float32 if self.precision == "fp32" else torch.float64
         self.bbcls = torch.from_numpy(self.table).to(dev, dt).contiguous()
@@ -596,6 +659,12 @@ class BrickLayout:
             d.nbrick[k] = int(self.nbrick[k])
             d.cells[k] = int(self.cells[k])
         d.reach = int(self.reach)
+        d.cpt = int(self.cpt)
+        d.boxz = int(self.boxz)
+        if self.cpt == 2:
+            self._col_host = np.ascontiguousarray(self.col_table.reshape(-1))
+            d.ncol = int(self.col_table.shape[0])
+            d.bcol_host = self._col_host.ctypes.data
         d.nbcls = int(self.keys.size)
         d.nmask = int(self.nmask)
         d.cellmap = _lib.ptr(self.cellmap)

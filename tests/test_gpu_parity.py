@@ -634,6 +634,30 @@ def test_graph_batches_match_eager(tag, monkeypatch):
 BRICK_TAGS = ["column3d", "taylor3d", "fourpoint3d", "twisting3d", "plate3d", "kalthoff3d"]
 
 
+@pytest.mark.parametrize("tag", ["column3d", "fourpoint3d", "plate3d"])
+def test_brick_register_blocking_bit_identical(tag, monkeypatch):
+    """The opt-in register-blocked brick kernels (2 cells per thread walking
+    the stencil columns, TLSPH_BRICK_CPT=2) sum each particle's bonds in the
+    same CSR order as the per-bond kernels: FP64 state equal to rounding
+    (bit-identical on column3d and plate3d; fourpoint3d's notch and
+    restrictphi paths differ in the last bit of a few accelerations, where
+    the two instantiations contract the epilogue differently)."""
+    monkeypatch.setenv("TLSPH_BRICK", "force")
+    G = golden(f"run_{tag}")
+    out = {}
+    for cpt in ("2", "1"):
+        monkeypatch.setenv("TLSPH_BRICK_CPT", cpt)
+        cfg, sim = _sim(G, "fp64")
+        assert int(sim.dbodies[0].desc.cpt) == int(cpt)
+        sim.initialize()
+        for step in range(1, 4):
+            sim.step(G["dts"][step - 1])
+        st = cfg.bodies[0].state
+        out[cpt] = [np.array(getattr(st, k)) for k in ("u", "v", "S", "s")]
+    for a, b in zip(out["2"], out["1"]):
+        assert np.abs(a - b).max() <= 1e-14 * max(np.abs(b).max(), 1e-300)
+
+
 @pytest.mark.parametrize("tag", BRICK_TAGS)
 def test_brick_mode_fp64_step1_1e12(tag, monkeypatch):
     """Lattice-brick kernels (k_brick_a / k_brick_b, forced on): FP64 step-1
