@@ -284,7 +284,7 @@ typedef struct {
     int64_t n_all;          /* owned + halo; plane stride */
     int32_t dim, model, fracture, visc, precision /* 4 | 8 */, kind;
     int32_t uniform, write_out, store_a, nbc, mk, restrict_prog;
-    int32_t bc_whole;       /* some BC targets the whole body */
+    int32_t bc_whole;       /* some BC targets the whole body (during [bcw_lo, bcw_hi]) */
     int32_t unroll;         /* gather group (1 = plain loop, 2, 4); 0 = default */
     /* material / kernel constants (core.py:95-139) */
     double h, inv_h, alpha, rho0, lam, mu, kappa, c0, beta1, beta2;
@@ -410,6 +410,9 @@ typedef struct {
      * alpha E / (2 rho0) */
     double hg_coef;
     void* Fh;
+    /* time window in which whole-body BC entries can apply: outside it the
+     * step treats particles without a BC bit as BC-free */
+    double bcw_lo, bcw_hi;
 } tl_body;
 
 #define TL_BRICK_MAX_CLASSES 256

@@ -87,7 +87,8 @@ _BODY_FIELDS += [("brick", I32 * 3), ("nbrick", I32 * 3), ("cells", I32 * 3), ("
                  ("bbcls", P), ("bdelta_host", P), ("bbcls_host", P), ("cpt", I32),
                  ("boxz", I32), ("ncol", I32), ("pad_col", I32), ("bcol_host", P),
                  ("restrict_bit", I32),
-                 ("pad_rb", I32), ("hg_coef", D), ("Fh", P)]
+                 ("pad_rb", I32), ("hg_coef", D), ("Fh", P),
+                 ("bcw_lo", D), ("bcw_hi", D)]
 
 
 class tl_body(C.Structure):

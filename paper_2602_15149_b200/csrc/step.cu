@@ -1438,6 +1438,15 @@ __device__ __forceinline__ void note_err(const BcCtx& b, int err) {
     }
 }
 
+// a whole-body BC entry can apply during this step: the step evaluates BCs
+// at times within [t, t + dt] (tl_body.bcw_lo/hi bound the entries' windows)
+__device__ __forceinline__ bool whole_active(const tl_body& b) {
+    if (!b.bc_whole) return false;
+    const double t0 = b.clock ? b.clock->t : 0.0;
+    const double dt = b.clock ? b.clock->dt : 0.0;
+    return t0 <= b.bcw_hi && t0 + dt >= b.bcw_lo;
+}
+
 __device__ __forceinline__ bool bc_applies(const tl_bc& c, uint32_t mask, double t) {
     if (!(c.tst <= t && t <= c.tend)) return false;
     return c.bit < 0 || ((mask >> c.bit) & 1u);
@@ -1575,7 +1584,7 @@ __device__ __forceinline__ EpiOut epi_body(const tl_body& b, int64_t i, uint32_t
     acc[2] = tl::add_rn(acc[2], b.f0[2]);
     const R* us = static_cast<const R*>(b.us);
     const auto ui = tl::ld4(us + 4 * i);
-    const bool has_bc = BC && b.nbc && (mask || b.bc_whole);
+    const bool has_bc = BC && b.nbc && (mask || whole_active(b));
     const double t0 = b.clock ? b.clock->t : 0.0;
     const double dt = b.clock ? b.clock->dt : 0.0;
     const double tf = MODE == TL_B_INIT ? 0.0 : (MODE == TL_B_SYMPL ? t0 + 0.5 * dt : t0);
@@ -1702,7 +1711,7 @@ __device__ __forceinline__ EpiOut b_finish(const tl_body& b, int64_t i, R* s1, R
     // expressions only on the (rare) particles that carry them, out of
     // line, so the common path holds no call frame
     const uint32_t mask = b.bcmask ? b.bcmask[i] : 0u;
-    const bool slow = (b.nbc && (mask || b.bc_whole)) || (FRAC && restrict_applies(b, mask));
+    const bool slow = (b.nbc && (mask || whole_active(b))) || (FRAC && restrict_applies(b, mask));
     const EpiOut o = slow ? epi_slow<R, DIM, MODE, FRAC>(&b, i, mask, acc[0], acc[1], acc[2],
                                                          vi0, vi1, vi2)
                           : epi_body<R, DIM, MODE, FRAC, false>(b, i, mask, acc[0], acc[1],
@@ -2382,7 +2391,7 @@ __global__ void __launch_bounds__(kThreads) k_predict(const tl_body b) {
            double(tl::axpy_rn(vp[2 * N + i], R(half), ap[2 * N + i]))};
     const uint32_t mask = b.bcmask ? b.bcmask[i] : 0u;
     const D3 X0{xi, yi, zi};
-    if (b.nbc && (mask || b.bc_whole))
+    if (b.nbc && (mask || whole_active(b)))
         vel = velocity_bcs(bc_ctx(b), mask, X0, D3{double(ui.x), double(ui.y), double(ui.z)}, th, dt, vel);
     R vR[3] = {R(vel.x), R(vel.y), R(vel.z)};
     R un[4] = {tl::axpy_rn(ui.x, R(half), vR[0]), DIM == 3 ? tl::axpy_rn(ui.y, R(half), vR[1]) : R(0),

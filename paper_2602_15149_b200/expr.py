@@ -610,3 +610,73 @@ def nonskip_mask(ast, X0):
         return walk(root, np.ones(n, dtype=bool))
     except _NotStatic:
         return None
+
+
+# -- skip patterns static after a time threshold ----------------------------
+# ``if(x0<=0.0, 0.0, if(t<=0.0, v, skip))`` (an initial condition) selects
+# every particle at t = 0 and the clamped end afterwards: its skip pattern is
+# static once t exceeds the constants t is compared with.
+
+_T_FLIP = {"<": ">", ">": "<", "<=": ">=", ">=": "<="}
+
+
+def _t_compare(node):
+    """(op, c) for ``t op c`` (``c op t`` mirrored), else None."""
+    if node[0] != "bin" or node[1] not in _T_FLIP:
+        return None
+    a, b = node[2], node[3]
+    if a[0] == "var" and a[1] == "t" and b[0] == "num":
+        return node[1], float(b[1])
+    if b[0] == "var" and b[1] == "t" and a[0] == "num":
+        return _T_FLIP[node[1]], float(a[1])
+    return None
+
+
+def skip_static_after(ast):
+    """Threshold T such that whether ``ast`` is skip depends on x0, y0, z0
+    only for t > T (-inf when it never depends on t), or None."""
+    T = [-math.inf]
+
+    def ok(node):
+        if not _has_skip(node) or node[0] == "skip":
+            return True
+        cond = node[1]
+        tc = _t_compare(cond)
+        if tc is not None:
+            T[0] = max(T[0], tc[1])
+        elif not frozenset(_walk_vars(cond)) <= STATIC_VARS:
+            return False
+        return ok(node[2]) and ok(node[3])
+
+    root = ast.root if isinstance(ast, ExprAst) else ast
+    return T[0] if ok(root) else None
+
+
+def nonskip_mask_after(ast, X0):
+    """(T, mask): for t > T, ``ast`` is not skip exactly on ``mask`` (n,);
+    None when its skip pattern depends on more than x0, y0, z0 and t
+    thresholds."""
+    T = skip_static_after(ast)
+    if T is None:
+        return None
+    X0 = np.asarray(X0, dtype=np.float64)
+    env = {"x0": X0[:, 0], "y0": X0[:, 1], "z0": X0[:, 2]}
+    n = X0.shape[0]
+
+    def walk(node, sel):
+        if node[0] == "skip":
+            return np.zeros(n, dtype=bool)
+        if not _has_skip(node):
+            return sel
+        tc = _t_compare(node[1])
+        if tc is not None:      # t > T >= c: the comparison's late-time value
+            late = tc[0] in (">", ">=")
+            return walk(node[2] if late else node[3], sel)
+        c = np.broadcast_to(_veval(node[1], env), (n,)) != 0.0
+        return walk(node[2], sel & c) | walk(node[3], sel & ~c)
+
+    root = ast.root if isinstance(ast, ExprAst) else ast
+    try:
+        return T, walk(root, np.ones(n, dtype=bool))
+    except _NotStatic:
+        return None

@@ -250,40 +250,64 @@ class DeviceBody:
         if len(bcs) > _lib_max_bc():
             raise CaseError(f"body {body.mk}: more than {_lib_max_bc()} boundary conditions")
         mask = np.zeros(self.host.X.shape[0], dtype=np.uint32)
-        arr = (_lib.tl_bc * max(len(bcs), 1))()
         bit = 0
-        self.bc_whole = 0
         X0 = np.asarray(self.host.X, dtype=np.float64)
-        # static skip patterns (expr.nonskip_mask) become targeted bits while
-        # bits remain for the explicit targets and restrictphi;
-        # TLSPH_STATIC_SKIP=0 keeps every whole-body expression whole
+        # static skip patterns (expr.nonskip_mask / nonskip_mask_after) become
+        # targeted bits while bits remain for the explicit targets and
+        # restrictphi.  Bodies whose pass B is a single wave (under ~38 k
+        # particles) keep whole-body expressions whole: there the kernel is
+        # latency-bound and warps mixing BC and BC-free particles run both
+        # paths (C1: 32 -> 37 us); TLSPH_STATIC_SKIP=1 forces, =0 disables.
         n_explicit = sum(1 for bc in bcs if bc.target is not None)
-        static_ok = os.environ.get("TLSPH_STATIC_SKIP", "1") != "0"
-        for k, bc in enumerate(bcs):
+        env_ss = os.environ.get("TLSPH_STATIC_SKIP", "auto")
+        static_ok = env_ss == "1" or (env_ss != "0" and X0.shape[0] > 148 * 256)
+        # device entries in file order: (bc, bit, tst, tend); a whole-body BC
+        # whose pattern is static after a time T becomes two time-disjoint
+        # entries, whole-body up to T and targeted after it (the windows are
+        # inclusive on the device, so the second starts at the next double)
+        entries = []
+        for bc in bcs:
+            if bc.kind == "force" and int(getattr(bc, "ftype", 0) or 0) not in (1, 2, 3):
+                raise CaseError(f"unknown force BC type {bc.ftype}")
+            tst = float(bc.tst)
+            tend = float(bc.tend) if math.isfinite(bc.tend) else 1e308
+            if bc.target is not None:
+                if bit >= 32:
+                    raise CaseError(f"body {body.mk}: more than 32 targeted boundary conditions")
+                mask[np.asarray(bc.target, dtype=np.int64)] |= np.uint32(1 << bit)
+                entries.append((bc, bit, tst, tend))
+                bit += 1
+                continue
+            got = (self._static_targets(bc, config, X0)
+                   if static_ok and bit + n_explicit < 31 and len(entries) < len(bcs) + 8
+                   else None)
+            if got is None:
+                entries.append((bc, -1, tst, tend))
+                continue
+            T, tgt = got
+            if T >= tend:                  # static only after the BC has ended
+                entries.append((bc, -1, tst, tend))
+                continue
+            if T >= tst:
+                entries.append((bc, -1, tst, T))
+                tst = float(np.nextafter(T, np.inf))
+            mask[tgt] |= np.uint32(1 << bit)
+            entries.append((bc, bit, tst, tend))
+            bit += 1
+        if len(entries) > _lib_max_bc():
+            raise CaseError(f"body {body.mk}: more than {_lib_max_bc()} boundary conditions")
+        arr = (_lib.tl_bc * max(len(entries), 1))()
+        self.bc_whole = 0
+        self.bcw_lo, self.bcw_hi = math.inf, -math.inf   # activity window of whole-body entries
+        for k, (bc, bbit, tst, tend) in enumerate(entries):
             d = arr[k]
             d.kind = 0 if bc.kind == "vel" else 1
             d.ftype = int(getattr(bc, "ftype", 0) or 0)
-            if d.kind == 1 and d.ftype not in (1, 2, 3):
-                raise CaseError(f"unknown force BC type {bc.ftype}")
-            tgt_static = None
-            if bc.target is None and static_ok and bit + n_explicit < 31:
-                tgt_static = self._static_targets(bc, config, X0)
-            if bc.target is None and tgt_static is None:
-                d.bit = -1
+            d.bit = bbit
+            if bbit < 0:
                 self.bc_whole = 1
-            elif tgt_static is not None:
-                # whole-body BC whose skip pattern is fixed by x0, y0, z0: a
-                # targeted BC on the particles where it is not skip
-                d.bit = bit
-                mask[tgt_static] |= np.uint32(1 << bit)
-                bit += 1
-            else:
-                if bit >= 32:
-                    raise CaseError(f"body {body.mk}: more than 32 targeted boundary conditions")
-                d.bit = bit
-                tgt = np.asarray(bc.target, dtype=np.int64)
-                mask[tgt] |= np.uint32(1 << bit)      # original order; permuted below
-                bit += 1
+                self.bcw_lo = min(self.bcw_lo, tst)
+                self.bcw_hi = max(self.bcw_hi, tend)
             for ax in range(3):
                 c = bc.const[ax]
                 e = bc.expr[ax]
@@ -297,11 +321,11 @@ class DeviceBody:
                     d.prog[ax] = programs.index_of(e, ast)
                 else:
                     d.prog[ax] = -1
-            d.tst = float(bc.tst)
-            d.tend = float(bc.tend) if math.isfinite(bc.tend) else 1e308
-        self.nbc = len(bcs)
+            d.tst = tst
+            d.tend = tend
+        self.nbc = len(entries)
         self._bc_arr = arr
-        nbytes = C.sizeof(_lib.tl_bc) * max(len(bcs), 1)
+        nbytes = C.sizeof(_lib.tl_bc) * max(len(entries), 1)
         self.bcs_dev = torch.empty(nbytes, dtype=torch.uint8, device=self.dev)
         host = torch.frombuffer(bytearray(C.string_at(C.addressof(arr), nbytes)), dtype=torch.uint8)
         self.bcs_dev.copy_(host)
@@ -324,10 +348,13 @@ class DeviceBody:
 
     @staticmethod
     def _static_targets(bc, config, X0):
-        """Particles a whole-body BC can act on when every expression axis
-        has a static skip pattern (expr.nonskip_mask) and no axis is a
-        constant; None otherwise (or when that is every particle)."""
+        """(T, particles) for a whole-body BC whose every expression axis has
+        a skip pattern fixed by x0, y0, z0 for t > T (expr.nonskip_mask_after;
+        T = -inf when it never depends on t) and no axis is a constant: the
+        particles it can act on after T.  None otherwise (or when that is
+        every particle)."""
         sel = np.zeros(X0.shape[0], dtype=bool)
+        T = -math.inf
         any_expr = False
         for ax in range(3):
             c, e = bc.const[ax], bc.expr[ax]
@@ -338,14 +365,15 @@ class DeviceBody:
             ast = config.expressions.get(e)
             if ast is None:
                 return None            # _setup_bcs raises the reference's error
-            nz = ex.nonskip_mask(ast, X0)
-            if nz is None:
+            got = ex.nonskip_mask_after(ast, X0)
+            if got is None:
                 return None
-            sel |= nz
+            T = max(T, got[0])
+            sel |= got[1]
             any_expr = True
         if not any_expr or sel.all():
             return None
-        return np.flatnonzero(sel)
+        return T, np.flatnonzero(sel)
 
     def _descriptor(self, mat, body, kind, precision):
         b = _lib.tl_body()
@@ -365,6 +393,7 @@ class DeviceBody:
         b.restrict_prog = self.restrict_prog
         b.restrict_bit = self.restrict_bit
         b.bc_whole = self.bc_whole
+        b.bcw_lo, b.bcw_hi = float(self.bcw_lo), float(self.bcw_hi)
         h = float(body.h)
         b.h, b.inv_h = h, 1.0 / h
         b.alpha = kernel_geom.kernel_alpha(h, body.dim, kind)

@@ -216,3 +216,17 @@ def test_static_skip_patterns_of_shipped_expressions():
                     is not ex.SKIP for p in Xb])
     assert np.array_equal(m, ref) and 0 < m.sum() < m.size
     assert ex.nonskip_mask(ex.parse("if(x0/(x0-x0)>0,1,skip)"), X) is None   # domain error
+
+
+def test_skip_patterns_static_after_a_time():
+    """expr.nonskip_mask_after: beam2d's initial-condition BC selects every
+    particle at t <= 0 and only the clamped end (x0 <= 0) afterwards."""
+    from paper_2602_15149_b200 import cases, expr as ex
+    b = cases.make_case("beam2d", dp_scale=8, build_adjacency=False)
+    X = np.array([[-1e-3, 0, 0], [0.0, 0, 0], [0.05, 0, 0.0]])
+    T, m = ex.nonskip_mask_after(b.expressions[1], X)
+    assert T == 0.0 and m.tolist() == [True, True, False]
+    assert ex.nonskip_mask_after(b.expressions[2], X)[0] == -np.inf
+    assert ex.nonskip_mask_after(ex.parse("if(t>2e-6, skip, if(x0>0.01, 1.0, skip))"),
+                                 X)[1].tolist() == [False, False, False]
+    assert ex.nonskip_mask_after(ex.parse("if(z<1.0e-12,0.0,if(t<=0.0,1.0,skip))"), X) is None

@@ -739,8 +739,13 @@ def test_static_skip_bcs_bit_identical(tag, monkeypatch):
         st = cfg.bodies[0].state
         out[mode] = [np.array(getattr(st, k)) for k in ("u", "v", "a", "s")]
         out[mode + "w"] = db.bc_whole
+        out[mode + "n"] = db.nbc
     if tag in ("column3d", "fourpoint3d"):
         assert out["1w"] == 0 and out["0w"] == 1      # the conversion happened
+    if tag == "beam2d":
+        # the initial-condition BC (static after t = 0) splits into a
+        # whole-body entry for t <= 0 and a targeted one after it
+        assert out["1n"] == out["0n"] + 1 and out["1w"] == 1
     for a, b in zip(out["1"], out["0"]):
         assert np.array_equal(a, b)
 
