@@ -398,7 +398,9 @@ typedef struct {
      * the stencil (HOST array of 4 ints each: box offset of the (qx, qy)
      * column, qz_lo, qz_hi, class of qz_hi), classes of a column consecutive
      * in CSR order with qz descending */
-    int32_t cpt, boxz, ncol, pad_col;
+    int32_t cpt, boxz, ncol;
+    int32_t a_split;        /* pass A runs bricks of brick[0] / a_split cells in x (more,
+                               smaller CTAs: its records are a third of pass B's) */
     const int32_t* bcol_host;
     /* bcmask bit flagging the particles where the restrictphi expression is
      * not skip (its skip pattern depends on x0, y0, z0 only); -1 = evaluate

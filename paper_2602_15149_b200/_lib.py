@@ -85,7 +85,7 @@ _BODY_FIELDS += [(k, P) for k in ("Xs", "L", "V0", "m0", "ac", "us", "rb", "v", 
 _BODY_FIELDS += [("brick", I32 * 3), ("nbrick", I32 * 3), ("cells", I32 * 3), ("reach", I32),
                  ("nbcls", I32), ("nmask", I32), ("cellmap", P), ("bmask", P), ("bdelta", P),
                  ("bbcls", P), ("bdelta_host", P), ("bbcls_host", P), ("cpt", I32),
-                 ("boxz", I32), ("ncol", I32), ("pad_col", I32), ("bcol_host", P),
+                 ("boxz", I32), ("ncol", I32), ("a_split", I32), ("bcol_host", P),
                  ("restrict_bit", I32),
                  ("pad_rb", I32), ("hg_coef", D), ("Fh", P),
                  ("bcw_lo", D), ("bcw_hi", D)]

@@ -2534,8 +2534,13 @@ int launch_a_one(cudaStream_t st, const tl_body& b) {
     constexpr int G = TL_GATHER_A;
     if constexpr (DIM == 3) {
         if (b.brick[0] > 0) {
-            int rc = b.cpt == 2 ? launch_brick<R>(k_brick_a<R, MODEL, FRAC, KIND, 2>, st, b, 1)
-                                : launch_brick<R>(k_brick_a<R, MODEL, FRAC, KIND, 1>, st, b, 1);
+            tl_body ba = b;       // pass A may run smaller bricks (same box offsets)
+            if (b.a_split > 1 && b.brick[0] % b.a_split == 0) {
+                ba.brick[0] = b.brick[0] / b.a_split;
+                ba.nbrick[0] = (b.cells[0] + ba.brick[0] - 1) / ba.brick[0];
+            }
+            int rc = b.cpt == 2 ? launch_brick<R>(k_brick_a<R, MODEL, FRAC, KIND, 2>, st, ba, 1)
+                                : launch_brick<R>(k_brick_a<R, MODEL, FRAC, KIND, 1>, st, ba, 1);
             return rc ? rc : tl_check_launch("k_brick_a");
         }
     }

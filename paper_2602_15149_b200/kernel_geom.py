@@ -600,6 +600,11 @@ class BrickLayout:
         self.q = qk
         self.cpt = cpt
         self.boxz = boxz
+        # pass A on half-width bricks where the pass-B brick is 16 wide: two
+        # 512-thread CTAs per SM instead of one of 1024 (TLSPH_BRICK_A_SPLIT)
+        asp = int(os.environ.get("TLSPH_BRICK_A_SPLIT", "2"))
+        self.a_split = asp if (asp > 1 and B[0] % asp == 0
+                               and (B[0] // asp) * B[1] * B[2] // cpt >= 64) else 1
         self.cols = cols if cpt == 2 else None
         self.table = class_geometry(qk, dp, h, kind, precision)
         self.precision = precision
@@ -649,6 +654,9 @@ class BrickLayout:
         dt = torch.float32 if self.precision == "fp32" else torch.float64
         self.bbcls = torch.from_numpy(self.table).to(dev, dt).contiguous()
         self.nbricks = int(np.prod(self.nbrick))
+        if self.a_split > 1:      # pass A's (more) CTAs write plastic-work partials too
+            nba = -(-int(self.cells[0]) // (self.brick[0] // self.a_split))
+            self.nbricks = max(self.nbricks, nba * int(self.nbrick[1]) * int(self.nbrick[2]))
         del self.c
         return self
 
@@ -659,6 +667,7 @@ class BrickLayout:
             d.nbrick[k] = int(self.nbrick[k])
             d.cells[k] = int(self.cells[k])
         d.reach = int(self.reach)
+        d.a_split = int(self.a_split)
         d.cpt = int(self.cpt)
         d.boxz = int(self.boxz)
         if self.cpt == 2:
