@@ -57,13 +57,19 @@ using tl::mm3;
 #define TL_MINB_A_GATHER 3
 #endif
 #ifndef TL_MINB_A
-#define TL_MINB_A(R, TILED) (sizeof(R) == 4 ? ((TILED) ? 4 : TL_MINB_A_GATHER) : 2)
+#ifndef TL_MINB_A_F64
+#define TL_MINB_A_F64 2
+#endif
+#define TL_MINB_A(R, TILED) (sizeof(R) == 4 ? ((TILED) ? 4 : TL_MINB_A_GATHER) : TL_MINB_A_F64)
 #endif
 #ifndef TL_MINB_B
 #ifndef TL_MINB_B_F32
 #define TL_MINB_B_F32 4
 #endif
-#define TL_MINB_B(R) (sizeof(R) == 4 ? TL_MINB_B_F32 : 2)
+#ifndef TL_MINB_B_F64
+#define TL_MINB_B_F64 2
+#endif
+#define TL_MINB_B(R) (sizeof(R) == 4 ? TL_MINB_B_F32 : TL_MINB_B_F64)
 #endif
 static_assert(TL_SELL_GROUP % TL_GATHER_A == 0 && TL_SELL_GROUP % TL_GATHER_B == 0, "gather group");
 static_assert(TL_SELL_GROUP == 4, "tiled neighbour loops read 4 slots per group");

@@ -1220,11 +1220,30 @@ class DeviceSimulation:
         eps = 1e-12 * max(t_max, 1.0)
         verlet = int(cfg.step_algorithm) != 2
         dto = -1.0 if cfg.dt_override is None else float(cfg.dt_override)
+        dt_hint = None
         while self.t < t_max - eps:
             self._set_clock(t=self.t, next_out=next_out, t_max=t_max, eps=eps, dt_override=dto,
                             max_steps=-1 if max_steps is None else int(max_steps))
-            self._launch_batch(batch, verlet)
+            # batch length: the steps to the next stop (output, t_max or
+            # max_steps) at the last dt, so few launches run halted after the
+            # device clock stops; powers of two replay cached graphs
+            if dt_hint is None:
+                dt_hint = self.pick_dt()
+            n = batch
+            if dt_hint > 0.0 and math.isfinite(dt_hint):
+                n = min(n, int((min(next_out, t_max) - self.t) / dt_hint) + 1)
+            if max_steps is not None:
+                n = min(n, int(max_steps) - self.step_index)
+            n = max(n, 1)
+            p = batch
+            while n > 0:
+                while p > n:
+                    p //= 2
+                self._launch_batch(p, verlet)
+                n -= p
             c = self._get_clock()
+            if float(c.dt) > 0.0:
+                dt_hint = float(c.dt)
             for db in self.dbodies:
                 db.dirty = True           # host mirrors refresh on read (also after a raise)
             steps_done = int(c.step) - self.step_index
