@@ -488,6 +488,14 @@ int tl_energies(tl_stream_t st, const tl_body* b, double* partials);
  * pos[0..m) (output.py:63-71) */
 int tl_measure(tl_stream_t st, const tl_body* b, const int32_t* pos, int64_t m, double* partials);
 
+/* VTK snapshot fields of the owned particles (output.py:84-127 write_vtk_snapshot:
+ * current position, displacement, velocity, phase field or equivalent plastic
+ * strain, and constitutive.py:154-165 cauchy_batch's stress xx yy zz xy xz yz):
+ * 16 doubles per particle at row dst[i] of out, in the caller's order, from
+ * the F/S mirrors of the last output step.  One contiguous buffer, for an
+ * asynchronous device->host copy that overlaps the next steps. */
+int tl_snapshot(tl_stream_t st, const tl_body* b, const int64_t* dst, double* out);
+
 /* ---------------------------------------------------------------------------
  * Penalty contact between two bodies (contact.cu; dynamics.py:81-135,
  * backends/fast.py:426-469).  Current positions x = X + u, velocities v.

@@ -146,6 +146,7 @@ _SIGS = {
     "tl_energy_blocks": (I64, [I64]),
     "tl_energies": (INT, [P, C.POINTER(tl_body), P]),
     "tl_measure": (INT, [P, C.POINTER(tl_body), P, I64, P]),
+    "tl_snapshot": (INT, [P, C.POINTER(tl_body), P, P]),
     "tl_contact_workspace_bytes": (INT, [I64, I64, I64, C.POINTER(I64)]),
     "tl_contact_pair": (INT, [P, C.POINTER(tl_contact_side), C.POINTER(tl_contact_side), INT, D, D,
                               D, D, I64, P, I64, P, P, P]),

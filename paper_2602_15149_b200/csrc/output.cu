@@ -116,6 +116,49 @@ void launch_energies(cudaStream_t st, const tl_body& b, double* part) {
     else k_energies<R, DIM, 2><<<g, kThreads, 0, st>>>(b, part);
 }
 
+// VTK snapshot record of every owned particle (output.py:84-127 reads x, u,
+// v, the phase field or equivalent plastic strain, and the Cauchy stress of
+// constitutive.cauchy_batch): 16 FP64 per particle written at row dst[i] (the
+// caller's order), so one contiguous device->host copy delivers the snapshot
+// a VTK writer needs.  sigma = sym(F S F^T) / J, zero where J <= J_MIN.
+template <typename R>
+__global__ void __launch_bounds__(kThreads) k_snapshot(const tl_body b, const int64_t* dst,
+                                                       double* out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= b.n) return;
+    const int64_t N = b.n_all;
+    const R* us = static_cast<const R*>(b.us);
+    const R* v = static_cast<const R*>(b.v);
+    double* o = out + 16 * dst[i];
+    const double u0 = double(us[4 * i]), u1 = double(us[4 * i + 1]), u2 = double(us[4 * i + 2]);
+    o[0] = b.Xs[i] + u0;
+    o[1] = b.Xs[N + i] + u1;
+    o[2] = b.Xs[2 * N + i] + u2;
+    o[3] = u0; o[4] = u1; o[5] = u2;
+    o[6] = double(v[i]); o[7] = double(v[N + i]); o[8] = double(v[2 * N + i]);
+    o[9] = b.model == 3 ? double(static_cast<const R*>(b.epbar)[i]) : double(us[4 * i + 3]);
+    const double* F = b.F_out + 9 * i;
+    const double* S = b.S_out + 9 * i;
+    const double J = F[0] * (F[4] * F[8] - F[5] * F[7]) - F[1] * (F[3] * F[8] - F[5] * F[6]) +
+                     F[2] * (F[3] * F[7] - F[4] * F[6]);
+    double sg[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    if (J > TL_J_MIN) {
+        double FS[9], sig[9];
+        for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c)
+                FS[3 * r + c] = F[3 * r] * S[c] + F[3 * r + 1] * S[3 + c] + F[3 * r + 2] * S[6 + c];
+        for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c)
+                sig[3 * r + c] = (FS[3 * r] * F[3 * c] + FS[3 * r + 1] * F[3 * c + 1] +
+                                  FS[3 * r + 2] * F[3 * c + 2]) / J;
+        sg[0] = sig[0]; sg[1] = sig[4]; sg[2] = sig[8];
+        sg[3] = 0.5 * (sig[1] + sig[3]);
+        sg[4] = 0.5 * (sig[2] + sig[6]);
+        sg[5] = 0.5 * (sig[5] + sig[7]);
+    }
+    for (int k = 0; k < 6; ++k) o[10 + k] = sg[k];
+}
+
 }  // namespace
 
 extern "C" int64_t tl_energy_blocks(int64_t n) { return (int64_t)tl_blocks(n, kThreads); }
@@ -148,4 +191,16 @@ extern "C" int tl_measure(tl_stream_t st_, const tl_body* b, const int32_t* pos,
     if (b->precision == 4) k_measure<float><<<g, kThreads, 0, st>>>(*b, pos, m, partials);
     else k_measure<double><<<g, kThreads, 0, st>>>(*b, pos, m, partials);
     return tl_check_launch("k_measure");
+}
+
+extern "C" int tl_snapshot(tl_stream_t st_, const tl_body* b, const int64_t* dst, double* out) {
+    if (!b || b->n <= 0 || !b->F_out || !b->S_out || !b->us || !b->v || !dst || !out) {
+        tl_set_error("tl_snapshot: descriptor needs the F/S host-layout mirrors, u|s and v");
+        return TL_ERR_ARG;
+    }
+    cudaStream_t st = (cudaStream_t)st_;
+    const unsigned g = tl_blocks(b->n, kThreads);
+    if (b->precision == 4) k_snapshot<float><<<g, kThreads, 0, st>>>(*b, dst, out);
+    else k_snapshot<double><<<g, kThreads, 0, st>>>(*b, dst, out);
+    return tl_check_launch("k_snapshot");
 }

@@ -117,3 +117,68 @@ def install(module):
     module.compute_energies = compute_energies
     module.measure_row = measure_row
     return module
+
+
+class Snapshot:
+    """Asynchronous VTK snapshot of every body (the fields output.py:84-127
+    writes: position, displacement, velocity, phase field or equivalent
+    plastic strain, Cauchy stress).  ``tl_snapshot`` packs them on the device
+    into one (n, 16) FP64 buffer in the caller's order, and a side stream
+    copies it into page-locked host memory while the next steps run.
+    ``fields(bi)`` waits for body bi's copy and returns numpy views; they stay
+    valid until the next snapshot of the simulation.  Needs the F/S mirrors
+    (mirrors=True), written on output steps, so take it from ``on_output``."""
+
+    LAYOUT = {"x": (0, 3), "u": (3, 6), "v": (6, 9), "scalar": (9, 10), "cauchy": (10, 16)}
+
+    def __init__(self, sim):
+        import torch
+        self.parts = []
+        L = _lib.lib()
+        for db in sim.dbodies:
+            if db.F_out is None:
+                raise ValueError("snapshots need the stress mirrors: construct the simulation "
+                                 "with mirrors=True")
+            nh = int(db.host.X.shape[0])
+            buf = getattr(db, "_snap", None)
+            if buf is None:
+                buf = {"dev": torch.zeros((nh, 16), dtype=torch.float64, device=db.dev),
+                       "host": torch.zeros((nh, 16), dtype=torch.float64, pin_memory=True),
+                       "stream": torch.cuda.Stream(), "done": None}
+                db._snap = buf
+            if buf["done"] is not None:      # the previous copy still reads these buffers
+                buf["done"].synchronize()
+            dst, _ = db._gid_dev()
+            _lib.check(L.tl_snapshot(sim._st(), _lib.C.byref(db.desc), _lib.ptr(dst),
+                                     _lib.ptr(buf["dev"])), "tl_snapshot")
+            ready = torch.cuda.Event()
+            ready.record(sim.stream)
+            with torch.cuda.stream(buf["stream"]):
+                buf["stream"].wait_event(ready)
+                buf["host"].copy_(buf["dev"], non_blocking=True)
+                done = torch.cuda.Event()
+                done.record(buf["stream"])
+            buf["done"] = done
+            self.parts.append(buf)
+        self.t = sim.t
+        self.step = sim.step_index
+
+    @property
+    def nbytes(self):
+        return sum(int(b["host"].numel()) * 8 for b in self.parts)
+
+    def wait(self):
+        for b in self.parts:
+            b["done"].synchronize()
+        return self
+
+    def fields(self, bi=0):
+        b = self.parts[bi]
+        b["done"].synchronize()
+        a = b["host"].numpy()
+        return {k: a[:, lo:hi] if hi - lo > 1 else a[:, lo] for k, (lo, hi) in self.LAYOUT.items()}
+
+
+def snapshot_async(sim):
+    """Start an asynchronous snapshot of ``sim`` (see Snapshot)."""
+    return Snapshot(sim)

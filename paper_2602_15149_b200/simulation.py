@@ -1135,6 +1135,27 @@ class DeviceSimulation:
             self._clock_steps(nsteps, verlet)
             return
         torch = _torch()
+        g = self._graph(nsteps, verlet)
+        with torch.cuda.stream(self.stream):
+            g.replay()
+
+    def prepare_graphs(self, batch=64):
+        """Capture the step graphs run() and advance() replay (power-of-two
+        batch lengths up to ``batch``) ahead of time; otherwise each is
+        captured on first use.  Launches nothing."""
+        if not self.use_graphs:
+            return
+        if not self._initialized:
+            self.initialize()
+        verlet = int(self.config.step_algorithm) != 2
+        p = 1
+        while p <= batch:
+            self._graph(p, verlet)
+            p *= 2
+
+    def _graph(self, nsteps, verlet):
+        """The captured graph of nsteps device-clock steps (captured once)."""
+        torch = _torch()
         key = (int(nsteps), bool(verlet))
         g = self._graphs.get(key)
         if g is None:
@@ -1150,8 +1171,7 @@ class DeviceSimulation:
                 self.stream = saved
             self.stream.wait_stream(cap)
             self._graphs[key] = g
-        with torch.cuda.stream(self.stream):
-            g.replay()
+        return g
 
     def advance(self, nsteps, pass_events=None):
         """Launch exactly ``nsteps`` device-clock steps (adaptive dt, or the

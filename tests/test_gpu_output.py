@@ -216,3 +216,34 @@ def test_branch2d_crack_branching_matches_reference(precision):
           f"FE end {fe[-1]:.4g} (ref {G['series.fe'][-1]:.4g})")
     assert jac >= 0.8, jac
     assert abs(fe[-1] - G["series.fe"][-1]) <= 0.05 * abs(G["series.fe"][-1])
+
+
+@pytest.mark.parametrize("tag,precision", [("kalthoff3d", "fp64"), ("taylor3d", "fp64"),
+                                           ("kalthoff2d_p", "fp32")])
+def test_snapshot_async_matches_state(tag, precision):
+    """output.snapshot_async: the packed VTK fields copied asynchronously
+    equal the host state after the output step (x = X + u, u, v, s or
+    epbar) and the reference's cauchy_batch of its F and S."""
+    from paper_2602_15149_b200 import output
+    from paper_2602_15149_b200.simulation import DeviceSimulation
+    G = golden(f"run_{tag}")
+    cfg = run_case(G)
+    sim = DeviceSimulation(cfg, precision=precision)
+    snaps = []
+    sim.run(time_max=1e30, time_out=1e30, max_steps=3,
+            on_output=lambda s: snaps.append(output.snapshot_async(s).wait()))
+    snap = output.snapshot_async(sim)
+    st = cfg.bodies[0].state
+    f = snap.fields(0)
+    assert np.array_equal(f["u"], st.u) and np.array_equal(f["v"], st.v)
+    assert np.array_equal(f["x"], st.X + st.u)
+    scal = st.epbar if int(cfg.bodies[0].material.model) == 3 else st.s
+    assert np.array_equal(f["scalar"], scal)
+    F, S = st.F, st.S
+    J = np.linalg.det(F)
+    sig = np.matmul(np.matmul(F, S), np.swapaxes(F, 1, 2)) / J[:, None, None]
+    sig = 0.5 * (sig + np.swapaxes(sig, 1, 2))
+    ref = np.stack([sig[:, 0, 0], sig[:, 1, 1], sig[:, 2, 2], sig[:, 0, 1], sig[:, 0, 2],
+                    sig[:, 1, 2]], axis=1)
+    assert np.abs(f["cauchy"] - ref).max() <= 1e-13 * max(np.abs(ref).max(), 1e-300)
+    assert snap.nbytes == 16 * 8 * st.X.shape[0]
