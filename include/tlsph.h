@@ -415,6 +415,15 @@ typedef struct {
     /* time window in which whole-body BC entries can apply: outside it the
      * step treats particles without a BC bit as BC-free */
     double bcw_lo, bcw_hi;
+    /* peer-memory halo exchange (multi-GPU slabs, dist.PeerHalo): pass A also
+     * stores each boundary particle's pass-B record, and pass B its (u, s)
+     * record, straight into the neighbouring ranks' halo rows over NVLink
+     * (peer_rb / peer_us: the peers' record arrays, mapped by CUDA IPC).
+     * peer_slot: 2 planes of n_all int32, the row of particle i in the side-k
+     * peer's arrays, -1 when it is not sent there.  NULL: no peer stores. */
+    const int32_t* peer_slot;
+    void* peer_us[2];
+    void* peer_rb[2];
 } tl_body;
 
 #define TL_BRICK_MAX_CLASSES 256

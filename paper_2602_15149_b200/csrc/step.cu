@@ -1254,6 +1254,18 @@ __device__ __forceinline__ double a_finish(const tl_body& b, int64_t i, R* D, R*
     tl::st4(rb, PL[0], PL[3], PL[1], PL[4]);
     tl::st4(rb + 4, PL[2], PL[5], PL[6], PL[7]);
     tl::st4(rb + 8, vv[i], vv[N + i], vv[2 * N + i], PL[8]);
+    if (b.peer_slot) {   // the record into the neighbouring ranks' halo rows (NVLink)
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int32_t slot = b.peer_slot[k * N + i];
+            if (slot >= 0) {
+                R* pr = static_cast<R*>(b.peer_rb[k]) + 12 * (int64_t)slot;
+                tl::st4(pr, PL[0], PL[3], PL[1], PL[4]);
+                tl::st4(pr + 4, PL[2], PL[5], PL[6], PL[7]);
+                tl::st4(pr + 8, vv[i], vv[N + i], vv[2 * N + i], PL[8]);
+            }
+        }
+    }
     if (mirror_out(b)) {
 #pragma unroll
         for (int q = 0; q < 9; ++q) {
@@ -1641,6 +1653,15 @@ __device__ __forceinline__ EpiOut epi_body(const tl_body& b, int64_t i, uint32_t
             sdp[i] = sd;
         }
         tl::st4(static_cast<R*>(b.us) + 4 * i, us_new[0], us_new[1], us_new[2], us_new[3]);
+        if (b.peer_slot) {   // (u, s) into the neighbouring ranks' halo rows (NVLink)
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const int32_t slot = b.peer_slot[k * N + i];
+                if (slot >= 0)
+                    tl::st4(static_cast<R*>(b.peer_us[k]) + 4 * (int64_t)slot, us_new[0], us_new[1],
+                            us_new[2], us_new[3]);
+            }
+        }
     }
     vout[i] = R(vel.x);
     vout[N + i] = R(vel.y);

@@ -278,3 +278,73 @@ class BodyPartition:
         off = self.owner[gid] != self.rank
         self.needed_gid = halo_order(gid[off], self.owner)
         self.halo_rows = np.searchsorted(self.sub, self.needed_gid).astype(np.int64)   # sub ascending
+
+
+class PeerHalo:
+    """Halo exchange through peer memory instead of messages.
+
+    Each rank maps its slab neighbours' `us` and `rb` record arrays (CUDA IPC
+    handles shared through the process group; over NVLink on an 8-GPU box)
+    and the step kernels store every boundary particle's records straight
+    into the neighbours' halo rows as they produce them: pass A the pass-B
+    record, pass B the new (u, s).  The transfer rides on the compute -- no
+    pack kernel, no send/recv.  Ordering comes from the per-step collectives
+    the step already has or adds: a barrier all-reduce after pass A (the
+    neighbours' records have landed before pass B reads them, and they are
+    done reading their (u, s) halo before pass B overwrites it) and the dt
+    all-reduce after pass B (the new (u, s) have landed before the next pass
+    A; the neighbours are done with their pass-B records before the next
+    pass A overwrites them).
+
+    ``peer_slot`` (2, n_all) int32: for each owned particle, its row in the
+    side-k neighbour's arrays (-1: not sent there).  Up to two neighbours per
+    rank (slabs); None from ``build`` when the plan needs more."""
+
+    def __init__(self, slot, peers, keep):
+        self.slot = slot
+        self.peers = peers          # [(us, rb)] per side: the neighbours' tensors (mapped)
+        self._keep = keep
+
+    @classmethod
+    def build(cls, plan, us, rb, group=None):
+        """Collective.  plan: this rank's HaloPlan; us, rb: its record arrays."""
+        import torch
+        import torch.distributed as dist
+        from torch.multiprocessing.reductions import reduce_tensor
+        me = plan.rank
+        mine = {"n_own": plan.n_own, "recv_off": plan.recv_off.tolist(),
+                "us": reduce_tensor(us), "rb": reduce_tensor(rb),
+                "sides": [q for q in range(plan.nranks) if plan.send_cnt[q] > 0]}
+        allinfo = [None] * plan.nranks
+        dist.all_gather_object(allinfo, mine, group=group)
+        send_to = mine["sides"]
+        ok = len(send_to) <= 2 and all(len(a["sides"]) <= 2 for a in allinfo)
+        if not ok:
+            return None
+        n_all = int(us.shape[0])
+        slot = torch.full((2, n_all), -1, dtype=torch.int32)
+        peers, keep = [], []
+        for side, q in enumerate(send_to):
+            info = allinfo[q]
+            base = int(info["n_own"]) + int(info["recv_off"][me])
+            rows = torch.from_numpy(np.asarray(plan.send_rows[q], dtype=np.int64))
+            slot[side, rows] = torch.arange(base, base + rows.shape[0], dtype=torch.int32)
+            fn, args = info["us"]
+            pu = fn(*args)
+            fn, args = info["rb"]
+            pr = fn(*args)
+            peers.append((pu, pr))
+            keep.extend([pu, pr])
+        return cls(slot.to(us.device).contiguous(), peers, keep)
+
+    def fill(self, d):
+        """Set the peer-store fields of a tl_body descriptor."""
+        import ctypes as C
+        d.peer_slot = C.c_void_p(self.slot.data_ptr())
+        for k in range(2):
+            if k < len(self.peers):
+                d.peer_us[k] = C.c_void_p(self.peers[k][0].data_ptr())
+                d.peer_rb[k] = C.c_void_p(self.peers[k][1].data_ptr())
+            else:
+                d.peer_us[k] = None
+                d.peer_rb[k] = None

@@ -57,7 +57,8 @@ def compute_energies(body, be=None, grad_buf=None):
     if db.psi_out is None:
         raise ValueError("energies need the stress mirrors: construct the simulation "
                          "with mirrors=True")
-    if db.body.fracture and getattr(db, "exchange", None) is not None:
+    if (db.body.fracture and getattr(db, "exchange", None) is not None
+            and getattr(db, "peer", None) is None):
         # the fracture energy's grad s reads halo s, last exchanged before pass A:
         # refresh the halo rows from their owners (collective)
         db.exchange.exchange(db.us)

@@ -685,6 +685,7 @@ class DeviceSimulation:
         if tdist.is_available() and tdist.is_initialized():
             self.world = tdist.get_world_size(group)
         self.partitioned = self.world > 1 if partition is None else bool(partition)
+        self.peer = False
         if self.partitioned and not (tdist.is_available() and tdist.is_initialized()):
             raise ValueError("partition=True needs an initialised torch.distributed group")
         if len(self.bodies) > 1 and self.partitioned:
@@ -710,6 +711,22 @@ class DeviceSimulation:
                 assert plan.n_halo == db.n_all - db.n
                 db.exchange = dist.HaloExchange(plan, "cuda", group=group)
                 db.comm_stream = torch.cuda.Stream()
+        # peer-memory halo (dist.PeerHalo, TLSPH_PEER=1; Verlet): the step
+        # kernels store boundary records into the neighbours' halo rows
+        self.peer = (self.partitioned and os.environ.get("TLSPH_PEER", "0") == "1"
+                     and int(config.step_algorithm) != 2)
+        if self.peer:
+            halos = [dist.PeerHalo.build(db.exchange.plan, db.us, db.rb, group=group)
+                     for db in self.dbodies]
+            flag = torch.tensor([int(all(h is not None for h in halos))], dtype=torch.int64,
+                                device="cuda")
+            dist.allreduce(flag, "min", group)
+            self.peer = bool(int(flag.item()))
+            for db, h in zip(self.dbodies, halos):
+                db.peer = h if self.peer else None
+                if db.peer is not None:
+                    db.peer.fill(db.desc)
+            self._barrier_t = torch.zeros(1, dtype=torch.int64, device="cuda")
         for b, db in zip(self.bodies, self.dbodies):
             b.state = DeviceState(db.host, db)
         self._setup_contact(torch)
@@ -914,7 +931,13 @@ class DeviceSimulation:
             finally:
                 d.tile, d.tlist = tile, tl
 
-        if db.tile_a:
+        if self.peer:
+            # the halo (u, s) rows were stored by the neighbours' pass B, ordered
+            # by the dt all-reduce; after pass A, a barrier all-reduce orders
+            # the pass-B records this pass A stored into the neighbours
+            launch()
+            dist.allreduce(self._barrier_t, "max", self.group)
+        elif db.tile_a:
             self._exchange_and_launch(db, db.us, launch)   # halo (u, s) from the owners
         else:
             self._exchange_plain(db, db.us, launch)
@@ -934,7 +957,9 @@ class DeviceSimulation:
             finally:
                 d.tile, d.tlist = tile, tl
 
-        if db.tile_b:
+        if self.peer:
+            launch()                                   # halo records stored by the neighbours
+        elif db.tile_b:
             self._exchange_and_launch(db, db.rb, launch)   # halo (P L, v) from the owners
         else:
             self._exchange_plain(db, db.rb, launch)        # no tile split: exchange first

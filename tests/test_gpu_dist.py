@@ -51,7 +51,7 @@ def _worker(rank, world, port, tag, precision, out_dir):
     mrow = np.array(output.measure_row(cfg.bodies[0], idx, sim.t)[1:7])  # collective
     np.savez(os.path.join(out_dir, f"r{rank}.npz"), gid=g, u=st.u[g], v=st.v[g], s=st.s[g],
              S=st.S[g], n_halo=db.n_all - db.n, dt=dt_next, energies=energies, mrow=mrow,
-             bsplit=db.bsplit, tile=db.layout.tile)
+             bsplit=db.bsplit, tile=db.layout.tile, peer=int(sim.peer))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -253,3 +253,16 @@ def test_slab_local_ranks_bit_identical(tmp_path):
         for k in ("u", "v", "s", "S"):
             assert np.array_equal(d[k], getattr(st, k)[g]), (r, k)
     assert seen.all()
+
+
+@pytest.mark.parametrize("tag,world", [("kalthoff3d", 2), ("kalthoff2d_p", 3), ("taylor3d", 2)])
+def test_peer_memory_halo_bit_identical(tag, world, tmp_path, monkeypatch):
+    """Peer-memory halo exchange (dist.PeerHalo, TLSPH_PEER=1): the step
+    kernels store boundary records straight into the neighbours' halo rows
+    (CUDA IPC mappings; ranks share the one GPU here, NVLink peers on a
+    multi-GPU box), ordered by the per-step all-reduces.  FP64 owned rows stay
+    bit-identical to one GPU."""
+    monkeypatch.setenv("TLSPH_PEER", "1")          # inherited by the spawned ranks
+    test_multi_rank_device_bit_identical(tag, world, "fp64", tmp_path, monkeypatch)
+    for r in range(world):
+        assert int(np.load(tmp_path / f"r{r}.npz")["peer"]) == 1, r

@@ -50,8 +50,9 @@ def line_table(obj, mangled):
 def main():
     rep, kre, obj, mangled_sub = sys.argv[1:5]
     top = int(sys.argv[5]) if len(sys.argv) > 5 else 40
-    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass",
-                          "-k", f"regex:{kre}"], capture_output=True, text=True).stdout
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    import ncu_io
+    out = ncu_io.source(rep, kre)
     rows = list(csv.reader(io.StringIO(out)))
     name = mangled_sub
     hdr = rows[1]
