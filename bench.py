@@ -503,9 +503,10 @@ def measure(args, cfg, precision, world, local, clocks_on):
     passes = {"pass_a_ms": ma, "pass_b_ms": mb, "bytes_a": ba, "bytes_b": bb,
               "frac_a": ba * n / (ma / 1e3) / 1e9 / peak,
               "frac_b": bb * n / (mb / 1e3) / 1e9 / peak}
-    # kernels per timed step: clock begin + commit, and per body pass A, the
-    # dt-maxima reset, pass B (+ the plastic-work reduction for J2 bodies)
-    per_step = 2 + sum(3 + (int(db.body.material.model) == 3) for db in sim.dbodies)
+    # our kernels per timed step: clock begin + commit, and per body pass A and
+    # pass B (+ the plastic-work reduction for J2 bodies); the dt-maxima reset
+    # is a memset
+    per_step = 2 + sum(2 + (int(db.body.material.model) == 3) for db in sim.dbodies)
     mem = torch.cuda.max_memory_allocated()
     return {"sim": sim, "n": n, "n_total": n_total, "k_mean": k_mean, "value": value,
             "device_bytes_per_particle": mem / max(n, 1),
