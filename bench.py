@@ -318,7 +318,8 @@ def main():
                 "ms_per_step": 1e3 * ref["seconds"] / max(ref["steps"], 1),
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": "f64", "data": "synthetic (seeded perturbed lattice state)",
-                "config": {"workload": f"{args.config} CPU sample", "sample": ref["sample"]},
+                "config": {"workload": WORKLOAD_NAMES[args.config],
+                           "cpu_sample": ref["sample"], "precision": "fp64"},
                 "impl": "reference",
                 "cpu_baseline": {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")},
                 "e2e": {"value": ref["value"], "unit": "particle-steps/s",
