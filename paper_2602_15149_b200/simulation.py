@@ -38,7 +38,10 @@ INT64_MAX = np.iinfo(np.int64).max
 N_COUNTERS = 8
 # particles per CTA / shared-memory tile, one per thread (TLSPH_TILE overrides;
 # a multiple of 32, at most 256)
-DEFAULT_TILE = {"fp32": 160, "fp64": 160}   # measured on B200 (C4): 160 best in both modes
+# measured on B200 (C4, bond classes): FP32 256 particles per tile (6.90 -> 6.99
+# G particle-steps/s against 160; pass B 1.31 -> 1.28 ms); FP64 (128 registers per
+# thread) 128 (2.69 -> 2.91)
+DEFAULT_TILE = {"fp32": 256, "fp64": 128}
 TILE_SMEM_LIMIT = 200 * 1024  # bytes of shared memory a pass-B tile may take
 
 

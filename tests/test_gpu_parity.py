@@ -485,8 +485,8 @@ def test_long_run_beam2d_2000_steps_fp64():
 def test_bench_scale_c4_fp32_vs_oracle(oracle_mod):
     """C4 at bench layout: the 255k-particle sample bench.py times on the CPU
     (kalthoff3d, dp_scale 0.918*4, mapfac 5, SURVEY.md 8(d) perturbed state)
-    on 160-particle tiles with residue-aligned halos and tile-relative FP32
-    positions, against the FP64 oracle from the same state: step-1 F, S, a,
+    on 256-particle tiles with residue-aligned halos and bond classes,
+    against the FP64 oracle from the same state: step-1 F, S, a,
     u, v within 1e-5; after 10 steps u 2e-5, v and S 2e-4, and |s| within
     2e-3 absolute: the synthetic s ~ U(0.3, 1) field is white noise with an
     O(1) Laplacian, so s sweeps its whole range in 10 steps (max |s(10) -
@@ -512,7 +512,7 @@ def test_bench_scale_c4_fp32_vs_oracle(oracle_mod):
     cfg = make()
     sim = DeviceSimulation(cfg, precision="fp32")
     db = sim.dbodies[0]
-    assert db.n > 250_000 and db.layout.tile == 160 and db.tile_a and db.tile_b
+    assert db.n > 250_000 and db.layout.tile == 256 and db.tile_a and db.tile_b
     assert db.layout.hmax > 0
     so.initialize()
     sim.initialize()
