@@ -562,7 +562,11 @@ class BrickLayout:
         rsz = 16 if precision == "fp32" else 32
         cols = cls._columns(qk)
         best = None
-        for B in cls.CANDIDATES:
+        cands = cls.CANDIDATES
+        env_dims = os.environ.get("TLSPH_BRICK_DIMS")     # "bx,by,bz": measurement override
+        if env_dims:
+            cands = [tuple(int(v) for v in env_dims.split(","))]
+        for B in cands:
             # register blocking (2 cells per thread) measured slower on B200 --
             # C2 0.98 vs 1.50 G particle-steps/s: half the warps per SM for a
             # walk with data-dependent bounds -- so it is opt-in
