@@ -269,7 +269,7 @@ class DeviceBody:
         # entries, whole-body up to T and targeted after it (the windows are
         # inclusive on the device, so the second starts at the next double)
         entries = []
-        for bc in bcs:
+        for k, bc in enumerate(bcs):
             if bc.kind == "force" and int(getattr(bc, "ftype", 0) or 0) not in (1, 2, 3):
                 raise CaseError(f"unknown force BC type {bc.ftype}")
             tst = float(bc.tst)
@@ -281,9 +281,10 @@ class DeviceBody:
                 entries.append((bc, bit, tst, tend))
                 bit += 1
                 continue
+            # a split adds one device entry: room for it and every BC still to come
+            room = _lib_max_bc() - (len(entries) + len(bcs) - k)
             got = (self._static_targets(bc, config, X0)
-                   if static_ok and bit + n_explicit < 31 and len(entries) < len(bcs) + 8
-                   else None)
+                   if static_ok and bit + n_explicit < 31 and room >= 1 else None)
             if got is None:
                 entries.append((bc, -1, tst, tend))
                 continue

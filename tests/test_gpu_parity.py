@@ -541,6 +541,50 @@ def test_bench_scale_c4_fp32_vs_oracle(oracle_mod):
     assert errs["u"] <= 2e-5 and errs["v"] <= 2e-4 and errs["S"] <= 2e-4 and errs["s"] <= 2e-3
 
 
+def test_bench_scale_c4_fp64_vs_oracle(oracle_mod):
+    """The same 255k-particle C4 sample in FP64 (bond-class tiles, the
+    closed-form FP64 split): step-1 F, S, a at 1e-12 and, after 10 adaptive
+    steps, u, v, S and s at the FP64 run tolerances against the oracle, with
+    the dt sequence matching to 1e-12."""
+    import bench
+    from paper_2602_15149_b200 import cases
+    from paper_2602_15149_b200.simulation import DeviceSimulation
+    smp = bench.CPU_SAMPLE["C4"]
+
+    def make():
+        cfg = cases.make_case(smp["spec"], dp_scale=smp["dp_scale"], mapfac=smp["mapfac"],
+                              build_adjacency=False)
+        bench.perturb(cfg)
+        return cfg
+    cfg_o = make()
+    b = cfg_o.bodies[0]
+    b.adjacency = oracle_mod.build_adjacency(b.state.X, b.state.V0, b.h, b.dim,
+                                             int(cfg_o.kernel), nbsrange=b.nbsrange,
+                                             dp_body=b.dp_body, notches=b.notches)
+    so = oracle_mod.OracleSimulation(cfg_o)
+    cfg = make()
+    sim = DeviceSimulation(cfg, precision="fp64")
+    db = sim.dbodies[0]
+    assert db.n > 250_000 and db.bcls is not None
+    so.initialize()
+    sim.initialize()
+    sd, sr = cfg.bodies[0].state, b.state
+    for step in range(1, 11):
+        dt = so.pick_dt()
+        assert abs(sim.pick_dt() - dt) <= 1e-12 * dt, step
+        so.step(dt)
+        sim.step(dt)
+        if step == 1:
+            for k in ("F", "S", "a"):
+                x, ref = getattr(sd, k), getattr(sr, k)
+                if k == "F":
+                    x, ref = x - np.eye(3), ref - np.eye(3)
+                assert relerr(x, ref) <= 1e-12, ("step1", k, relerr(x, ref))
+    for k, tol in (("u", 1e-10), ("v", 1e-10), ("S", 1e-9)):
+        assert relerr(getattr(sd, k), getattr(sr, k)) <= tol, k
+    assert np.abs(sd.s - sr.s).max() <= 1e-10
+
+
 def _strain_from_eigs(lams, rng):
     """H = F - I (symmetric) whose Green strain E = (H + H^T + H^T H)/2 has
     eigenvalues lams: I + H = Q diag(sqrt(1 + 2 l)) Q^T."""
