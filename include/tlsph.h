@@ -249,6 +249,12 @@ typedef struct {
     int32_t prog[3];       /* program index or -1 (axis untouched unless const) */
     double cval[3];
     double tst, tend;
+    /* skip guard of a whole-body entry (expr.skip_guard_after): for t > gt the
+     * entry is skip for every particle where `var gop gc` is false (var in
+     * x0 y0 z0 x y z ux uy uz, expr.VARIABLES order; gop 0 <, 1 >, 2 <=, 3 >=),
+     * so the step evaluates it on the other particles only; gvar -1 = none */
+    int32_t gvar, gop;
+    double gc, gt;
 } tl_bc;
 
 /* device clock: time integration state kept on the device so steps never

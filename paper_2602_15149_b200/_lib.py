@@ -49,7 +49,8 @@ class tl_prog(C.Structure):
 
 class tl_bc(C.Structure):
     _fields_ = [("kind", I32), ("ftype", I32), ("bit", I32), ("has_const", I32 * 3),
-                ("prog", I32 * 3), ("cval", D * 3), ("tst", D), ("tend", D)]
+                ("prog", I32 * 3), ("cval", D * 3), ("tst", D), ("tend", D),
+                ("gvar", I32), ("gop", I32), ("gc", D), ("gt", D)]
 
 
 class tl_clock(C.Structure):

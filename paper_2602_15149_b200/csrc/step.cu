@@ -1465,6 +1465,35 @@ __device__ __forceinline__ bool whole_active(const tl_body& b) {
     return t0 <= b.bcw_hi && t0 + dt >= b.bcw_lo;
 }
 
+// some whole-body BC entry may act on particle i this step: its window meets
+// [t, t + dt] and it has no skip guard valid for this step (t > gt) or the
+// guard holds for i -- the same comparison the expression VM would make, on
+// the same FP64 variables (make_vars), so the particles it skips are exactly
+// those where every such entry evaluates to skip
+template <typename R>
+__device__ __forceinline__ bool whole_needed(const tl_body& b, int64_t i) {
+    if (!whole_active(b)) return false;
+    const double t0 = b.clock ? b.clock->t : 0.0;
+    const double dt = b.clock ? b.clock->dt : 0.0;
+    const int64_t N = b.n_all;
+    for (int k = 0; k < b.nbc; ++k) {
+        const tl_bc& c = b.bcs[k];
+        if (c.bit >= 0 || t0 > c.tend || t0 + dt < c.tst) continue;
+        if (c.gvar < 0 || !(t0 > c.gt)) return true;
+        const int a = c.gvar % 3;
+        double v;
+        if (c.gvar < 3) {
+            v = b.Xs[a * N + i];
+        } else {
+            const double u = double(static_cast<const R*>(b.us)[4 * i + a]);
+            v = c.gvar < 6 ? b.Xs[a * N + i] + u : u;
+        }
+        const bool g = c.gop == 0 ? v < c.gc : (c.gop == 1 ? v > c.gc : (c.gop == 2 ? v <= c.gc : v >= c.gc));
+        if (g) return true;
+    }
+    return false;
+}
+
 __device__ __forceinline__ bool bc_applies(const tl_bc& c, uint32_t mask, double t) {
     if (!(c.tst <= t && t <= c.tend)) return false;
     return c.bit < 0 || ((mask >> c.bit) & 1u);
@@ -1602,7 +1631,7 @@ __device__ __forceinline__ EpiOut epi_body(const tl_body& b, int64_t i, uint32_t
     acc[2] = tl::add_rn(acc[2], b.f0[2]);
     const R* us = static_cast<const R*>(b.us);
     const auto ui = tl::ld4(us + 4 * i);
-    const bool has_bc = BC && b.nbc && (mask || whole_active(b));
+    const bool has_bc = BC && b.nbc && (mask || whole_needed<R>(b, i));
     const double t0 = b.clock ? b.clock->t : 0.0;
     const double dt = b.clock ? b.clock->dt : 0.0;
     const double tf = MODE == TL_B_INIT ? 0.0 : (MODE == TL_B_SYMPL ? t0 + 0.5 * dt : t0);
@@ -1738,7 +1767,7 @@ __device__ __forceinline__ EpiOut b_finish(const tl_body& b, int64_t i, R* s1, R
     // expressions only on the (rare) particles that carry them, out of
     // line, so the common path holds no call frame
     const uint32_t mask = b.bcmask ? b.bcmask[i] : 0u;
-    const bool slow = (b.nbc && (mask || whole_active(b))) || (FRAC && restrict_applies(b, mask));
+    const bool slow = (b.nbc && (mask || whole_needed<R>(b, i))) || (FRAC && restrict_applies(b, mask));
     const EpiOut o = slow ? epi_slow<R, DIM, MODE, FRAC>(&b, i, mask, acc[0], acc[1], acc[2],
                                                          vi0, vi1, vi2)
                           : epi_body<R, DIM, MODE, FRAC, false>(b, i, mask, acc[0], acc[1],
@@ -2418,7 +2447,7 @@ __global__ void __launch_bounds__(kThreads) k_predict(const tl_body b) {
            double(tl::axpy_rn(vp[2 * N + i], R(half), ap[2 * N + i]))};
     const uint32_t mask = b.bcmask ? b.bcmask[i] : 0u;
     const D3 X0{xi, yi, zi};
-    if (b.nbc && (mask || whole_active(b)))
+    if (b.nbc && (mask || whole_needed<R>(b, i)))
         vel = velocity_bcs(bc_ctx(b), mask, X0, D3{double(ui.x), double(ui.y), double(ui.z)}, th, dt, vel);
     R vR[3] = {R(vel.x), R(vel.y), R(vel.z)};
     R un[4] = {tl::axpy_rn(ui.x, R(half), vR[0]), DIM == 3 ? tl::axpy_rn(ui.y, R(half), vR[1]) : R(0),

@@ -680,3 +680,45 @@ def nonskip_mask_after(ast, X0):
         return T, walk(root, np.ones(n, dtype=bool))
     except _NotStatic:
         return None
+
+
+# -- skip guards ---------------------------------------------------------------
+# ``if(z<1.0e-12, 0.0, if(t<=0.0, Vinit, skip))`` (a wall) depends on the
+# current z, so no particle set is fixed -- but after t = 0 it is skip wherever
+# the single comparison z < 1e-12 is false.  The step tests that comparison
+# inline and runs the expression only where it holds.
+
+_GUARD_OPS = {"<": 0, ">": 1, "<=": 2, ">=": 3}
+_GUARD_VARS = ("x0", "y0", "z0", "x", "y", "z", "ux", "uy", "uz")
+
+
+def skip_guard_after(ast):
+    """(T, var index, op code, const): for t > T, ``ast`` is skip wherever
+    ``var op const`` is false (expr.VARIABLES index; op 0 <, 1 >, 2 <=, 3 >=).
+    None when its late-time skip pattern is not one such comparison."""
+    T = [-math.inf]
+
+    def late(node):
+        """The node with t-comparisons on skip paths resolved for t -> inf."""
+        while node[0] == "if" and _has_skip(node):
+            tc = _t_compare(node[1])
+            if tc is None:
+                return node
+            T[0] = max(T[0], tc[1])
+            node = node[2] if tc[0] in (">", ">=") else node[3]
+        return node
+
+    node = late(ast.root if isinstance(ast, ExprAst) else ast)
+    if node[0] != "if" or not _has_skip(node):
+        return None
+    cond, a, b = node[1], late(node[2]), late(node[3])
+    if cond[0] != "bin" or cond[1] not in _GUARD_OPS:
+        return None
+    lhs, rhs, op = cond[2], cond[3], cond[1]
+    if lhs[0] == "num" and rhs[0] == "var":
+        lhs, rhs, op = rhs, lhs, _T_FLIP[op]
+    if lhs[0] != "var" or lhs[1] not in _GUARD_VARS or rhs[0] != "num":
+        return None
+    if b[0] == "skip" and not _has_skip(a):          # if(guard, value, skip)
+        return T[0], VARIABLES.index(lhs[1]), _GUARD_OPS[op], float(rhs[1])
+    return None

@@ -278,7 +278,7 @@ class DeviceBody:
                 if bit >= 32:
                     raise CaseError(f"body {body.mk}: more than 32 targeted boundary conditions")
                 mask[np.asarray(bc.target, dtype=np.int64)] |= np.uint32(1 << bit)
-                entries.append((bc, bit, tst, tend))
+                entries.append((bc, bit, tst, tend, None))
                 bit += 1
                 continue
             # a split adds one device entry: room for it and every BC still to come
@@ -286,28 +286,32 @@ class DeviceBody:
             got = (self._static_targets(bc, config, X0)
                    if static_ok and bit + n_explicit < 31 and room >= 1 else None)
             if got is None:
-                entries.append((bc, -1, tst, tend))
+                entries.append((bc, -1, tst, tend, self._skip_guard(bc, config)
+                                if static_ok else None))
                 continue
             T, tgt = got
             if T >= tend:                  # static only after the BC has ended
-                entries.append((bc, -1, tst, tend))
+                entries.append((bc, -1, tst, tend, None))
                 continue
             if T >= tst:
-                entries.append((bc, -1, tst, T))
+                entries.append((bc, -1, tst, T, None))
                 tst = float(np.nextafter(T, np.inf))
             mask[tgt] |= np.uint32(1 << bit)
-            entries.append((bc, bit, tst, tend))
+            entries.append((bc, bit, tst, tend, None))
             bit += 1
         if len(entries) > _lib_max_bc():
             raise CaseError(f"body {body.mk}: more than {_lib_max_bc()} boundary conditions")
         arr = (_lib.tl_bc * max(len(entries), 1))()
         self.bc_whole = 0
         self.bcw_lo, self.bcw_hi = math.inf, -math.inf   # activity window of whole-body entries
-        for k, (bc, bbit, tst, tend) in enumerate(entries):
+        for k, (bc, bbit, tst, tend, guard) in enumerate(entries):
             d = arr[k]
             d.kind = 0 if bc.kind == "vel" else 1
             d.ftype = int(getattr(bc, "ftype", 0) or 0)
             d.bit = bbit
+            d.gvar = -1
+            if guard is not None:
+                d.gt, d.gvar, d.gop, d.gc = guard
             if bbit < 0:
                 self.bc_whole = 1
                 self.bcw_lo = min(self.bcw_lo, tst)
@@ -349,6 +353,27 @@ class DeviceBody:
         else:
             self.restrict_prog = -1
         self.bcmask = torch.from_numpy(mask[self.hrow].view(np.int32)).to(self.dev)
+
+    @staticmethod
+    def _skip_guard(bc, config):
+        """(T, var, op, c) when every expression axis of a whole-body BC is
+        skip for t > T wherever the same single comparison ``var op c`` is
+        false (expr.skip_guard_after) and no axis is a constant; else None."""
+        guard = None
+        T = -math.inf
+        for ax in range(3):
+            c, e = bc.const[ax], bc.expr[ax]
+            if c is not None:
+                return None
+            if e is None:
+                continue
+            ast = config.expressions.get(e)
+            g = ex.skip_guard_after(ast) if ast is not None else None
+            if g is None or (guard is not None and g[1:] != guard):
+                return None
+            guard = g[1:]
+            T = max(T, g[0])
+        return None if guard is None else (T,) + guard
 
     @staticmethod
     def _static_targets(bc, config, X0):

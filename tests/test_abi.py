@@ -230,3 +230,13 @@ def test_skip_patterns_static_after_a_time():
     assert ex.nonskip_mask_after(ex.parse("if(t>2e-6, skip, if(x0>0.01, 1.0, skip))"),
                                  X)[1].tolist() == [False, False, False]
     assert ex.nonskip_mask_after(ex.parse("if(z<1.0e-12,0.0,if(t<=0.0,1.0,skip))"), X) is None
+
+
+def test_skip_guards():
+    """expr.skip_guard_after: the late-time skip pattern as one comparison."""
+    from paper_2602_15149_b200 import expr as ex
+    assert ex.skip_guard_after(ex.parse("if(z<1.0e-12,0.0,if(t<=0.0,Vinit,skip))",
+                                        "Vinit=-227;")) == (0.0, 5, 0, 1e-12)
+    assert ex.skip_guard_after(ex.parse("if(1.0>ux,3.0,skip)")) == (-np.inf, 6, 0, 1.0)
+    assert ex.skip_guard_after(ex.parse("if(z<0.0, skip, 1.0)")) is None
+    assert ex.skip_guard_after(ex.parse("if(x*x<1.0, 1.0, skip)")) is None

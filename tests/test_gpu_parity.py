@@ -764,7 +764,7 @@ def test_brick_mode_plastic_work_and_graphs(monkeypatch):
     assert relerr(out["force"][1], out["0"][1]) <= 1e-10
 
 
-@pytest.mark.parametrize("tag", ["column3d", "fourpoint3d", "beam2d", "kalthoff2d"])
+@pytest.mark.parametrize("tag", ["column3d", "fourpoint3d", "beam2d", "kalthoff2d", "taylor3d"])
 def test_static_skip_bcs_bit_identical(tag, monkeypatch):
     """Whole-body BC / restrictphi expressions whose skip pattern depends on
     x0, y0, z0 only run on their non-skip particles alone: the FP64 state is
@@ -784,8 +784,12 @@ def test_static_skip_bcs_bit_identical(tag, monkeypatch):
         out[mode] = [np.array(getattr(st, k)) for k in ("u", "v", "a", "s")]
         out[mode + "w"] = db.bc_whole
         out[mode + "n"] = db.nbc
+        out[mode + "g"] = int(any(db._bc_arr[k].gvar >= 0 for k in range(db.nbc)))
     if tag in ("column3d", "fourpoint3d"):
         assert out["1w"] == 0 and out["0w"] == 1      # the conversion happened
+    if tag == "taylor3d":
+        # its wall BC tests the current z: no fixed set, but a skip guard
+        assert out["1w"] == 1 and out["1g"] == 1 and out["0g"] == 0
     if tag == "beam2d":
         # the initial-condition BC (static after t = 0) splits into a
         # whole-body entry for t <= 0 and a targeted one after it
