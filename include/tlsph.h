@@ -315,7 +315,10 @@ typedef struct {
     int32_t ncls;           /* bond classes (FP32, uniform lattice bodies): 0 = the pair
                                geometry comes from staged positions; > 0 = slots hold
                                (class << 10) | slot and bcls holds ncls entries */
-    int32_t ncls_pad;
+    int32_t lpp;            /* L2-gather pass B (tile 0 or the untiled pass B): 1, 2, 4 or
+                               8 lanes per particle, each summing every lpp-th group of the
+                               row (small FP32 bodies: one latency chain per lane is shorter);
+                               0 reads as 1 */
     const int64_t* hoff;
     const int32_t* halo;
     const uint16_t* slots;
@@ -454,10 +457,12 @@ int tl_predict(tl_stream_t st, const tl_body* b);
 
 typedef struct {
     double h, c0;
-    const unsigned long long* red;
+    unsigned long long* red;   /* the body's dt maxima words (tl_body.red) */
 } tl_dtinfo;
 
-/* dt = min(pick_dt, next_out - t, t_max - t) on the device (stepper.py:221-256) */
+/* dt = min(pick_dt, next_out - t, t_max - t) on the device (stepper.py:221-256).
+ * When the step proceeds, the maxima words are zeroed after they are read, so
+ * the step's pass B accumulates into clean words with no tl_reset_red. */
 int tl_clock_begin(tl_stream_t st, tl_clock* clock, int nbody, const tl_dtinfo* info);
 /* t += dt, step += 1, output/max_steps halting (stepper.py:199-209, 257-263) */
 int tl_clock_commit(tl_stream_t st, tl_clock* clock);

@@ -76,7 +76,7 @@ _BODY_FIELDS += [(k, D) for k in ("h", "inv_h", "alpha", "rho0", "lam", "mu", "k
                                   "inv_c0")]
 _BODY_FIELDS += [("f0", D * 3)]
 _BODY_FIELDS += [("soff", P), ("sidx", P), ("wlen", P), ("tile", I32), ("hmax", I32), ("slmax", I32), ("bsplit", I32),
-                 ("ncls", I32), ("ncls_pad", I32), ("hoff", P),
+                 ("ncls", I32), ("lpp", I32), ("hoff", P),
                  ("halo", P), ("slots", P), ("hslot", P), ("tlist", P), ("tbase", I64),
                  ("tcount", I64), ("toff", P), ("tpos_a", P), ("tpos_b", P), ("bcls", P)]
 _BODY_FIELDS += [(k, P) for k in ("Xs", "L", "V0", "m0", "ac", "us", "rb", "v", "al",

@@ -31,6 +31,14 @@ int tl_check_launch(const char* what) {
     return TL_OK;
 }
 
+bool tl_pdl_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("TLSPH_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 extern "C" int tl_abi_version(void) { return TL_ABI_VERSION; }
 extern "C" int64_t tl_struct_size(int which) {
     switch (which) {

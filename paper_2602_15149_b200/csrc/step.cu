@@ -1288,6 +1288,7 @@ __device__ __forceinline__ double a_finish(const tl_body& b, int64_t i, R* D, R*
 template <typename R, int DIM, int MODEL, bool FRAC, int KIND, int G, bool TILED>
 __global__ void __launch_bounds__(kThreads, TL_MINB_A(R, TILED)) k_pass_a(const tl_body b) {
     extern __shared__ __align__(16) unsigned char smem[];
+    tl::pdl_enter();
     // a CTA of blockDim.x threads owns blockDim.x consecutive particles (TILED:
     // one shared tile of b.tile == blockDim.x particles); one particle per
     // thread -- larger tiles looped over by 256 threads measured slower
@@ -1793,13 +1794,19 @@ template <typename R, int DIM, int MODE, bool FRAC, int KIND, int G, bool TILED,
 __global__ void __launch_bounds__(b_threads<SPLIT>(), b_minb<R, SPLIT>())
     k_pass_b(const __grid_constant__ tl_body b) {
     extern __shared__ __align__(16) unsigned char smem[];
+    tl::pdl_enter();
     // a CTA of blockDim.x threads owns blockDim.x consecutive particles (TILED:
     // one shared tile of b.tile == blockDim.x particles); one particle per
     // thread -- larger tiles looped over by 256 threads measured slower
     // (shared memory per CTA cuts residency)
     const int T = SPLIT > 1 ? b.tile : (int)blockDim.x;
     const int64_t tb = tile_of(b, TILED);
-    const int64_t p0 = tb * (int64_t)T;
+    // L2 gather: lpp consecutive lanes per particle (tl_body.lpp), each summing
+    // every lpp-th group of G slots of the row; the partial sums meet in a
+    // butterfly, so every lane of a particle holds the same total
+    const int lpp = TILED ? 1 : max(b.lpp, 1);
+    const int sub = TILED ? 0 : (int)threadIdx.x & (lpp - 1);
+    const int64_t p0 = tb * (int64_t)(T / lpp);
     if (halted(b) || stress_failed(b)) return;
     double v2 = 0.0, a2 = 0.0;
     long long bad_acc = LLONG_MAX;
@@ -1812,7 +1819,7 @@ __global__ void __launch_bounds__(b_threads<SPLIT>(), b_minb<R, SPLIT>())
         tl_ = tile_layout<R, 3>(smem, b.tile + b.hmax, b.slmax, SPLIT == 1 ? b.ncls : 0);
         stage_tile<R, 3>(b, tl_, tb, b.tpos_b, rbp, &bar);
     }
-    const int ms = SPLIT > 1 ? (int)threadIdx.x % T : (int)threadIdx.x;   // member slot
+    const int ms = SPLIT > 1 ? (int)threadIdx.x % T : (int)threadIdx.x / lpp;   // member slot
     const int part = SPLIT > 1 ? (int)threadIdx.x / T : 0;
     const bool live = p0 + ms < b.n;
     // SPLIT: every thread takes part in the share reduction; the dead ones of a
@@ -1897,7 +1904,7 @@ if (visc) TL_LOOP_B(U, ST, true); else TL_LOOP_B(U, ST, false)
             const double* __restrict__ Xp = b.Xs;
             const double* __restrict__ Yp = b.Xs + N;
             const double* __restrict__ Zp = b.Xs + 2 * N;
-            for (int k = 0; k < len; k += G) {
+            for (int k = sub * G; k < len; k += G * lpp) {
                 int32_t jj[G];
 #pragma unroll
                 for (int q = 0; q < G; ++q) jj[q] = __ldg(sidx + 32 * (k + q));
@@ -1920,6 +1927,17 @@ if (visc) TL_LOOP_B(U, ST, true); else TL_LOOP_B(U, ST, false)
                     pair_b<R, DIM, KIND>(R(xi - xj[q]), DIM == 3 ? R(yi - yj[q]) : R(0),
                                          R(zi - zj[q]), q0[q], q1[q], q2[q], mj[q], uni, vi0, vi1,
                                          vi2, visc, inv_h, eps_h2, B2, B1, s1, s2, s3);
+            }
+            if (lpp > 1) {   // a particle's lanes are live together (lpp divides 32)
+                const unsigned am = __activemask();
+                for (int o = 1; o < lpp; o <<= 1) {
+#pragma unroll
+                    for (int q = 0; q < 3; ++q) {
+                        s1[q] += __shfl_xor_sync(am, s1[q], o);
+                        s2[q] += __shfl_xor_sync(am, s2[q], o);
+                        s3[q] += __shfl_xor_sync(am, s3[q], o);
+                    }
+                }
             }
         }
         if constexpr (SPLIT > 1) {   // add the shares in part order
@@ -1946,7 +1964,7 @@ if (visc) TL_LOOP_B(U, ST, true); else TL_LOOP_B(U, ST, false)
                 }
             }
         }
-        if (live) {   // the dead lanes of a split tile still join the warp reductions
+        if (live && sub == 0) {   // the dead lanes of a split tile still join the warp reductions
             const auto r0i = TILED ? tl_.rec[3 * ms] : tl::ld4(rbp + 12 * i);
             const auto r1i = TILED ? tl_.rec[3 * ms + 1] : tl::ld4(rbp + 12 * i + 4);
             const R PLi[9] = {r0i.x, r0i.z, r1i.x, r0i.y, r0i.w, r1i.y, r1i.z, r1i.w, r2i.w};
@@ -2125,6 +2143,7 @@ template <typename R, int MODEL, bool FRAC, int KIND, int CPT>
 __global__ void __launch_bounds__(1024 / CPT, 1)
     k_brick_a(const __grid_constant__ tl_body b, const __grid_constant__ BrickTab<R> tab) {
     extern __shared__ __align__(16) unsigned char smem[];
+    tl::pdl_enter();
     __shared__ double s_pw[32];
     if (halted(b)) return;
     const int64_t t = blockIdx.x;
@@ -2243,6 +2262,7 @@ template <typename R, int MODE, bool FRAC, int KIND, int CPT>
 __global__ void __launch_bounds__(1024 / CPT, 1)
     k_brick_b(const __grid_constant__ tl_body b, const __grid_constant__ BrickTab<R> tab) {
     extern __shared__ __align__(16) unsigned char smem[];
+    tl::pdl_enter();
     if (halted(b) || stress_failed(b)) return;
     const int64_t t = blockIdx.x;
     const BrickGeo g = brick_geo(b, t, CPT);
@@ -2432,6 +2452,7 @@ __global__ void __launch_bounds__(kThreads) k_hourglass(const tl_body b) {
 // symplectic predictor (stepper.py:168-175)
 template <typename R, int DIM, bool FRAC>
 __global__ void __launch_bounds__(kThreads) k_predict(const tl_body b) {
+    tl::pdl_enter();
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (halted(b) || i >= b.n) return;
     const int64_t N = b.n_all;
@@ -2474,50 +2495,73 @@ struct DtInfos {
 };
 
 __global__ void k_clock_begin(tl_clock* c, DtInfos info) {
-    if (c->halted) return;
-    if (c->err) {          // the previous step raised: nothing more runs
+    tl::pdl_enter();
+    // every word the clock reads, loaded up front: one memory round trip
+    // instead of a chain of dependent ones (the kernel is on the critical
+    // path of every step)
+    const tl_clock cl = *c;
+    unsigned long long rv[8], ra[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        rv[k] = k < info.n ? info.d[k].red[0] : 0ull;
+        ra[k] = k < info.n ? info.d[k].red[1] : 0ull;
+    }
+    if (cl.halted) return;
+    if (cl.err) {          // the previous step raised: nothing more runs
         c->halted = 5;
         return;
     }
     c->nf_now = 0;
-    if (!(c->t < c->t_max - c->eps)) {
+    if (!(cl.t < cl.t_max - cl.eps)) {
         c->halted = 1;
         return;
     }
     double dt;
-    if (c->dt_override >= 0.0) {
-        dt = c->dt_override;
+    if (cl.dt_override >= 0.0) {
+        dt = cl.dt_override;
     } else {
         dt = INFINITY;
-        for (int k = 0; k < info.n; ++k) {
-            const double vmax = sqrt(__longlong_as_double((long long)info.d[k].red[0]));
-            const double amax = sqrt(__longlong_as_double((long long)info.d[k].red[1]));
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            if (k >= info.n) break;
+            const double vmax = sqrt(__longlong_as_double((long long)rv[k]));
+            const double amax = sqrt(__longlong_as_double((long long)ra[k]));
             const double dtv = info.d[k].h / (info.d[k].c0 + vmax);
-            double cand = amax > 0.0 ? c->cfl * fmin(dtv, sqrt(info.d[k].h / amax)) : c->cfl * dtv;
+            double cand = amax > 0.0 ? cl.cfl * fmin(dtv, sqrt(info.d[k].h / amax)) : cl.cfl * dtv;
             // a NaN maximum (non-finite state) must stop the clock, not vanish in fmin
             dt = (isnan(cand) || cand < dt) ? cand : dt;
         }
     }
-    dt = fmin(fmin(dt, c->next_out - c->t), c->t_max - c->t);
+    dt = fmin(fmin(dt, cl.next_out - cl.t), cl.t_max - cl.t);
     if (!(dt > 0.0) || isinf(dt)) {
         c->halted = 4;
         c->dt = dt;
         return;
     }
     c->dt = dt;
-    const double tn = c->t + dt;
-    c->out_step = (tn >= c->next_out - c->eps) || (tn >= c->t_max - c->eps) ||
-                  (c->max_steps >= 0 && c->step + 1 >= c->max_steps);
+    // the maxima are read: clear them for this step's pass B (replaces a
+    // memset node per body per step)
+    for (int k = 0; k < info.n; ++k) {
+        info.d[k].red[0] = 0ull;
+        info.d[k].red[1] = 0ull;
+    }
+    const double tn = cl.t + dt;
+    c->out_step = (tn >= cl.next_out - cl.eps) || (tn >= cl.t_max - cl.eps) ||
+                  (cl.max_steps >= 0 && cl.step + 1 >= cl.max_steps);
 }
 
 __global__ void k_clock_commit(tl_clock* c) {
-    if (c->halted || c->err) return;   // a step that raised is not committed
-    c->t += c->dt;
-    c->step += 1;
+    tl::pdl_enter();
+    const tl_clock cl = *c;            // one round trip (see k_clock_begin)
+    if (cl.halted || cl.err) return;   // a step that raised is not committed
+    const double t = cl.t + cl.dt;
+    const int64_t step = cl.step + 1;
+    c->t = t;
+    c->step = step;
     // stepper.py:203-209: the state check of every 64th commit
-    if (c->step % 64 == 0 && c->nf_now) c->halted = 6;
-    else if (c->t >= c->next_out - c->eps) c->halted = 2;
-    else if (c->max_steps >= 0 && c->step >= c->max_steps) c->halted = 3;
+    if (step % 64 == 0 && cl.nf_now) c->halted = 6;
+    else if (t >= cl.next_out - cl.eps) c->halted = 2;
+    else if (cl.max_steps >= 0 && step >= cl.max_steps) c->halted = 3;
 }
 
 __global__ void k_reduce_partials(const double* p, int64_t n, double* acc) {
@@ -2581,7 +2625,7 @@ int launch_brick(K kern, cudaStream_t st, const tl_body& b, int nrec) {
     int rc = smem_opt_in(kern, bytes);
     if (rc) return rc;
     const int64_t nb = (int64_t)b.nbrick[0] * b.nbrick[1] * b.nbrick[2];
-    kern<<<(unsigned)nb, T, bytes, st>>>(b, tab);
+    TL_TRY_CUDA(tl_launch(kern, dim3((unsigned)nb), dim3(T), bytes, st, b, tab));
     return TL_OK;
 }
 
@@ -2609,9 +2653,11 @@ int launch_a_one(cudaStream_t st, const tl_body& b) {
         const size_t bytes = tile_bytes<R, 1>(b.tile + b.hmax, b.slmax, b.ncls);
         int rc = smem_opt_in(kern, bytes);
         if (rc) return rc;
-        kern<<<b.tlist ? (unsigned)b.tcount : tl_blocks(b.n, b.tile), b.tile, bytes, st>>>(b);
+        TL_TRY_CUDA(tl_launch(kern, dim3(b.tlist ? (unsigned)b.tcount : tl_blocks(b.n, b.tile)),
+                              dim3(b.tile), bytes, st, b));
     } else {
-        k_pass_a<R, DIM, MODEL, FRAC, KIND, G, false><<<tl_blocks(b.n, kThreads), kThreads, 0, st>>>(b);
+        TL_TRY_CUDA(tl_launch(k_pass_a<R, DIM, MODEL, FRAC, KIND, G, false>,
+                              dim3(tl_blocks(b.n, kThreads)), dim3(kThreads), 0, st, b));
     }
     return tl_check_launch("k_pass_a");
 }
@@ -2656,7 +2702,8 @@ int launch_b_one(cudaStream_t st, const tl_body& b) {
                                  (size_t)(SP - 1) * 9 * b.tile * sizeof(R);
             int rc = smem_opt_in(kern, bytes);
             if (rc) return rc;
-            kern<<<b.tlist ? (unsigned)b.tcount : tl_blocks(b.n, b.tile), b.tile * SP, bytes, st>>>(b);
+            TL_TRY_CUDA(tl_launch(kern, dim3(b.tlist ? (unsigned)b.tcount : tl_blocks(b.n, b.tile)),
+                                  dim3(b.tile * SP), bytes, st, b));
             return tl_check_launch("k_pass_b");
         }
     }
@@ -2673,9 +2720,16 @@ int launch_b_one(cudaStream_t st, const tl_body& b) {
         const size_t bytes = tile_bytes<R, 3>(b.tile + b.hmax, b.slmax, b.ncls);
         int rc = smem_opt_in(kern, bytes);
         if (rc) return rc;
-        kern<<<b.tlist ? (unsigned)b.tcount : tl_blocks(b.n, b.tile), b.tile, bytes, st>>>(b);
+        TL_TRY_CUDA(tl_launch(kern, dim3(b.tlist ? (unsigned)b.tcount : tl_blocks(b.n, b.tile)),
+                              dim3(b.tile), bytes, st, b));
     } else {
-        k_pass_b<R, DIM, MODE, FRAC, KIND, G, false><<<tl_blocks(b.n, kThreads), kThreads, 0, st>>>(b);
+        const int lpp = max(b.lpp, 1);
+        if (lpp > 8 || (lpp & (lpp - 1))) {
+            tl_set_error("lpp %d: 1, 2, 4 or 8 lanes per particle", lpp);
+            return TL_ERR_ARG;
+        }
+        TL_TRY_CUDA(tl_launch(k_pass_b<R, DIM, MODE, FRAC, KIND, G, false>,
+                              dim3(tl_blocks(b.n * lpp, kThreads)), dim3(kThreads), 0, st, b));
     }
     return tl_check_launch("k_pass_b");
 }
@@ -2701,8 +2755,8 @@ int launch_b(cudaStream_t st, const tl_body& b, int mode) {
 template <typename R, int DIM>
 int launch_p(cudaStream_t st, const tl_body& b) {
     const unsigned g = tl_blocks(b.n, kThreads);
-    if (b.fracture) k_predict<R, DIM, true><<<g, kThreads, 0, st>>>(b);
-    else k_predict<R, DIM, false><<<g, kThreads, 0, st>>>(b);
+    if (b.fracture) TL_TRY_CUDA(tl_launch(k_predict<R, DIM, true>, dim3(g), dim3(kThreads), 0, st, b));
+    else TL_TRY_CUDA(tl_launch(k_predict<R, DIM, false>, dim3(g), dim3(kThreads), 0, st, b));
     return tl_check_launch("k_predict");
 }
 
@@ -2776,12 +2830,12 @@ extern "C" int tl_clock_begin(tl_stream_t st, tl_clock* clock, int nbody, const 
     DtInfos d;
     d.n = nbody;
     for (int k = 0; k < nbody; ++k) d.d[k] = info[k];
-    k_clock_begin<<<1, 1, 0, (cudaStream_t)st>>>(clock, d);
+    TL_TRY_CUDA(tl_launch(k_clock_begin, dim3(1), dim3(1), 0, (cudaStream_t)st, clock, d));
     return tl_check_launch("k_clock_begin");
 }
 
 extern "C" int tl_clock_commit(tl_stream_t st, tl_clock* clock) {
-    k_clock_commit<<<1, 1, 0, (cudaStream_t)st>>>(clock);
+    TL_TRY_CUDA(tl_launch(k_clock_commit, dim3(1), dim3(1), 0, (cudaStream_t)st, clock));
     return tl_check_launch("k_clock_commit");
 }
 

@@ -263,7 +263,37 @@ __device__ __forceinline__ long long warp_min_ll(long long v) {
     return v;
 }
 
+// Programmatic dependent launch: the step kernels (clock, passes, predictor)
+// are launched with programmatic stream serialisation (tl_launch), so a
+// kernel's CTAs are scheduled while its predecessor drains and its launch
+// latency overlaps the predecessor's tail.  Every such kernel first waits for
+// the predecessor grid to complete and flush its memory (griddepcontrol.wait,
+// a no-op for a normal launch), then lets its own dependents launch.
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 }  // namespace tl
+
+// launch with programmatic stream serialisation (TLSPH_PDL=0: plain launch);
+// only for kernels that call tl::pdl_enter() before touching global memory
+bool tl_pdl_enabled();
+template <typename... P, typename... A>
+cudaError_t tl_launch(void (*kern)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                      A&&... args) {
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = tl_pdl_enabled() ? 1 : 0;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<A&&>(args)...);
+}
 
 // error plumbing for the C ABI: every entry point returns 0 or a negative
 // code; the message is kept per thread and read with tl_last_error().

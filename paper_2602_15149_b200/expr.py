@@ -682,6 +682,56 @@ def nonskip_mask_after(ast, X0):
         return None
 
 
+def _literal(node):
+    """The value of a literal number (or its negation), else None."""
+    if node[0] == "num":
+        return float(node[1])
+    if node[0] == "un" and node[2][0] == "num":
+        return -float(node[2][1])
+    return None
+
+
+def late_constant(ast, X0):
+    """The one value ``ast`` takes wherever it is not skip for t > T
+    (nonskip_mask_after's T) when every branch reached there is the same
+    literal number -- ``if(x0<=0.0, 0.0, if(t<=0.0, v, skip))`` is 0.0 on
+    the clamped end after t = 0 -- else None.  The device then stores the
+    constant instead of running the expression: the VM would push the same
+    double, so the result is bit-identical."""
+    T = skip_static_after(ast)
+    if T is None:
+        return None
+    X0 = np.asarray(X0, dtype=np.float64)
+    env = {"x0": X0[:, 0], "y0": X0[:, 1], "z0": X0[:, 2]}
+    n = X0.shape[0]
+    vals = {}
+
+    def walk(node, sel):
+        if node[0] == "skip" or not sel.any():
+            return
+        if not _has_skip(node):
+            v = _literal(node)
+            if v is None:
+                raise _NotStatic
+            vals[np.float64(v).tobytes()] = v     # by bit pattern: 0.0 and -0.0 differ
+            return
+        tc = _t_compare(node[1])
+        if tc is not None:
+            late = tc[0] in (">", ">=")
+            walk(node[2] if late else node[3], sel)
+            return
+        c = np.broadcast_to(_veval(node[1], env), (n,)) != 0.0
+        walk(node[2], sel & c)
+        walk(node[3], sel & ~c)
+
+    root = ast.root if isinstance(ast, ExprAst) else ast
+    try:
+        walk(root, np.ones(n, dtype=bool))
+    except _NotStatic:
+        return None
+    return next(iter(vals.values())) if len(vals) == 1 else None
+
+
 # -- skip guards ---------------------------------------------------------------
 # ``if(z<1.0e-12, 0.0, if(t<=0.0, Vinit, skip))`` (a wall) depends on the
 # current z, so no particle set is fixed -- but after t = 0 it is skip wherever

@@ -261,13 +261,19 @@ class DeviceBody:
         # particles) keep whole-body expressions whole: there the kernel is
         # latency-bound and warps mixing BC and BC-free particles run both
         # paths (C1: 32 -> 37 us); TLSPH_STATIC_SKIP=1 forces, =0 disables.
+        # A targeted entry whose late-time value is one literal number on all
+        # its particles (expr.late_constant: C1's clamped end is 0.0 after
+        # t = 0) stores the constant and runs no expression at all, so small
+        # bodies convert those too (C1 pass B 31 -> 24 us).
         n_explicit = sum(1 for bc in bcs if bc.target is not None)
         env_ss = os.environ.get("TLSPH_STATIC_SKIP", "auto")
         static_ok = env_ss == "1" or (env_ss != "0" and X0.shape[0] > 148 * 256)
-        # device entries in file order: (bc, bit, tst, tend); a whole-body BC
-        # whose pattern is static after a time T becomes two time-disjoint
-        # entries, whole-body up to T and targeted after it (the windows are
-        # inclusive on the device, so the second starts at the next double)
+        const_ok = static_ok or env_ss == "auto"
+        # device entries in file order: (bc, bit, tst, tend, guard, late-time
+        # constants); a whole-body BC whose pattern is static after a time T
+        # becomes two time-disjoint entries, whole-body up to T and targeted
+        # after it (the windows are inclusive on the device, so the second
+        # starts at the next double)
         entries = []
         for k, bc in enumerate(bcs):
             if bc.kind == "force" and int(getattr(bc, "ftype", 0) or 0) not in (1, 2, 3):
@@ -278,33 +284,36 @@ class DeviceBody:
                 if bit >= 32:
                     raise CaseError(f"body {body.mk}: more than 32 targeted boundary conditions")
                 mask[np.asarray(bc.target, dtype=np.int64)] |= np.uint32(1 << bit)
-                entries.append((bc, bit, tst, tend, None))
+                entries.append((bc, bit, tst, tend, None, None))
                 bit += 1
                 continue
             # a split adds one device entry: room for it and every BC still to come
             room = _lib_max_bc() - (len(entries) + len(bcs) - k)
             got = (self._static_targets(bc, config, X0)
-                   if static_ok and bit + n_explicit < 31 and room >= 1 else None)
+                   if const_ok and bit + n_explicit < 31 and room >= 1 else None)
+            lconst = self._late_constants(bc, config, X0) if got is not None else None
+            if got is not None and not static_ok and lconst is None:
+                got = None                 # small body: only constant-folded entries pay
             if got is None:
                 entries.append((bc, -1, tst, tend, self._skip_guard(bc, config)
-                                if static_ok else None))
+                                if static_ok else None, None))
                 continue
             T, tgt = got
             if T >= tend:                  # static only after the BC has ended
-                entries.append((bc, -1, tst, tend, None))
+                entries.append((bc, -1, tst, tend, None, None))
                 continue
             if T >= tst:
-                entries.append((bc, -1, tst, T, None))
+                entries.append((bc, -1, tst, T, None, None))
                 tst = float(np.nextafter(T, np.inf))
             mask[tgt] |= np.uint32(1 << bit)
-            entries.append((bc, bit, tst, tend, None))
+            entries.append((bc, bit, tst, tend, None, lconst))
             bit += 1
         if len(entries) > _lib_max_bc():
             raise CaseError(f"body {body.mk}: more than {_lib_max_bc()} boundary conditions")
         arr = (_lib.tl_bc * max(len(entries), 1))()
         self.bc_whole = 0
         self.bcw_lo, self.bcw_hi = math.inf, -math.inf   # activity window of whole-body entries
-        for k, (bc, bbit, tst, tend, guard) in enumerate(entries):
+        for k, (bc, bbit, tst, tend, guard, lconst) in enumerate(entries):
             d = arr[k]
             d.kind = 0 if bc.kind == "vel" else 1
             d.ftype = int(getattr(bc, "ftype", 0) or 0)
@@ -319,6 +328,8 @@ class DeviceBody:
             for ax in range(3):
                 c = bc.const[ax]
                 e = bc.expr[ax]
+                if lconst is not None and lconst[ax] is not None:
+                    c, e = lconst[ax], None    # the expression's late-time literal
                 d.has_const[ax] = int(c is not None)
                 d.cval[ax] = float(c) if c is not None else 0.0
                 if c is None and e is not None:
@@ -374,6 +385,28 @@ class DeviceBody:
             guard = g[1:]
             T = max(T, g[0])
         return None if guard is None else (T,) + guard
+
+    @staticmethod
+    def _late_constants(bc, config, X0):
+        """Per-axis literal (None for an axis without an expression) when every
+        expression axis of the BC takes one literal number wherever it is not
+        skip after its threshold (expr.late_constant); else None."""
+        out = [None, None, None]
+        sel = None
+        for ax in range(3):
+            e = bc.expr[ax]
+            if bc.const[ax] is not None or e is None:
+                continue
+            ast = config.expressions.get(e)
+            v = ex.late_constant(ast, X0) if ast is not None else None
+            got = ex.nonskip_mask_after(ast, X0) if v is not None else None
+            # the entry targets the union of the axes' non-skip sets: a
+            # constant must not land where its own axis is skip
+            if got is None or (sel is not None and not np.array_equal(sel, got[1])):
+                return None
+            sel = got[1]
+            out[ax] = v
+        return tuple(out) if sel is not None else None
 
     @staticmethod
     def _static_targets(bc, config, X0):
@@ -445,6 +478,17 @@ class DeviceBody:
         lay = self.layout
         b.tile, b.hmax, b.slmax = int(lay.tile), int(lay.hmax), int(lay.slmax)
         b.bsplit = int(getattr(self, "bsplit", 1))
+        # L2-gather pass B on small FP32 bodies: up to 4 lanes per particle
+        # while the grid stays one wave (148 SMs x 1024 threads) -- each lane's
+        # chain of dependent gathers is 1/lpp as long (C1 pass B 24 -> 21 us;
+        # 8 lanes measured slower: the epilogue runs on one lane in eight).
+        # FP64, the parity mode, sums every row in CSR order (lpp 1).
+        # TLSPH_LPP overrides.
+        lpp = 1
+        if precision == "fp32":
+            while lpp < 4 and self.n * lpp * 2 <= 148 * 1024:
+                lpp *= 2
+        b.lpp = int(os.environ.get("TLSPH_LPP", str(lpp)))
         if lay.tile:
             b.hoff, b.halo, b.slots, b.hslot = (P(lay.hoff), P(lay.halo), P(lay.slots),
                                                 P(lay.hslot))
@@ -971,8 +1015,10 @@ class DeviceSimulation:
         else:
             self._exchange_plain(db, db.us, launch)
 
-    def _pass_b(self, db, mode):
-        _lib.check(self._lib.tl_reset_red(self._st(), _lib.ptr(db.red)), "tl_reset_red")
+    def _pass_b(self, db, mode, reset=True):
+        # device-clock steps: k_clock_begin cleared the maxima after reading them
+        if reset:
+            _lib.check(self._lib.tl_reset_red(self._st(), _lib.ptr(db.red)), "tl_reset_red")
 
         def launch():
             d = db.desc
@@ -999,13 +1045,15 @@ class DeviceSimulation:
                                                     db.nblocks, _lib.ptr(db.pw_acc)),
                        "tl_reduce_partials")
 
-    def _launch_step(self, mode_verlet):
+    def _launch_step(self, mode_verlet, reset=True):
+        """One step's launches; reset=False under the device clock (its
+        k_clock_begin clears the dt maxima)."""
         if mode_verlet:
             for db in self.dbodies:
                 self._pass_a(db)
             self._between_passes()
             for db in self.dbodies:
-                self._pass_b(db, 1)
+                self._pass_b(db, 1, reset)
         else:
             for db in self.dbodies:
                 _lib.check(self._lib.tl_predict(self._st(), C.byref(db.desc)), "tl_predict")
@@ -1013,7 +1061,7 @@ class DeviceSimulation:
                 self._pass_a(db)
             self._between_passes()
             for db in self.dbodies:
-                self._pass_b(db, 2)
+                self._pass_b(db, 2, reset)
 
     def _check_errors(self, clock=None):
         """Raise the reference's exceptions for events recorded on the device.
@@ -1179,7 +1227,7 @@ class DeviceSimulation:
         for _ in range(nsteps):
             _lib.check(self._lib.tl_clock_begin(self._st(), _lib.ptr(self.clock_dev),
                                                  len(self.dbodies), self._dt_arr), "clock")
-            self._launch_step(verlet)
+            self._launch_step(verlet, reset=False)
             _lib.check(self._lib.tl_clock_commit(self._st(), _lib.ptr(self.clock_dev)), "commit")
 
     def _launch_batch(self, nsteps, verlet):
@@ -1259,7 +1307,7 @@ class DeviceSimulation:
                 ev[1].record(self.stream)
                 ev[2].record(self.stream)
                 for db in self.dbodies:
-                    self._pass_b(db, 1 if verlet else 2)
+                    self._pass_b(db, 1 if verlet else 2, reset=False)
                 ev[3].record(self.stream)
                 pass_events.append(ev)
                 _lib.check(self._lib.tl_clock_commit(self._st(), _lib.ptr(self.clock_dev)),

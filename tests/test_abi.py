@@ -232,6 +232,23 @@ def test_skip_patterns_static_after_a_time():
     assert ex.nonskip_mask_after(ex.parse("if(z<1.0e-12,0.0,if(t<=0.0,1.0,skip))"), X) is None
 
 
+def test_late_constants():
+    """expr.late_constant: the literal an expression takes wherever it is not
+    skip after its threshold (beam2d: 0.0 on the clamped end after t = 0)."""
+    from paper_2602_15149_b200 import cases, expr as ex
+    b = cases.make_case("beam2d", dp_scale=8, build_adjacency=False)
+    X = np.array([[-1e-3, 0, 0], [0.0, 0, 0], [0.05, 0, 0.0]])
+    for k in (1, 2):
+        v = ex.late_constant(b.expressions[k], X)
+        assert v == 0.0 and np.signbit(v) == False  # noqa: E712
+    assert ex.late_constant(ex.parse("if(x0<=0,-2.5,skip)"), X) == -2.5
+    assert ex.late_constant(ex.parse("if(x0<=0,1.0,if(x0>0.04,2.0,skip))"), X) is None
+    assert ex.late_constant(ex.parse("if(x0<=0,1.0,if(x0>0.06,2.0,skip))"), X) == 1.0
+    assert ex.late_constant(ex.parse("if(x0<=0,t,skip)"), X) is None
+    assert ex.late_constant(ex.parse("if(x0<=0,0.0,if(x0>0.04,-0.0,skip))"), X) is None
+    assert ex.late_constant(ex.parse("if(z<1.0e-12,0.0,if(t<=0.0,1.0,skip))"), X) is None
+
+
 def test_skip_guards():
     """expr.skip_guard_after: the late-time skip pattern as one comparison."""
     from paper_2602_15149_b200 import expr as ex

@@ -276,6 +276,36 @@ def test_device_step1_fp32(tag):
         assert e1[k] <= 1e-5, (k, e1[k])
 
 
+@pytest.mark.parametrize("tag", ["kalthoff2d_p", "branch2d", "taylor3d"])
+def test_lanes_per_particle_pass_b(tag, monkeypatch):
+    """L2-gather pass B with 1, 2, 4 or 8 lanes per particle (small FP32
+    bodies): the same step-1 fields within FP32 rounding of the one-lane
+    sums, all within the FP32 tolerance of the reference; an lpp that does
+    not divide a warp is rejected."""
+    from paper_2602_15149_b200 import _lib
+    monkeypatch.setenv("TLSPH_TILE_B", "0")
+    monkeypatch.setenv("TLSPH_BRICK", "0")     # 3D: the L2-gather pass B, not bricks
+    G = golden(f"run_{tag}")
+    out = {}
+    for lpp in ("1", "2", "4", "8"):
+        monkeypatch.setenv("TLSPH_LPP", lpp)
+        cfg, sim = _sim(G, "fp32")
+        assert sim.dbodies[0].desc.lpp == int(lpp) and not sim.dbodies[0].tile_b
+        sim.initialize()
+        sim.step(G["dts"][0])
+        st = cfg.bodies[0].state
+        e = _errors(st, G, 1)
+        for k in ("F", "S", "a", "u", "v"):
+            assert e[k] <= 1e-5, (lpp, k, e[k])
+        out[lpp] = np.array(st.a)
+    for lpp in ("2", "4", "8"):
+        assert relerr(out[lpp], out["1"]) <= 1e-6, lpp
+    monkeypatch.setenv("TLSPH_LPP", "3")
+    cfg, sim = _sim(G, "fp32")
+    with pytest.raises(_lib.TLError, match="lanes per particle"):
+        sim.initialize()
+
+
 @pytest.mark.parametrize("tag,expect", [("kalthoff3d", True), ("kalthoff2d_p", True),
                                         ("branch2d", True), ("fourpoint3d", None),
                                         ("beam2d", None), ("plate3d", None)])
@@ -771,7 +801,7 @@ def test_static_skip_bcs_bit_identical(tag, monkeypatch):
     bit-identical to evaluating them on every particle."""
     G = golden(f"run_{tag}")
     out = {}
-    for mode in ("1", "0"):
+    for mode in ("1", "0", "auto"):
         monkeypatch.setenv("TLSPH_STATIC_SKIP", mode)
         cfg, sim = _sim(G, "fp64")
         db = sim.dbodies[0]
@@ -785,6 +815,8 @@ def test_static_skip_bcs_bit_identical(tag, monkeypatch):
         out[mode + "w"] = db.bc_whole
         out[mode + "n"] = db.nbc
         out[mode + "g"] = int(any(db._bc_arr[k].gvar >= 0 for k in range(db.nbc)))
+        out[mode + "c"] = sum(int(db._bc_arr[k].has_const[ax]) for k in range(db.nbc)
+                              for ax in range(3))
     if tag in ("column3d", "fourpoint3d"):
         assert out["1w"] == 0 and out["0w"] == 1      # the conversion happened
     if tag == "taylor3d":
@@ -794,8 +826,13 @@ def test_static_skip_bcs_bit_identical(tag, monkeypatch):
         # the initial-condition BC (static after t = 0) splits into a
         # whole-body entry for t <= 0 and a targeted one after it
         assert out["1n"] == out["0n"] + 1 and out["1w"] == 1
-    for a, b in zip(out["1"], out["0"]):
-        assert np.array_equal(a, b)
+        # ... whose late-time value on the clamped end is the literal 0.0 on
+        # every axis: stored as constants, no expression runs after t = 0;
+        # a small body converts it too (expr.late_constant)
+        assert out["1c"] == out["0c"] + 3 and out["autoc"] == out["1c"]
+    for m in ("1", "auto"):
+        for a, b in zip(out[m], out["0"]):
+            assert np.array_equal(a, b)
 
 
 def _accel(G, hourglass, u=None, v0=False):
