@@ -377,7 +377,7 @@ def main():
     fp64 = None
     if args.precision == "fp32" and not args.no_fp64:
         cfg64, _ = make_cfg()
-        r64 = measure(args, cfg64, "fp64", world, local, clocks_on=False)
+        r64 = measure(args, cfg64, "fp64", world, local, clocks_on=False, e2e=False)
         del r64["sim"]
         fp64 = {k: r64[k] for k in ("value", "ms_per_step", "roofline", "passes",
                                     "device_bytes_per_particle")}
@@ -419,7 +419,7 @@ def main():
         dist.destroy_process_group()
 
 
-def measure(args, cfg, precision, world, local, clocks_on):
+def measure(args, cfg, precision, world, local, clocks_on, e2e=True):
     """Device throughput of `args.steps` timed steps (inputs resident in HBM),
     max over ranks, plus per-pass kernel times for the roofline."""
     import torch
@@ -427,7 +427,7 @@ def measure(args, cfg, precision, world, local, clocks_on):
     from paper_2602_15149_b200.simulation import DeviceSimulation
     t0 = time.perf_counter()
     # host-layout FP64 mirrors (F, S, psi) only when the e2e outputs need them
-    sim = DeviceSimulation(cfg, precision=precision, mirrors=args.e2e_steps > 0)
+    sim = DeviceSimulation(cfg, precision=precision, mirrors=e2e and args.e2e_steps > 0)
     torch.cuda.synchronize()
     t_setup = time.perf_counter() - t0
     n = sum(db.n for db in sim.dbodies)

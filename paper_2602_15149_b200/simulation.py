@@ -182,13 +182,15 @@ class DeviceBody:
         self.S_out = f64(n, 3, 3) if mirrors else None
         self.psi_out = f64(n) if mirrors else None
         self.psip_out = f64(n) if mirrors else None
-        # pass B tiling: with few neighbours per particle (2D stencils) a tile's
-        # short compute cannot hide its staging latency, and the L2-gather
-        # pass B measured faster on B200 (C5: 1.75 vs 2.45 ms); pass A keeps
-        # its tiles either way.  TLSPH_TILE_B=0/1 overrides.
+        # pass B tiling: with few neighbours per particle (2D stencils) an FP32
+        # tile's short compute cannot hide its staging latency, and the
+        # L2-gather pass B measured faster on B200 (C5: 8.96 vs 11.9 ms); FP64
+        # 2D gathers twice the bytes per pair and the tiles win there (C5
+        # FP64: 12.5 vs 16.4 ms).  Pass A keeps its tiles either way.
+        # TLSPH_TILE_B=0/1 overrides.
         env_b = os.environ.get("TLSPH_TILE_B")
         self.tile_b = bool(lay.tile) and (int(env_b) != 0 if env_b is not None
-                                          else int(body.dim) == 3)
+                                          else (int(body.dim) == 3 or precision == "fp64"))
         # pass A tiling: radial 3D stencils (k ~ 165) on 160-particle tiles
         # (FP64) stage ~13 halo records per member and gather faster from L2
         # (measured in FP32: C2 0.60 vs 0.68 ms, C3 3.0 vs 3.55 ms); on the
