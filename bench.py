@@ -556,6 +556,8 @@ def e2e_run(sim, steps, n_total):
                 setattr(st, k, np.zeros(shape))
     sim.pull_host()                  # the host state a user of the API holds
     sim.pin_host_state()             # page-locked once, as a user's repeated runs would
+    on_output(sim)                   # output kernels loaded once (lazy module loading), untimed
+    rows.clear()
     torch.cuda.synchronize()
     t_out = float(sim.config.time_out)
     # a fresh run from t = 0 (the reference's run() puts its first output

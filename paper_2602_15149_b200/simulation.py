@@ -545,7 +545,10 @@ class DeviceBody:
         g, _ = self._gid_dev()
 
         def up(arr):
-            t = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64)).to(dev)
+            # asynchronous from page-locked arrays: the fields' copies run back
+            # to back on the stream (DeviceSimulation.push_state syncs once)
+            t = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64)).to(
+                dev, non_blocking=True)
             return t.index_select(0, g)
 
         self.us[:, :3].copy_(up(st.u))
@@ -561,6 +564,7 @@ class DeviceBody:
                                Cp[:, 1], Cp[:, 2], Cp[:, 5]])
             self.Cpd.copy_(cpd)
         self.refresh_dt_maxima()
+        torch.cuda.current_stream().synchronize()     # the host arrays are free again
 
     def pin_host(self):
         """Page-lock the host state arrays (cudaHostRegister) so push_state /
@@ -596,7 +600,10 @@ class DeviceBody:
                 return
             val = val[:n].double()
             if inv is not None and dst.flags.c_contiguous and dst.dtype == np.float64:
-                torch.from_numpy(dst).copy_(val.index_select(0, inv).reshape(dst.shape))
+                # asynchronous into page-locked arrays (DeviceSimulation.pull_host
+                # syncs once after every field is queued)
+                torch.from_numpy(dst).copy_(val.index_select(0, inv).reshape(dst.shape),
+                                            non_blocking=True)
             else:
                 dst[pm] = val.cpu().numpy().reshape((n,) + dst.shape[1:])
 
@@ -618,6 +625,7 @@ class DeviceBody:
             Cp = torch.stack([1.0 + c[0], c[3], c[4], c[3], 1.0 + c[1], c[5],
                               c[4], c[5], 1.0 + c[2]], dim=1).reshape(n, 3, 3)
             put(st.Cp, Cp)
+        torch.cuda.current_stream().synchronize()     # every queued copy has landed
 
     def refresh_dt_maxima(self):
         """max |v|^2 and max |a|^2 of the owned rows into ``red`` (what pass B
@@ -1274,8 +1282,25 @@ class DeviceSimulation:
             finally:
                 self.stream = saved
             self.stream.wait_stream(cap)
+            self._upload_graph(g)
             self._graphs[key] = g
         return g
+
+    def _upload_graph(self, g):
+        """Upload the instantiated graph to the device now (cuGraphUpload), so
+        its first replay inside run() does not pay for it (about 28 ms over
+        the six batch lengths of a C4 run).  Best effort: without cuda-python
+        the first replay uploads it, as before.  TLSPH_GRAPH_UPLOAD=0 skips."""
+        if os.environ.get("TLSPH_GRAPH_UPLOAD", "1") == "0":
+            return
+        try:
+            from cuda.bindings import driver as drv
+        except ImportError:
+            return
+        ex = int(g.raw_cuda_graph_exec())
+        (err,) = drv.cuGraphUpload(drv.CUgraphExec(ex), drv.CUstream(int(self.stream.cuda_stream)))
+        if int(err) != 0:
+            raise SimulationError(f"cuGraphUpload failed: {err}")
 
     def advance(self, nsteps, pass_events=None):
         """Launch exactly ``nsteps`` device-clock steps (adaptive dt, or the
