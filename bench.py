@@ -19,10 +19,11 @@ no flush is needed between steps.
 
 Extra keys: roofline (dominant kernel vs measured HBM copy bandwidth,
 SURVEY.md 8(d) algorithmic bytes), cpu_baseline (the CPU oracle port, a
-bounded sample of the same case on this host's cores), e2e (the public
-Simulation.run() API: device-clock batches of 64 steps, one host round trip
-per batch; per_step_api = pick_dt() + step() with a round trip per step),
-clocks, passes.
+bounded sample of the same case on this host's cores), e2e (the public API
+with host buffers: push_state() of the page-locked host state, run() with the
+case's output cadence and the OutputManager's energy / measure rows, then
+pull_host() of every field), fp64 (the same workload in the reference's
+precision), clocks, passes.
 
 --impl reference times the reference algorithm on the host CPU (the oracle
 port of solidsph's numba/numpy backends, oracle/; the reference itself is a
