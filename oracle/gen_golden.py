@@ -377,6 +377,46 @@ def gen_crack():
     save("crack_kalthoff2d", **out)
 
 
+def gen_crack3d():
+    """3D Kalthoff-Winkler (C4's body: the 2D case promoted to 3D with the
+    notch through the thickness, dp_scale=3, 3,267 particles) run to t = 2e-4 s
+    through the reference's run loop: the crack leaves the notch tip at about
+    75 deg in the x-z plane.  Same metric as gen_crack (bench.py:237-260)."""
+    import math
+    cfg = caseio.build_case(_kalthoff3d_raw(), dp_scale=3, mapfac=1)
+    out = dict(case_to_dict(cfg))
+    b = cfg.bodies[0]
+    out["adj0.indptr"] = b.adjacency.indptr
+    out["adj0.indices"] = b.adjacency.indices
+    sim = stepper.Simulation(cfg)
+    dts = []
+    orig_step = sim.step
+
+    def step(dt):
+        dts.append(dt)
+        orig_step(dt)
+
+    sim.step = step
+    sim.run(time_max=CRACK_T, time_out=CRACK_T)
+    st = b.state
+    quad = b.notches[0].points
+    tip = quad[int(np.argmax(quad[:, 0]))]
+    damaged = np.flatnonzero((st.s < 0.5) & (st.X[:, 0] > tip[0] + 2.0 * b.dp_body))
+    pts = st.X[damaged][:, [0, 2]]
+    _, _, vt = np.linalg.svd(pts - pts.mean(axis=0), full_matrices=False)
+    angle = math.degrees(math.atan2(abs(vt[0][1]), abs(vt[0][0])))
+    print(f"crack3d: {len(dts)} steps, t={sim.t:.6g}, {damaged.size} damaged ahead of the tip, "
+          f"kink {angle:.2f} deg")
+    for k in ("u", "v", "s", "sdot", "Hhist"):
+        out[f"end.{k}"] = getattr(st, k).copy()
+    out["end.t"] = np.array([sim.t])
+    out["end.energies"] = _outputs(sim)["b0.energies"]
+    out["dts"] = np.array(dts)
+    out["kink_angle_deg"] = np.array([angle])
+    out["damaged"] = damaged
+    save("crack_kalthoff3d", **out)
+
+
 def _touching(cfg):
     """flyer2d with the upper body displaced (u, a rigid shift) so its lowest
     layer sits 0.6 dp_contact above the plate: contact acts from step 1."""
@@ -627,7 +667,7 @@ def gen_targets():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["adjacency", "kernels", "runs", "expr", "targets", "crack",
+    which = sys.argv[1:] or ["adjacency", "kernels", "runs", "expr", "targets", "crack", "crack3d",
                              "long", "branch", "errors"]
     for w in which:
         globals()[f"gen_{w}"]()

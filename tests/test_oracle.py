@@ -182,6 +182,39 @@ def test_oracle_run_matches_reference(tag, oracle_mod):
     assert sim.t == pytest.approx(float(G[f"s{max(checks)}.t"][0]), rel=1e-14)
 
 
+def test_oracle_crack3d_matches_reference(oracle_mod):
+    """The oracle through the reference's run loop on the 3D Kalthoff crack
+    golden (1,094 adaptive steps, generated by the reference itself): the
+    same adjacency, dt sequence, crack and end state (u at 1e-12)."""
+    G = golden("crack_kalthoff3d")
+    cfg = run_case(G)
+    b = cfg.bodies[0]
+    b.adjacency = oracle_mod.build_adjacency(
+        b.state.X, b.state.V0, b.h, b.dim, int(cfg.kernel), nbsrange=b.nbsrange,
+        dp_body=b.dp_body, notches=b.notches, correction=b.kernel_correction)
+    assert np.array_equal(b.adjacency.indices, G["adj0.indices"])
+    sim = oracle_mod.OracleSimulation(cfg)
+    dts = []
+    orig = sim.step
+
+    def step(dt):
+        dts.append(dt)
+        orig(dt)
+
+    sim.step = step
+    t_end = float(G["end.t"][0])
+    sim.run(time_max=t_end, time_out=t_end)
+    assert len(dts) == len(G["dts"])
+    assert np.abs(np.array(dts) - G["dts"]).max() <= 1e-12 * G["dts"].max()
+    st = b.state
+    assert relerr(st.u, G["end.u"]) <= 1e-12
+    assert np.abs(st.s - G["end.s"]).max() <= 1e-10
+    quad = b.notches[0].points
+    tip = quad[int(np.argmax(quad[:, 0]))]
+    damaged = np.flatnonzero((st.s < 0.5) & (st.X[:, 0] > tip[0] + 2.0 * b.dp_body))
+    assert np.array_equal(damaged, G["damaged"])
+
+
 def test_oracle_expressions():
     G = golden("expr")
     srcs = bytes(G["sources"]).decode().split("\n")
