@@ -433,6 +433,10 @@ typedef struct {
     const int32_t* peer_slot;
     void* peer_us[2];
     void* peer_rb[2];
+    /* HOST copy of bcls (ncls entries): the tiled FP32 pass B takes (W, kappa)
+     * of each pair's class from the constant bank (a kernel parameter) instead
+     * of shared memory; NULL keeps the shared-memory table */
+    const void* bcls_host;
 } tl_body;
 
 #define TL_BRICK_MAX_CLASSES 256

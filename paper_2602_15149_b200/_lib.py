@@ -90,7 +90,7 @@ _BODY_FIELDS += [("brick", I32 * 3), ("nbrick", I32 * 3), ("cells", I32 * 3), ("
                  ("restrict_bit", I32),
                  ("pad_rb", I32), ("hg_coef", D), ("Fh", P),
                  ("bcw_lo", D), ("bcw_hi", D), ("peer_slot", P), ("peer_us", P * 2),
-                 ("peer_rb", P * 2)]
+                 ("peer_rb", P * 2), ("bcls_host", P)]
 
 
 class tl_body(C.Structure):

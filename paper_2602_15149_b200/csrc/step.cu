@@ -867,18 +867,29 @@ __device__ __forceinline__ void loop_a_geo_2d(uint32_t rec_sh, uint32_t cls_sh, 
 // packed FP32x2: the RecB layout pairs rows 0 and 1 of PL_j column by column,
 // so (s2_0, s2_1) takes three FFMA2 with a broadcast W component, and
 // (s1_0, s1_1), (s3_0, s3_1) and (v_i - v_j)_{0,1} are register pairs too.
-template <int DIM, bool STAGED, bool VISC>
+// The tiled passes' bond-class (W, kappa) entries as a kernel parameter:
+// read through the constant cache (a broadcast where a warp's lanes share the
+// class, which a lattice interior's CSR-ordered rows do) instead of a
+// shared-memory load on the record loads' pipe
+#define TL_TILE_MAX_CLASSES 64
+template <typename R>
+struct ClsTab {
+    V4<R> W[TL_TILE_MAX_CLASSES];
+};
+
+// CC: (W, kappa) from the ClsTab kernel parameter, else from shared memory
+template <int DIM, bool STAGED, bool VISC, bool CC = false>
 __device__ __forceinline__ void loop_b_geo(uint32_t rec_sh, uint32_t cls_sh, uint32_t sl_sh,
                                            const uint16_t* sl_g, int len, float vi0, float vi1,
                                            float vi2, float B2, float B1, float* s1, float* s2,
-                                           float* s3) {
+                                           float* s3, const ClsTab<float>* ct = nullptr) {
     if constexpr (DIM == 3) {
         float2 s1a = make_float2(0.f, 0.f), s2a = s1a, s3a = s1a;
         float s1b = 0.f, s2b = 0.f, s3b = 0.f;
         const float2 vi01 = make_float2(vi0, vi1);
         const float2 neg1 = make_float2(-1.f, -1.f);
         each_slot<STAGED>(sl_sh, sl_g, len, [&](uint32_t e) {
-            const float4 W = lds4<float>(cls_sh + geo_cls(e));
+            const float4 W = CC ? ct->W[e >> 10] : lds4<float>(cls_sh + geo_cls(e));
             const uint32_t ra = rec_sh + 48u * geo_slot(e);
             const float4 q0 = lds4<float>(ra), q1 = lds4<float>(ra + 16u), q2 = lds4<float>(ra + 32u);
             const float2 wxy = make_float2(W.x, W.y);
@@ -903,7 +914,7 @@ __device__ __forceinline__ void loop_b_geo(uint32_t rec_sh, uint32_t cls_sh, uin
         s3[0] = s3a.x; s3[1] = s3a.y; s3[2] = s3b;
     } else {
         each_slot<STAGED>(sl_sh, sl_g, len, [&](uint32_t e) {
-            const float4 W = lds4<float>(cls_sh + geo_cls(e));
+            const float4 W = CC ? ct->W[e >> 10] : lds4<float>(cls_sh + geo_cls(e));
             const uint32_t ra = rec_sh + 48u * geo_slot(e);
             const float4 q0 = lds4<float>(ra), q1 = lds4<float>(ra + 16u), q2 = lds4<float>(ra + 32u);
             s1[0] += W.x; s1[2] += W.z;
@@ -1792,7 +1803,7 @@ __host__ __device__ constexpr size_t split_off(int S, int slmax) {
 
 template <typename R, int DIM, int MODE, bool FRAC, int KIND, int G, bool TILED, int SPLIT = 1>
 __global__ void __launch_bounds__(b_threads<SPLIT>(), b_minb<R, SPLIT>())
-    k_pass_b(const __grid_constant__ tl_body b) {
+    k_pass_b(const __grid_constant__ tl_body b, const __grid_constant__ ClsTab<R> ct) {
     extern __shared__ __align__(16) unsigned char smem[];
     tl::pdl_enter();
     // a CTA of blockDim.x threads owns blockDim.x consecutive particles (TILED:
@@ -1864,11 +1875,13 @@ __global__ void __launch_bounds__(b_threads<SPLIT>(), b_minb<R, SPLIT>())
             float* f3 = reinterpret_cast<float*>(s3);
             const float v0 = float(vi0), v1 = float(vi1), v2f = float(vi2);
             const float fB2 = float(B2), fB1 = float(B1);
-#define TL_LOOP_G(ST, V) loop_b_geo<DIM, ST, V>(rec_sh, cls_sh, sl_sh, slg, lenr, v0, v1, v2f, fB2, fB1, f1, f2, f3)
-            if (b.slmax > 0) {
-                if (visc) TL_LOOP_G(true, true); else TL_LOOP_G(true, false);
+#define TL_LOOP_G(ST, V, CC) loop_b_geo<DIM, ST, V, CC>(rec_sh, cls_sh, sl_sh, slg, lenr, v0, v1, v2f, fB2, fB1, f1, f2, f3, &ct)
+            if (b.bcls_host && b.slmax > 0) {   // the common case: constant-bank classes
+                if (visc) TL_LOOP_G(true, true, true); else TL_LOOP_G(true, false, true);
+            } else if (b.slmax > 0) {
+                if (visc) TL_LOOP_G(true, true, false); else TL_LOOP_G(true, false, false);
             } else {
-                if (visc) TL_LOOP_G(false, true); else TL_LOOP_G(false, false);
+                if (visc) TL_LOOP_G(false, true, false); else TL_LOOP_G(false, false, false);
             }
 #undef TL_LOOP_G
           }
@@ -2686,6 +2699,17 @@ int launch_b_one(cudaStream_t st, const tl_body& b) {
             return rc ? rc : tl_check_launch("k_brick_b");
         }
     }
+    // the class table's (W, kappa) entries for the constant bank (tl_body.bcls_host)
+    ClsTab<R> ct{};
+    if (b.tile > 0 && b.ncls > 0 && b.bcls_host) {
+        if (b.ncls > TL_TILE_MAX_CLASSES) {
+            tl_set_error("%d bond classes: at most %d", b.ncls, TL_TILE_MAX_CLASSES);
+            return TL_ERR_ARG;
+        }
+        const R* hc = static_cast<const R*>(b.bcls_host);
+        for (int c = 0; c < b.ncls; ++c)
+            ct.W[c] = V4<R>{hc[8 * c], hc[8 * c + 1], hc[8 * c + 2], hc[8 * c + 3]};
+    }
     if constexpr (sizeof(R) == 4 && DIM == 3) {
         if (b.tile > 0 && b.bsplit == 4) {
             constexpr int SP = 4;
@@ -2703,7 +2727,7 @@ int launch_b_one(cudaStream_t st, const tl_body& b) {
             int rc = smem_opt_in(kern, bytes);
             if (rc) return rc;
             TL_TRY_CUDA(tl_launch(kern, dim3(b.tlist ? (unsigned)b.tcount : tl_blocks(b.n, b.tile)),
-                                  dim3(b.tile * SP), bytes, st, b));
+                                  dim3(b.tile * SP), bytes, st, b, ct));
             return tl_check_launch("k_pass_b");
         }
     }
@@ -2721,7 +2745,7 @@ int launch_b_one(cudaStream_t st, const tl_body& b) {
         int rc = smem_opt_in(kern, bytes);
         if (rc) return rc;
         TL_TRY_CUDA(tl_launch(kern, dim3(b.tlist ? (unsigned)b.tcount : tl_blocks(b.n, b.tile)),
-                              dim3(b.tile), bytes, st, b));
+                              dim3(b.tile), bytes, st, b, ct));
     } else {
         const int lpp = max(b.lpp, 1);
         if (lpp > 8 || (lpp & (lpp - 1))) {
@@ -2729,7 +2753,7 @@ int launch_b_one(cudaStream_t st, const tl_body& b) {
             return TL_ERR_ARG;
         }
         TL_TRY_CUDA(tl_launch(k_pass_b<R, DIM, MODE, FRAC, KIND, G, false>,
-                              dim3(tl_blocks(b.n * lpp, kThreads)), dim3(kThreads), 0, st, b));
+                              dim3(tl_blocks(b.n * lpp, kThreads)), dim3(kThreads), 0, st, b, ct));
     }
     return tl_check_launch("k_pass_b");
 }

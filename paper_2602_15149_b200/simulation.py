@@ -497,6 +497,11 @@ class DeviceBody:
             b.toff, b.tpos_a, b.tpos_b = P(lay.toff), P(self.tpos_a), P(self.tpos_b)
         if self.bcls is not None:
             b.ncls, b.bcls = int(self.bcls.shape[0]), P(self.bcls)
+            # pass B reads (W, kappa) from the constant bank (TLSPH_CLS_CONST=0:
+            # from the staged shared-memory table)
+            if os.environ.get("TLSPH_CLS_CONST", "1") != "0":
+                self._bcls_host = np.ascontiguousarray(self.bcls.cpu().numpy())
+                b.bcls_host = self._bcls_host.ctypes.data
         if self.brick is not None:
             self.brick.fill(b)
         b.perm = P(self.perm_global)
