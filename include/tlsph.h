@@ -433,9 +433,10 @@ typedef struct {
     const int32_t* peer_slot;
     void* peer_us[2];
     void* peer_rb[2];
-    /* HOST copy of bcls (ncls entries): the tiled FP32 pass B takes (W, kappa)
-     * of each pair's class from the constant bank (a kernel parameter) instead
-     * of shared memory; NULL keeps the shared-memory table */
+    /* HOST copy of bcls (ncls entries): the tiled passes take each pair's class
+     * geometry (pass B: W, kappa; FP32 2D pass A: W, U) from the constant bank
+     * (a kernel parameter) instead of shared memory; NULL keeps the
+     * shared-memory table */
     const void* bcls_host;
 } tl_body;
 

@@ -802,18 +802,34 @@ __device__ __forceinline__ uint32_t geo_slot(uint32_t e) { return e & 1023u; }
 __device__ __forceinline__ uint32_t geo_cls(uint32_t e) { return (e >> 10) * 32u; }
 __device__ __forceinline__ uint32_t geo_cls64(uint32_t e) { return (e >> 10) * 64u; }
 
+// The tiled passes' bond-class entries as kernel parameters: read through
+// the constant cache (a broadcast where a warp's lanes share the class, which
+// a lattice interior's CSR-ordered rows do) instead of shared-memory loads on
+// the record loads' pipe.  Pass B needs (W, kappa), pass A also U.
+#define TL_TILE_MAX_CLASSES 64
+template <typename R>
+struct ClsTab {
+    V4<R> W[TL_TILE_MAX_CLASSES];
+};
+template <typename R>
+struct ClsTabA {
+    V4<R> W[TL_TILE_MAX_CLASSES];
+    V4<R> U[TL_TILE_MAX_CLASSES];
+};
+
 // pass A, FP32 3D, packed FP32x2: D += (u_j - u_i) (x) W ; M += (s_i - s_j) W (x) U
-template <bool FRAC, bool STAGED>
+template <bool FRAC, bool STAGED, bool CC = false>
 __device__ __forceinline__ void loop_a_geo_f2(uint32_t rec_sh, uint32_t cls_sh, uint32_t sl_sh,
                                               const uint16_t* sl_g, int len, const float4& ui,
-                                              float* D, float* M) {
+                                              float* D, float* M,
+                                              const ClsTabA<float>* ct = nullptr) {
     float2 D01 = make_float2(0.f, 0.f), D34 = D01, D67 = D01, D25 = D01, M01 = D01;
     float D8 = 0.f, M2 = 0.f, M3 = 0.f, M4 = 0.f, M5 = 0.f;
     const float2 nui = make_float2(-ui.x, -ui.y);
     const float nuz = -ui.z;
     each_slot<STAGED>(sl_sh, sl_g, len, [&](uint32_t e) {
         const uint32_t c = cls_sh + geo_cls(e);
-        const float4 W = lds4<float>(c);
+        const float4 W = CC ? ct->W[e >> 10] : lds4<float>(c);
         const float4 uj = lds4<float>(rec_sh + 16u * geo_slot(e));
         const float2 wxy = make_float2(W.x, W.y);
         const float2 du01 = __fadd2_rn(make_float2(uj.x, uj.y), nui);
@@ -824,7 +840,7 @@ __device__ __forceinline__ void loop_a_geo_f2(uint32_t rec_sh, uint32_t cls_sh, 
         D25 = __ffma2_rn(du01, make_float2(W.z, W.z), D25);
         D8 = fmaf(du2, W.z, D8);
         if (FRAC) {
-            const float4 U = lds4<float>(c + 16u);
+            const float4 U = CC ? ct->U[e >> 10] : lds4<float>(c + 16u);
             const float ds = ui.w - uj.w;
             const float2 cw = __fmul2_rn(make_float2(ds, ds), wxy);
             const float cz = ds * W.z;
@@ -842,19 +858,20 @@ __device__ __forceinline__ void loop_a_geo_f2(uint32_t rec_sh, uint32_t cls_sh, 
 }
 
 // pass A, FP32 2D (x-z plane): the scalar form of the same terms
-template <bool FRAC, bool STAGED>
+template <bool FRAC, bool STAGED, bool CC = false>
 __device__ __forceinline__ void loop_a_geo_2d(uint32_t rec_sh, uint32_t cls_sh, uint32_t sl_sh,
                                               const uint16_t* sl_g, int len, const float4& ui,
-                                              float* D, float* M) {
+                                              float* D, float* M,
+                                              const ClsTabA<float>* ct = nullptr) {
     each_slot<STAGED>(sl_sh, sl_g, len, [&](uint32_t e) {
         const uint32_t c = cls_sh + geo_cls(e);
-        const float4 W = lds4<float>(c);
+        const float4 W = CC ? ct->W[e >> 10] : lds4<float>(c);
         const float4 uj = lds4<float>(rec_sh + 16u * geo_slot(e));
         const float du0 = uj.x - ui.x, du2 = uj.z - ui.z;
         D[0] = fmaf(du0, W.x, D[0]); D[2] = fmaf(du0, W.z, D[2]);
         D[6] = fmaf(du2, W.x, D[6]); D[8] = fmaf(du2, W.z, D[8]);
         if (FRAC) {
-            const float4 U = lds4<float>(c + 16u);
+            const float4 U = CC ? ct->U[e >> 10] : lds4<float>(c + 16u);
             const float ds = ui.w - uj.w;
             const float cx = ds * W.x, cz = ds * W.z;
             M[0] = fmaf(cx, U.x, M[0]); M[2] = fmaf(cz, U.z, M[2]); M[4] = fmaf(cx, U.z, M[4]);
@@ -867,16 +884,6 @@ __device__ __forceinline__ void loop_a_geo_2d(uint32_t rec_sh, uint32_t cls_sh, 
 // packed FP32x2: the RecB layout pairs rows 0 and 1 of PL_j column by column,
 // so (s2_0, s2_1) takes three FFMA2 with a broadcast W component, and
 // (s1_0, s1_1), (s3_0, s3_1) and (v_i - v_j)_{0,1} are register pairs too.
-// The tiled passes' bond-class (W, kappa) entries as a kernel parameter:
-// read through the constant cache (a broadcast where a warp's lanes share the
-// class, which a lattice interior's CSR-ordered rows do) instead of a
-// shared-memory load on the record loads' pipe
-#define TL_TILE_MAX_CLASSES 64
-template <typename R>
-struct ClsTab {
-    V4<R> W[TL_TILE_MAX_CLASSES];
-};
-
 // CC: (W, kappa) from the ClsTab kernel parameter, else from shared memory
 template <int DIM, bool STAGED, bool VISC, bool CC = false>
 __device__ __forceinline__ void loop_b_geo(uint32_t rec_sh, uint32_t cls_sh, uint32_t sl_sh,
@@ -961,13 +968,14 @@ __device__ __forceinline__ void loop_a_geo64(uint32_t rec_sh, uint32_t cls_sh, u
     });
 }
 
-template <int DIM, bool STAGED, bool VISC>
+template <int DIM, bool STAGED, bool VISC, bool CC = false>
 __device__ __forceinline__ void loop_b_geo64(uint32_t rec_sh, uint32_t cls_sh, uint32_t sl_sh,
                                              const uint16_t* sl_g, int len, double vi0, double vi1,
                                              double vi2, double B2, double B1, double* s1,
-                                             double* s2, double* s3) {
+                                             double* s2, double* s3,
+                                             const ClsTab<double>* ct = nullptr) {
     each_slot<STAGED>(sl_sh, sl_g, len, [&](uint32_t e) {
-        const double4 W = lds4<double>(cls_sh + geo_cls64(e));
+        const double4 W = CC ? ct->W[e >> 10] : lds4<double>(cls_sh + geo_cls64(e));
         const uint32_t ra = rec_sh + 96u * geo_slot(e);
         const double4 q0 = lds4<double>(ra), q1 = lds4<double>(ra + 32u), q2 = lds4<double>(ra + 64u);
         s1[0] += W.x; s1[2] += W.z;
@@ -1297,7 +1305,8 @@ __device__ __forceinline__ double a_finish(const tl_body& b, int64_t i, R* D, R*
 }
 
 template <typename R, int DIM, int MODEL, bool FRAC, int KIND, int G, bool TILED>
-__global__ void __launch_bounds__(kThreads, TL_MINB_A(R, TILED)) k_pass_a(const tl_body b) {
+__global__ void __launch_bounds__(kThreads, TL_MINB_A(R, TILED))
+    k_pass_a(const __grid_constant__ tl_body b, const __grid_constant__ ClsTabA<R> ct) {
     extern __shared__ __align__(16) unsigned char smem[];
     tl::pdl_enter();
     // a CTA of blockDim.x threads owns blockDim.x consecutive particles (TILED:
@@ -1352,10 +1361,14 @@ __global__ void __launch_bounds__(kThreads, TL_MINB_A(R, TILED)) k_pass_a(const 
             float* Df = reinterpret_cast<float*>(D);
             float* Mf = reinterpret_cast<float*>(M);
             if constexpr (DIM == 3) {
+                // 3D keeps the shared-memory table: the constant-bank one measured
+                // flat here and the extra loop variant cost pass A 0.7 % (C4)
                 if (b.slmax > 0) loop_a_geo_f2<FRAC, true>(rec_sh, cls_sh, sl_sh, slg, lenr, uif, Df, Mf);
                 else loop_a_geo_f2<FRAC, false>(rec_sh, cls_sh, sl_sh, slg, lenr, uif, Df, Mf);
             } else {
-                if (b.slmax > 0) loop_a_geo_2d<FRAC, true>(rec_sh, cls_sh, sl_sh, slg, lenr, uif, Df, Mf);
+                if (b.bcls_host && b.slmax > 0)
+                    loop_a_geo_2d<FRAC, true, true>(rec_sh, cls_sh, sl_sh, slg, lenr, uif, Df, Mf, &ct);
+                else if (b.slmax > 0) loop_a_geo_2d<FRAC, true>(rec_sh, cls_sh, sl_sh, slg, lenr, uif, Df, Mf);
                 else loop_a_geo_2d<FRAC, false>(rec_sh, cls_sh, sl_sh, slg, lenr, uif, Df, Mf);
             }
           }
@@ -1862,11 +1875,13 @@ __global__ void __launch_bounds__(b_threads<SPLIT>(), b_minb<R, SPLIT>())
             double* d2 = reinterpret_cast<double*>(s2);
             double* d3 = reinterpret_cast<double*>(s3);
             const double B2d = double(B2), B1d = double(B1);
-#define TL_LOOP_G64(ST, V) loop_b_geo64<DIM, ST, V>(rec_sh, cls_sh, sl_sh, slg, lenr, double(vi0), double(vi1), double(vi2), B2d, B1d, d1, d2, d3)
-            if (b.slmax > 0) {
-                if (visc) TL_LOOP_G64(true, true); else TL_LOOP_G64(true, false);
+#define TL_LOOP_G64(ST, V, CC) loop_b_geo64<DIM, ST, V, CC>(rec_sh, cls_sh, sl_sh, slg, lenr, double(vi0), double(vi1), double(vi2), B2d, B1d, d1, d2, d3, reinterpret_cast<const ClsTab<double>*>(&ct))
+            if (b.bcls_host && b.slmax > 0) {
+                if (visc) TL_LOOP_G64(true, true, true); else TL_LOOP_G64(true, false, true);
+            } else if (b.slmax > 0) {
+                if (visc) TL_LOOP_G64(true, true, false); else TL_LOOP_G64(true, false, false);
             } else {
-                if (visc) TL_LOOP_G64(false, true); else TL_LOOP_G64(false, false);
+                if (visc) TL_LOOP_G64(false, true, false); else TL_LOOP_G64(false, false, false);
             }
 #undef TL_LOOP_G64
           } else if constexpr (SPLIT == 1) {
@@ -2661,16 +2676,28 @@ int launch_a_one(cudaStream_t st, const tl_body& b) {
         tl_set_error("tile %d: pass A needs a multiple of 32, at most %d", b.tile, kThreads);
         return TL_ERR_ARG;
     }
+    ClsTabA<R> ct{};   // the class table for the constant bank (tl_body.bcls_host)
+    if (b.tile > 0 && b.ncls > 0 && b.bcls_host) {
+        if (b.ncls > TL_TILE_MAX_CLASSES) {
+            tl_set_error("%d bond classes: at most %d", b.ncls, TL_TILE_MAX_CLASSES);
+            return TL_ERR_ARG;
+        }
+        const R* hc = static_cast<const R*>(b.bcls_host);
+        for (int c = 0; c < b.ncls; ++c) {
+            ct.W[c] = V4<R>{hc[8 * c], hc[8 * c + 1], hc[8 * c + 2], hc[8 * c + 3]};
+            ct.U[c] = V4<R>{hc[8 * c + 4], hc[8 * c + 5], hc[8 * c + 6], hc[8 * c + 7]};
+        }
+    }
     if (b.tile > 0) {
         auto kern = k_pass_a<R, DIM, MODEL, FRAC, KIND, G, true>;
         const size_t bytes = tile_bytes<R, 1>(b.tile + b.hmax, b.slmax, b.ncls);
         int rc = smem_opt_in(kern, bytes);
         if (rc) return rc;
         TL_TRY_CUDA(tl_launch(kern, dim3(b.tlist ? (unsigned)b.tcount : tl_blocks(b.n, b.tile)),
-                              dim3(b.tile), bytes, st, b));
+                              dim3(b.tile), bytes, st, b, ct));
     } else {
         TL_TRY_CUDA(tl_launch(k_pass_a<R, DIM, MODEL, FRAC, KIND, G, false>,
-                              dim3(tl_blocks(b.n, kThreads)), dim3(kThreads), 0, st, b));
+                              dim3(tl_blocks(b.n, kThreads)), dim3(kThreads), 0, st, b, ct));
     }
     return tl_check_launch("k_pass_a");
 }

@@ -497,9 +497,13 @@ class DeviceBody:
             b.toff, b.tpos_a, b.tpos_b = P(lay.toff), P(self.tpos_a), P(self.tpos_b)
         if self.bcls is not None:
             b.ncls, b.bcls = int(self.bcls.shape[0]), P(self.bcls)
-            # pass B reads (W, kappa) from the constant bank (TLSPH_CLS_CONST=0:
-            # from the staged shared-memory table)
-            if os.environ.get("TLSPH_CLS_CONST", "1") != "0":
+            # the tiled passes read the class geometry from the constant bank
+            # (tl_body.bcls_host): C4 FP32 pass B 1.30 -> 1.26 ms, C5 FP32 pass A
+            # 5.65 -> 5.58 ms, C5 FP64 pass B flat; FP64 3D keeps the shared-
+            # memory table (C4 FP64 pass B 3.34 vs 3.43 ms).  TLSPH_CLS_CONST=0
+            # keeps it everywhere.
+            if (os.environ.get("TLSPH_CLS_CONST", "1") != "0"
+                    and (precision == "fp32" or int(body.dim) == 2)):
                 self._bcls_host = np.ascontiguousarray(self.bcls.cpu().numpy())
                 b.bcls_host = self._bcls_host.ctypes.data
         if self.brick is not None:
