@@ -1926,6 +1926,47 @@ if (visc) TL_LOOP_B(U, ST, true); else TL_LOOP_B(U, ST, false)
             }
 #undef TL_LOOP_B2
 #undef TL_LOOP_B
+        } else if (sizeof(R) == 4 && DIM == 2 && G == 4 && b.ncls > 0 && b.bcls_host && b.slots) {
+            // L2 gather on a 2D lattice body with bond classes: the pair's class
+            // is in the tiled layout's slot entry (same sliced shape, 2 bytes),
+            // its (W, kappa) in the constant bank -- no position gathers and no
+            // per-pair r or kernel shape.  The pair terms are loop_b_geo's.
+            const int32_t* sidx = b.sidx + base + lane;
+            const uint16_t* slg = b.slots + base + lane * G;
+            const ClsTab<float>* ctf = reinterpret_cast<const ClsTab<float>*>(&ct);
+            const float v0 = float(vi0), v2 = float(vi2), fB1 = float(B1), fB2 = float(B2);
+            float a1x = 0.f, a1z = 0.f, a2x = 0.f, a2z = 0.f, a3x = 0.f, a3z = 0.f;
+            for (int k = sub * G; k < len; k += G * lpp) {
+                int32_t jj[G];
+#pragma unroll
+                for (int q = 0; q < G; ++q) jj[q] = __ldg(sidx + 32 * (k + q));
+                const uint2 sg = __ldg(reinterpret_cast<const uint2*>(slg + 32 * k));
+                const uint32_t e[G] = {sg.x & 0xffffu, sg.x >> 16, sg.y & 0xffffu, sg.y >> 16};
+                float4 q0[G], q1[G], q2[G];
+#pragma unroll
+                for (int q = 0; q < G; ++q) {
+                    const float* rj = reinterpret_cast<const float*>(rbp) + 12 * (int64_t)jj[q];
+                    q0[q] = tl::ldg4(rj);
+                    q1[q] = tl::ldg4(rj + 4);
+                    q2[q] = tl::ldg4(rj + 8);
+                }
+#pragma unroll
+                for (int q = 0; q < G; ++q) {
+                    const float4 W = ctf->W[e[q] >> 10];
+                    a1x += W.x; a1z += W.z;
+                    a2x = fmaf(q1[q].x, W.z, fmaf(q0[q].x, W.x, a2x));
+                    a2z = fmaf(q2[q].w, W.z, fmaf(q1[q].z, W.x, a2z));
+                    if (visc) {
+                        const float dvw = (v0 - q2[q].x) * W.x + (v2 - q2[q].z) * W.z;
+                        const float g = dvw * W.w;
+                        const float pw = (fB2 * g - fB1) * g;
+                        a3x = fmaf(pw, W.x, a3x); a3z = fmaf(pw, W.z, a3z);
+                    }
+                }
+            }
+            s1[0] = R(a1x); s1[2] = R(a1z);
+            s2[0] = R(a2x); s2[2] = R(a2z);
+            s3[0] = R(a3x); s3[2] = R(a3z);
         } else {
             const double xi = b.Xs[i], yi = b.Xs[N + i], zi = b.Xs[2 * N + i];
             const int32_t* sidx = b.sidx + base + lane;
@@ -1956,15 +1997,15 @@ if (visc) TL_LOOP_B(U, ST, true); else TL_LOOP_B(U, ST, false)
                                          R(zi - zj[q]), q0[q], q1[q], q2[q], mj[q], uni, vi0, vi1,
                                          vi2, visc, inv_h, eps_h2, B2, B1, s1, s2, s3);
             }
-            if (lpp > 1) {   // a particle's lanes are live together (lpp divides 32)
-                const unsigned am = __activemask();
-                for (int o = 1; o < lpp; o <<= 1) {
+        }
+        if (lpp > 1) {   // a particle's lanes are live together (lpp divides 32)
+            const unsigned am = __activemask();
+            for (int o = 1; o < lpp; o <<= 1) {
 #pragma unroll
-                    for (int q = 0; q < 3; ++q) {
-                        s1[q] += __shfl_xor_sync(am, s1[q], o);
-                        s2[q] += __shfl_xor_sync(am, s2[q], o);
-                        s3[q] += __shfl_xor_sync(am, s3[q], o);
-                    }
+                for (int q = 0; q < 3; ++q) {
+                    s1[q] += __shfl_xor_sync(am, s1[q], o);
+                    s2[q] += __shfl_xor_sync(am, s2[q], o);
+                    s3[q] += __shfl_xor_sync(am, s3[q], o);
                 }
             }
         }
@@ -2727,8 +2768,8 @@ int launch_b_one(cudaStream_t st, const tl_body& b) {
         }
     }
     // the class table's (W, kappa) entries for the constant bank (tl_body.bcls_host)
-    ClsTab<R> ct{};
-    if (b.tile > 0 && b.ncls > 0 && b.bcls_host) {
+    ClsTab<R> ct{};   // also for the L2 gather (tile 0), whose 2D class mode reads it
+    if (b.ncls > 0 && b.bcls_host) {
         if (b.ncls > TL_TILE_MAX_CLASSES) {
             tl_set_error("%d bond classes: at most %d", b.ncls, TL_TILE_MAX_CLASSES);
             return TL_ERR_ARG;

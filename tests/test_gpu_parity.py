@@ -306,6 +306,34 @@ def test_lanes_per_particle_pass_b(tag, monkeypatch):
         sim.initialize()
 
 
+@pytest.mark.parametrize("tag", ["kalthoff2d_p", "branch2d"])
+def test_class_mode_l2_gather_pass_b(tag, monkeypatch):
+    """2D FP32 lattice bodies: the L2-gather pass B takes each pair's class
+    from the slot entry and (W, kappa) from the constant bank (no position
+    gathers).  Step-1 fields within the FP32 tolerance of the reference and
+    within FP32 rounding of the position path."""
+    monkeypatch.setenv("TLSPH_TILE_B", "0")
+    G = golden(f"run_{tag}")
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("TLSPH_CLS_CONST", mode)
+        cfg, sim = _sim(G, "fp32")
+        db = sim.dbodies[0]
+        assert db.bcls is not None and not db.tile_b
+        assert bool(db.desc.bcls_host) == (mode == "1")
+        sim.initialize()
+        sim.step(G["dts"][0])
+        st = cfg.bodies[0].state
+        e = _errors(st, G, 1)
+        for k in ("F", "S", "a", "u", "v"):
+            assert e[k] <= 1e-5, (mode, k, e[k])
+        out[mode] = np.array(st.a)
+    assert relerr(out["1"], out["0"]) <= 2e-6
+    # (beam2d is not in the FP32 step-1 set: its golden starts unstressed, so a
+    # is a cancellation residue -- 1.07e-5 relative on every path, with or
+    # without classes or lanes)
+
+
 @pytest.mark.parametrize("tag,expect", [("kalthoff3d", True), ("kalthoff2d_p", True),
                                         ("branch2d", True), ("fourpoint3d", None),
                                         ("beam2d", None), ("plate3d", None)])
