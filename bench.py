@@ -504,7 +504,8 @@ def measure(args, cfg, precision, world, local, clocks_on, e2e=True):
                 "step_frac": (ba + bb) * value / max(world, 1) / 1e9 / peak}
     passes = {"pass_a_ms": ma, "pass_b_ms": mb, "bytes_a": ba, "bytes_b": bb,
               "frac_a": ba * n / (ma / 1e3) / 1e9 / peak,
-              "frac_b": bb * n / (mb / 1e3) / 1e9 / peak}
+              "frac_b": bb * n / (mb / 1e3) / 1e9 / peak,
+              "samples_ms": {"a": [round(x, 4) for x in ta], "b": [round(x, 4) for x in tb]}}
     # our kernels per timed step: clock begin + commit, and per body pass A and
     # pass B (+ the plastic-work reduction for J2 bodies); the dt-maxima reset
     # is a memset

@@ -1843,6 +1843,16 @@ __global__ void __launch_bounds__(b_threads<SPLIT>(), b_minb<R, SPLIT>())
         tl_ = tile_layout<R, 3>(smem, b.tile + b.hmax, b.slmax, SPLIT == 1 ? b.ncls : 0);
         stage_tile<R, 3>(b, tl_, tb, b.tpos_b, rbp, &bar);
     }
+    // 2D class-mode L2 gather: the class table's (W, kappa) entries in shared
+    // memory (the per-lane class lookups of a constant-bank table measured
+    // bimodal from launch to launch, 7.5-12.5 ms on C5)
+    __shared__ V4<R> s_cls[(!TILED && DIM == 2) ? TL_TILE_MAX_CLASSES : 1];
+    if constexpr (!TILED && DIM == 2) {
+        if (b.ncls > 0 && b.bcls_host) {
+            for (int c = threadIdx.x; c < b.ncls; c += blockDim.x) s_cls[c] = ct.W[c];
+            __syncthreads();
+        }
+    }
     const int ms = SPLIT > 1 ? (int)threadIdx.x % T : (int)threadIdx.x / lpp;   // member slot
     const int part = SPLIT > 1 ? (int)threadIdx.x / T : 0;
     const bool live = p0 + ms < b.n;
@@ -1926,47 +1936,47 @@ if (visc) TL_LOOP_B(U, ST, true); else TL_LOOP_B(U, ST, false)
             }
 #undef TL_LOOP_B2
 #undef TL_LOOP_B
-        } else if (sizeof(R) == 4 && DIM == 2 && G == 4 && b.ncls > 0 && b.bcls_host && b.slots) {
+        } else if (DIM == 2 && G == 4 && b.ncls > 0 && b.bcls_host && b.slots) {
             // L2 gather on a 2D lattice body with bond classes: the pair's class
             // is in the tiled layout's slot entry (same sliced shape, 2 bytes),
             // its (W, kappa) in the constant bank -- no position gathers and no
-            // per-pair r or kernel shape.  The pair terms are loop_b_geo's.
+            // per-pair r or kernel shape.  The pair terms are loop_b_geo's
+            // (loop_b_geo64's in FP64).
             const int32_t* sidx = b.sidx + base + lane;
             const uint16_t* slg = b.slots + base + lane * G;
-            const ClsTab<float>* ctf = reinterpret_cast<const ClsTab<float>*>(&ct);
-            const float v0 = float(vi0), v2 = float(vi2), fB1 = float(B1), fB2 = float(B2);
-            float a1x = 0.f, a1z = 0.f, a2x = 0.f, a2z = 0.f, a3x = 0.f, a3z = 0.f;
+            const R v0 = vi0, v2 = vi2;
+            R a1x = R(0), a1z = R(0), a2x = R(0), a2z = R(0), a3x = R(0), a3z = R(0);
             for (int k = sub * G; k < len; k += G * lpp) {
                 int32_t jj[G];
 #pragma unroll
                 for (int q = 0; q < G; ++q) jj[q] = __ldg(sidx + 32 * (k + q));
                 const uint2 sg = __ldg(reinterpret_cast<const uint2*>(slg + 32 * k));
                 const uint32_t e[G] = {sg.x & 0xffffu, sg.x >> 16, sg.y & 0xffffu, sg.y >> 16};
-                float4 q0[G], q1[G], q2[G];
+                V4<R> q0[G], q1[G], q2[G];
 #pragma unroll
                 for (int q = 0; q < G; ++q) {
-                    const float* rj = reinterpret_cast<const float*>(rbp) + 12 * (int64_t)jj[q];
+                    const R* rj = rbp + 12 * (int64_t)jj[q];
                     q0[q] = tl::ldg4(rj);
                     q1[q] = tl::ldg4(rj + 4);
                     q2[q] = tl::ldg4(rj + 8);
                 }
 #pragma unroll
                 for (int q = 0; q < G; ++q) {
-                    const float4 W = ctf->W[e[q] >> 10];
+                    const V4<R> W = s_cls[e[q] >> 10];
                     a1x += W.x; a1z += W.z;
-                    a2x = fmaf(q1[q].x, W.z, fmaf(q0[q].x, W.x, a2x));
-                    a2z = fmaf(q2[q].w, W.z, fmaf(q1[q].z, W.x, a2z));
+                    a2x = fma(q1[q].x, W.z, fma(q0[q].x, W.x, a2x));
+                    a2z = fma(q2[q].w, W.z, fma(q1[q].z, W.x, a2z));
                     if (visc) {
-                        const float dvw = (v0 - q2[q].x) * W.x + (v2 - q2[q].z) * W.z;
-                        const float g = dvw * W.w;
-                        const float pw = (fB2 * g - fB1) * g;
-                        a3x = fmaf(pw, W.x, a3x); a3z = fmaf(pw, W.z, a3z);
+                        const R dvw = (v0 - q2[q].x) * W.x + (v2 - q2[q].z) * W.z;
+                        const R g = dvw * W.w;
+                        const R pw = (B2 * g - B1) * g;
+                        a3x = fma(pw, W.x, a3x); a3z = fma(pw, W.z, a3z);
                     }
                 }
             }
-            s1[0] = R(a1x); s1[2] = R(a1z);
-            s2[0] = R(a2x); s2[2] = R(a2z);
-            s3[0] = R(a3x); s3[2] = R(a3z);
+            s1[0] = a1x; s1[2] = a1z;
+            s2[0] = a2x; s2[2] = a2z;
+            s3[0] = a3x; s3[2] = a3z;
         } else {
             const double xi = b.Xs[i], yi = b.Xs[N + i], zi = b.Xs[2 * N + i];
             const int32_t* sidx = b.sidx + base + lane;

@@ -334,6 +334,29 @@ def test_class_mode_l2_gather_pass_b(tag, monkeypatch):
     # without classes or lanes)
 
 
+@pytest.mark.parametrize("tag", ["kalthoff2d_p", "branch2d"])
+def test_class_mode_l2_gather_pass_b_fp64(tag, monkeypatch):
+    """The same class-mode L2 gather in FP64 (2D bodies with the untiled
+    pass B): F - I, S, a, u, v, s within 1e-12 of the reference at the initial
+    evaluation and after step 1."""
+    monkeypatch.setenv("TLSPH_TILE_B", "0")
+    G = golden(f"run_{tag}")
+    cfg, sim = _sim(G, "fp64")
+    db = sim.dbodies[0]
+    assert db.bcls is not None and not db.tile_b and bool(db.desc.bcls_host)
+    sim.initialize()
+    st = cfg.bodies[0].state
+    e0 = _errors(st, G, 0)
+    sim.step(G["dts"][0])
+    e1 = _errors(st, G, 1)
+    for k in ("F", "S", "a"):
+        assert e0[k] <= TOL_STEP1_64, ("init", k, e0[k])
+        assert e1[k] <= TOL_STEP1_64, ("step1", k, e1[k])
+    for k in ("u", "v", "s"):
+        if k in e1:
+            assert e1[k] <= TOL_STEP1_64, ("step1", k, e1[k])
+
+
 @pytest.mark.parametrize("tag,expect", [("kalthoff3d", True), ("kalthoff2d_p", True),
                                         ("branch2d", True), ("fourpoint3d", None),
                                         ("beam2d", None), ("plate3d", None)])
